@@ -1,0 +1,523 @@
+"""Generate the golden fixtures from the *reference* implementation.
+
+Run here (the container that has ``/root/reference``), never on the GPU box:
+
+    OPENBLAS_CORETYPE=Haswell OPENBLAS_NUM_THREADS=1 \
+        python tests/golden/make_goldens.py
+
+Everything in ``tests/golden/*.npz`` is produced by this script from the
+reference package ``rearrange_sim`` (``/root/reference/pkg/src``) imported
+as-is.  Fixtures:
+
+* ``scene_tables.npz``  body / part / facet / joint / walk-grid tables of
+  layouts 0-2 with the 20-object flat clutter set, as the reference builds
+  them (``physics.py:257-330``, ``scene.py:475-588``) -> pins our scene
+  compiler.
+* ``settled_pool.npz``  snapshots (``WorldState.to_bytes``) of settled
+  clutter states built by the SURVEY §8d recipe (``Simulator.settle``).
+* ``traj_<name>.npz``  teacher-forcing records: per control step the input
+  snapshot, the joint targets, the output snapshot, the contact events and
+  counter deltas, and per substep the admitted pair list and narrowphase
+  contacts (``physics.py:575-719``).
+* ``render.npz``  per-pixel nearest-hit range and body id for head + arm
+  cameras, computed with the reference ray primitive ``parts_ray_hits``
+  (``geometry.py:772-776``) in body-id order with the pinned tie rule
+  (|t_b - t_min| <= 1e-9 -> lowest body id; ``physics.py:1096-1100`` keeps
+  the lowest id on exact ties).
+* ``kat.npz``  known-answer values (SPEC.md examples) from the reference.
+
+The numpy/scipy versions and the OpenBLAS core type are recorded in every
+file (``meta`` key): the oracle's float64 last bits depend on them
+(SURVEY.md §8c).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+from rearrange_sim import builtin, geometry as geo, physics, robot as rb, scene  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+FLAT = ["pudding_box", "gelatin_box", "sponge", "plate", "tuna_fish_can", "bowl",
+        "potted_meat_can", "apple", "orange"]
+SLOT_RECEPTACLES = ["counter_left", "counter_right", "light_table", "dark_table", "sofa", "shelves"]
+KIND = {"static": 0, "kinematic": 1, "dynamic": 2}
+PKIND = {"box": 0, "sphere": 1, "hull": 2}
+NO_GROUP = -(2**31)
+
+
+def meta():
+    import scipy
+
+    return json.dumps({
+        "numpy": np.__version__, "scipy": scipy.__version__,
+        "openblas_coretype": os.environ.get("OPENBLAS_CORETYPE", "default"),
+        "generator": "tests/golden/make_goldens.py",
+    })
+
+
+def make_sim(variant, config=None):
+    cache = builtin.default_cache()
+    sh = scene.load_scene(builtin.make_layout(variant), cache)
+    names = [FLAT[i % len(FLAT)] for i in range(20)]
+    sim = physics.Simulator(sh, rb.default_model(),
+                            [(cache.get_asset(n), f"{n}#{i}") for i, n in enumerate(names)],
+                            config or physics.PhysicsConfig())
+    return sim, cache
+
+
+# --------------------------------------------------------------------------
+# scene tables
+# --------------------------------------------------------------------------
+
+def dump_tables(sim, prefix, out):
+    bodies = sim.bodies
+    out[prefix + "body_kind"] = np.array([KIND[b.kind] for b in bodies], np.int32)
+    out[prefix + "body_robot"] = np.array([b.is_robot for b in bodies], np.int32)
+    out[prefix + "body_group"] = np.array([sim._same_group.get(b.body_id, NO_GROUP) for b in bodies], np.int64)
+    out[prefix + "body_joint"] = np.array([b.scene_joint for b in bodies], np.int32)
+    out[prefix + "body_inv_mass"] = np.array([b.inv_mass for b in bodies])
+    out[prefix + "body_com"] = np.array([b.com_local for b in bodies])
+    out[prefix + "body_inv_inertia"] = np.array([b.inv_inertia_local for b in bodies])
+    out[prefix + "body_friction"] = np.array([b.friction for b in bodies])
+    out[prefix + "body_restitution"] = np.array([b.restitution for b in bodies])
+    pb, pk, pl, pp, fb, nrm, off, vb, vert, tb, tri = [], [], [], [], [0], [], [], [0], [], [0], []
+    for b in bodies:
+        for local, prim in b.parts:
+            pb.append(b.body_id)
+            pk.append(PKIND[prim.kind])
+            pl.append(np.concatenate([local.rot.reshape(9), local.pos]))
+            if prim.kind == "sphere":
+                pp.append([prim.radius, 0, 0])
+                fb.append(fb[-1]); vb.append(vb[-1]); tb.append(tb[-1])
+                continue
+            pp.append(prim.half if prim.kind == "box" else [0, 0, 0])
+            nrm.append(prim.normals); off.append(prim.offsets); vert.append(prim.vertices)
+            fb.append(fb[-1] + len(prim.normals)); vb.append(vb[-1] + len(prim.vertices))
+            t = prim.triangles if prim.kind == "hull" else np.zeros((0, 3), int)
+            tri.append(t); tb.append(tb[-1] + len(t))
+    out[prefix + "part_body"] = np.array(pb, np.int32)
+    out[prefix + "part_kind"] = np.array(pk, np.int32)
+    out[prefix + "part_local"] = np.array(pl)
+    out[prefix + "part_param"] = np.array(pp, dtype=float)
+    out[prefix + "part_facet_begin"] = np.array(fb, np.int32)
+    out[prefix + "part_vert_begin"] = np.array(vb, np.int32)
+    out[prefix + "part_tri_begin"] = np.array(tb, np.int32)
+    out[prefix + "facet_normal"] = np.concatenate(nrm)
+    out[prefix + "facet_offset"] = np.concatenate(off)
+    out[prefix + "vert"] = np.concatenate(vert)
+    out[prefix + "tri"] = np.concatenate(tri).astype(np.int32)
+    js = sim.scene.joints
+    out[prefix + "joint_type"] = np.array([0 if j.joint.joint_type == "revolute" else 1 for j in js], np.int32)
+    out[prefix + "joint_body"] = np.array([j.body_id for j in js], np.int32)
+    out[prefix + "joint_parent"] = np.array([j.parent_body for j in js], np.int32)
+    out[prefix + "joint_axis"] = np.array([j.joint.axis for j in js])
+    out[prefix + "joint_origin"] = np.array([np.concatenate([j.joint.origin.rot.reshape(9), j.joint.origin.pos]) for j in js])
+    out[prefix + "joint_limits"] = np.array([j.joint.limits for j in js])
+    out[prefix + "joint_handle"] = np.array([j.joint.handle_point for j in js])
+    ng = sim.scene.navgrid
+    out[prefix + "nav_walkable"] = ng.walkable.astype(np.uint8)
+    out[prefix + "nav_origin"] = np.asarray(ng.origin, float)
+    st = sim.park_state()
+    out[prefix + "park_state"] = np.frombuffer(st.to_bytes(), np.uint8)
+
+
+def gen_tables():
+    out = {"meta": meta()}
+    for v in range(3):
+        sim, _ = make_sim(v)
+        dump_tables(sim, f"l{v}_", out)
+    m = rb.default_model()
+    rng = np.random.default_rng(11)
+    qs = np.stack([m.resting_joints, np.zeros(7)] + [rng.uniform(m.limits_lo(), m.limits_hi()) for _ in range(6)])
+    bases = np.stack([[0.0, 0.0, 0.0], [2.3, -0.2, 0.7]] + [[rng.uniform(-3, 3), rng.uniform(-2, 2), rng.uniform(-3, 3)] for _ in range(6)])
+    link_pose, ee = [], []
+    for q, b in zip(qs, bases):
+        links, e = rb.link_poses(m, q, b)
+        link_pose.append([np.concatenate([lp.rot.reshape(9), lp.pos]) for lp in links])
+        ee.append(np.concatenate([e.rot.reshape(9), e.pos]))
+    out["fk_q"], out["fk_base"] = qs, bases
+    out["fk_links"], out["fk_ee"] = np.array(link_pose), np.array(ee)
+    out["cam_head"] = np.concatenate([m.cameras["head"].pose.rot.reshape(9), m.cameras["head"].pose.pos])
+    out["cam_arm"] = np.concatenate([m.cameras["arm"].pose.rot.reshape(9), m.cameras["arm"].pose.pos])
+    np.savez_compressed(os.path.join(OUT, "scene_tables.npz"), **out)
+
+
+# --------------------------------------------------------------------------
+# settled pool (SURVEY.md §8d recipe)
+# --------------------------------------------------------------------------
+
+def slots_for(sim):
+    out = []
+    for name in SLOT_RECEPTACLES:
+        rec = sim.scene.receptacles[name]
+        owner = sim.scene.bodies[rec.owner_body].initial_pose
+        for box in rec.boxes:
+            if box.kind != "on_top":
+                continue
+            hx, hy = box.half_extents[:2] - 0.1
+            for gx in np.linspace(-hx, hx, 4):
+                for gy in np.linspace(-hy, hy, 2):
+                    out.append((owner, np.array([gx, gy, box.center[2] - box.half_extents[2]])))
+    return out
+
+
+def settle_seed(sim, seed):
+    base = sim.park_state()
+    slots = slots_for(sim)
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(len(slots))
+    placements = []
+    for k, bid in enumerate(sim.clutter_body_ids):
+        owner, local = slots[order[k]]
+        lo, _ = geo.parts_aabb(sim.bodies[bid].parts, geo.Pose())
+        pos = owner.apply(local) + np.array([0.0, 0.0, -lo[2] + 0.01])
+        rot = geo.rot_z(rng.uniform(-math.pi, math.pi))
+        placements.append((bid, geo.Pose(rot, pos)))
+    _, st = sim.settle(placements, max_time=10.0, base_state=base)
+    return st
+
+
+def gen_pool(seeds=range(8)):
+    blobs, tags = [], []
+    for v in range(3):
+        sim, _ = make_sim(v)
+        for s in seeds:
+            try:
+                st = settle_seed(sim, s)
+            except physics.SettleUnstable as exc:
+                print(f"  layout {v} seed {s}: {exc}")
+                continue
+            blobs.append(np.frombuffer(st.to_bytes(), np.uint8))
+            tags.append((v, s))
+            print(f"  layout {v} seed {s}: settled at step {st.step_index}, hash {st.state_hash()[:16]}")
+    np.savez_compressed(os.path.join(OUT, "settled_pool.npz"), meta=meta(), snapshots=np.stack(blobs),
+                        tags=np.array(tags, np.int32))
+    return blobs, tags
+
+
+# --------------------------------------------------------------------------
+# trajectories with per-substep instrumentation
+# --------------------------------------------------------------------------
+
+class Recorder:
+    """Wraps one Simulator's broadphase/narrowphase to log per-substep data."""
+
+    def __init__(self, sim):
+        self.sim = sim
+        self.sub_pairs, self.sub_contacts = [], []
+        bp, npf = sim._broadphase_pairs, sim._narrowphase
+
+        def bp_wrap(state):
+            pairs = bp(state)
+            self.sub_pairs.append(list(pairs))
+            return pairs
+
+        def np_wrap(state, pairs):
+            out = npf(state, pairs)
+            rows = []
+            for a, b, cl in out:
+                for c in cl:
+                    rows.append([a, b, *c.point, *c.normal, c.depth])
+            self.sub_contacts.append(rows)
+            return out
+
+        sim._broadphase_pairs = bp_wrap
+        sim._narrowphase = np_wrap
+
+    def reset(self):
+        self.sub_pairs, self.sub_contacts = [], []
+
+
+def record(sim, st, targets_seq, name, grasp_fn=None):
+    """Step `st` through `targets_seq`; teacher-forcing records per step."""
+    rec = Recorder(sim)
+    cols = {k: [] for k in ("pre", "post", "arm", "base", "has_targets", "counters")}
+    pairs, pair_off, contacts, contact_off, events, event_off = [], [0], [], [0], [], [0]
+    for t, tg in enumerate(targets_seq):
+        if callable(tg):
+            tg = tg(sim, st)
+        rec.reset()
+        c0 = dict(sim.counters)
+        pre = st
+        st, ev = sim.step_physics(st, tg)
+        cols["pre"].append(np.frombuffer(pre.to_bytes(), np.uint8))
+        cols["post"].append(np.frombuffer(st.to_bytes(), np.uint8))
+        cols["has_targets"].append(tg is not None)
+        cols["arm"].append(np.asarray(tg.arm, float) if tg is not None else np.zeros(7))
+        cols["base"].append([tg.base.linear_velocity, tg.base.angular_velocity] if tg is not None else [0.0, 0.0])
+        cols["counters"].append([sim.counters[k] - c0[k] for k in ("narrowphase_tests", "skipped_sleeping_pairs", "wakes")])
+        assert len(rec.sub_pairs) == 4
+        for sp, sc in zip(rec.sub_pairs, rec.sub_contacts):
+            pairs.extend(sp); pair_off.append(len(pairs))
+            contacts.extend(sc); contact_off.append(len(contacts))
+        for e in ev:
+            events.append([e.bodies[0], e.bodies[1], e.impulse, e.force, *e.point])
+        event_off.append(len(events))
+    out = {k: np.array(v) for k, v in cols.items()}
+    out.update(
+        meta=meta(),
+        pairs=np.array(pairs, np.int32).reshape(-1, 2), pair_off=np.array(pair_off, np.int64),
+        contacts=np.array(contacts, float).reshape(-1, 9), contact_off=np.array(contact_off, np.int64),
+        events=np.array(events, float).reshape(-1, 7), event_off=np.array(event_off, np.int64),
+        final=np.frombuffer(st.to_bytes(), np.uint8),
+    )
+    np.savez_compressed(os.path.join(OUT, f"traj_{name}.npz"), **out)
+    print(f"  traj_{name}: {len(targets_seq)} steps, {len(pairs)} pairs, {len(contacts)} contacts, {len(events)} events")
+    return st
+
+
+def idle_targets(sim, st, n, seed=3):
+    """Random EE deltas through the reference IK + random base velocities."""
+    m = sim.robot
+    rng = np.random.default_rng(seed)
+    seq = []
+
+    def make(d, lin, ang):
+        def f(sim, st):
+            q = st.joints[sim.arm_slice()]
+            tg = rb.apply_arm_action(m, q, rb.ArmAction(d, 0.0), sim.counters)
+            tg.base = rb.BaseAction(lin, ang)
+            return tg
+        return f
+
+    for _ in range(n):
+        d = rng.uniform(-0.02, 0.02, 3)
+        seq.append(make(d, rng.uniform(-0.5, 1.0), rng.uniform(-1, 1)))
+    return seq
+
+
+def gen_trajectories(pool_blobs, pool_tags):
+    first = {v: physics.WorldState.from_bytes(b.tobytes()) for b, (v, s) in reversed(list(zip(pool_blobs, pool_tags)))}
+
+    # idle (the benchmark scenario): living-room centre, random actions
+    sim, _ = make_sim(0)
+    st = first[0].clone()
+    st.base = np.array([2.3, -0.2, 0.0])
+    sim._update_robot_link_poses(st, 0.0)
+    record(sim, st, idle_targets(sim, st, 20), "idle")
+
+    # zero action, all asleep: the bit-exact fixed point
+    sim, _ = make_sim(1)
+    st = first[1].clone()
+    st.base = np.array([2.3, -0.2, 1.0])
+    sim._update_robot_link_poses(st, 0.0)
+    q = st.joints[sim.arm_slice()].copy()
+    record(sim, st, [rb.JointTargets(arm=q.copy()) for _ in range(3)], "fixed")
+
+    # interact: arm sweeping into the light-table clutter
+    sim, _ = make_sim(0)
+    st = first[0].clone()
+    st.base = np.array([1.6, 0.2, math.pi / 2])
+    sim._update_robot_link_poses(st, 0.0)
+    m = sim.robot
+
+    def scripted(k):
+        def f(sim, st):
+            d = np.array([0.015, 0.0, -0.012]) if k < 60 else np.array([0.0, 0.015 if (k // 10) % 2 else -0.015, 0.0])
+            return rb.apply_arm_action(m, st.joints[sim.arm_slice()], rb.ArmAction(d, 0.0), sim.counters)
+        return f
+    record(sim, st, [scripted(k) for k in range(90)], "interact")
+
+    # physics opts off: every dynamic body awake, every pair tested (block LCP heavy)
+    sim, _ = make_sim(2, physics.PhysicsConfig(sleeping_enabled=False))
+    st = first[2].clone()
+    st.base = np.array([2.3, -0.2, 0.0])
+    sim._update_robot_link_poses(st, 0.0)
+    record(sim, st, [None] * 4, "awake")
+
+    # free drop: a box 1 m above the floor in open space
+    sim, _ = make_sim(0)
+    st = sim.park_state()
+    bid = sim.clutter_body_ids[0]
+    st.set_body_pose(bid, geo.Pose(geo.rot_z(0.3), np.array([0.0, 0.0, 1.0])))
+    st.asleep[bid] = False
+    record(sim, st, [None] * 32, "drop")
+
+    # free drop onto open floor, tilted so it lands on an edge
+    sim, _ = make_sim(0)
+    st = sim.park_state()
+    bid = sim.clutter_body_ids[6]
+    st.set_body_pose(bid, geo.Pose(geo.rot_axis_angle(np.array([1.0, 0.4, 0.0]), 0.5), np.array([0.0, -1.5, 0.6])))
+    st.asleep[bid] = False
+    record(sim, st, [None] * 30, "drop_floor")
+
+    # settle: all 20 clutter bodies spawned 1 cm above their slots, awake (physics.py:1113-1154)
+    sim, _ = make_sim(1)
+    base = sim.park_state()
+    slots = slots_for(sim)
+    rng = np.random.default_rng(2)
+    order = rng.permutation(len(slots))
+    st = base.clone()
+    for k, bid in enumerate(sim.clutter_body_ids):
+        owner, local = slots[order[k]]
+        lo, _ = geo.parts_aabb(sim.bodies[bid].parts, geo.Pose())
+        pos = owner.apply(local) + np.array([0.0, 0.0, -lo[2] + 0.01])
+        st.set_body_pose(bid, geo.Pose(geo.rot_z(rng.uniform(-math.pi, math.pi)), pos))
+        st.asleep[bid] = False
+        st.rider_joint[bid] = -1
+    record(sim, st, [None] * 6, "settle")
+
+    # tilt: settled clutter tilted 0.2 rad and raised 3 cm, all awake
+    sim, _ = make_sim(0)
+    st = first[0].clone()
+    for bid in sim.clutter_body_ids:
+        p = st.body_pose(bid)
+        rot = geo.rot_axis_angle(np.array([1.0, 0.0, 0.0]), 0.2) @ p.rot
+        st.set_body_pose(bid, geo.Pose(rot, p.pos + np.array([0.0, 0.0, 0.03])))
+        st.asleep[bid] = False
+    record(sim, st, [None] * 24, "tilt")
+
+    # drawer drag: handle grasp on drawer_2, base backing away (physics.py:623-655)
+    sim, _ = make_sim(0)
+    st = first[0].clone()
+    st.base = np.array([-3.55, -0.45, math.pi])
+    sim._update_robot_link_poses(st, 0.0)
+    ji = [j.joint_id for j in sim.scene.joints].index("kitchen_cabinet#1:drawer_2")
+    st.held_joint = ji
+    st.held = sim.scene.joints[ji].body_id
+    st.grab_q = float(st.joints[ji])
+    st.grab_ee = sim.ee_pose(st).pos.copy()
+    q = st.joints[sim.arm_slice()].copy()
+    record(sim, st, [rb.JointTargets(arm=q.copy(), base=rb.BaseAction(-0.5, 0.0)) for _ in range(20)], "drawer")
+
+    # fridge door drag (revolute branch of _drag_held_joint)
+    sim, _ = make_sim(0)
+    st = first[0].clone()
+    st.base = np.array([-2.6, 1.7, math.pi / 2])
+    sim._update_robot_link_poses(st, 0.0)
+    ji = [j.joint_id for j in sim.scene.joints].index("fridge#2:door")
+    st.held_joint = ji
+    st.held = sim.scene.joints[ji].body_id
+    st.grab_q = float(st.joints[ji])
+    st.grab_ee = sim.ee_pose(st).pos.copy()
+    q = st.joints[sim.arm_slice()].copy()
+    record(sim, st, [rb.JointTargets(arm=q.copy(), base=rb.BaseAction(-0.4, 0.3)) for _ in range(15)], "fridge")
+
+    # held object: snap the nearest clutter body and carry it while turning
+    sim, _ = make_sim(0)
+    st = first[0].clone()
+    cands = sorted(sim.grasp_candidates(st), key=lambda c: (c[0], c[1]))
+    obj = [c for c in cands if c[2] is None][0][1]
+    com = st.body_pose(obj).apply(sim.bodies[obj].com_local)
+    st.base = np.array([com[0] - 0.8, com[1], 0.0])
+    sim._update_robot_link_poses(st, 0.0)
+    sim.apply_grasp(st, rb.GraspTransition("snap", body=obj))
+    q = st.joints[sim.arm_slice()].copy()
+    q2 = q + np.array([0.2, -0.1, 0.1, 0.2, 0.0, -0.1, 0.3])
+    record(sim, st, [rb.JointTargets(arm=q2.copy(), base=rb.BaseAction(-0.3, 0.5)) for _ in range(12)], "held")
+
+
+# --------------------------------------------------------------------------
+# render restatement through the reference ray primitive
+# --------------------------------------------------------------------------
+
+W = H = 128
+FOV = math.pi / 2
+NEAR, FAR = 0.1, 10.0
+TIE_EPS = 1e-9
+
+
+def camera_rays(cam_pose):
+    f = (W / 2) / math.tan(FOV / 2)
+    u = (np.arange(W) + 0.5 - W / 2) / f
+    v = (np.arange(H) + 0.5 - H / 2) / f
+    vv, uu = np.meshgrid(v, u, indexing="ij")
+    d = np.stack([uu, vv, np.ones_like(uu)], axis=-1).reshape(-1, 3)
+    d = d / np.linalg.norm(d, axis=1, keepdims=True)
+    return np.tile(cam_pose.pos, (len(d), 1)), d @ cam_pose.rot.T
+
+
+def render_ref(sim, st, cam):
+    m = sim.robot
+    mount = m.cameras[cam]
+    parent = rb.base_pose3(st.base) if mount.parent == "base" else sim.ee_pose(st)
+    pose = parent.compose(mount.pose)
+    o, d = camera_rays(pose)
+    ts = np.stack([geo.parts_ray_hits(sim.bodies[b].parts, st.body_pose(b), o, d) for b in range(sim.n_bodies)])
+    tmin = ts.min(axis=0)
+    ids = np.full(len(tmin), -1, np.int32)
+    finite = np.isfinite(tmin)
+    within = ts <= (tmin + TIE_EPS)[None, :]
+    ids[finite] = np.argmax(within[:, finite], axis=0)
+    return tmin.reshape(H, W), ids.reshape(H, W), pose
+
+
+def gen_render():
+    out = {"meta": meta(), "fov": FOV, "near": NEAR, "far": FAR, "tie_eps": TIE_EPS}
+    frames = []
+    for name, step in (("idle", 0), ("idle", 19), ("interact", 70), ("drawer", 19), ("held", 11), ("fridge", 14)):
+        tr = np.load(os.path.join(OUT, f"traj_{name}.npz"))
+        blob = tr["post"][step].tobytes()
+        st = physics.WorldState.from_bytes(blob)
+        variant = 0
+        sim, _ = make_sim(variant)
+        for cam in ("head", "arm"):
+            t, ids, pose = render_ref(sim, st, cam)
+            frames.append(dict(state=np.frombuffer(blob, np.uint8), cam=0 if cam == "head" else 1, t=t, ids=ids,
+                               cam_pose=np.concatenate([pose.rot.reshape(9), pose.pos]), layout=variant))
+    for k in frames[0]:
+        out[k] = np.stack([f[k] for f in frames])
+    np.savez_compressed(os.path.join(OUT, "render.npz"), **out)
+    print(f"  render: {len(frames)} frames")
+
+
+# --------------------------------------------------------------------------
+# known-answer tests
+# --------------------------------------------------------------------------
+
+def gen_kat():
+    out = {"meta": meta()}
+    box = geo.Box([0.5, 0.5, 0.5])
+    out["ray_box_t"] = geo.prim_ray_hits(box, geo.Pose(), np.array([[-2.0, 0, 0]]), np.array([[1.0, 0, 0]]))
+    m = rb.default_model()
+    out["fk_zero_ee"] = rb.forward_kinematics(m, np.zeros(7)).pos
+    out["fk_rest_ee"] = rb.forward_kinematics(m, m.resting_joints).pos
+    out["clamp"] = rb.ArmAction(np.array([0.10, 0, 0]), 0.0).clamped_delta()
+    cands = [(0.10, 30, None), (0.16, 22, None)]
+    out["grasp_snap"] = rb.grasp_rule(1.0, False, cands).body
+    out["grasp_none"] = rb.grasp_rule(1.0, False, [(0.16, 22, None)]).kind == "none"
+    out["grasp_tie"] = rb.grasp_rule(1.0, False, [(0.1, 31, None), (0.1, 25, None)]).body
+    # nearest-walkable queries (navgrid.py:70-105), incl. blocked and out-of-grid points
+    sim, _ = make_sim(0)
+    ng = sim.scene.navgrid
+    rng = np.random.default_rng(5)
+    q = np.concatenate([rng.uniform([-5.2, -3.2], [5.2, 3.2], (400, 2)),
+                        np.array([[-4.65, -0.5], [1.6, 1.1], [9.0, 0.0], [0.0, -4.0]])])
+    out["nav_query"] = q
+    out["nav_walkable"] = np.array([ng.is_walkable(p) for p in q])
+    out["nav_nearest"] = np.array([ng.nearest_walkable(p) for p in q])
+    # move_base on the grid (robot.py:349-372)
+    mb_in = np.concatenate([rng.uniform([-4.5, -2.5, -3.1], [4.5, 2.5, 3.1], (200, 3))])
+    mb_act = rng.uniform([-1.0, -2.0], [2.0, 2.0], (200, 2))
+    out["mb_in"], out["mb_act"] = mb_in, mb_act
+    out["mb_out"] = np.array([rb.move_base(b, ng, rb.BaseAction(a[0], a[1]), 1 / 120) for b, a in zip(mb_in, mb_act)])
+    np.savez_compressed(os.path.join(OUT, "kat.npz"), **out)
+
+
+if __name__ == "__main__":
+    t0 = time.time()
+    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat"]
+    if "tables" in what:
+        gen_tables(); print("tables", time.time() - t0)
+    blobs = tags = None
+    if "pool" in what:
+        blobs, tags = gen_pool(); print("pool", time.time() - t0)
+    if "traj" in what:
+        if blobs is None:
+            p = np.load(os.path.join(OUT, "settled_pool.npz"))
+            blobs, tags = list(p["snapshots"]), [tuple(t) for t in p["tags"]]
+        gen_trajectories(blobs, tags); print("traj", time.time() - t0)
+    if "render" in what:
+        gen_render(); print("render", time.time() - t0)
+    if "kat" in what:
+        gen_kat(); print("kat", time.time() - t0)
