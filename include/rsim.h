@@ -1,0 +1,183 @@
+/*
+ * rsim.h -- C ABI of the B200 batched rearrangement-simulator step.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (SURVEY.md §8b).  The reference's operator API is the Python class
+ * `rearrange_sim.physics.Simulator` plus the (specified but unshipped)
+ * sensors/pipeline modules; every entry point below replaces one of them,
+ * with a leading environment dimension added:
+ *
+ *   rs_scene_create   <- Simulator.__init__ body tables       physics.py:257-330
+ *                        (+ scene.load_scene tables             scene.py:475-588)
+ *   rs_batch_create   <- one Simulator per env + PhysicsConfig physics.py:54-74
+ *   rs_set_state      <- WorldState.from_bytes                 physics.py:166-203
+ *   rs_get_state      <- WorldState.to_bytes                   physics.py:147-164
+ *   rs_step           <- Simulator.step_physics                physics.py:575-594
+ *   rs_render         <- sensors.render_depth (SPEC only)
+ *                        restated over geometry.parts_ray_hits geometry.py:772-776
+ *   rs_step_host      <- pipeline.step (SPEC only)
+ *                        physics + render with host buffers
+ *   rs_grasp          <- grasp_rule + apply_grasp              robot.py:323-346, physics.py:1039-1079
+ *
+ * Conventions:
+ *   - every call is stream-ordered on the cudaStream_t passed as `stream`
+ *     (NULL = legacy default stream); a batch is owned by one host thread;
+ *   - device pointers are caller-allocated and never freed by the library;
+ *   - return value 0 = success; non-zero = error code, message in
+ *     rs_last_error() (thread-local).  Per-env physics faults (non-finite
+ *     state, the reference's PhysicsFault physics.py:596-606) are reported
+ *     in the fault word of rs_buffers, not as a return code;
+ *   - snapshot buffers are the reference's WorldState byte format.
+ */
+#ifndef RSIM_H
+#define RSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+enum { RS_STATIC = 0, RS_KINEMATIC = 1, RS_DYNAMIC = 2 };
+enum { RS_BOX = 0, RS_SPHERE = 1, RS_HULL = 2 };
+enum { RS_REVOLUTE = 0, RS_PRISMATIC = 1 };
+enum {
+  RS_OK = 0,
+  RS_ERR_ARG = 1,     /* bad argument / shape */
+  RS_ERR_CUDA = 2,    /* CUDA runtime error */
+  RS_ERR_SNAPSHOT = 3,/* malformed snapshot (bad magic/version/size) */
+  RS_ERR_CAPACITY = 4 /* scene exceeds compiled kernel capacities */
+};
+/* fault word kinds (high 16 bits; low 16 bits = body or joint index) */
+enum {
+  RS_FAULT_NONE = 0,
+  RS_FAULT_NONFINITE_POS = 1,
+  RS_FAULT_NONFINITE_QUAT = 2,
+  RS_FAULT_NONFINITE_VEL = 3,
+  RS_FAULT_NONFINITE_JOINT = 4,
+  RS_FAULT_OVERFLOW = 5 /* contact/pair capacity exceeded: result invalid */
+};
+
+#define RS_NO_GROUP ((int32_t)0x80000000)
+
+/* Static scene tables of one layout (see paper_2106_14405_b200/compiler.py). */
+typedef struct {
+  int32_t n_bodies, n_parts, n_facets, n_verts, n_tris;
+  int32_t n_scene_joints, n_arm, robot_base;
+  /* bodies [n_bodies] */
+  const int32_t *body_kind, *body_robot, *body_group, *body_joint;
+  const double *body_inv_mass, *body_com /*3*/, *body_inv_inertia /*9*/;
+  const double *body_friction, *body_restitution;
+  const int32_t *body_part_begin; /* n_bodies + 1 */
+  const float *body_color;        /* 3 */
+  /* parts [n_parts] */
+  const int32_t *part_body, *part_kind;
+  const double *part_local; /* 12: row-major R, t */
+  const double *part_param; /* 3: box half extents | sphere radius */
+  const int32_t *part_facet_begin, *part_vert_begin, *part_tri_begin; /* n_parts + 1 */
+  const double *facet; /* 4: n, offset (n.x <= offset inside) */
+  const double *vert;  /* 3 */
+  const int32_t *tri;  /* 3, part-local vertex indices */
+  /* scene joints [n_scene_joints] */
+  const int32_t *joint_type, *joint_body, *joint_parent;
+  const double *joint_axis /*3*/, *joint_origin /*12*/, *joint_limits /*2*/, *joint_handle /*3*/;
+  /* arm chain [n_arm] */
+  const double *arm_offset /*3*/, *arm_axis /*3*/, *arm_limits /*2*/;
+  double gripper_offset[3];
+  /* cameras */
+  int32_t n_cameras;
+  const int32_t *cam_parent; /* 0 = base, 1 = end effector */
+  const double *cam_mount;   /* 12 */
+  /* walk grid, x-major [nav_nx][nav_ny] */
+  int32_t nav_nx, nav_ny;
+  double nav_origin[2], nav_cell;
+  const uint8_t *nav_walkable;
+} rs_scene_desc;
+
+/* physics.py:54-74 PhysicsConfig, field for field */
+typedef struct {
+  double gravity;
+  int32_t solver_iterations;
+  double correction_factor, slop, restitution_threshold, contact_margin;
+  double sleep_lin_threshold, sleep_ang_threshold;
+  int32_t sleep_substeps;
+  double wake_margin, lin_damping, ang_damping, joint_damping;
+  double joint_inertia_revolute, joint_inertia_prismatic, kp, motor_impulse_cap;
+  int32_t impulse_cap_per_control_step, sleeping_enabled;
+} rs_physics_config;
+
+/* pinned sensor conventions */
+typedef struct {
+  int32_t width, height;
+  double fov;      /* radians, horizontal = vertical */
+  double znear, zfar;
+  double tie_eps;  /* |t_b - t_min| <= tie_eps -> lowest body id */
+} rs_render_config;
+
+/* device-side views owned by the batch (valid until rs_batch_destroy) */
+typedef struct {
+  int32_t n_env, n_bodies, n_joints, event_cap;
+  uint32_t *fault;        /* [n_env] */
+  int32_t *event_count;   /* [n_env] events of the last rs_step (may exceed cap: overflow) */
+  double *events;         /* [n_env][event_cap][7]: a, b, impulse, force, point xyz */
+  int64_t *counters;      /* [n_env][3] narrowphase_tests, skipped_sleeping_pairs, wakes (cumulative) */
+  double *acc_force;      /* [n_env] accumulated_contact_force (alias into the state) */
+} rs_buffers;
+
+typedef struct rs_scene rs_scene;
+typedef struct rs_batch rs_batch;
+
+int rs_abi_version(void);
+const char *rs_last_error(void);
+/* bytes of one snapshot for (n_bodies, n_joints) */
+int64_t rs_snapshot_size(int32_t n_bodies, int32_t n_joints);
+
+int rs_scene_create(const rs_scene_desc *desc, rs_scene **out);
+void rs_scene_destroy(rs_scene *scene);
+
+/* env e simulates scenes[env_scene[e]]; all scenes must share body/joint counts */
+int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *env_scene, int32_t n_env,
+                    const rs_physics_config *cfg, const rs_render_config *rcfg, int32_t event_cap,
+                    rs_batch **out);
+void rs_batch_destroy(rs_batch *batch);
+int rs_batch_buffers(rs_batch *batch, rs_buffers *out);
+
+/* host snapshots <-> device state; env_ids NULL = 0..n-1; stride = bytes between snapshots */
+int rs_set_state(rs_batch *batch, const uint8_t *snapshots, int64_t stride, const int32_t *env_ids,
+                 int32_t n, void *stream);
+int rs_get_state(rs_batch *batch, uint8_t *snapshots, int64_t stride, const int32_t *env_ids,
+                 int32_t n, void *stream);
+
+/* one control step for every env (device pointers):
+ *   arm_targets [n_env][n_arm] f64 joint targets (JointTargets.arm)
+ *   base_cmd    [n_env][2] f64 linear, angular velocity (BaseAction)
+ *   has_targets [n_env] u8, 0 = targets None (settle mode); NULL = all 1 */
+int rs_step(rs_batch *batch, const double *arm_targets, const double *base_cmd, const uint8_t *has_targets,
+            double dt, int32_t substeps, void *stream);
+
+/* render cameras in cam_mask for every env into device tensors
+ *   rgba [n_env][n_cam_out][H][W][4] u8, depth [..][H][W] f32, ids [..][H][W] i32;
+ * n_cam_out = popcount(cam_mask); any output pointer may be NULL. */
+int rs_render(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream);
+
+/* grasp transition per env between steps (robot.py:323-346 + physics.py:1055-1079):
+ * gripper [n_env] f64 device; scalar > 0 snaps the nearest candidate within 0.15 m,
+ * < 0 releases. */
+int rs_grasp(rs_batch *batch, const double *gripper, void *stream);
+
+/* End-to-end env step with HOST buffers (pipeline.step restated):
+ * copies arm_targets/base_cmd (host) to the device, runs rs_step then rs_render
+ * (cam_mask) into the device observation tensors, and copies per-env step
+ * results back to host: out_stats [n_env][4] = accumulated_contact_force,
+ * fault word, event count, sleeping-body count.  Synchronises `stream`. */
+int rs_step_host(rs_batch *batch, const double *h_arm_targets, const double *h_base_cmd, double dt,
+                 int32_t substeps, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                 double *h_out_stats, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSIM_H */

@@ -1,0 +1,148 @@
+"""ctypes front end of the C oracle (TEST INFRASTRUCTURE ONLY).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU legs may
+import this module; the product package never does.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2106_14405_b200.abi import SceneDesc, physics_config, render_config
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "_build", "liboracle.so")
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(HERE, "rsim_oracle.c")
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", HERE], check=True)
+    return LIB
+
+
+class _Trace(C.Structure):
+    _fields_ = [("cap_pairs", C.c_int32), ("cap_contacts", C.c_int32), ("cap_events", C.c_int32),
+                ("n_pairs", C.c_int32), ("n_contacts", C.c_int32), ("n_events", C.c_int32),
+                ("pairs", C.POINTER(C.c_int32)), ("contacts", C.POINTER(C.c_double)),
+                ("events", C.POINTER(C.c_double)), ("counters", C.c_int64 * 3)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB)
+        L.orc_create.restype = C.c_void_p
+        L.orc_create.argtypes = [C.c_void_p, C.c_void_p]
+        L.orc_destroy.argtypes = [C.c_void_p]
+        L.orc_step.restype = C.c_int
+        L.orc_step.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                               C.c_void_p, C.POINTER(C.c_uint32)]
+        L.orc_render.restype = C.c_int
+        L.orc_render.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p]
+        L.orc_camera_pose.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_void_p]
+        L.orc_move_base.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_void_p]
+        L.orc_nearest_walkable.restype = C.c_int
+        L.orc_nearest_walkable.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_void_p]
+        L.orc_link_poses.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_snapshot_size.restype = C.c_int64
+        L.orc_snapshot_size.argtypes = [C.c_int, C.c_int]
+        _lib = L
+    return _lib
+
+
+class StepResult:
+    def __init__(self, snapshot, fault, pairs, contacts, events, counters):
+        self.snapshot = snapshot
+        self.fault = fault
+        self.pairs = pairs          # [n, 3] substep, a, b
+        self.contacts = contacts    # [n, 10] substep, a, b, p, n, depth
+        self.events = events        # [n, 7]
+        self.counters = counters    # narrowphase_tests, skipped_sleeping_pairs, wakes
+
+
+class Oracle:
+    """One CPU world (scene tables + PhysicsConfig)."""
+
+    def __init__(self, tables: dict, **config):
+        self.desc = SceneDesc(tables)
+        self.cfg = physics_config(**config)
+        self.h = lib().orc_create(C.byref(self.desc.desc), C.byref(self.cfg))
+        if not self.h:
+            raise RuntimeError("oracle: scene exceeds capacities")
+        self.snap_size = lib().orc_snapshot_size(self.desc.n_bodies, self.desc.n_joints)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_destroy(self.h)
+            self.h = None
+
+    def step(self, snapshot: bytes, arm=None, base_cmd=(0.0, 0.0), dt=1.0 / 30.0, substeps=4,
+             cap=(8192, 16384, 16384)) -> StepResult:
+        out = np.zeros(self.snap_size, np.uint8)
+        tr = _Trace()
+        tr.cap_pairs, tr.cap_contacts, tr.cap_events = cap
+        pairs = np.zeros((cap[0], 3), np.int32)
+        contacts = np.zeros((cap[1], 10))
+        events = np.zeros((cap[2], 7))
+        tr.pairs = pairs.ctypes.data_as(C.POINTER(C.c_int32))
+        tr.contacts = contacts.ctypes.data_as(C.POINTER(C.c_double))
+        tr.events = events.ctypes.data_as(C.POINTER(C.c_double))
+        fault = C.c_uint32(0)
+        armp = basep = None
+        if arm is not None:
+            arm_a = np.ascontiguousarray(arm, dtype=np.float64)
+            base_a = np.ascontiguousarray(base_cmd, dtype=np.float64)
+            armp, basep = arm_a.ctypes.data, base_a.ctypes.data
+        rc = lib().orc_step(self.h, bytes(snapshot), out.ctypes.data, armp, basep, dt, substeps, C.byref(tr),
+                            C.byref(fault))
+        if rc not in (0, 0x7FFFFFFF):
+            raise ValueError(f"oracle step error {rc}")
+        return StepResult(out.tobytes() if rc == 0 else None, fault.value, pairs[:tr.n_pairs].copy(),
+                          contacts[:tr.n_contacts].copy(), events[:tr.n_events].copy(), list(tr.counters))
+
+    def render(self, snapshot: bytes, cam: int, **rcfg):
+        rc = render_config(**rcfg)
+        H, W = rc.height, rc.width
+        rgba = np.zeros((H, W, 4), np.uint8)
+        depth = np.zeros((H, W), np.float32)
+        ids = np.zeros((H, W), np.int32)
+        t = np.zeros((H, W))
+        r = lib().orc_render(self.h, bytes(snapshot), cam, C.byref(rc), rgba.ctypes.data, depth.ctypes.data,
+                             ids.ctypes.data, t.ctypes.data)
+        if r:
+            raise ValueError(f"oracle render error {r}")
+        return rgba, depth, ids, t
+
+    def camera_pose(self, snapshot: bytes, cam: int) -> np.ndarray:
+        out = np.zeros(12)
+        lib().orc_camera_pose(self.h, bytes(snapshot), cam, out.ctypes.data)
+        return out
+
+    def move_base(self, base, lin, ang, dt):
+        b = np.ascontiguousarray(base, dtype=np.float64)
+        out = np.zeros(3)
+        lib().orc_move_base(self.h, b.ctypes.data, lin, ang, dt, out.ctypes.data)
+        return out
+
+    def nearest_walkable(self, x, y):
+        out = np.zeros(2)
+        lib().orc_nearest_walkable(self.h, x, y, out.ctypes.data)
+        return out
+
+    def link_poses(self, q, base):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        b = np.ascontiguousarray(base, dtype=np.float64)
+        links = np.zeros((len(q), 12))
+        ee = np.zeros(12)
+        lib().orc_link_poses(self.h, q.ctypes.data, b.ctypes.data, links.ctypes.data, ee.ctypes.data)
+        return links, ee

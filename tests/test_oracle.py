@@ -1,0 +1,138 @@
+"""Pin the C oracle against the reference's golden vectors (CPU only).
+
+Teacher-forced: every recorded control step is replayed from the
+reference's own input snapshot with the recorded joint targets, and the
+oracle's output is compared with the reference's:
+
+* admitted pair lists per substep, contact (a, b) sequences per substep,
+  sleep flags / counters / rider bindings, the three live counters:
+  bit-exact;
+* poses, velocities, contact geometry: float64 tolerance (the reference's
+  3x3 products run through OpenBLAS FMA kernels);
+* contact events: same (a, b) sequence after dropping rounding-noise
+  impulses (< 1e-12 N s; the reference emits events for lambda = 1.7e-18).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle.oracle import Oracle
+from paper_2106_14405_b200.compiler import compile_world
+from paper_2106_14405_b200.scene import build_world, flat_clutter
+from paper_2106_14405_b200.state import WorldState
+
+LAYOUT = {"idle": 0, "fixed": 1, "interact": 0, "awake": 2, "drop": 0, "drop_floor": 0, "settle": 1,
+          "tilt": 0, "drawer": 0, "fridge": 0, "held": 0}
+EV_NOISE = 1e-12
+POS_TOL, VEL_TOL = 1e-12, 1e-10
+
+_oracles = {}
+
+
+def oracle_for(layout, **cfg):
+    key = (layout, tuple(sorted(cfg.items())))
+    if key not in _oracles:
+        _oracles[key] = Oracle(compile_world(build_world(layout, flat_clutter())), **cfg)
+    return _oracles[key]
+
+
+def split(arr, off, i):
+    return arr[off[i]:off[i + 1]]
+
+
+def events_clean(ev):
+    return ev[ev[:, 2] > EV_NOISE]
+
+
+@pytest.mark.parametrize("name", sorted(LAYOUT))
+def test_teacher_forced_steps(name):
+    g = golden(f"traj_{name}.npz")
+    cfg = {"sleeping_enabled": 0} if name == "awake" else {}
+    orc = oracle_for(LAYOUT[name], **cfg)
+    for s in range(len(g["pre"])):
+        arm = g["arm"][s] if g["has_targets"][s] else None
+        r = orc.step(g["pre"][s].tobytes(), arm, g["base"][s])
+        assert r.snapshot is not None and r.fault == 0
+        for k in range(4):
+            ref_pairs = split(g["pairs"], g["pair_off"], 4 * s + k)
+            np.testing.assert_array_equal(r.pairs[r.pairs[:, 0] == k][:, 1:], ref_pairs, err_msg=f"{name} step {s} sub {k}")
+            ref_c = split(g["contacts"], g["contact_off"], 4 * s + k)
+            mine = r.contacts[r.contacts[:, 0] == k][:, 1:]
+            np.testing.assert_array_equal(mine[:, :2], ref_c[:, :2])
+            np.testing.assert_allclose(mine[:, 2:], ref_c[:, 2:], rtol=0, atol=1e-12)
+        assert list(g["counters"][s]) == r.counters
+        ref, me = WorldState.from_bytes(g["post"][s].tobytes()), WorldState.from_bytes(r.snapshot)
+        for f in ("asleep", "sleep_counter", "rider_joint"):
+            np.testing.assert_array_equal(getattr(me, f), getattr(ref, f), err_msg=f)
+        assert (me.held, me.held_joint, me.step_index) == (ref.held, ref.held_joint, ref.step_index)
+        for f in ("pos", "quat", "joints", "base", "rider_offset", "held_offset", "grab_ee"):
+            np.testing.assert_allclose(getattr(me, f), getattr(ref, f), rtol=0, atol=POS_TOL, err_msg=f)
+        for f in ("lin_vel", "ang_vel", "joint_vel"):
+            np.testing.assert_allclose(getattr(me, f), getattr(ref, f), rtol=0, atol=VEL_TOL, err_msg=f)
+        assert abs(me.accumulated_contact_force - ref.accumulated_contact_force) <= 1e-9 * max(1.0, ref.accumulated_contact_force)
+        ev_ref, ev_me = events_clean(split(g["events"], g["event_off"], s)), events_clean(r.events)
+        np.testing.assert_array_equal(ev_me[:, :2], ev_ref[:, :2])
+        np.testing.assert_allclose(ev_me[:, 2:], ev_ref[:, 2:], rtol=1e-9, atol=1e-9)
+
+
+def test_fixed_point_bit_exact():
+    """Zero action, everything asleep: successor identical except time/step
+    (SPEC.md:109).  The first step re-derives the robot link poses with the
+    oracle's own FK (the golden input holds the reference's FK bits); from
+    then on the state must be an exact fixed point."""
+    g = golden("traj_fixed.npz")
+    orc = oracle_for(1)
+    snap = orc.step(g["pre"][0].tobytes(), g["arm"][0], g["base"][0]).snapshot
+    for _ in range(3):
+        a = WorldState.from_bytes(snap)
+        snap = orc.step(snap, a.joints[4:], (0.0, 0.0)).snapshot
+        b = WorldState.from_bytes(snap)
+        for f in ("pos", "quat", "lin_vel", "ang_vel", "asleep", "sleep_counter", "joints", "base"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+        assert b.step_index == a.step_index + 1
+
+
+def test_render_matches_reference_primitive():
+    g = golden("render.npz")
+    orc = oracle_for(0)
+    for i in range(len(g["cam"])):
+        snap = g["state"][i].tobytes()
+        rgba, depth, ids, t = orc.render(snap, int(g["cam"][i]))
+        np.testing.assert_allclose(orc.camera_pose(snap, int(g["cam"][i])), g["cam_pose"][i], rtol=0, atol=1e-14)
+        ref_t = g["t"][i]
+        miss = ~(np.isfinite(ref_t) & (ref_t <= float(g["far"])))
+        np.testing.assert_array_equal(ids, np.where(miss, -1, g["ids"][i]))
+        fin = np.isfinite(ref_t)
+        assert (np.isfinite(t) == fin).all()
+        np.testing.assert_allclose(t[fin], ref_t[fin], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(depth[~miss], np.maximum(ref_t[~miss], 0.1).astype(np.float32), rtol=1e-6)
+        assert (depth[miss] == 0).all() and (rgba[miss] == 0).all() and (rgba[~miss][:, 3] == 255).all()
+
+
+def test_walk_grid_and_base_motion_kat():
+    k = golden("kat.npz")
+    orc = oracle_for(0)
+    for q, near in zip(k["nav_query"], k["nav_nearest"]):
+        np.testing.assert_array_equal(orc.nearest_walkable(*q), near)
+    for b, a, out in zip(k["mb_in"], k["mb_act"], k["mb_out"]):
+        np.testing.assert_allclose(orc.move_base(b, a[0], a[1], 1 / 120), out, rtol=0, atol=1e-15)
+
+
+def test_fk_kat(tables_golden):
+    orc = oracle_for(0)
+    for q, b, links, ee in zip(tables_golden["fk_q"], tables_golden["fk_base"], tables_golden["fk_links"],
+                               tables_golden["fk_ee"]):
+        l, e = orc.link_poses(q, b)
+        np.testing.assert_allclose(l, links, rtol=0, atol=1e-14)
+        np.testing.assert_allclose(e, ee, rtol=0, atol=1e-14)
+    k = golden("kat.npz")
+    _, e = orc.link_poses(np.zeros(7), np.zeros(3))
+    np.testing.assert_allclose(e[9:], k["fk_zero_ee"], atol=1e-15)
+
+
+def test_nonfinite_state_faults_naming_body():
+    g = golden("traj_idle.npz")
+    st = WorldState.from_bytes(g["pre"][0].tobytes())
+    st.pos[30, 1] = np.nan
+    r = oracle_for(0).step(st.to_bytes(), g["arm"][0], g["base"][0])
+    assert r.snapshot is None and r.fault == (1 << 16) | 30
