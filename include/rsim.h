@@ -177,6 +177,13 @@ int rs_step_host(rs_batch *batch, const double *h_arm_targets, const double *h_b
                  int32_t substeps, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                  double *h_out_stats, void *stream);
 
+/* Debug trace for parity tests (not on the hot path): when set, every rs_step
+ * records per env and substep the admitted broadphase pairs in sorted order
+ * with their narrowphase contact counts:
+ *   pairs [n_env][max_substeps][cap][3] = (a, b, n_contacts), count [n_env][max_substeps]
+ * (count may exceed cap).  Pass NULL pointers to disable. */
+int rs_set_trace(rs_batch *batch, int32_t *pairs, int32_t *count, int32_t cap, int32_t max_substeps);
+
 #ifdef __cplusplus
 }
 #endif

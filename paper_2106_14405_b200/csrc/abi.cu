@@ -1,0 +1,403 @@
+// abi.cu -- C-ABI implementation (include/rsim.h): scene/batch lifetime,
+// snapshot <-> device-slab conversion, launches.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rsim.h"
+#include "device.cuh"
+
+namespace rsim {
+cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, const uint8_t *has_targets,
+                        double dt, int substeps, cudaStream_t stream);
+cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                          cudaStream_t stream);
+cudaError_t launch_grasp(const DevBatch &B, const double *gripper, cudaStream_t stream);
+cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream);
+size_t step_scratch_doubles_per_env(int row_cap);
+int step_row_cap();
+}  // namespace rsim
+
+using namespace rsim;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+#define CUDA_TRY(x)                                                                                  \
+  do {                                                                                               \
+    cudaError_t e_ = (x);                                                                            \
+    if (e_ != cudaSuccess) return fail(RS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct rs_scene {
+  DevScene d;
+  std::vector<void *> allocs;
+};
+
+struct rs_batch {
+  DevBatch d;
+  DevScene *d_scenes = nullptr;
+  int32_t *d_env_scene = nullptr;
+  std::vector<void *> allocs;
+  int narm = 0;
+  // lazily allocated staging for rs_step_host
+  double *h_pin = nullptr, *d_act = nullptr, *d_stats = nullptr;
+};
+
+// exported functions take C linkage from their declarations in rsim.h
+int rs_abi_version(void) { return RS_ABI_VERSION; }
+const char *rs_last_error(void) { return g_err.c_str(); }
+
+int64_t rs_snapshot_size(int32_t nb, int32_t nj) {
+  return 16 + 8 * 13 * (int64_t)nb + nb + 8 * nb + 16 * (int64_t)nj + 8 * 13 + 8 * nb + 56 * nb + 40;
+}
+
+template <typename T>
+static int upload(rs_scene *s, const T *src, size_t n, const T **dst) {
+  void *p = nullptr;
+  size_t bytes = sizeof(T) * (n ? n : 1);
+  CUDA_TRY(cudaMalloc(&p, bytes));
+  s->allocs.push_back(p);
+  if (n) CUDA_TRY(cudaMemcpy(p, src, sizeof(T) * n, cudaMemcpyHostToDevice));
+  *dst = static_cast<const T *>(p);
+  return 0;
+}
+
+int rs_scene_create(const rs_scene_desc *D, rs_scene **out) {
+  if (!D || !out) return fail(RS_ERR_ARG, "null argument");
+  const int nb = D->n_bodies, np = D->n_parts, nf = D->n_facets, nj = D->n_scene_joints + D->n_arm;
+  if (nb > kMaxBodies || nj > kMaxJoints || D->n_arm > kMaxArm || np > 128 || nf > 1024 || D->n_scene_joints > 30)
+    return fail(RS_ERR_CAPACITY, "scene exceeds compiled capacities (bodies<=48, joints<=16, parts<=128, facets<=1024)");
+  for (int p = 0; p < np; ++p)
+    if (D->part_facet_begin[p + 1] - D->part_facet_begin[p] > kMaxFacetsPerPart)
+      return fail(RS_ERR_CAPACITY, "part with more than 48 facets");
+  if (D->robot_base < 0 || D->robot_base + D->n_arm >= nb) return fail(RS_ERR_ARG, "robot bodies out of range");
+  rs_scene *s = new rs_scene();
+  DevScene &d = s->d;
+  memset(&d, 0, sizeof d);
+  d.nb = nb; d.np = np; d.nf = nf; d.nv = D->n_verts; d.nt = D->n_tris;
+  d.nsj = D->n_scene_joints; d.narm = D->n_arm; d.robot_base = D->robot_base;
+  // bounding radius of each convex part about its origin
+  std::vector<double> bound(np, 0.0);
+  for (int p = 0; p < np; ++p) {
+    if (D->part_kind[p] == RS_BOX) {
+      const double *h = D->part_param + 3 * p;
+      bound[p] = sqrt(h[0] * h[0] + h[1] * h[1] + h[2] * h[2]);
+    } else if (D->part_kind[p] == RS_HULL) {
+      for (int v = D->part_vert_begin[p]; v < D->part_vert_begin[p + 1]; ++v) {
+        const double *x = D->vert + 3 * v;
+        bound[p] = fmax(bound[p], sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]));
+      }
+    } else {
+      bound[p] = D->part_param[3 * p];
+    }
+    bound[p] = bound[p] * (1.0 + 1e-12) + 1e-12;
+  }
+  std::vector<int32_t> clutter;
+  for (int b = 0; b < nb; ++b)
+    if (D->body_kind[b] == RS_DYNAMIC && b > D->robot_base) clutter.push_back(b);
+  d.nclutter = (int)clutter.size();
+  int rc = 0;
+#define UP(field, src, n) \
+  if (!rc) rc = upload(s, src, (size_t)(n), &d.field)
+  UP(body_kind, D->body_kind, nb); UP(body_robot, D->body_robot, nb); UP(body_group, D->body_group, nb);
+  UP(body_joint, D->body_joint, nb); UP(body_part_begin, D->body_part_begin, nb + 1);
+  UP(inv_mass, D->body_inv_mass, nb); UP(com, D->body_com, 3 * nb); UP(inv_inertia, D->body_inv_inertia, 9 * nb);
+  UP(friction, D->body_friction, nb); UP(restitution, D->body_restitution, nb); UP(color, D->body_color, 3 * nb);
+  UP(part_body, D->part_body, np); UP(part_kind, D->part_kind, np);
+  UP(part_facet_begin, D->part_facet_begin, np + 1); UP(part_vert_begin, D->part_vert_begin, np + 1);
+  UP(part_tri_begin, D->part_tri_begin, np + 1); UP(part_local, D->part_local, 12 * np);
+  UP(part_param, D->part_param, 3 * np); UP(part_bound, bound.data(), np);
+  UP(facet, D->facet, 4 * nf); UP(vert, D->vert, 3 * D->n_verts); UP(tri, D->tri, 3 * D->n_tris);
+  UP(joint_type, D->joint_type, d.nsj); UP(joint_body, D->joint_body, d.nsj); UP(joint_parent, D->joint_parent, d.nsj);
+  UP(joint_axis, D->joint_axis, 3 * d.nsj); UP(joint_origin, D->joint_origin, 12 * d.nsj);
+  UP(joint_limits, D->joint_limits, 2 * d.nsj); UP(joint_handle, D->joint_handle, 3 * d.nsj);
+  UP(arm_offset, D->arm_offset, 3 * d.narm); UP(arm_axis, D->arm_axis, 3 * d.narm);
+  UP(arm_limits, D->arm_limits, 2 * d.narm);
+  UP(cam_parent, D->cam_parent, D->n_cameras); UP(cam_mount, D->cam_mount, 12 * D->n_cameras);
+  UP(nav, D->nav_walkable, (size_t)D->nav_nx * D->nav_ny);
+  UP(clutter, clutter.data(), clutter.size());
+#undef UP
+  if (rc) {
+    rs_scene_destroy(s);
+    return rc;
+  }
+  memcpy(d.gripper, D->gripper_offset, sizeof d.gripper);
+  d.ncam = D->n_cameras;
+  d.nav_nx = D->nav_nx; d.nav_ny = D->nav_ny;
+  d.nav_origin[0] = D->nav_origin[0]; d.nav_origin[1] = D->nav_origin[1]; d.nav_cell = D->nav_cell;
+  *out = s;
+  return RS_OK;
+}
+
+void rs_scene_destroy(rs_scene *s) {
+  if (!s) return;
+  for (void *p : s->allocs) cudaFree(p);
+  delete s;
+}
+
+static int balloc(rs_batch *b, void **p, size_t bytes) {
+  CUDA_TRY(cudaMalloc(p, bytes ? bytes : 1));
+  b->allocs.push_back(*p);
+  CUDA_TRY(cudaMemset(*p, 0, bytes ? bytes : 1));
+  return 0;
+}
+
+int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *env_scene, int32_t n_env,
+                    const rs_physics_config *cfg, const rs_render_config *rcfg, int32_t event_cap, rs_batch **out) {
+  if (!scenes || n_scenes < 1 || n_env < 1 || !cfg || !rcfg || !out || event_cap < 0)
+    return fail(RS_ERR_ARG, "bad batch arguments");
+  const DevScene &s0 = scenes[0]->d;
+  for (int i = 1; i < n_scenes; ++i)
+    if (scenes[i]->d.nb != s0.nb || scenes[i]->d.nsj != s0.nsj || scenes[i]->d.narm != s0.narm)
+      return fail(RS_ERR_ARG, "all scenes of a batch must share body and joint counts");
+  if (env_scene)
+    for (int e = 0; e < n_env; ++e)
+      if (env_scene[e] < 0 || env_scene[e] >= n_scenes) return fail(RS_ERR_ARG, "env_scene index out of range");
+  if (rcfg->width % 16 || rcfg->height % 16 || rcfg->width > 128 || rcfg->height > 128 || rcfg->width <= 0 ||
+      rcfg->height <= 0)
+    return fail(RS_ERR_ARG, "render width/height must be multiples of 16 and <= 128");
+  if (cfg->solver_iterations < 0 || cfg->sleep_substeps < 0) return fail(RS_ERR_ARG, "bad physics config");
+  rs_batch *b = new rs_batch();
+  DevBatch &d = b->d;
+  memset(&d, 0, sizeof d);
+  d.n_env = n_env; d.nb = s0.nb; d.nj = s0.nsj + s0.narm;
+  d.L = StateLayout::make(d.nb, d.nj);
+  d.cfg = *cfg; d.rcfg = *rcfg; d.event_cap = event_cap;
+  d.row_cap = step_row_cap();
+  b->narm = s0.narm;
+  int rc = 0;
+  void *p;
+#define BA(field, bytes)                          \
+  if (!rc) {                                      \
+    rc = balloc(b, &p, (bytes));                  \
+    d.field = reinterpret_cast<decltype(d.field)>(p); \
+  }
+  BA(sd, sizeof(double) * d.L.dbl_size * (size_t)n_env);
+  BA(si, sizeof(int32_t) * d.L.int_size * (size_t)n_env);
+  BA(step_index, sizeof(int64_t) * n_env);
+  BA(fault, sizeof(uint32_t) * n_env);
+  BA(event_count, sizeof(int32_t) * n_env);
+  BA(events, sizeof(double) * 7 * (size_t)(event_cap ? event_cap : 1) * n_env);
+  BA(counters, sizeof(int64_t) * 3 * n_env);
+  BA(row_scratch, sizeof(double) * step_scratch_doubles_per_env(d.row_cap) * (size_t)n_env);
+#undef BA
+  if (!rc) rc = balloc(b, &p, sizeof(DevScene) * n_scenes), b->d_scenes = (DevScene *)p;
+  if (!rc) rc = balloc(b, &p, sizeof(int32_t) * n_env), b->d_env_scene = (int32_t *)p;
+  if (rc) {
+    rs_batch_destroy(b);
+    return rc;
+  }
+  std::vector<DevScene> hs(n_scenes);
+  for (int i = 0; i < n_scenes; ++i) hs[i] = scenes[i]->d;
+  std::vector<int32_t> es(n_env, 0);
+  if (env_scene) memcpy(es.data(), env_scene, sizeof(int32_t) * n_env);
+  cudaError_t e1 = cudaMemcpy(b->d_scenes, hs.data(), sizeof(DevScene) * n_scenes, cudaMemcpyHostToDevice);
+  cudaError_t e2 = cudaMemcpy(b->d_env_scene, es.data(), sizeof(int32_t) * n_env, cudaMemcpyHostToDevice);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    rs_batch_destroy(b);
+    return fail(RS_ERR_CUDA, "batch table upload failed");
+  }
+  d.scenes = b->d_scenes;
+  d.env_scene = b->d_env_scene;
+  *out = b;
+  return RS_OK;
+}
+
+void rs_batch_destroy(rs_batch *b) {
+  if (!b) return;
+  for (void *p : b->allocs) cudaFree(p);
+  if (b->h_pin) cudaFreeHost(b->h_pin);
+  if (b->d_act) cudaFree(b->d_act);
+  if (b->d_stats) cudaFree(b->d_stats);
+  delete b;
+}
+
+int rs_batch_buffers(rs_batch *b, rs_buffers *o) {
+  if (!b || !o) return fail(RS_ERR_ARG, "null argument");
+  o->n_env = b->d.n_env; o->n_bodies = b->d.nb; o->n_joints = b->d.nj; o->event_cap = b->d.event_cap;
+  o->fault = b->d.fault; o->event_count = b->d.event_count; o->events = b->d.events; o->counters = b->d.counters;
+  o->acc_force = b->d.sd + b->d.L.acc;  // stride = L.dbl_size doubles
+  return RS_OK;
+}
+
+// snapshot bytes (physics.py:147-203) <-> slab
+static int unpack_snapshot(const uint8_t *s, const StateLayout &L, double *sd, int32_t *si, int64_t *step) {
+  if (memcmp(s, "RSIM", 4) != 0) return fail(RS_ERR_SNAPSHOT, "bad snapshot magic");
+  uint32_t ver, nb, nj;
+  memcpy(&ver, s + 4, 4); memcpy(&nb, s + 8, 4); memcpy(&nj, s + 12, 4);
+  if (ver != 1) return fail(RS_ERR_SNAPSHOT, "unsupported snapshot version");
+  if ((int)nb != L.nb || (int)nj != L.nj) return fail(RS_ERR_SNAPSHOT, "snapshot body/joint count mismatch");
+  const uint8_t *p = s + 16;
+  auto take = [&](void *dst, size_t n) { memcpy(dst, p, n); p += n; };
+  memset(sd, 0, sizeof(double) * L.dbl_size);
+  memset(si, 0, sizeof(int32_t) * L.int_size);
+  take(sd + L.pos, 24 * nb); take(sd + L.quat, 32 * nb); take(sd + L.lv, 24 * nb); take(sd + L.av, 24 * nb);
+  for (uint32_t b = 0; b < nb; ++b) si[L.asleep + b] = p[b] ? 1 : 0;
+  p += nb;
+  for (uint32_t b = 0; b < nb; ++b) { int64_t v; take(&v, 8); si[L.sleep_ctr + b] = (int32_t)v; }
+  take(sd + L.joints, 8 * nj); take(sd + L.jvel, 8 * nj);
+  take(sd + L.base, 24); take(sd + L.held_off, 56); take(sd + L.grab_ee, 24);
+  for (uint32_t b = 0; b < nb; ++b) { int64_t v; take(&v, 8); si[L.rider_joint + b] = (int32_t)v; }
+  take(sd + L.rider_off, 56 * nb);
+  int32_t held, held_joint;
+  take(&held, 4); take(&held_joint, 4);
+  si[L.held] = held; si[L.held_joint] = held_joint;
+  take(sd + L.grab_q, 8); take(sd + L.acc, 8); take(sd + L.time, 8); take(step, 8);
+  return 0;
+}
+
+static void pack_snapshot(const StateLayout &L, const double *sd, const int32_t *si, int64_t step, uint8_t *s) {
+  const int nb = L.nb, nj = L.nj;
+  memcpy(s, "RSIM", 4);
+  uint32_t hdr[3] = {1u, (uint32_t)nb, (uint32_t)nj};
+  memcpy(s + 4, hdr, 12);
+  uint8_t *p = s + 16;
+  auto put = [&](const void *src, size_t n) { memcpy(p, src, n); p += n; };
+  put(sd + L.pos, 24 * nb); put(sd + L.quat, 32 * nb); put(sd + L.lv, 24 * nb); put(sd + L.av, 24 * nb);
+  for (int b = 0; b < nb; ++b) p[b] = si[L.asleep + b] ? 1 : 0;
+  p += nb;
+  for (int b = 0; b < nb; ++b) { int64_t v = si[L.sleep_ctr + b]; put(&v, 8); }
+  put(sd + L.joints, 8 * nj); put(sd + L.jvel, 8 * nj);
+  put(sd + L.base, 24); put(sd + L.held_off, 56); put(sd + L.grab_ee, 24);
+  for (int b = 0; b < nb; ++b) { int64_t v = si[L.rider_joint + b]; put(&v, 8); }
+  put(sd + L.rider_off, 56 * nb);
+  int32_t held = si[L.held], held_joint = si[L.held_joint];
+  put(&held, 4); put(&held_joint, 4);
+  put(sd + L.grab_q, 8); put(sd + L.acc, 8); put(sd + L.time, 8); put(&step, 8);
+}
+
+int rs_set_state(rs_batch *b, const uint8_t *snaps, int64_t stride, const int32_t *env_ids, int32_t n, void *stream) {
+  if (!b || !snaps || n < 0) return fail(RS_ERR_ARG, "null argument");
+  const DevBatch &d = b->d;
+  const StateLayout &L = d.L;
+  if (stride <= 0) stride = rs_snapshot_size(L.nb, L.nj);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<double> sd((size_t)L.dbl_size * n);
+  std::vector<int32_t> si((size_t)L.int_size * n);
+  std::vector<int64_t> step(n);
+  for (int i = 0; i < n; ++i) {
+    int e = env_ids ? env_ids[i] : i;
+    if (e < 0 || e >= d.n_env) return fail(RS_ERR_ARG, "env id out of range");
+    int rc = unpack_snapshot(snaps + stride * i, L, sd.data() + (size_t)L.dbl_size * i,
+                             si.data() + (size_t)L.int_size * i, &step[i]);
+    if (rc) return rc;
+  }
+  bool contiguous = true;
+  for (int i = 0; i < n && contiguous; ++i) contiguous = (env_ids ? env_ids[i] : i) == (env_ids ? env_ids[0] : 0) + i;
+  int e0 = n ? (env_ids ? env_ids[0] : 0) : 0;
+  std::vector<int64_t> zeros(3, 0);
+  if (contiguous && n) {
+    CUDA_TRY(cudaMemcpyAsync(d.sd + (size_t)L.dbl_size * e0, sd.data(), sizeof(double) * L.dbl_size * n,
+                             cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d.si + (size_t)L.int_size * e0, si.data(), sizeof(int32_t) * L.int_size * n,
+                             cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d.step_index + e0, step.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(d.counters + 3 * (size_t)e0, 0, sizeof(int64_t) * 3 * n, st));
+    CUDA_TRY(cudaMemsetAsync(d.fault + e0, 0, sizeof(uint32_t) * n, st));
+    CUDA_TRY(cudaMemsetAsync(d.event_count + e0, 0, sizeof(int32_t) * n, st));
+  } else {
+    for (int i = 0; i < n; ++i) {
+      int e = env_ids[i];
+      CUDA_TRY(cudaMemcpyAsync(d.sd + (size_t)L.dbl_size * e, sd.data() + (size_t)L.dbl_size * i,
+                               sizeof(double) * L.dbl_size, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(d.si + (size_t)L.int_size * e, si.data() + (size_t)L.int_size * i,
+                               sizeof(int32_t) * L.int_size, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(d.step_index + e, &step[i], sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemsetAsync(d.counters + 3 * (size_t)e, 0, sizeof(int64_t) * 3, st));
+      CUDA_TRY(cudaMemsetAsync(d.fault + e, 0, sizeof(uint32_t), st));
+      CUDA_TRY(cudaMemsetAsync(d.event_count + e, 0, sizeof(int32_t), st));
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));  // host staging goes out of scope
+  return RS_OK;
+}
+
+int rs_get_state(rs_batch *b, uint8_t *snaps, int64_t stride, const int32_t *env_ids, int32_t n, void *stream) {
+  if (!b || !snaps || n < 0) return fail(RS_ERR_ARG, "null argument");
+  const DevBatch &d = b->d;
+  const StateLayout &L = d.L;
+  if (stride <= 0) stride = rs_snapshot_size(L.nb, L.nj);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<double> sd((size_t)L.dbl_size * n);
+  std::vector<int32_t> si((size_t)L.int_size * n);
+  std::vector<int64_t> step(n);
+  for (int i = 0; i < n; ++i) {
+    int e = env_ids ? env_ids[i] : i;
+    if (e < 0 || e >= d.n_env) return fail(RS_ERR_ARG, "env id out of range");
+    CUDA_TRY(cudaMemcpyAsync(sd.data() + (size_t)L.dbl_size * i, d.sd + (size_t)L.dbl_size * e,
+                             sizeof(double) * L.dbl_size, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(si.data() + (size_t)L.int_size * i, d.si + (size_t)L.int_size * e,
+                             sizeof(int32_t) * L.int_size, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&step[i], d.step_index + e, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < n; ++i)
+    pack_snapshot(L, sd.data() + (size_t)L.dbl_size * i, si.data() + (size_t)L.int_size * i, step[i],
+                  snaps + stride * i);
+  return RS_OK;
+}
+
+int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_t *has_targets, double dt,
+            int32_t substeps, void *stream) {
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
+  if (!arm || !base_cmd) return fail(RS_ERR_ARG, "arm_targets and base_cmd are required device pointers");
+  CUDA_TRY(launch_step(b->d, arm, base_cmd, has_targets, dt, substeps, (cudaStream_t)stream));
+  return RS_OK;
+}
+
+int rs_render(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream) {
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  if (cam_mask >> 2) return fail(RS_ERR_ARG, "camera mask selects a camera the robot does not have");
+  CUDA_TRY(launch_render(b->d, cam_mask, rgba, depth, ids, (cudaStream_t)stream));
+  return RS_OK;
+}
+
+int rs_grasp(rs_batch *b, const double *gripper, void *stream) {
+  if (!b || !gripper) return fail(RS_ERR_ARG, "null argument");
+  CUDA_TRY(launch_grasp(b->d, gripper, (cudaStream_t)stream));
+  return RS_OK;
+}
+
+int rs_set_trace(rs_batch *b, int32_t *pairs, int32_t *count, int32_t cap, int32_t max_substeps) {
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  if ((pairs == nullptr) != (count == nullptr)) return fail(RS_ERR_ARG, "pairs and count must both be set or NULL");
+  b->d.trace_pairs = pairs;
+  b->d.trace_count = count;
+  b->d.trace_cap = pairs ? cap : 0;
+  b->d.trace_sub = pairs ? max_substeps : 0;
+  return RS_OK;
+}
+
+int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double dt, int32_t substeps,
+                 uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, double *h_out_stats, void *stream) {
+  if (!b || !h_arm || !h_base || !h_out_stats) return fail(RS_ERR_ARG, "null argument");
+  const int E = b->d.n_env, na = b->narm;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!b->d_act) {
+    CUDA_TRY(cudaMalloc(&b->d_act, sizeof(double) * (size_t)E * (na + 2)));
+    CUDA_TRY(cudaMalloc(&b->d_stats, sizeof(double) * (size_t)E * 4));
+  }
+  double *d_arm = b->d_act, *d_base = b->d_act + (size_t)E * na;
+  CUDA_TRY(cudaMemcpyAsync(d_arm, h_arm, sizeof(double) * (size_t)E * na, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_base, h_base, sizeof(double) * (size_t)E * 2, cudaMemcpyHostToDevice, st));
+  int rc = rs_step(b, d_arm, d_base, nullptr, dt, substeps, stream);
+  if (rc) return rc;
+  if (cam_mask) {
+    rc = rs_render(b, cam_mask, rgba, depth, ids, stream);
+    if (rc) return rc;
+  }
+  CUDA_TRY(launch_stats(b->d, b->d_stats, st));
+  CUDA_TRY(cudaMemcpyAsync(h_out_stats, b->d_stats, sizeof(double) * (size_t)E * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return RS_OK;
+}
+

@@ -1,0 +1,1453 @@
+// physics.cu -- fused 1/30 s control step (all substeps) for a batch of envs.
+//
+// One warp owns one environment for the whole control step: it stages the
+// env's state slab into shared memory, runs every substep of
+// Simulator.step_physics (physics.py:575-1035) there, and writes the slab
+// back once.  Work inside a substep is spread over the warp's lanes where
+// the reference's semantics allow it and kept on one lane where they are
+// order-dependent:
+//
+//   kinematics      lanes per joint/body; FK chain on lane 0 (robot.py:161)
+//   AABBs           lanes per body (geometry.py:278-296)
+//   overlap tests   lanes per pair, ballot-compacted in sorted (a, b) order
+//                   (== SAP on x + inclusive y/z, physics.py:498-526)
+//   admission       lane 0, sorted order (wakes mutate `asleep` mid-walk,
+//                   physics.py:528-571)
+//   narrowphase     lanes per vertex / facet, ballot-compacted in vertex
+//                   order (geometry.py:564-576, :667-716)
+//   row build       lanes per contact; block matrices lanes per entry
+//   GS sweeps       lane 0 (Gauss-Seidel order is the algorithm,
+//                   physics.py:915-937); block LCP with a Jacobi
+//                   pseudo-inverse matching lstsq(rcond=1e-8) (:760-816)
+//   integrate       lanes per body; per-body correction sums in contact
+//                   order (physics.py:962-1011)
+//
+// Float64 throughout; this translation unit is built with -fmad=false so
+// arithmetic rounds exactly like the C oracle (tests/test_gpu_physics.py).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "device.cuh"
+#include "se3.cuh"
+
+namespace rsim {
+
+constexpr int kWarpsPerBlock = 2;
+constexpr int kMaxCand = 512;
+constexpr int kMaxAdm = 256;
+constexpr int kMaxContacts = 128;
+constexpr int kMaxGroups = 96;
+constexpr int kMaxBlockRows = 32;
+constexpr int kRowD = 44;  // doubles per solver row in global scratch
+constexpr int kPairD = 32; // doubles per contact group (pair) in global scratch
+constexpr int kKCap = kMaxContacts * kMaxBlockRows;  // Sigma m^2 <= 32 * 128
+
+// ---- row field offsets (doubles) ------------------------------------------
+enum {
+  RN = 0, RT1 = 3, RT2 = 6, RRA = 9, RRB = 12, RK = 15, RMU = 16, RIMA = 17, RIMB = 18, RJACA = 19, RJACB = 22,
+  RJIA = 25, RJIB = 26, RLAM = 27, RLT1 = 28, RLT2 = 29, RVN = 30, RTGT = 31, RFRIC = 32, RJA = 33, RJB = 34,
+  RA = 35, RB = 36, RPT = 37, RDEPTH = 40, RGRP = 41
+};
+// ---- pair (group) field offsets --------------------------------------------
+enum { PIA = 0, PIB = 9, PCA = 18, PCB = 21, PIMA = 24, PIMB = 25, PMU = 26, PE = 27, PKOFF = 28, PHASK = 29 };
+
+struct WarpSmem {
+  double sd[1024];
+  int32_t si[160];
+  double R[kMaxBodies][9];
+  double lo[kMaxBodies][3], hi[kMaxBodies][3];
+  double vel[kMaxBodies][6];
+  double jdv[kMaxJoints];
+  double cp[kMaxContacts][3], cn[kMaxContacts][3], cd[kMaxContacts];
+  double planes[2][kMaxFacetsPerPart * 4];
+  double links[kMaxArm][12];
+  double ee[12];
+  double raa[kMaxArm][9];
+  double budget[kMaxArm];
+  uint16_t cand[kMaxCand];
+  uint16_t adm[kMaxAdm];
+  int16_t g_a[kMaxGroups], g_b[kMaxGroups], g_first[kMaxGroups], g_n[kMaxGroups];
+  int ncand, nadm, nc, ng, fault;
+  unsigned long long awake_dyn;
+  int moved_mask;
+  int64_t ctr[3];
+};
+
+struct Ctx {
+  const DevScene *sc;
+  const DevBatch *B;
+  const rs_physics_config *cfg;
+  WarpSmem *S;
+  double *rows;   // [row_cap][kRowD]
+  double *pairs;  // [kMaxGroups][kPairD]
+  double *K;      // [kKCap]
+  int env, lane;
+  const StateLayout *L;
+};
+
+// ------------------------------------------------------------------ access
+#define SD(ctx) ((ctx).S->sd)
+#define SI(ctx) ((ctx).S->si)
+__device__ __forceinline__ double *POS(Ctx &c, int b) { return c.S->sd + c.L->pos + 3 * b; }
+__device__ __forceinline__ double *QUAT(Ctx &c, int b) { return c.S->sd + c.L->quat + 4 * b; }
+__device__ __forceinline__ double *LV(Ctx &c, int b) { return c.S->sd + c.L->lv + 3 * b; }
+__device__ __forceinline__ double *AV(Ctx &c, int b) { return c.S->sd + c.L->av + 3 * b; }
+__device__ __forceinline__ int32_t &ASLEEP(Ctx &c, int b) { return c.S->si[c.L->asleep + b]; }
+__device__ __forceinline__ int32_t &SLEEPC(Ctx &c, int b) { return c.S->si[c.L->sleep_ctr + b]; }
+__device__ __forceinline__ int32_t &RIDER(Ctx &c, int b) { return c.S->si[c.L->rider_joint + b]; }
+__device__ __forceinline__ int32_t &HELD(Ctx &c) { return c.S->si[c.L->held]; }
+__device__ __forceinline__ int32_t &HELDJ(Ctx &c) { return c.S->si[c.L->held_joint]; }
+__device__ __forceinline__ double *JOINTS(Ctx &c) { return c.S->sd + c.L->joints; }
+__device__ __forceinline__ double *JVEL(Ctx &c) { return c.S->sd + c.L->jvel; }
+
+__device__ __forceinline__ void body_pose(Ctx &c, int b, Pose &o) {
+  quat_to_mat(QUAT(c, b), o.R);
+  const double *p = POS(c, b);
+  o.p[0] = p[0]; o.p[1] = p[1]; o.p[2] = p[2];
+}
+// pose from the rotation cache (valid between refresh_rot calls)
+__device__ __forceinline__ void body_pose_cached(Ctx &c, int b, Pose &o) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i) o.R[i] = c.S->R[b][i];
+  const double *p = POS(c, b);
+  o.p[0] = p[0]; o.p[1] = p[1]; o.p[2] = p[2];
+}
+
+// write a kinematic pose; 1 if it changed (physics.py:419-433, :441-453)
+__device__ int set_kinematic(Ctx &c, int b, const Pose &p, double dt, bool zero_if_same) {
+  double q[4];
+  mat_to_quat(p.R, q);
+  double *pos = POS(c, b), *qu = QUAT(c, b);
+  bool same = pos[0] == p.p[0] && pos[1] == p.p[1] && pos[2] == p.p[2] && qu[0] == q[0] && qu[1] == q[1] &&
+              qu[2] == q[2] && qu[3] == q[3];
+  if (same) {
+    if (zero_if_same && dt > 0) {
+      double *lv = LV(c, b), *av = AV(c, b);
+      lv[0] = lv[1] = lv[2] = 0.0;
+      av[0] = av[1] = av[2] = 0.0;
+    }
+    return 0;
+  }
+  double op[3] = {pos[0], pos[1], pos[2]}, oq[4] = {qu[0], qu[1], qu[2], qu[3]};
+  pos[0] = p.p[0]; pos[1] = p.p[1]; pos[2] = p.p[2];
+  qu[0] = q[0]; qu[1] = q[1]; qu[2] = q[2]; qu[3] = q[3];
+  if (dt > 0) {
+    double *lv = LV(c, b);
+    for (int i = 0; i < 3; ++i) lv[i] = (p.p[i] - op[i]) / dt;
+    quat_delta_omega(oq, q, dt, AV(c, b));
+  }
+  return 1;
+}
+
+// ---------------------------------------------------------------- kinematics
+
+// FK of the arm chain (robot.py:161-169): lanes compute the joint rotations,
+// lane 0 chains them; results in S->links / S->ee.
+__device__ void forward_kinematics(Ctx &c) {
+  const DevScene &sc = *c.sc;
+  if (c.lane < sc.narm) axis_angle_mat(sc.arm_axis + 3 * c.lane, JOINTS(c)[sc.nsj + c.lane], c.S->raa[c.lane]);
+  __syncwarp();
+  if (c.lane == 0) {
+    Pose t, off, rot;
+    base3(c.S->sd + c.L->base, t);
+    rot_z(0.0, off.R);
+    rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
+    for (int i = 0; i < sc.narm; ++i) {
+      off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
+      compose(t, off, t);
+      for (int k = 0; k < 9; ++k) rot.R[k] = c.S->raa[i][k];
+      compose(t, rot, t);
+      for (int k = 0; k < 9; ++k) c.S->links[i][k] = t.R[k];
+      for (int k = 0; k < 3; ++k) c.S->links[i][9 + k] = t.p[k];
+    }
+    Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}}, e;
+    compose(t, g, e);
+    for (int k = 0; k < 9; ++k) c.S->ee[k] = e.R[k];
+    for (int k = 0; k < 3; ++k) c.S->ee[9 + k] = e.p[k];
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ bool nav_ok(const DevScene &sc, long i, long j) {
+  return i >= 0 && i < sc.nav_nx && j >= 0 && j < sc.nav_ny && sc.nav[i * sc.nav_ny + j];
+}
+__device__ bool nav_ring(const DevScene &sc, long ci, long cj, long r, double x, double y, double &bd, long &bi,
+                         long &bj) {
+  bool found = false;
+  for (long i = ci - r; i <= ci + r; ++i)
+    for (long j = cj - r; j <= cj + r; ++j) {
+      long di = i > ci ? i - ci : ci - i, dj = j > cj ? j - cj : cj - j;
+      if ((di > dj ? di : dj) != r || !nav_ok(sc, i, j)) continue;
+      double cx = sc.nav_origin[0] + ((double)i + 0.5) * sc.nav_cell;
+      double cy = sc.nav_origin[1] + ((double)j + 0.5) * sc.nav_cell;
+      double ex = cx - x, ey = cy - y, d2 = ex * ex + ey * ey;
+      if (!found || d2 < bd || (d2 == bd && (i < bi || (i == bi && j < bj)))) { bd = d2; bi = i; bj = j; found = true; }
+    }
+  return found;
+}
+// robot.py:349-368 + navgrid.py:55-105
+__device__ void move_base(const DevScene &sc, double *base, double lin, double ang, double dt) {
+  double x = base[0], y = base[1], yaw = base[2];
+  double nx = x + cos(yaw) * lin * dt, ny = y + sin(yaw) * lin * dt;
+  double nyaw = py_mod(yaw + ang * dt + M_PI, 2.0 * M_PI) - M_PI;
+  long ci = (long)floor((nx - sc.nav_origin[0]) / sc.nav_cell);
+  long cj = (long)floor((ny - sc.nav_origin[1]) / sc.nav_cell);
+  if (!nav_ok(sc, ci, cj)) {
+    long maxr = sc.nav_nx > sc.nav_ny ? sc.nav_nx : sc.nav_ny;
+    for (long r = 0; r <= maxr; ++r) {
+      double bd, bd2;
+      long bi, bj, bi2, bj2;
+      if (!nav_ring(sc, ci, cj, r, nx, ny, bd, bi, bj)) continue;
+      if (nav_ring(sc, ci, cj, r + 1, nx, ny, bd2, bi2, bj2) && bd2 < bd) { bi = bi2; bj = bj2; }
+      nx = sc.nav_origin[0] + ((double)bi + 0.5) * sc.nav_cell;
+      ny = sc.nav_origin[1] + ((double)bj + 0.5) * sc.nav_cell;
+      break;
+    }
+  }
+  base[0] = nx; base[1] = ny; base[2] = nyaw;
+}
+
+__device__ void joint_child_pose(Ctx &c, int ji, double q, Pose &o) {
+  const DevScene &sc = *c.sc;
+  Pose parent, origin, motion, t;
+  body_pose(c, sc.joint_parent[ji], parent);
+  pose_load12(sc.joint_origin + 12 * ji, origin);
+  compose(parent, origin, t);
+  if (sc.joint_type[ji] == RS_REVOLUTE) {
+    axis_angle_mat(sc.joint_axis + 3 * ji, q, motion.R);
+    motion.p[0] = motion.p[1] = motion.p[2] = 0.0;
+  } else {
+    const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    for (int k = 0; k < 9; ++k) motion.R[k] = I[k];
+    for (int k = 0; k < 3; ++k) motion.p[k] = sc.joint_axis[3 * ji + k] * q;
+  }
+  compose(t, motion, o);
+}
+
+// physics.py:435-467; `mask` = joints to update; warp-collective
+__device__ void update_scene_joint_poses(Ctx &c, int mask, double dt) {
+  const DevScene &sc = *c.sc;
+  if (c.lane == 0) {
+    int moved = 0;
+    for (int ji = 0; ji < sc.nsj; ++ji) {
+      if (!(mask & (1 << ji))) continue;
+      Pose p;
+      joint_child_pose(c, ji, JOINTS(c)[ji], p);
+      if (set_kinematic(c, sc.joint_body[ji], p, dt, false)) moved |= 1 << ji;
+    }
+    c.S->moved_mask = moved;
+  }
+  __syncwarp();
+  int moved = c.S->moved_mask;
+  if (moved) {
+    for (int k = c.lane; k < sc.nclutter; k += 32) {
+      int b = sc.clutter[k];
+      int rj = RIDER(c, b);
+      if (rj < 0 || !(moved & (1 << rj)) || !ASLEEP(c, b)) continue;
+      Pose part, rel, np_;
+      body_pose(c, sc.joint_body[rj], part);
+      const double *ro = c.S->sd + c.L->rider_off + 7 * b;
+      quat_to_mat(ro + 3, rel.R);
+      rel.p[0] = ro[0]; rel.p[1] = ro[1]; rel.p[2] = ro[2];
+      compose(part, rel, np_);
+      double *pos = POS(c, b);
+      pos[0] = np_.p[0]; pos[1] = np_.p[1]; pos[2] = np_.p[2];
+      mat_to_quat(np_.R, QUAT(c, b));
+    }
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------- primitives
+
+__device__ __forceinline__ void part_world(Ctx &c, const Pose &bp, int p, Pose &o) {
+  Pose l;
+  pose_load12(c.sc->part_local + 12 * p, l);
+  compose(bp, l, o);
+}
+// geometry.py:278-286
+__device__ void prim_aabb(Ctx &c, int p, const Pose &wp, double *lo, double *hi) {
+  const DevScene &sc = *c.sc;
+  int k = sc.part_kind[p];
+  if (k == RS_BOX) {
+    const double *h = sc.part_param + 3 * p;
+    for (int i = 0; i < 3; ++i) {
+      double r = fabs(wp.R[3 * i]) * h[0] + fabs(wp.R[3 * i + 1]) * h[1] + fabs(wp.R[3 * i + 2]) * h[2];
+      lo[i] = wp.p[i] - r; hi[i] = wp.p[i] + r;
+    }
+  } else if (k == RS_SPHERE) {
+    double r = sc.part_param[3 * p];
+    for (int i = 0; i < 3; ++i) { lo[i] = wp.p[i] - r; hi[i] = wp.p[i] + r; }
+  } else {
+    for (int i = 0; i < 3; ++i) { lo[i] = INFINITY; hi[i] = -INFINITY; }
+    for (int v = sc.part_vert_begin[p]; v < sc.part_vert_begin[p + 1]; ++v) {
+      double x[3];
+      apply(wp, sc.vert + 3 * v, x);
+      for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], x[i]); hi[i] = fmax(hi[i], x[i]); }
+    }
+  }
+}
+
+// world planes of part p into S->planes[slot] (lanes per facet)
+__device__ void planes_world(Ctx &c, int p, const Pose &wp, int slot) {
+  const DevScene &sc = *c.sc;
+  int f0 = sc.part_facet_begin[p], nf = sc.part_facet_begin[p + 1] - f0;
+  for (int f = c.lane; f < nf; f += 32) {
+    const double *F = sc.facet + 4 * (f0 + f);
+    double *o = c.S->planes[slot] + 4 * f;
+    double n[3];
+    matvec(wp.R, F, n);
+    o[0] = n[0]; o[1] = n[1]; o[2] = n[2];
+    o[3] = F[3] + dot3(n, wp.p);
+  }
+}
+
+__device__ __forceinline__ int add_contact(Ctx &c, int idx, const double *p, const double *n, double depth) {
+  if (idx >= kMaxContacts) return 0;
+  for (int i = 0; i < 3; ++i) { c.S->cp[idx][i] = p[i]; c.S->cn[idx][i] = n[i]; }
+  c.S->cd[idx] = depth;
+  return 1;
+}
+
+// vertices of part pv (pose wv) against the planes in slot (part pf): geometry.py:564-576, :683-698.
+// warp-collective; appends in vertex order; returns the number of contacts.
+__device__ int vertices_vs_planes(Ctx &c, int pv, const Pose &wv, int pf, int slot, bool negate, double margin,
+                                  int base) {
+  const DevScene &sc = *c.sc;
+  int v0 = sc.part_vert_begin[pv], nv = sc.part_vert_begin[pv + 1] - v0;
+  int nf = sc.part_facet_begin[pf + 1] - sc.part_facet_begin[pf];
+  const double *pl = c.S->planes[slot];
+  int total = 0;
+  for (int k0 = 0; k0 < nv; k0 += 32) {
+    int v = k0 + c.lane;
+    bool inside = false;
+    double x[3], best = 0.0;
+    int face = 0;
+    if (v < nv) {
+      apply(wv, sc.vert + 3 * (v0 + v), x);
+      int neg = 0;
+      for (int f = 0; f < nf; ++f) {
+        const double *P = pl + 4 * f;
+        double s = P[3] - (x[0] * P[0] + x[1] * P[1] + x[2] * P[2]);
+        if (f == 0 || s < best) { best = s; face = f; }
+        neg += (s < 0.0);
+      }
+      inside = neg == 0 || (neg == 1 && best >= -margin);
+    }
+    unsigned m = __ballot_sync(0xffffffffu, inside);
+    if (inside) {
+      int idx = base + total + __popc(m & ((1u << c.lane) - 1));
+      double n[3];
+      for (int i = 0; i < 3; ++i) n[i] = negate ? -pl[4 * face + i] : pl[4 * face + i];
+      add_contact(c, idx, x, n, best);
+    }
+    total += __popc(m);
+  }
+  return total;
+}
+
+// geometry.py:602-630
+__device__ void closest_on_triangle(const double *p, const double *a, const double *b, const double *cc, double *o) {
+  double ab[3], ac[3], ap[3], bp[3], cp[3];
+  for (int i = 0; i < 3; ++i) { ab[i] = b[i] - a[i]; ac[i] = cc[i] - a[i]; ap[i] = p[i] - a[i]; }
+  double d1 = dot3(ab, ap), d2 = dot3(ac, ap);
+  if (d1 <= 0 && d2 <= 0) { for (int i = 0; i < 3; ++i) o[i] = a[i]; return; }
+  for (int i = 0; i < 3; ++i) bp[i] = p[i] - b[i];
+  double d3 = dot3(ab, bp), d4 = dot3(ac, bp);
+  if (d3 >= 0 && d4 <= d3) { for (int i = 0; i < 3; ++i) o[i] = b[i]; return; }
+  double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0 && d1 >= 0 && d3 <= 0) {
+    double t = d1 / (d1 - d3);
+    for (int i = 0; i < 3; ++i) o[i] = a[i] + ab[i] * t;
+    return;
+  }
+  for (int i = 0; i < 3; ++i) cp[i] = p[i] - cc[i];
+  double d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+  if (d6 >= 0 && d5 <= d6) { for (int i = 0; i < 3; ++i) o[i] = cc[i]; return; }
+  double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) {
+    double t = d2 / (d2 - d6);
+    for (int i = 0; i < 3; ++i) o[i] = a[i] + ac[i] * t;
+    return;
+  }
+  double va = d3 * d6 - d5 * d4;
+  if (va <= 0 && (d4 - d3) >= 0 && (d5 - d6) >= 0) {
+    double t = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+    for (int i = 0; i < 3; ++i) o[i] = b[i] + (cc[i] - b[i]) * t;
+    return;
+  }
+  double den = va + vb + vc, v = vb / den, w = vc / den;
+  for (int i = 0; i < 3; ++i) o[i] = a[i] + ab[i] * v + ac[i] * w;
+}
+
+// sphere part ps vs convex part pc (planes already in `slot`): geometry.py:633-653. lane 0 only.
+__device__ int sphere_convex(Ctx &c, int ps, const Pose &ws, int pc, const Pose &wc, int slot, bool flip,
+                             double margin, int idx) {
+  const DevScene &sc = *c.sc;
+  double r = sc.part_param[3 * ps];
+  const double *ctr = ws.p;
+  const double *pl = c.S->planes[slot];
+  int nf = sc.part_facet_begin[pc + 1] - sc.part_facet_begin[pc];
+  bool inside = true;
+  int f = 0;
+  double best = 0.0;
+  for (int k = 0; k < nf; ++k) {
+    double s = pl[4 * k + 3] - dot3(pl + 4 * k, ctr);
+    if (s < 0.0) inside = false;
+    if (k == 0 || s < best) { best = s; f = k; }
+  }
+  double n[3], pt[3], depth;
+  if (inside) {
+    depth = r + best;
+    for (int i = 0; i < 3; ++i) { n[i] = pl[4 * f + i]; pt[i] = ctr[i] - n[i] * best; }
+  } else {
+    double q[3];
+    if (sc.part_kind[pc] == RS_BOX) {
+      const double *h = sc.part_param + 3 * pc;
+      double d[3], l[3];
+      for (int i = 0; i < 3; ++i) d[i] = ctr[i] - wc.p[i];
+      mattvec(wc.R, d, l);
+      for (int i = 0; i < 3; ++i) l[i] = l[i] < -h[i] ? -h[i] : (l[i] > h[i] ? h[i] : l[i]);
+      apply(wc, l, q);
+    } else {
+      int v0 = sc.part_vert_begin[pc];
+      double bd = 0.0;
+      bool first = true;
+      for (int t = sc.part_tri_begin[pc]; t < sc.part_tri_begin[pc + 1]; ++t) {
+        double A[3], Bv[3], C[3], qq[3];
+        apply(wc, sc.vert + 3 * (v0 + sc.tri[3 * t]), A);
+        apply(wc, sc.vert + 3 * (v0 + sc.tri[3 * t + 1]), Bv);
+        apply(wc, sc.vert + 3 * (v0 + sc.tri[3 * t + 2]), C);
+        closest_on_triangle(ctr, A, Bv, C, qq);
+        double e[3] = {ctr[0] - qq[0], ctr[1] - qq[1], ctr[2] - qq[2]}, d2 = dot3(e, e);
+        if (first || d2 < bd) { bd = d2; q[0] = qq[0]; q[1] = qq[1]; q[2] = qq[2]; first = false; }
+      }
+    }
+    double d[3] = {ctr[0] - q[0], ctr[1] - q[1], ctr[2] - q[2]};
+    double dist = sqrt(dot3(d, d));
+    depth = r - dist;
+    if (depth <= -margin) return 0;
+    if (dist > 0) for (int i = 0; i < 3; ++i) n[i] = d[i] / dist;
+    else { n[0] = 0; n[1] = 0; n[2] = 1; }
+    pt[0] = q[0]; pt[1] = q[1]; pt[2] = q[2];
+  }
+  if (flip) for (int i = 0; i < 3; ++i) n[i] = -n[i];
+  add_contact(c, idx, pt, n, depth);
+  return 1;
+}
+
+__device__ int sphere_sphere(Ctx &c, int pa, const Pose &wa, int pb, const Pose &wb, double margin, int idx) {
+  const DevScene &sc = *c.sc;
+  double ra = sc.part_param[3 * pa], rb = sc.part_param[3 * pb], d[3], n[3];
+  for (int i = 0; i < 3; ++i) d[i] = wa.p[i] - wb.p[i];
+  double dist = sqrt(dot3(d, d)), depth = ra + rb - dist;
+  if (depth <= -margin) return 0;
+  if (dist > 0) for (int i = 0; i < 3; ++i) n[i] = d[i] / dist;
+  else { n[0] = 0; n[1] = 0; n[2] = 1; }
+  double pt[3];
+  for (int i = 0; i < 3; ++i) pt[i] = wb.p[i] + n[i] * rb;
+  add_contact(c, idx, pt, n, depth);
+  return 1;
+}
+
+// geometry.py:701-716: contacts of body pair (a, b), appended at S->nc. warp-collective.
+__device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
+  const DevScene &sc = *c.sc;
+  Pose pa, pb, wa, wb;
+  body_pose_cached(c, a, pa);
+  body_pose_cached(c, b, pb);
+  int base = c.S->nc, n = 0;
+  for (int i = sc.body_part_begin[a]; i < sc.body_part_begin[a + 1]; ++i) {
+    double loa[3], hia[3];
+    part_world(c, pa, i, wa);
+    prim_aabb(c, i, wa, loa, hia);
+    for (int j = sc.body_part_begin[b]; j < sc.body_part_begin[b + 1]; ++j) {
+      double lob[3], hib[3];
+      part_world(c, pb, j, wb);
+      prim_aabb(c, j, wb, lob, hib);
+      bool sep = false;
+      for (int k = 0; k < 3; ++k) sep |= (loa[k] > hib[k] + margin) || (lob[k] > hia[k] + margin);
+      if (sep) continue;
+      int ka = sc.part_kind[i], kb = sc.part_kind[j];
+      if (ka == RS_SPHERE && kb == RS_SPHERE) {
+        int r = 0;
+        if (c.lane == 0) r = sphere_sphere(c, i, wa, j, wb, margin, base + n);
+        n += __shfl_sync(0xffffffffu, r, 0);
+      } else if (ka == RS_SPHERE || kb == RS_SPHERE) {
+        bool flip = kb == RS_SPHERE;
+        int ps = flip ? j : i, pc = flip ? i : j;
+        const Pose &ws = flip ? wb : wa, &wc = flip ? wa : wb;
+        planes_world(c, pc, wc, 0);
+        __syncwarp();
+        int r = 0;
+        if (c.lane == 0) r = sphere_convex(c, ps, ws, pc, wc, 0, flip, margin, base + n);
+        n += __shfl_sync(0xffffffffu, r, 0);
+        __syncwarp();
+      } else {
+        planes_world(c, j, wb, 0);
+        planes_world(c, i, wa, 1);
+        __syncwarp();
+        n += vertices_vs_planes(c, i, wa, j, 0, false, margin, base + n);
+        n += vertices_vs_planes(c, j, wb, i, 1, true, margin, base + n);
+        __syncwarp();
+      }
+    }
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ solver
+
+__device__ __forceinline__ void row_rel_vel(Ctx &c, const double *r, double *o) {
+  const double *va = c.S->vel[(int)r[RA]], *vb = c.S->vel[(int)r[RB]];
+  const double *ra = r + RRA, *rb = r + RRB;
+  double ax = va[0] + va[4] * ra[2] - va[5] * ra[1];
+  double ay = va[1] + va[5] * ra[0] - va[3] * ra[2];
+  double az = va[2] + va[3] * ra[1] - va[4] * ra[0];
+  double bx = vb[0] + vb[4] * rb[2] - vb[5] * rb[1];
+  double by = vb[1] + vb[5] * rb[0] - vb[3] * rb[2];
+  double bz = vb[2] + vb[3] * rb[1] - vb[4] * rb[0];
+  int ja = (int)r[RJA], jb = (int)r[RJB];
+  if (ja >= 0) {
+    double dv = c.S->jdv[ja];
+    ax += r[RJACA] * dv; ay += r[RJACA + 1] * dv; az += r[RJACA + 2] * dv;
+  }
+  if (jb >= 0) {
+    double dv = c.S->jdv[jb];
+    bx += r[RJACB] * dv; by += r[RJACB + 1] * dv; bz += r[RJACB + 2] * dv;
+  }
+  o[0] = ax - bx; o[1] = ay - by; o[2] = az - bz;
+}
+__device__ __forceinline__ double row_vn(Ctx &c, const double *r) {
+  double v[3];
+  row_rel_vel(c, r, v);
+  return v[0] * r[RN] + v[1] * r[RN + 1] + v[2] * r[RN + 2];
+}
+// physics.py:1257-1291
+__device__ void row_apply(Ctx &c, const double *r, double ix, double iy, double iz) {
+  const double *pg = c.pairs + kPairD * (int)r[RGRP];
+  if (r[RIMA] > 0.0) {
+    double *va = c.S->vel[(int)r[RA]], m = r[RIMA];
+    va[0] += ix * m; va[1] += iy * m; va[2] += iz * m;
+    const double *ra = r + RRA;
+    double tx = ra[1] * iz - ra[2] * iy, ty = ra[2] * ix - ra[0] * iz, tz = ra[0] * iy - ra[1] * ix;
+    const double *I = pg + PIA;
+    va[3] += I[0] * tx + I[1] * ty + I[2] * tz;
+    va[4] += I[3] * tx + I[4] * ty + I[5] * tz;
+    va[5] += I[6] * tx + I[7] * ty + I[8] * tz;
+  }
+  if (r[RIMB] > 0.0) {
+    double *vb = c.S->vel[(int)r[RB]], m = r[RIMB];
+    vb[0] -= ix * m; vb[1] -= iy * m; vb[2] -= iz * m;
+    const double *rb = r + RRB;
+    double tx = rb[1] * iz - rb[2] * iy, ty = rb[2] * ix - rb[0] * iz, tz = rb[0] * iy - rb[1] * ix;
+    const double *I = pg + PIB;
+    vb[3] -= I[0] * tx + I[1] * ty + I[2] * tz;
+    vb[4] -= I[3] * tx + I[4] * ty + I[5] * tz;
+    vb[5] -= I[6] * tx + I[7] * ty + I[8] * tz;
+  }
+  int ja = (int)r[RJA], jb = (int)r[RJB];
+  if (ja >= 0) c.S->jdv[ja] += (r[RJACA] * ix + r[RJACA + 1] * iy + r[RJACA + 2] * iz) * r[RJIA];
+  if (jb >= 0) c.S->jdv[jb] -= (r[RJACB] * ix + r[RJACB + 1] * iy + r[RJACB + 2] * iz) * r[RJIB];
+}
+// physics.py:1309-1326
+__device__ void row_friction(Ctx &c, double *r) {
+  if (r[RK] <= 0.0 || r[RFRIC] == 0.0) return;
+  double max_t = r[RMU] * r[RLAM];
+  for (int w = 0; w < 2; ++w) {
+    const double *t = r + (w ? RT2 : RT1);
+    double *acc = r + (w ? RLT2 : RLT1);
+    double v[3];
+    row_rel_vel(c, r, v);
+    double vt = v[0] * t[0] + v[1] * t[1] + v[2] * t[2];
+    double lt = -vt / r[RK], nt = *acc + lt;
+    if (nt > max_t) nt = max_t;
+    else if (nt < -max_t) nt = -max_t;
+    lt = nt - *acc;
+    *acc = nt;
+    if (lt != 0.0) row_apply(c, r, t[0] * lt, t[1] * lt, t[2] * lt);
+  }
+}
+// physics.py:1293-1307
+__device__ void row_solve(Ctx &c, double *r) {
+  if (r[RK] <= 0.0) return;
+  double vn = row_vn(c, r);
+  double lam = -(vn - r[RTGT]) / r[RK], tot = r[RLAM] + lam;
+  if (tot < 0.0) tot = 0.0;
+  lam = tot - r[RLAM];
+  r[RLAM] = tot;
+  if (lam != 0.0) row_apply(c, r, r[RN] * lam, r[RN + 1] * lam, r[RN + 2] * lam);
+  row_friction(c, r);
+}
+
+// cyclic Jacobi eigen-decomposition (same sweep order / stopping rule as the oracle)
+__device__ void sym_eig(int m, double *A, double *V, double *ev) {
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) V[i * m + j] = (i == j);
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        double a2 = A[i * m + j] * A[i * m + j];
+        tot += a2;
+        if (i != j) off += a2;
+      }
+    if (off <= 1e-32 * tot || off == 0.0) break;
+    for (int p = 0; p < m - 1; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        double apq = A[p * m + q];
+        if (apq == 0.0) continue;
+        double app = A[p * m + p], aqq = A[q * m + q];
+        double theta = (aqq - app) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double cs = 1.0 / sqrt(t * t + 1.0), s = t * cs;
+        for (int k = 0; k < m; ++k) {
+          double akp = A[k * m + p], akq = A[k * m + q];
+          A[k * m + p] = cs * akp - s * akq;
+          A[k * m + q] = s * akp + cs * akq;
+        }
+        for (int k = 0; k < m; ++k) {
+          double apk = A[p * m + k], aqk = A[q * m + k];
+          A[p * m + k] = cs * apk - s * aqk;
+          A[q * m + k] = s * apk + cs * aqk;
+        }
+        for (int k = 0; k < m; ++k) {
+          double vkp = V[k * m + p], vkq = V[k * m + q];
+          V[k * m + p] = cs * vkp - s * vkq;
+          V[k * m + q] = s * vkp + cs * vkq;
+        }
+      }
+  }
+  for (int i = 0; i < m; ++i) ev[i] = A[i * m + i];
+}
+
+// min-norm solve with lstsq's rcond cutoff (physics.py:782), scratch in global memory
+__device__ void pinv_solve(int m, const double *A, const double *b, double rcond, double *x, double *W, double *V) {
+  double ev[kMaxBlockRows];
+  for (int i = 0; i < m * m; ++i) W[i] = A[i];
+  sym_eig(m, W, V, ev);
+  double smax = 0.0;
+  for (int i = 0; i < m; ++i) smax = fmax(smax, fabs(ev[i]));
+  for (int i = 0; i < m; ++i) x[i] = 0.0;
+  for (int k = 0; k < m; ++k) {
+    if (fabs(ev[k]) <= rcond * smax) continue;
+    double cc = 0.0;
+    for (int i = 0; i < m; ++i) cc += V[i * m + k] * b[i];
+    cc /= ev[k];
+    for (int i = 0; i < m; ++i) x[i] += cc * V[i * m + k];
+  }
+}
+
+// physics.py:760-816 (lane 0)
+__device__ void solve_block(Ctx &c, int first, int m, const double *K, double *scratch) {
+  double cur[kMaxBlockRows], q[kMaxBlockRows], lam[kMaxBlockRows], wv[kMaxBlockRows], rhs[kMaxBlockRows],
+      sol[kMaxBlockRows];
+  int active[kMaxBlockRows], na = 0;
+  double *sub = scratch, *W = scratch + kMaxBlockRows * kMaxBlockRows, *V = W + kMaxBlockRows * kMaxBlockRows;
+  for (int i = 0; i < m; ++i) {
+    double *r = c.rows + kRowD * (first + i);
+    cur[i] = r[RLAM];
+    wv[i] = row_vn(c, r) - r[RTGT];
+  }
+  for (int i = 0; i < m; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < m; ++j) s += K[i * m + j] * cur[j];
+    q[i] = wv[i] - s;
+  }
+  for (int i = 0; i < m; ++i)
+    if (cur[i] > 0.0 || wv[i] < 0.0) active[na++] = i;
+  bool converged = false;
+  for (int it = 0; it < 4 * m + 4; ++it) {
+    for (int i = 0; i < m; ++i) lam[i] = 0.0;
+    if (na) {
+      for (int i = 0; i < na; ++i) {
+        for (int j = 0; j < na; ++j) sub[i * na + j] = K[active[i] * m + active[j]];
+        rhs[i] = -q[active[i]];
+      }
+      pinv_solve(na, sub, rhs, 1e-8, sol, W, V);
+      for (int i = 0; i < na; ++i) lam[active[i]] = sol[i];
+    }
+    int worst = -1;
+    for (int i = 0; i < na; ++i) {
+      int ii = active[i];
+      if (lam[ii] < -1e-10 && (worst < 0 || lam[ii] < lam[worst] || (lam[ii] == lam[worst] && ii < worst))) worst = ii;
+    }
+    if (worst >= 0) {
+      int k = 0;
+      for (int i = 0; i < na; ++i) if (active[i] != worst) active[k++] = active[i];
+      na = k;
+      continue;
+    }
+    worst = -1;
+    for (int i = 0; i < m; ++i) {
+      bool in = false;
+      for (int j = 0; j < na; ++j) in |= (active[j] == i);
+      if (in) continue;
+      double wi = 0.0;
+      for (int j = 0; j < m; ++j) wi += K[i * m + j] * lam[j];
+      wi += q[i];
+      wv[i] = wi;
+      if (wi < -1e-10 && (worst < 0 || wi < wv[worst] || (wi == wv[worst] && i < worst))) worst = i;
+    }
+    if (worst >= 0) {
+      int k = na;
+      while (k > 0 && active[k - 1] > worst) { active[k] = active[k - 1]; --k; }
+      active[k] = worst;
+      ++na;
+      continue;
+    }
+    converged = true;
+    break;
+  }
+  if (!converged) {
+    for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
+    return;
+  }
+  for (int i = 0; i < m; ++i) {
+    double *r = c.rows + kRowD * (first + i);
+    double l = lam[i] > 0.0 ? lam[i] : 0.0;
+    double d = l - r[RLAM];
+    r[RLAM] = l;
+    if (d != 0.0) row_apply(c, r, r[RN] * d, r[RN + 1] * d, r[RN + 2] * d);
+  }
+  for (int i = 0; i < m; ++i) row_friction(c, c.rows + kRowD * (first + i));
+}
+
+__device__ __forceinline__ bool solver_dynamic(Ctx &c, int b) {
+  return c.sc->body_kind[b] == RS_DYNAMIC && !ASLEEP(c, b) && b != HELD(c);
+}
+
+// physics.py:827-844
+__device__ int joint_jacobian(Ctx &c, int b, const double *pt, double *jac, double &inv_i) {
+  const DevScene &sc = *c.sc;
+  int ji = sc.body_joint[b];
+  if (ji < 0 || HELDJ(c) == ji) return -1;
+  Pose parent, origin, jf;
+  body_pose_cached(c, sc.joint_parent[ji], parent);
+  pose_load12(sc.joint_origin + 12 * ji, origin);
+  compose(parent, origin, jf);
+  double ax[3];
+  matvec(jf.R, sc.joint_axis + 3 * ji, ax);
+  if (sc.joint_type[ji] == RS_PRISMATIC) {
+    jac[0] = ax[0]; jac[1] = ax[1]; jac[2] = ax[2];
+    inv_i = 1.0 / c.cfg->joint_inertia_prismatic;
+  } else {
+    double d[3] = {pt[0] - jf.p[0], pt[1] - jf.p[1], pt[2] - jf.p[2]};
+    cross3(ax, d, jac);
+    inv_i = 1.0 / c.cfg->joint_inertia_revolute;
+  }
+  return ji;
+}
+
+// rotation cache refresh (lanes per body)
+__device__ __forceinline__ void refresh_rot(Ctx &c) {
+  for (int b = c.lane; b < c.sc->nb; b += 32) quat_to_mat(QUAT(c, b), c.S->R[b]);
+  __syncwarp();
+}
+
+__device__ __forceinline__ void wake(Ctx &c, int b) {
+  if (c.sc->body_kind[b] != RS_DYNAMIC) return;
+  if (ASLEEP(c, b)) c.S->ctr[2]++;
+  ASLEEP(c, b) = 0;
+  SLEEPC(c, b) = 0;
+  RIDER(c, b) = -1;
+}
+
+// ------------------------------------------------------------------ substep
+
+__device__ void emit_event(Ctx &c, const double *r, double lam, double force) {
+  int k = c.B->event_count[c.env]++;
+  if (k < c.B->event_cap) {
+    double *o = c.B->events + ((size_t)c.env * c.B->event_cap + k) * 7;
+    o[0] = r[RA]; o[1] = r[RB]; o[2] = lam; o[3] = force;
+    o[4] = r[RPT]; o[5] = r[RPT + 1]; o[6] = r[RPT + 2];
+  }
+}
+
+// physics.py:657-701; returns false on capacity overflow
+__device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double dt, int sub) {
+  const DevScene &sc = *c.sc;
+  const rs_physics_config &cfg = *c.cfg;
+  WarpSmem &S = *c.S;
+  const int lane = c.lane, nb = sc.nb, nsj = sc.nsj;
+
+  if (!cfg.sleeping_enabled) {
+    for (int b = lane; b < nb; b += 32)
+      if (sc.body_kind[b] == RS_DYNAMIC && ASLEEP(c, b)) { ASLEEP(c, b) = 0; SLEEPC(c, b) = 0; RIDER(c, b) = -1; }
+    __syncwarp();
+  }
+  bool need_fk = arm != nullptr || HELDJ(c) >= 0 || HELD(c) >= 0;
+  if (arm) {
+    if (lane == 0) move_base(sc, S.sd + c.L->base, basecmd[0], basecmd[1], dt);
+    if (lane < sc.narm) {  // _drive_arm physics.py:608-621
+      double q = JOINTS(c)[nsj + lane], err = arm[lane] - q, vdes = cfg.kp * err / dt, v;
+      double cap = cfg.impulse_cap_per_control_step ? S.budget[lane] : cfg.motor_impulse_cap;
+      v = vdes < -cap ? -cap : (vdes > cap ? cap : vdes);
+      if (cfg.impulse_cap_per_control_step) S.budget[lane] = cap - fabs(v);
+      double nq = q + v * dt, lo = sc.arm_limits[2 * lane], hi = sc.arm_limits[2 * lane + 1];
+      JOINTS(c)[nsj + lane] = nq < lo ? lo : (nq > hi ? hi : nq);
+    }
+    __syncwarp();
+  }
+  if (need_fk) forward_kinematics(c);
+  if (arm) {
+    if (lane <= sc.narm) {
+      Pose p;
+      if (lane == 0) {
+        base3(S.sd + c.L->base, p);
+      } else {
+        pose_load12(S.links[lane - 1], p);
+      }
+      set_kinematic(c, sc.robot_base + lane, p, dt, true);
+    }
+    __syncwarp();
+  }
+  int dragged = HELDJ(c);
+  if (dragged >= 0) {
+    if (lane == 0) {  // physics.py:623-655
+      int ji = dragged;
+      Pose parent, origin, jf;
+      body_pose(c, sc.joint_parent[ji], parent);
+      pose_load12(sc.joint_origin + 12 * ji, origin);
+      compose(parent, origin, jf);
+      const double *ee = S.ee + 9;
+      double ax[3], qn = 0.0;
+      matvec(jf.R, sc.joint_axis + 3 * ji, ax);
+      bool skip = false;
+      const double *ge = S.sd + c.L->grab_ee;
+      double grab_q = S.sd[c.L->grab_q];
+      if (sc.joint_type[ji] == RS_PRISMATIC) {
+        double d[3] = {ee[0] - ge[0], ee[1] - ge[1], ee[2] - ge[2]};
+        qn = grab_q + dot3(ax, d);
+      } else {
+        double ref[3], cur[3], cr[3];
+        for (int i = 0; i < 3; ++i) { ref[i] = ge[i] - jf.p[i]; cur[i] = ee[i] - jf.p[i]; }
+        double pr = dot3(ax, ref), pc = dot3(ax, cur);
+        for (int i = 0; i < 3; ++i) { ref[i] -= ax[i] * pr; cur[i] -= ax[i] * pc; }
+        double nr = sqrt(dot3(ref, ref)), nc = sqrt(dot3(cur, cur));
+        if (nr < 1e-9 || nc < 1e-9) {
+          skip = true;
+        } else {
+          double ca = dot3(ref, cur) / (nr * nc);
+          ca = ca < -1.0 ? -1.0 : (ca > 1.0 ? 1.0 : ca);
+          cross3(ref, cur, cr);
+          double sgn = dot3(ax, cr);
+          qn = grab_q + acos(ca) * (sgn >= 0 ? 1.0 : -1.0);
+        }
+      }
+      if (!skip) {
+        double lo = sc.joint_limits[2 * ji], hi = sc.joint_limits[2 * ji + 1];
+        qn = fmin(fmax(qn, lo), hi);
+        double old = JOINTS(c)[ji];
+        if (qn != old) {
+          JOINTS(c)[ji] = qn;
+          JVEL(c)[ji] = dt > 0 ? (qn - old) / dt : 0.0;
+        }
+      }
+    }
+    __syncwarp();
+    update_scene_joint_poses(c, 1 << dragged, dt);
+  }
+  if (HELD(c) >= 0 && HELDJ(c) < 0) {
+    if (lane == 0) {  // physics.py:671-684
+      Pose ee, off, hp;
+      pose_load12(S.ee, ee);
+      const double *ho = S.sd + c.L->held_off;
+      quat_to_mat(ho + 3, off.R);
+      off.p[0] = ho[0]; off.p[1] = ho[1]; off.p[2] = ho[2];
+      compose(ee, off, hp);
+      set_kinematic(c, HELD(c), hp, dt, false);
+    }
+    __syncwarp();
+  }
+  // gravity + damping on awake dynamics; awake_dyn fixed here (physics.py:686-695)
+  {
+    unsigned long long mine = 0ull;
+    for (int b = lane; b < nb; b += 32) {
+      if (sc.body_kind[b] != RS_DYNAMIC || ASLEEP(c, b) || b == HELD(c)) continue;
+      mine |= 1ull << b;
+      double *lv = LV(c, b), *av = AV(c, b);
+      lv[2] -= cfg.gravity * dt;
+      for (int i = 0; i < 3; ++i) lv[i] *= cfg.lin_damping;
+      for (int i = 0; i < 3; ++i) av[i] *= cfg.ang_damping;
+    }
+    unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)(mine & 0xffffffffu));
+    unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(mine >> 32));
+    S.awake_dyn = ((unsigned long long)hi32 << 32) | lo32;
+  }
+  refresh_rot(c);
+
+  // ---- broadphase: AABBs (lanes per body)
+  for (int b = lane; b < nb; b += 32) {
+    Pose bp, wp;
+    body_pose_cached(c, b, bp);
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int p = sc.body_part_begin[b]; p < sc.body_part_begin[b + 1]; ++p) {
+      double l[3], h[3];
+      part_world(c, bp, p, wp);
+      prim_aabb(c, p, wp, l, h);
+      for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], l[i]); hi[i] = fmax(hi[i], h[i]); }
+    }
+    if (sc.body_kind[b] == RS_KINEMATIC)
+      for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
+    for (int i = 0; i < 3; ++i) { S.lo[b][i] = lo[i]; S.hi[b][i] = hi[i]; }
+  }
+  __syncwarp();
+  // ---- overlap candidates in sorted (a, b) order (lanes per pair, ballot compaction)
+  int ncand = 0;
+  bool overflow = false;
+  for (int a = 0; a < nb - 1; ++a) {
+    const int ka = sc.body_kind[a], ga = sc.body_group[a];
+    for (int b0 = a + 1; b0 < nb; b0 += 32) {
+      int b = b0 + lane;
+      bool ov = false;
+      if (b < nb) {
+        const int kb = sc.body_kind[b];
+        ov = !(ka == RS_STATIC && kb == RS_STATIC) && !(ga != RS_NO_GROUP && ga == sc.body_group[b]) &&
+             S.lo[a][0] <= S.hi[b][0] && S.lo[b][0] <= S.hi[a][0] && S.lo[b][1] <= S.hi[a][1] &&
+             S.lo[a][1] <= S.hi[b][1] && S.lo[b][2] <= S.hi[a][2] && S.lo[a][2] <= S.hi[b][2];
+      }
+      unsigned m = __ballot_sync(0xffffffffu, ov);
+      if (ov) {
+        int idx = ncand + __popc(m & ((1u << lane) - 1));
+        if (idx < kMaxCand) S.cand[idx] = (uint16_t)((a << 8) | b);
+      }
+      ncand += __popc(m);
+    }
+  }
+  if (ncand > kMaxCand) overflow = true;
+  __syncwarp();
+  // ---- admission walk (lane 0, physics.py:528-571)
+  if (lane == 0 && !overflow) {
+    int nadm = 0;
+    const int held = HELD(c);
+    for (int k = 0; k < ncand; ++k) {
+      int a = S.cand[k] >> 8, b = S.cand[k] & 0xff;
+      int ka = sc.body_kind[a], kb = sc.body_kind[b];
+      bool dyn_a = ka == RS_DYNAMIC, dyn_b = kb == RS_DYNAMIC, kin_a = ka == RS_KINEMATIC, kin_b = kb == RS_KINEMATIC;
+      bool adm;
+      if (!dyn_a && !dyn_b) {
+        bool robot = sc.body_robot[a] || sc.body_robot[b] || a == held || b == held;
+        adm = robot || sc.body_joint[a] >= 0 || sc.body_joint[b] >= 0;
+      } else {
+        bool sa = dyn_a && ASLEEP(c, a), sb = dyn_b && ASLEEP(c, b);
+        if (sa && sb) { S.ctr[1]++; continue; }
+        if ((sa && kb == RS_STATIC) || (sb && ka == RS_STATIC)) { S.ctr[1]++; continue; }
+        if (sa && kin_b && sc.body_joint[b] >= 0 && RIDER(c, a) == sc.body_joint[b]) continue;
+        if (sb && kin_a && sc.body_joint[a] >= 0 && RIDER(c, b) == sc.body_joint[a]) continue;
+        bool rkb = kin_b && (sc.body_robot[b] || b == held), rka = kin_a && (sc.body_robot[a] || a == held);
+        if (sa && rkb) wake(c, a);
+        if (sb && rka) wake(c, b);
+        adm = true;
+      }
+      if (!adm) continue;
+      if (nadm < kMaxAdm) S.adm[nadm] = S.cand[k];
+      ++nadm;
+    }
+    S.nadm = nadm;
+  }
+  __syncwarp();
+  if (overflow || S.nadm > kMaxAdm) return false;
+
+  // ---- narrowphase (physics.py:703-719)
+  if (lane == 0) {
+    S.nc = 0;
+    S.ng = 0;
+    if (c.B->trace_pairs && sub < c.B->trace_sub) c.B->trace_count[(size_t)c.env * c.B->trace_sub + sub] = 0;
+  }
+  __syncwarp();
+  const int nadm = S.nadm;
+  for (int k = 0; k < nadm; ++k) {
+    int a = S.adm[k] >> 8, b = S.adm[k] & 0xff;
+    int n = pair_contacts(c, a, b, cfg.contact_margin);
+    if (lane == 0) {
+      S.ctr[0]++;
+      if (c.B->trace_pairs && sub < c.B->trace_sub) {
+        int32_t *cnt = c.B->trace_count + (size_t)c.env * c.B->trace_sub + sub;
+        int t = (*cnt)++;
+        if (t < c.B->trace_cap) {
+          int32_t *o = c.B->trace_pairs + (((size_t)c.env * c.B->trace_sub + sub) * c.B->trace_cap + t) * 3;
+          o[0] = a; o[1] = b; o[2] = n;
+        }
+      }
+      if (n > 0) {
+        if (sc.body_kind[a] == RS_DYNAMIC && ASLEEP(c, a)) wake(c, a);
+        if (sc.body_kind[b] == RS_DYNAMIC && ASLEEP(c, b)) wake(c, b);
+        if (S.ng < kMaxGroups) {
+          S.g_a[S.ng] = a; S.g_b[S.ng] = b; S.g_first[S.ng] = S.nc; S.g_n[S.ng] = n;
+        }
+        S.ng++;
+        S.nc += n;
+      }
+    }
+    __syncwarp();
+    if (S.nc > kMaxContacts || S.ng > kMaxGroups) return false;
+  }
+  const int nc = S.nc, ng = S.ng;
+
+  // ---- solver (physics.py:846-960)
+  for (int b = lane; b < nb; b += 32) {
+    const double *lv = LV(c, b), *av = AV(c, b);
+    for (int i = 0; i < 3; ++i) { S.vel[b][i] = lv[i]; S.vel[b][3 + i] = av[i]; }
+  }
+  for (int j = lane; j < kMaxJoints; j += 32) S.jdv[j] = 0.0;
+  // per-pair solver data (lanes per group)
+  for (int g = lane; g < ng; g += 32) {
+    double *P = c.pairs + kPairD * g;
+    for (int side = 0; side < 2; ++side) {
+      int bb = side ? S.g_b[g] : S.g_a[g];
+      Pose bp;
+      body_pose_cached(c, bb, bp);
+      apply(bp, sc.com + 3 * bb, P + (side ? PCB : PCA));
+      double *I = P + (side ? PIB : PIA);
+      if (solver_dynamic(c, bb)) {
+        double T[9], Rt[9];
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) Rt[3 * i + j] = bp.R[3 * j + i];
+        matmul(bp.R, sc.inv_inertia + 9 * bb, T);
+        matmul(T, Rt, I);
+        P[side ? PIMB : PIMA] = sc.inv_mass[bb];
+      } else {
+        for (int i = 0; i < 9; ++i) I[i] = 0.0;
+        P[side ? PIMB : PIMA] = 0.0;
+      }
+    }
+    int a = S.g_a[g], b = S.g_b[g];
+    P[PMU] = sqrt(sc.friction[a] * sc.friction[b]);
+    P[PE] = fmax(sc.restitution[a], sc.restitution[b]);
+  }
+  __syncwarp();
+  // rows (lanes per contact)
+  for (int g = 0; g < ng; ++g) {
+    const int first = S.g_first[g], m = S.g_n[g];
+    const double *P = c.pairs + kPairD * g;
+    for (int i = lane; i < m; i += 32) {
+      const int ci = first + i;
+      double *r = c.rows + kRowD * ci;
+      const double *n = S.cn[ci], *pt = S.cp[ci];
+      r[RA] = S.g_a[g]; r[RB] = S.g_b[g]; r[RGRP] = g;
+      for (int k = 0; k < 3; ++k) {
+        r[RN + k] = n[k];
+        r[RRA + k] = pt[k] - P[PCA + k];
+        r[RRB + k] = pt[k] - P[PCB + k];
+        r[RPT + k] = pt[k];
+      }
+      double kk = P[PIMA] + P[PIMB], t[3], u[3], v[3];
+      cross3(r + RRA, n, t); matvec(P + PIA, t, u); cross3(u, r + RRA, v); kk += dot3(n, v);
+      cross3(r + RRB, n, t); matvec(P + PIB, t, u); cross3(u, r + RRB, v); kk += dot3(n, v);
+      double jia = 0.0, jib = 0.0;
+      int ja = joint_jacobian(c, S.g_a[g], pt, r + RJACA, jia);
+      int jb = joint_jacobian(c, S.g_b[g], pt, r + RJACB, jib);
+      r[RJA] = ja; r[RJB] = jb; r[RJIA] = jia; r[RJIB] = jib;
+      if (ja >= 0) { double jn = dot3(r + RJACA, n); kk += jn * jn * jia; }
+      if (jb >= 0) { double jn = dot3(r + RJACB, n); kk += jn * jn * jib; }
+      // tangents physics.py:1329-1336
+      double ref[3] = {0.0, 0.0, 0.0};
+      if (fabs(n[0]) < 0.9) ref[0] = 1.0; else ref[1] = 1.0;
+      double *t1 = r + RT1, *t2 = r + RT2;
+      cross3(n, ref, t1);
+      double l = sqrt(dot3(t1, t1));
+      for (int k = 0; k < 3; ++k) t1[k] /= l;
+      cross3(n, t1, t2);
+      l = sqrt(dot3(t2, t2));
+      for (int k = 0; k < 3; ++k) t2[k] /= l;
+      r[RK] = kk; r[RMU] = P[PMU]; r[RIMA] = P[PIMA]; r[RIMB] = P[PIMB];
+      r[RLAM] = r[RLT1] = r[RLT2] = 0.0;
+      r[RDEPTH] = S.cd[ci];
+      double vn = row_vn(c, r);
+      r[RVN] = vn;
+      double sep = -S.cd[ci] > 0.0 ? -S.cd[ci] : 0.0;
+      if (sep > 0.0) {
+        r[RTGT] = -sep / dt;
+        r[RFRIC] = 0.0;
+      } else {
+        r[RTGT] = vn < -cfg.restitution_threshold ? -P[PE] * vn : 0.0;
+        r[RFRIC] = 1.0;
+      }
+    }
+  }
+  __syncwarp();
+  if (nc) {
+    // block matrices (physics.py:721-758): lanes per entry
+    int koff = 0;
+    for (int g = 0; g < ng; ++g) {
+      const int first = S.g_first[g], m = S.g_n[g];
+      double *P = c.pairs + kPairD * g;
+      bool hask = m > 1 && c.rows[kRowD * first + RK] > 0.0;
+      if (hask && m > kMaxBlockRows) return false;
+      if (hask && koff + m * m > kKCap) return false;
+      if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; }
+      if (hask) {
+        double *K = c.K + koff;
+        const double *r0 = c.rows + kRowD * first;
+        for (int e = lane; e < m * m; e += 32) {
+          int i = e / m, j = e % m;
+          if (j < i) continue;
+          const double *ri = c.rows + kRowD * (first + i), *rj = c.rows + kRowD * (first + j);
+          double val = (r0[RIMA] + r0[RIMB]) * dot3(ri + RN, rj + RN);
+          if (r0[RIMA] > 0.0) {
+            double li[3], lj[3], t[3];
+            cross3(ri + RRA, ri + RN, li); cross3(rj + RRA, rj + RN, lj);
+            matvec(P + PIA, lj, t);
+            val += dot3(li, t);
+          }
+          if (r0[RIMB] > 0.0) {
+            double li[3], lj[3], t[3];
+            cross3(ri + RRB, ri + RN, li); cross3(rj + RRB, rj + RN, lj);
+            matvec(P + PIB, lj, t);
+            val += dot3(li, t);
+          }
+          if (ri[RJA] >= 0 && rj[RJA] >= 0 && ri[RJA] == rj[RJA])
+            val += dot3(ri + RJACA, ri + RN) * dot3(rj + RJACA, rj + RN) * ri[RJIA];
+          if (ri[RJB] >= 0 && rj[RJB] >= 0 && ri[RJB] == rj[RJB])
+            val += dot3(ri + RJACB, ri + RN) * dot3(rj + RJACB, rj + RN) * ri[RJIB];
+          if (i == j) val += 1e-9;
+          K[i * m + j] = val;
+          K[j * m + i] = val;
+        }
+        koff += m * m;
+      }
+    }
+    __syncwarp();
+    // Gauss-Seidel sweeps: lane 0, blocks in sorted pair order
+    if (lane == 0) {
+      double *scratch = c.K + kKCap;  // 3 * 32 * 32 doubles
+      for (int it = 0; it < cfg.solver_iterations; ++it)
+        for (int g = 0; g < ng; ++g) {
+          const int first = S.g_first[g], m = S.g_n[g];
+          const double *P = c.pairs + kPairD * g;
+          if (P[PHASK] == 0.0) {
+            for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
+          } else {
+            solve_block(c, first, m, c.K + (int)P[PKOFF], scratch);
+          }
+        }
+    }
+    __syncwarp();
+    for (int b = lane; b < nb; b += 32)
+      if (solver_dynamic(c, b)) {
+        double *lv = LV(c, b), *av = AV(c, b);
+        for (int i = 0; i < 3; ++i) { lv[i] = S.vel[b][i]; av[i] = S.vel[b][3 + i]; }
+      }
+    // events + force tally in row order (lane 0)
+    if (lane == 0) {
+      const int held = HELD(c);
+      double acc = S.sd[c.L->acc];
+      for (int i = 0; i < nc; ++i) {
+        const double *r = c.rows + kRowD * i;
+        double lam = r[RLAM];
+        if (r[RK] <= 0.0) lam = fmax(-r[RVN], 0.0);
+        if (lam <= 0.0) continue;
+        double force = lam / dt;
+        emit_event(c, r, lam, force);
+        int a = (int)r[RA], b = (int)r[RB];
+        if (sc.body_robot[a] || sc.body_robot[b] || a == held || b == held) acc += force;
+      }
+      S.sd[c.L->acc] = acc;
+    }
+    __syncwarp();
+  }
+
+  // ---- integrate (physics.py:962-1011): lanes per body
+  {
+    const int held = HELD(c);
+    for (int b = lane; b < nb; b += 32) {
+      if (!((S.awake_dyn >> b) & 1ull)) continue;
+      double corr[3] = {0.0, 0.0, 0.0};
+      int cnt = 0;
+      for (int g = 0; g < ng; ++g) {
+        int a = S.g_a[g], bb = S.g_b[g];
+        if (a != b && bb != b) continue;
+        double ima = (!ASLEEP(c, a) && a != held) ? sc.inv_mass[a] : 0.0;
+        double imb = (!ASLEEP(c, bb) && bb != held) ? sc.inv_mass[bb] : 0.0;
+        double tot = ima + imb;
+        if (tot <= 0.0) continue;
+        for (int i = S.g_first[g]; i < S.g_first[g] + S.g_n[g]; ++i) {
+          double push = cfg.correction_factor * fmax(S.cd[i] - cfg.slop, 0.0);
+          if (push <= 0.0) continue;
+          if (a == b && ima > 0.0) {
+            double s = push * ima / tot;
+            for (int k = 0; k < 3; ++k) corr[k] += S.cn[i][k] * s;
+            cnt++;
+          }
+          if (bb == b && imb > 0.0) {
+            double s = push * imb / tot;
+            for (int k = 0; k < 3; ++k) corr[k] -= S.cn[i][k] * s;
+            cnt++;
+          }
+        }
+      }
+      if (cnt > 1) for (int k = 0; k < 3; ++k) corr[k] /= cnt;
+      double *lv = LV(c, b), *av = AV(c, b);
+      double lin = sqrt(dot3(lv, lv)), ang = sqrt(dot3(av, av));
+      bool below = lin < cfg.sleep_lin_threshold && ang < cfg.sleep_ang_threshold;
+      bool has_corr = cnt > 0 && dot3(corr, corr) >= 1e-14;
+      if (below && cfg.sleeping_enabled && !has_corr) {
+        SLEEPC(c, b)++;
+        if (SLEEPC(c, b) >= cfg.sleep_substeps) {
+          ASLEEP(c, b) = 1;
+          lv[0] = lv[1] = lv[2] = 0.0;
+          av[0] = av[1] = av[2] = 0.0;
+        }
+        continue;
+      }
+      SLEEPC(c, b) = 0;
+      double *pos = POS(c, b);
+      for (int k = 0; k < 3; ++k) pos[k] = pos[k] + lv[k] * dt;
+      if (ang > 0.0) {  // geometry.py:110-114
+        double wq[4] = {0.0, av[0], av[1], av[2]}, d[4], *q = QUAT(c, b);
+        quat_mul(wq, q, d);
+        double h = 0.5 * dt;
+        for (int k = 0; k < 4; ++k) q[k] = q[k] + h * d[k];
+        double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+        for (int k = 0; k < 4; ++k) q[k] /= n;
+      }
+      if (has_corr) for (int k = 0; k < 3; ++k) pos[k] += corr[k];
+    }
+    __syncwarp();
+  }
+  // ---- scene joints (physics.py:1013-1035)
+  if (lane == 0) {
+    int moved = 0;
+    for (int ji = 0; ji < nsj; ++ji) {
+      if (ji == dragged) continue;
+      double *jv = JVEL(c) + ji;
+      *jv += S.jdv[ji];
+      *jv *= cfg.joint_damping;
+      if (fabs(*jv) < 1e-4) { *jv = 0.0; continue; }
+      double lo = sc.joint_limits[2 * ji], hi = sc.joint_limits[2 * ji + 1];
+      double q = JOINTS(c)[ji] + *jv * dt;
+      if (q <= lo) { q = lo; *jv = 0.0; }
+      else if (q >= hi) { q = hi; *jv = 0.0; }
+      if (q != JOINTS(c)[ji]) { JOINTS(c)[ji] = q; moved |= 1 << ji; }
+    }
+    S.moved_mask = moved;
+  }
+  __syncwarp();
+  int moved = S.moved_mask;
+  if (moved) update_scene_joint_poses(c, moved, dt);
+  return true;
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, const double *arm_targets,
+                                                                   const double *base_cmd, const uint8_t *has_targets,
+                                                                   double dt, int substeps) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  WarpSmem *smem = reinterpret_cast<WarpSmem *>(dsm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int env = blockIdx.x * kWarpsPerBlock + warp;
+  if (env >= B.n_env) return;
+  WarpSmem &S = smem[warp];
+  const StateLayout &L = B.L;
+  Ctx c;
+  c.sc = &B.scenes[B.env_scene[env]];
+  c.B = &B;
+  c.cfg = &B.cfg;
+  c.S = &S;
+  c.env = env;
+  c.lane = lane;
+  c.L = &L;
+  const size_t per_env = (size_t)B.row_cap * kRowD + kMaxGroups * kPairD + kKCap + 3 * kMaxBlockRows * kMaxBlockRows;
+  c.rows = B.row_scratch + per_env * env;
+  c.pairs = c.rows + (size_t)B.row_cap * kRowD;
+  c.K = c.pairs + kMaxGroups * kPairD;
+
+  // stage the state slab (coalesced)
+  const double *gsd = B.sd + (size_t)env * L.dbl_size;
+  const int32_t *gsi = B.si + (size_t)env * L.int_size;
+  for (int i = lane; i < L.dbl_size; i += 32) S.sd[i] = gsd[i];
+  for (int i = lane; i < L.int_size; i += 32) S.si[i] = gsi[i];
+  if (lane < 3) S.ctr[lane] = 0;
+  if (lane == 0) { B.event_count[env] = 0; S.fault = 0; }
+  __syncwarp();
+  const DevScene &sc = *c.sc;
+  // _check_finite (physics.py:596-606): first offending body per field class
+  {
+    uint32_t f = 0;
+    for (int cls = 0; cls < 4 && !f; ++cls) {
+      int n = cls == 3 ? L.nj : sc.nb, best = 1 << 30;
+      for (int i = lane; i < n; i += 32) {
+        bool bad = false;
+        if (cls == 0) { const double *p = POS(c, i); bad = !isfinite(p[0]) || !isfinite(p[1]) || !isfinite(p[2]); }
+        if (cls == 1) { const double *q = QUAT(c, i); bad = !isfinite(q[0]) || !isfinite(q[1]) || !isfinite(q[2]) || !isfinite(q[3]); }
+        if (cls == 2) { const double *v = LV(c, i); bad = !isfinite(v[0]) || !isfinite(v[1]) || !isfinite(v[2]); }
+        if (cls == 3) bad = !isfinite(JOINTS(c)[i]);
+        if (bad && i < best) best = i;
+      }
+      best = __reduce_min_sync(0xffffffffu, best);
+      if (best < (1 << 30)) f = ((uint32_t)(cls + 1) << 16) | (uint32_t)best;
+    }
+    if (f) {
+      if (lane == 0) B.fault[env] = f;
+      return;
+    }
+  }
+  const bool ht = has_targets == nullptr || has_targets[env];
+  const double *arm = ht ? arm_targets + (size_t)env * sc.narm : nullptr;
+  const double *bc = base_cmd + (size_t)env * 2;
+  if (lane < kMaxArm) S.budget[lane] = B.cfg.motor_impulse_cap;
+  __syncwarp();
+  const double dts = dt / substeps;
+  bool ok = true;
+  for (int s = 0; s < substeps && ok; ++s) ok = substep(c, arm, bc, dts, s);
+  if (!ok) {
+    if (lane == 0) B.fault[env] = (uint32_t)RS_FAULT_OVERFLOW << 16;
+    return;
+  }
+  if (lane == 0) {
+    S.sd[L.time] += dt;
+    B.step_index[env] += 1;
+    B.fault[env] = 0;
+    for (int i = 0; i < 3; ++i) B.counters[3 * env + i] += S.ctr[i];
+  }
+  __syncwarp();
+  double *wsd = B.sd + (size_t)env * L.dbl_size;
+  int32_t *wsi = B.si + (size_t)env * L.int_size;
+  for (int i = lane; i < L.dbl_size; i += 32) wsd[i] = S.sd[i];
+  for (int i = lane; i < L.int_size; i += 32) wsi[i] = S.si[i];
+}
+
+size_t step_scratch_doubles_per_env(int row_cap) {
+  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + kKCap + 3 * kMaxBlockRows * kMaxBlockRows;
+}
+int step_row_cap() { return kMaxContacts; }
+
+cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, const uint8_t *has_targets,
+                        double dt, int substeps, cudaStream_t stream) {
+  static bool configured = false;
+  const size_t smem = sizeof(WarpSmem) * kWarpsPerBlock;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((B.n_env + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  step_kernel<<<grid, 32 * kWarpsPerBlock, smem, stream>>>(B, arm, base_cmd, has_targets, dt, substeps);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ grasp
+// robot.py:323-346 grasp_rule + physics.py:1039-1079 grasp_candidates /
+// apply_grasp; one thread per env, between control steps.
+__global__ void grasp_kernel(DevBatch B, const double *gripper) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env >= B.n_env) return;
+  const DevScene &sc = B.scenes[B.env_scene[env]];
+  const StateLayout &L = B.L;
+  double *sd = B.sd + (size_t)env * L.dbl_size;
+  int32_t *si = B.si + (size_t)env * L.int_size;
+  const double g = gripper[env];
+  const bool holding = si[L.held] >= 0;
+  if (g < 0 && holding) {
+    int h = si[L.held];
+    if (si[L.held_joint] < 0) { si[L.asleep + h] = 0; si[L.sleep_ctr + h] = 0; }
+    si[L.held] = -1;
+    si[L.held_joint] = -1;
+    return;
+  }
+  if (!(g > 0) || holding) return;
+  // end-effector pose (robot.py:161-169)
+  Pose t, off, rot, ee;
+  base3(sd + L.base, t);
+  rot_z(0.0, off.R);
+  rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
+  for (int i = 0; i < sc.narm; ++i) {
+    off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
+    compose(t, off, t);
+    axis_angle_mat(sc.arm_axis + 3 * i, sd[L.joints + sc.nsj + i], rot.R);
+    compose(t, rot, t);
+  }
+  Pose gp = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}};
+  compose(t, gp, ee);
+  double best_d = 0.0;
+  int best_b = -1, best_j = -1;
+  auto consider = [&](double d, int body, int joint) {
+    if (!(d <= 0.15)) return;
+    if (best_b < 0 || d < best_d || (d == best_d && body < best_b)) { best_d = d; best_b = body; best_j = joint; }
+  };
+  for (int k = 0; k < sc.nclutter; ++k) {
+    int b = sc.clutter[k];
+    if (b == si[L.held]) continue;
+    Pose bp;
+    quat_to_mat(sd + L.quat + 4 * b, bp.R);
+    bp.p[0] = sd[L.pos + 3 * b]; bp.p[1] = sd[L.pos + 3 * b + 1]; bp.p[2] = sd[L.pos + 3 * b + 2];
+    double com[3], e[3];
+    apply(bp, sc.com + 3 * b, com);
+    for (int i = 0; i < 3; ++i) e[i] = ee.p[i] - com[i];
+    consider(sqrt(dot3(e, e)), b, -1);
+  }
+  for (int ji = 0; ji < sc.nsj; ++ji) {
+    Pose parent, origin, motion, tt, child;
+    int pb = sc.joint_parent[ji];
+    quat_to_mat(sd + L.quat + 4 * pb, parent.R);
+    parent.p[0] = sd[L.pos + 3 * pb]; parent.p[1] = sd[L.pos + 3 * pb + 1]; parent.p[2] = sd[L.pos + 3 * pb + 2];
+    pose_load12(sc.joint_origin + 12 * ji, origin);
+    compose(parent, origin, tt);
+    double q = sd[L.joints + ji];
+    if (sc.joint_type[ji] == RS_REVOLUTE) {
+      axis_angle_mat(sc.joint_axis + 3 * ji, q, motion.R);
+      motion.p[0] = motion.p[1] = motion.p[2] = 0.0;
+    } else {
+      const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+      for (int k = 0; k < 9; ++k) motion.R[k] = I[k];
+      for (int k = 0; k < 3; ++k) motion.p[k] = sc.joint_axis[3 * ji + k] * q;
+    }
+    compose(tt, motion, child);
+    double h[3], e[3];
+    apply(child, sc.joint_handle + 3 * ji, h);
+    for (int i = 0; i < 3; ++i) e[i] = ee.p[i] - h[i];
+    consider(sqrt(dot3(e, e)), sc.joint_body[ji], ji);
+  }
+  if (best_b < 0) return;
+  if (best_j >= 0) {
+    si[L.held_joint] = best_j;
+    si[L.held] = best_b;
+    sd[L.grab_q] = sd[L.joints + best_j];
+    for (int i = 0; i < 3; ++i) sd[L.grab_ee + i] = ee.p[i];
+    return;
+  }
+  const int b = best_b;
+  if (si[L.asleep + b]) B.counters[3 * env + 2] += 1;  // wake() physics.py:471-478
+  si[L.asleep + b] = 0;
+  si[L.sleep_ctr + b] = 0;
+  si[L.rider_joint + b] = -1;
+  Pose inv, bp, rel;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) inv.R[3 * i + j] = ee.R[3 * j + i];
+  matvec(inv.R, ee.p, inv.p);
+  for (int i = 0; i < 3; ++i) inv.p[i] = -inv.p[i];
+  quat_to_mat(sd + L.quat + 4 * b, bp.R);
+  bp.p[0] = sd[L.pos + 3 * b]; bp.p[1] = sd[L.pos + 3 * b + 1]; bp.p[2] = sd[L.pos + 3 * b + 2];
+  compose(inv, bp, rel);
+  si[L.held] = b;
+  for (int i = 0; i < 3; ++i) sd[L.held_off + i] = rel.p[i];
+  mat_to_quat(rel.R, sd + L.held_off + 3);
+  for (int i = 0; i < 3; ++i) { sd[L.lv + 3 * b + i] = 0.0; sd[L.av + 3 * b + i] = 0.0; }
+}
+
+__global__ void stats_kernel(DevBatch B, double *out) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env >= B.n_env) return;
+  const StateLayout &L = B.L;
+  const int32_t *si = B.si + (size_t)env * L.int_size;
+  int asleep = 0;
+  for (int b = 0; b < L.nb; ++b) asleep += si[L.asleep + b];
+  out[4 * env + 0] = B.sd[(size_t)env * L.dbl_size + L.acc];
+  out[4 * env + 1] = (double)B.fault[env];
+  out[4 * env + 2] = (double)B.event_count[env];
+  out[4 * env + 3] = (double)asleep;
+}
+
+cudaError_t launch_grasp(const DevBatch &B, const double *gripper, cudaStream_t stream) {
+  grasp_kernel<<<(B.n_env + 127) / 128, 128, 0, stream>>>(B, gripper);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream) {
+  stats_kernel<<<(B.n_env + 255) / 256, 256, 0, stream>>>(B, out);
+  return cudaGetLastError();
+}
+
+}  // namespace rsim

@@ -1,0 +1,307 @@
+// render.cu -- batched 128x128 RGBD proxy ray caster (sm_100a).
+//
+// Restates the SPEC's depth sensor over the reference ray
+// primitive (geometry.py:734-776) with the reference's nearest-hit /
+// lowest-id rule (physics.py:1096-1100) and the pinned conventions of
+// DESIGN.md §5 (range depth, tie_eps, near clamp, far/miss sentinel, RGB
+// shading).
+//
+// One CTA renders one (env, camera) image:
+//   1. stage: body poses from the env's state slab -> world part frames ->
+//      world facet planes (n, b0 = d - n.o) in shared memory (~25 KB);
+//   2. cull: per 16x16-pixel tile, a bitmask of parts whose bounding sphere
+//      meets the tile frustum; per part a range lower bound |c - o| - r;
+//   3. trace: each warp walks its tiles; per pixel it visits only the tile's
+//      candidate parts in body-id order, skipping parts whose lower bound
+//      exceeds the running t_min + tie_eps, and tracks (t_min, id, t_2nd);
+//      near-ties (t_2nd - t_min <= tie_eps) take an exact slow path;
+//   4. write rgba (u32), depth (f32), id (i32) rows, coalesced per warp.
+// Float64 arithmetic throughout (parity with the float64 oracle); the
+// plane arg-max/arg-min uses division-free cross-multiplied compares and
+// only the two winning planes are divided.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "device.cuh"
+#include "se3.cuh"
+
+namespace rsim {
+
+constexpr int kTile = 16;
+constexpr int kMaxParts = 128;
+constexpr int kMaskWords = kMaxParts / 32;
+constexpr int kRenderThreads = 256;
+constexpr double kParallelEps = 1e-12;  // geometry.py:731
+
+struct PartW {
+  double c[3];   // world part origin (sphere centre)
+  double r;      // bounding radius / sphere radius
+  double lb;     // lower bound of any hit range from the camera origin
+  int f0, nf, kind, body;
+};
+
+struct RenderSmem {
+  double plane[4 * 1024];  // n.xyz, b0 per facet (world)
+  PartW part[kMaxParts];
+  uint32_t mask[(128 / kTile) * (128 / kTile)][kMaskWords];
+  Pose cam;
+};
+
+// ray vs one convex: reference _ray_halfspaces, one ray
+__device__ __forceinline__ double ray_convex(const double *pl, int nf, const double *d, int &face) {
+  int fe = -1, fx = -1, bad = 0;
+  double se = 0, be = 0, sx = 0, bx = 0;
+  for (int f = 0; f < nf; ++f) {
+    const double *P = pl + 4 * f;
+    double s = d[0] * P[0] + d[1] * P[1] + d[2] * P[2];
+    double b = P[3];
+    if (s < -kParallelEps) {
+      // ratio b/s > be/se  (s, se < 0)  <=>  b*se > be*s
+      if (fe < 0 || b * se > be * s) { fe = f; se = s; be = b; }
+    } else if (s > kParallelEps) {
+      // ratio b/s < bx/sx  (s, sx > 0)  <=>  b*sx < bx*s
+      if (fx < 0 || b * sx < bx * s) { fx = f; sx = s; bx = b; }
+    } else if (b < 0) {
+      bad = 1;
+    }
+  }
+  double te = fe >= 0 ? be / se : -INFINITY;
+  double tx = fx >= 0 ? bx / sx : INFINITY;
+  face = -1;
+  if (!(te <= tx && tx >= 0.0) || bad) return INFINITY;
+  if (te >= 0.0) { face = fe; return te; }
+  return 0.0;
+}
+
+// reference _ray_sphere, one ray (oc = o - c precomputed per part)
+__device__ __forceinline__ double ray_sphere(const PartW &p, const double *o, const double *d) {
+  double oc[3] = {o[0] - p.c[0], o[1] - p.c[1], o[2] - p.c[2]};
+  double b = oc[0] * d[0] + oc[1] * d[1] + oc[2] * d[2];
+  double c = oc[0] * oc[0] + oc[1] * oc[1] + oc[2] * oc[2] - p.r * p.r;
+  double disc = b * b - c;
+  if (!(disc >= 0)) return INFINITY;
+  double sq = sqrt(disc), t0 = -b - sq, t1 = -b + sq;
+  return t0 >= 0.0 ? t0 : (t1 >= 0.0 ? 0.0 : INFINITY);
+}
+
+__device__ __forceinline__ double part_hit(const RenderSmem &S, int p, const double *o, const double *d, int &face) {
+  const PartW &P = S.part[p];
+  if (P.kind == RS_SPHERE) {
+    face = -1;
+    return ray_sphere(P, o, d);
+  }
+  double t = ray_convex(S.plane + 4 * P.f0, P.nf, d, face);
+  if (face >= 0) face += P.f0;
+  return t;
+}
+
+// exact lowest-id rule for near-tie pixels
+__device__ __noinline__ void resolve_tie(const RenderSmem &S, const uint32_t *mask, const double *o, const double *d,
+                                         double tmin, double eps, int &id, int &wpart, int &wface) {
+  int cur_b = -1, cur_p = -1, cur_f = -1;
+  double cur_t = INFINITY;
+  for (int w = 0; w < kMaskWords; ++w) {
+    uint32_t m = mask[w];
+    while (m) {
+      int p = w * 32 + __ffs(m) - 1;
+      m &= m - 1;
+      int b = S.part[p].body;
+      if (b != cur_b) {
+        if (cur_b >= 0 && cur_t <= tmin + eps) { id = cur_b; wpart = cur_p; wface = cur_f; return; }
+        cur_b = b; cur_t = INFINITY;
+      }
+      int f;
+      double t = part_hit(S, p, o, d, f);
+      if (t < cur_t) { cur_t = t; cur_p = p; cur_f = f; }
+    }
+  }
+  if (cur_b >= 0 && cur_t <= tmin + eps) { id = cur_b; wpart = cur_p; wface = cur_f; }
+}
+
+__global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out,
+                                                                uint32_t *rgba, float *depth, int32_t *ids) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RenderSmem &S = *reinterpret_cast<RenderSmem *>(smem_raw);
+  const int env = blockIdx.x / n_cam_out, slot = blockIdx.x % n_cam_out;
+  int cam = -1;
+  for (int c = 0, k = 0; c < 32; ++c)
+    if (cam_mask & (1u << c)) { if (k == slot) { cam = c; break; } ++k; }
+  const DevScene &sc = B.scenes[B.env_scene[env]];
+  const StateLayout &L = B.L;
+  const double *sd = B.sd + (size_t)env * L.dbl_size;
+  const int tid = threadIdx.x;
+
+  // -- camera pose (robot.py:43-47 mounts; tools_make_robot_json.py:12-19 axes)
+  if (tid == 0) {
+    Pose parent, mount;
+    if (sc.cam_parent[cam] == 0) {
+      base3(sd + L.base, parent);
+    } else {
+      Pose t, off, rot;
+      base3(sd + L.base, t);
+      rot_z(0.0, off.R);
+      rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
+      for (int i = 0; i < sc.narm; ++i) {
+        off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
+        compose(t, off, t);
+        axis_angle_mat(sc.arm_axis + 3 * i, sd[L.joints + sc.nsj + i], rot.R);
+        compose(t, rot, t);
+      }
+      Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}};
+      compose(t, g, parent);
+    }
+    pose_load12(sc.cam_mount + 12 * cam, mount);
+    compose(parent, mount, S.cam);
+  }
+  __syncthreads();
+  const double *o = S.cam.p;
+
+  // -- world part frames + bounds
+  for (int p = tid; p < sc.np; p += blockDim.x) {
+    int b = sc.part_body[p];
+    Pose bp, lp, wp;
+    quat_to_mat(sd + L.quat + 4 * b, bp.R);
+    bp.p[0] = sd[L.pos + 3 * b]; bp.p[1] = sd[L.pos + 3 * b + 1]; bp.p[2] = sd[L.pos + 3 * b + 2];
+    pose_load12(sc.part_local + 12 * p, lp);
+    compose(bp, lp, wp);
+    PartW &P = S.part[p];
+    P.c[0] = wp.p[0]; P.c[1] = wp.p[1]; P.c[2] = wp.p[2];
+    P.kind = sc.part_kind[p];
+    P.body = b;
+    P.f0 = sc.part_facet_begin[p];
+    P.nf = sc.part_facet_begin[p + 1] - P.f0;
+    P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : (double)sc.part_bound[p];
+    double v[3] = {wp.p[0] - o[0], wp.p[1] - o[1], wp.p[2] - o[2]};
+    double dist = sqrt(dot3(v, v)) - P.r * (1.0 + 1e-9) - 1e-9;
+    P.lb = dist > 0.0 ? dist : 0.0;
+    // world planes of this part (geometry.py:554-557), then b0 = d - n.o
+    for (int f = P.f0; f < P.f0 + P.nf; ++f) {
+      const double *F = sc.facet + 4 * f;
+      double n[3];
+      matvec(wp.R, F, n);
+      double dw = F[3] + dot3(n, wp.p);
+      double *Q = S.plane + 4 * f;
+      Q[0] = n[0]; Q[1] = n[1]; Q[2] = n[2];
+      Q[3] = dw - dot3(o, n);
+    }
+  }
+  __syncthreads();
+
+  // -- tile culling: sphere vs the 4 side planes of the tile frustum (camera frame)
+  const int W = B.rcfg.width, H = B.rcfg.height;
+  const int tx_n = W / kTile, ty_n = H / kTile, ntiles = tx_n * ty_n;
+  const double f = (W / 2.0) / tan(B.rcfg.fov / 2.0);
+  for (int i = tid; i < ntiles * kMaskWords; i += blockDim.x) S.mask[i / kMaskWords][i % kMaskWords] = 0u;
+  __syncthreads();
+  for (int i = tid; i < ntiles * sc.np; i += blockDim.x) {
+    int tile = i / sc.np, p = i % sc.np;
+    const PartW &P = S.part[p];
+    double v[3] = {P.c[0] - o[0], P.c[1] - o[1], P.c[2] - o[2]}, c[3];
+    mattvec(S.cam.R, v, c);  // camera frame: x right, y down, z view
+    double r = P.r * (1.0 + 1e-9) + 1e-9;
+    bool in = c[2] > -r;
+    if (in) {
+      double u0 = ((tile % tx_n) * kTile - W / 2.0) / f, u1 = ((tile % tx_n) * kTile + kTile - W / 2.0) / f;
+      double v0 = ((tile / tx_n) * kTile - H / 2.0) / f, v1 = ((tile / tx_n) * kTile + kTile - H / 2.0) / f;
+      // plane x - u z >= 0 (left), -x + u1 z >= 0 (right), same in y; signed distances
+      double nl = sqrt(1.0 + u0 * u0), nr = sqrt(1.0 + u1 * u1), nt = sqrt(1.0 + v0 * v0), nbm = sqrt(1.0 + v1 * v1);
+      in = (c[0] - u0 * c[2]) / nl >= -r && (-c[0] + u1 * c[2]) / nr >= -r && (c[1] - v0 * c[2]) / nt >= -r &&
+           (-c[1] + v1 * c[2]) / nbm >= -r;
+    }
+    if (in) atomicOr(&S.mask[tile][p >> 5], 1u << (p & 31));
+  }
+  __syncthreads();
+
+  // -- trace
+  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const double eps = B.rcfg.tie_eps, zfar = B.rcfg.zfar, znear = B.rcfg.znear;
+  const size_t img = (size_t)(env * n_cam_out + slot) * H * W;
+  for (int tile = warp; tile < ntiles; tile += nwarps) {
+    const uint32_t *mask = S.mask[tile];
+    const int ux = (tile % tx_n) * kTile, vy = (tile / tx_n) * kTile;
+    for (int k = lane; k < kTile * kTile; k += 32) {
+      const int u = ux + (k % kTile), v = vy + (k / kTile);
+      double dc[3] = {(u + 0.5 - W / 2.0) / f, (v + 0.5 - H / 2.0) / f, 1.0};
+      double l = sqrt(dot3(dc, dc));
+      dc[0] /= l; dc[1] /= l; dc[2] /= l;
+      double d[3];
+      matvec(S.cam.R, dc, d);
+      double tmin = INFINITY, t2 = INFINITY, cur_t = INFINITY;
+      int id = -1, wpart = -1, wface = -1, cur_b = -1, cur_p = -1, cur_f = -1;
+      for (int w = 0; w < kMaskWords; ++w) {
+        uint32_t m = mask[w];
+        while (m) {
+          int p = w * 32 + __ffs(m) - 1;
+          m &= m - 1;
+          const int b = S.part[p].body;
+          if (b != cur_b) {
+            if (cur_t < tmin) { t2 = tmin; tmin = cur_t; id = cur_b; wpart = cur_p; wface = cur_f; }
+            else if (cur_t < t2) t2 = cur_t;
+            cur_b = b; cur_t = INFINITY;
+          }
+          if (S.part[p].lb > tmin + eps) continue;
+          int fc;
+          double t = part_hit(S, p, o, d, fc);
+          if (t < cur_t) { cur_t = t; cur_p = p; cur_f = fc; }
+        }
+      }
+      if (cur_t < tmin) { t2 = tmin; tmin = cur_t; id = cur_b; wpart = cur_p; wface = cur_f; }
+      else if (cur_t < t2) t2 = cur_t;
+      if (isfinite(tmin) && t2 - tmin <= eps) resolve_tie(S, mask, o, d, tmin, eps, id, wpart, wface);
+
+      const size_t px = img + (size_t)v * W + u;
+      if (!(tmin <= zfar)) {
+        if (rgba) rgba[px] = 0u;
+        if (depth) depth[px] = 0.0f;
+        if (ids) ids[px] = -1;
+        continue;
+      }
+      if (depth) depth[px] = (float)(tmin < znear ? znear : tmin);
+      if (ids) ids[px] = id;
+      if (rgba) {
+        double cosv = 0.0;
+        const PartW &P = S.part[wpart];
+        if (P.kind == RS_SPHERE) {
+          if (tmin > 0.0) {
+            double n[3];
+            for (int i = 0; i < 3; ++i) n[i] = (o[i] + tmin * d[i] - P.c[i]) / P.r;
+            cosv = -dot3(n, d);
+          }
+        } else if (wface >= 0) {
+          cosv = -dot3(S.plane + 4 * wface, d);
+        }
+        float shade = __fadd_rn(0.3f, __fmul_rn(0.7f, (float)(cosv > 0.0 ? cosv : 0.0)));
+        const float *col = sc.color + 3 * id;
+        uint32_t px4 = 0xff000000u;
+        for (int i = 0; i < 3; ++i) {
+          float cv = __fadd_rn(__fmul_rn(__fmul_rn(255.0f, col[i]), shade), 0.5f);
+          px4 |= (uint32_t)(cv > 255.0f ? 255.0f : cv) << (8 * i);
+        }
+        rgba[px] = px4;
+      }
+    }
+  }
+}
+
+size_t render_smem_bytes() { return sizeof(RenderSmem); }
+
+cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                          cudaStream_t stream) {
+  int n_cam_out = __builtin_popcount(cam_mask);
+  if (n_cam_out == 0) return cudaSuccess;
+  static bool configured = false;
+  size_t smem = sizeof(RenderSmem);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(B.n_env * n_cam_out);
+  render_kernel<<<grid, kRenderThreads, smem, stream>>>(B, cam_mask, n_cam_out, reinterpret_cast<uint32_t *>(rgba),
+                                                        depth, ids);
+  return cudaGetLastError();
+}
+
+}  // namespace rsim

@@ -1,0 +1,250 @@
+"""``BatchSimulator``: the reference ``physics.Simulator`` API with a leading
+env dimension, executed by the CUDA library through the C-ABI.
+
+Reference surface (physics.py:252-1101) -> batched equivalent:
+
+* ``Simulator(scene, robot, clutter, config)``  ->
+  ``BatchSimulator(layouts, n_env, clutter=..., config=...)``; env ``e``
+  simulates layout ``layouts[e % len(layouts)]`` unless ``env_layout`` is
+  given;
+* ``WorldState.to_bytes/from_bytes``  -> ``get_state / set_state`` (the
+  identical snapshot bytes);
+* ``step_physics(state, targets, dt, substeps)``  ->
+  ``step_physics(arm_targets[E,7], base_cmd[E,2], has_targets=None, ...)``
+  on device tensors; like the reference it is functional per control step
+  and raises ``PhysicsFault`` (naming env and body) when ``check=True``;
+* ``apply_grasp(grasp_rule(...))``  -> ``grasp(gripper[E])``;
+* sensors ``render_depth`` (SPEC only)  -> ``render(cams)`` -> RGBA8,
+  depth f32, body id i32 device tensors ``[E, C, H, W]``.
+
+All device memory for inputs/outputs is torch-allocated; the library owns
+the state slabs.  Every call is ordered on the current torch CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import abi, native
+from .compiler import compile_world
+from .scene import build_world, flat_clutter
+from .state import WorldState, snapshot_size
+
+CAMERAS = {"head": 0, "arm": 1}
+
+
+class PhysicsFault(RuntimeError):
+    """Non-finite state (physics.py:46-47, :596-606) or capacity overflow."""
+
+
+def _stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _dptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class BatchSimulator:
+    def __init__(self, layouts=(0,), n_env: int = 1, clutter: list[str] | None = None, env_layout=None,
+                 config: dict | None = None, render: dict | None = None, event_cap: int = 256,
+                 device: str | torch.device = "cuda"):
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise native.NativeLibraryError("BatchSimulator runs on CUDA devices only (no CPU fallback)")
+        self.L = native.lib()
+        clutter = clutter if clutter is not None else flat_clutter()
+        self.layouts = list(layouts)
+        self.worlds = [build_world(v, clutter) for v in self.layouts]
+        self.tables = [compile_world(w) for w in self.worlds]
+        self.n_env = int(n_env)
+        if env_layout is None:
+            env_scene = np.arange(self.n_env, dtype=np.int32) % len(self.layouts)
+        else:
+            env_scene = np.array([self.layouts.index(v) for v in env_layout], dtype=np.int32)
+        self.env_scene = env_scene
+        self.config = abi.physics_config(**(config or {}))
+        self.rconfig = abi.render_config(**(render or {}))
+        self.event_cap = int(event_cap)
+        w0 = self.worlds[0]
+        self.n_bodies, self.n_joints, self.n_arm = w0.n_bodies, w0.n_joints, w0.robot.dof
+        self.snap_size = snapshot_size(self.n_bodies, self.n_joints)
+        with torch.cuda.device(self.device):
+            self._descs = [abi.SceneDesc(t) for t in self.tables]
+            self._scenes = []
+            for d in self._descs:
+                h = C.c_void_p()
+                native.check(self.L.rs_scene_create(C.byref(d.desc), C.byref(h)), "rs_scene_create")
+                self._scenes.append(h)
+            arr = (C.c_void_p * len(self._scenes))(*[h.value for h in self._scenes])
+            b = C.c_void_p()
+            native.check(self.L.rs_batch_create(arr, len(self._scenes), env_scene.ctypes.data, self.n_env,
+                                                C.byref(self.config), C.byref(self.rconfig), self.event_cap,
+                                                C.byref(b)), "rs_batch_create")
+            self._batch = b
+            bufs = abi.rs_buffers()
+            native.check(self.L.rs_batch_buffers(b, C.byref(bufs)), "rs_batch_buffers")
+            self._bufs = bufs
+
+    # ---------------------------------------------------------------- lifetime
+    def close(self):
+        if getattr(self, "_batch", None):
+            self.L.rs_batch_destroy(self._batch)
+            self._batch = None
+        for h in getattr(self, "_scenes", []):
+            self.L.rs_scene_destroy(h)
+        self._scenes = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------- state
+    def set_state(self, snapshots, env_ids=None):
+        """Load reference-format snapshots (``WorldState.to_bytes``) into envs."""
+        blobs = [s.to_bytes() if isinstance(s, WorldState) else bytes(s) for s in snapshots]
+        buf = np.frombuffer(b"".join(blobs), dtype=np.uint8)
+        ids = None if env_ids is None else np.ascontiguousarray(env_ids, dtype=np.int32)
+        with torch.cuda.device(self.device):
+            native.check(self.L.rs_set_state(self._batch, buf.ctypes.data, self.snap_size,
+                                             None if ids is None else ids.ctypes.data, len(blobs),
+                                             _stream_ptr()), "rs_set_state")
+
+    def get_state(self, env_ids=None) -> list[bytes]:
+        ids = np.arange(self.n_env, dtype=np.int32) if env_ids is None else np.ascontiguousarray(env_ids, np.int32)
+        out = np.zeros(len(ids) * self.snap_size, np.uint8)
+        with torch.cuda.device(self.device):
+            native.check(self.L.rs_get_state(self._batch, out.ctypes.data, self.snap_size, ids.ctypes.data,
+                                             len(ids), _stream_ptr()), "rs_get_state")
+        return [out[i * self.snap_size:(i + 1) * self.snap_size].tobytes() for i in range(len(ids))]
+
+    def world_state(self, env: int) -> WorldState:
+        return WorldState.from_bytes(self.get_state([env])[0])
+
+    # ------------------------------------------------------------------- step
+    def step_physics(self, arm_targets: torch.Tensor, base_cmd: torch.Tensor, has_targets: torch.Tensor | None = None,
+                     dt: float = 1.0 / 30.0, substeps: int = 4, check: bool = False):
+        """One control step for every env (physics.py:575-594)."""
+        if dt <= 0 or substeps < 1:
+            raise PhysicsFault(f"bad step parameters dt={dt} substeps={substeps}")
+        arm = self._dev(arm_targets, (self.n_env, self.n_arm), torch.float64)
+        base = self._dev(base_cmd, (self.n_env, 2), torch.float64)
+        ht = None if has_targets is None else self._dev(has_targets, (self.n_env,), torch.uint8)
+        native.check(self.L.rs_step(self._batch, _dptr(arm), _dptr(base), _dptr(ht), float(dt), int(substeps),
+                                    _stream_ptr()), "rs_step")
+        if check:
+            self.raise_faults()
+
+    def _dev(self, t, shape, dtype):
+        if not isinstance(t, torch.Tensor):
+            t = torch.as_tensor(np.asarray(t))
+        t = t.to(device=self.device, dtype=dtype).contiguous()
+        if tuple(t.shape) != shape:
+            raise ValueError(f"expected shape {shape}, got {tuple(t.shape)}")
+        return t
+
+    # -------------------------------------------------------------- buffers
+    def faults(self) -> torch.Tensor:
+        return _ptr_tensor(self._bufs.fault, 4 * self.n_env, torch.int32, self.device)
+
+    def raise_faults(self):
+        f = self.faults().cpu().numpy().astype(np.uint32)
+        bad = np.nonzero(f)[0]
+        if len(bad):
+            e = int(bad[0])
+            kind, idx = int(f[e]) >> 16, int(f[e]) & 0xFFFF
+            name = abi.FAULT_KINDS.get(kind, f"fault {kind}")
+            what = self.worlds[self.layouts.index(self.layouts[self.env_scene[e]])].bodies
+            label = what[idx].name if kind in (1, 2, 3) and idx < len(what) else str(idx)
+            raise PhysicsFault(f"env {e}: {name} for {'body' if kind in (1, 2, 3) else 'index'} {idx} ({label})")
+
+    def event_counts(self) -> torch.Tensor:
+        return _ptr_tensor(self._bufs.event_count, 4 * self.n_env, torch.int32, self.device)
+
+    def events(self) -> torch.Tensor:
+        """[E, cap, 7] (a, b, impulse, force, point) of the last step."""
+        t = _ptr_tensor(self._bufs.events, 8 * 7 * max(self.event_cap, 1) * self.n_env, torch.float64, self.device)
+        return t.view(self.n_env, max(self.event_cap, 1), 7)
+
+    def counters(self) -> torch.Tensor:
+        """[E, 3] narrowphase_tests, skipped_sleeping_pairs, wakes (since set_state)."""
+        return _ptr_tensor(self._bufs.counters, 8 * 3 * self.n_env, torch.int64, self.device).view(self.n_env, 3)
+
+    def set_trace(self, cap: int = 128, max_substeps: int = 4):
+        """Enable the parity trace: admitted pairs + contact counts per substep."""
+        self._trace = (torch.zeros((self.n_env, max_substeps, cap, 3), dtype=torch.int32, device=self.device),
+                       torch.zeros((self.n_env, max_substeps), dtype=torch.int32, device=self.device))
+        native.check(self.L.rs_set_trace(self._batch, _dptr(self._trace[0]), _dptr(self._trace[1]), cap, max_substeps),
+                     "rs_set_trace")
+
+    def trace(self, env: int):
+        """[(substep, a, b, n_contacts)] recorded by the last step for `env`."""
+        pairs, count = (t.cpu().numpy() for t in self._trace)
+        out = []
+        for s in range(pairs.shape[1]):
+            n = int(count[env, s])
+            if n > pairs.shape[2]:
+                raise RuntimeError("trace capacity exceeded")
+            out.extend((s, *map(int, p)) for p in pairs[env, s, :n])
+        return out
+
+    # ------------------------------------------------------------------ grasp
+    def grasp(self, gripper: torch.Tensor):
+        g = self._dev(gripper, (self.n_env,), torch.float64)
+        native.check(self.L.rs_grasp(self._batch, _dptr(g), _stream_ptr()), "rs_grasp")
+
+    # ----------------------------------------------------------------- render
+    def alloc_obs(self, cams=("head", "arm")):
+        H, W, n = self.rconfig.height, self.rconfig.width, len(cams)
+        kw = dict(device=self.device)
+        return (torch.empty((self.n_env, n, H, W, 4), dtype=torch.uint8, **kw),
+                torch.empty((self.n_env, n, H, W), dtype=torch.float32, **kw),
+                torch.empty((self.n_env, n, H, W), dtype=torch.int32, **kw))
+
+    @staticmethod
+    def cam_mask(cams) -> int:
+        m = 0
+        for c in cams:
+            m |= 1 << CAMERAS[c]
+        return m
+
+    def render(self, cams=("head", "arm"), out=None):
+        """RGBD + ids of the current state, ``[E, len(cams), H, W]``; cameras are
+        written in mask order (head before arm)."""
+        cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
+        rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
+        native.check(self.L.rs_render(self._batch, self.cam_mask(cams), _dptr(rgba), _dptr(depth), _dptr(ids),
+                                      _stream_ptr()), "rs_render")
+        return rgba, depth, ids
+
+    # ------------------------------------------------------- end-to-end (host)
+    def step_host(self, h_arm: torch.Tensor, h_base: torch.Tensor, cams=("head", "arm"), out=None,
+                  h_stats: torch.Tensor | None = None, dt=1.0 / 30.0, substeps=4):
+        """Env step through the C-ABI with HOST action buffers and a HOST
+        result read-back (rs_step_host): [E, 4] acc. force, fault, events, asleep."""
+        cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
+        rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
+        if h_stats is None:
+            h_stats = torch.empty((self.n_env, 4), dtype=torch.float64).pin_memory()
+        native.check(self.L.rs_step_host(self._batch, C.c_void_p(h_arm.data_ptr()), C.c_void_p(h_base.data_ptr()),
+                                         float(dt), int(substeps), self.cam_mask(cams), _dptr(rgba), _dptr(depth),
+                                         _dptr(ids), C.c_void_p(h_stats.data_ptr()), _stream_ptr()), "rs_step_host")
+        return h_stats
+
+
+def _ptr_tensor(ptr, nbytes: int, dtype, device) -> torch.Tensor:
+    """Wrap library-owned device memory as a torch tensor without copying."""
+    class _Holder:
+        def __init__(self, p, n):
+            self.__cuda_array_interface__ = {
+                "shape": (n,), "typestr": "|u1", "data": (int(p), False), "version": 3, "strides": None,
+            }
+    u8 = torch.as_tensor(_Holder(ptr, nbytes), device=device)
+    return u8.view(dtype)

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the C oracle and
+the reference golden fixtures.  Requires a B200 (sm_100a)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from conftest import golden  # noqa: E402
+from oracle.oracle import Oracle  # noqa: E402
+from paper_2106_14405_b200 import native  # noqa: E402
+from paper_2106_14405_b200.compiler import compile_world  # noqa: E402
+from paper_2106_14405_b200.scene import build_world, flat_clutter  # noqa: E402
+from paper_2106_14405_b200.sim import BatchSimulator, PhysicsFault  # noqa: E402
+from paper_2106_14405_b200.state import WorldState  # noqa: E402
+
+LAYOUT = {"idle": 0, "fixed": 1, "interact": 0, "awake": 2, "drop": 0, "drop_floor": 0, "settle": 1,
+          "tilt": 0, "drawer": 0, "fridge": 0, "held": 0}
+EV_NOISE = 1e-12
+_orc = {}
+
+
+def oracle(layout, **cfg):
+    key = (layout, tuple(sorted(cfg.items())))
+    if key not in _orc:
+        _orc[key] = Oracle(compile_world(build_world(layout, flat_clutter())), **cfg)
+    return _orc[key]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    native.lib()
+
+
+def _cmp_state(me: WorldState, ref: WorldState, pos_tol, vel_tol, what=""):
+    for f in ("asleep", "sleep_counter", "rider_joint"):
+        np.testing.assert_array_equal(getattr(me, f), getattr(ref, f), err_msg=f"{what} {f}")
+    assert (me.held, me.held_joint, me.step_index) == (ref.held, ref.held_joint, ref.step_index), what
+    for f in ("pos", "quat", "joints", "base", "rider_offset", "held_offset", "grab_ee"):
+        np.testing.assert_allclose(getattr(me, f), getattr(ref, f), rtol=0, atol=pos_tol, err_msg=f"{what} {f}")
+    for f in ("lin_vel", "ang_vel", "joint_vel"):
+        np.testing.assert_allclose(getattr(me, f), getattr(ref, f), rtol=0, atol=vel_tol, err_msg=f"{what} {f}")
+    assert abs(me.accumulated_contact_force - ref.accumulated_contact_force) <= 1e-9 * max(1.0, ref.accumulated_contact_force)
+
+
+@pytest.mark.parametrize("name", sorted(LAYOUT))
+def test_teacher_forced_vs_oracle_and_reference(name):
+    """Every golden control step runs as one env of a batch (teacher forcing).
+    Admitted pair lists and per-pair contact counts: bit-exact vs the oracle
+    and the reference; state vs oracle to 1e-12, vs reference to its tolerance."""
+    g = golden(f"traj_{name}.npz")
+    cfg = {"sleeping_enabled": 0} if name == "awake" else {}
+    n = len(g["pre"])
+    sim = BatchSimulator(layouts=(LAYOUT[name],), n_env=n, config=cfg, event_cap=512)
+    sim.set_trace(cap=256)
+    sim.set_state([g["pre"][s].tobytes() for s in range(n)])
+    arm = torch.tensor(g["arm"], dtype=torch.float64)
+    base = torch.tensor(g["base"], dtype=torch.float64)
+    ht = torch.tensor(g["has_targets"].astype(np.uint8))
+    sim.step_physics(arm, base, ht, check=True)
+    torch.cuda.synchronize()
+    out = sim.get_state()
+    counters = sim.counters().cpu().numpy()
+    ev_cnt = sim.event_counts().cpu().numpy()
+    events = sim.events().cpu().numpy()
+    orc = oracle(LAYOUT[name], **cfg)
+    for s in range(n):
+        arm_s = g["arm"][s] if g["has_targets"][s] else None
+        r = orc.step(g["pre"][s].tobytes(), arm_s, g["base"][s])
+        trace = np.array(sim.trace(s), dtype=np.int64).reshape(-1, 4)
+        # pair lists vs the reference golden, per substep
+        for k in range(4):
+            ref_pairs = g["pairs"][g["pair_off"][4 * s + k]:g["pair_off"][4 * s + k + 1]]
+            mine = trace[trace[:, 0] == k]
+            np.testing.assert_array_equal(mine[:, 1:3], ref_pairs, err_msg=f"{name} step {s} substep {k}")
+            ref_c = g["contacts"][g["contact_off"][4 * s + k]:g["contact_off"][4 * s + k + 1]]
+            ref_counts = [int(((ref_c[:, 0] == a) & (ref_c[:, 1] == b)).sum()) for a, b in ref_pairs]
+            np.testing.assert_array_equal(mine[:, 3], ref_counts, err_msg=f"{name} step {s} substep {k} contacts")
+        assert list(counters[s]) == list(g["counters"][s]) == r.counters
+        me = WorldState.from_bytes(out[s])
+        _cmp_state(me, WorldState.from_bytes(r.snapshot), 1e-12, 1e-10, f"{name}[{s}] vs oracle")
+        _cmp_state(me, WorldState.from_bytes(g["post"][s].tobytes()), 1e-12, 1e-10, f"{name}[{s}] vs reference")
+        ev = events[s, :ev_cnt[s]]
+        ev = ev[ev[:, 2] > EV_NOISE]
+        ev_o = r.events[r.events[:, 2] > EV_NOISE]
+        np.testing.assert_array_equal(ev[:, :2], ev_o[:, :2])
+        np.testing.assert_allclose(ev[:, 2:], ev_o[:, 2:], rtol=1e-9, atol=1e-9)
+    sim.close()
+
+
+def test_free_running_matches_oracle():
+    """20 control steps free-running on the GPU and the oracle from the same
+    settled state with random joint targets: identical pair lists each step,
+    poses within 1e-9 (-fmad=false keeps float64 rounding identical to the
+    oracle's scalar C; only libm sin/cos/acos can differ in the last bit)."""
+    pool = golden("settled_pool.npz")
+    blobs = [b.tobytes() for b, t in zip(pool["snapshots"], pool["tags"]) if t[0] == 0][:4]
+    sim = BatchSimulator(layouts=(0,), n_env=len(blobs))
+    sim.set_trace(cap=256)
+    rng = np.random.default_rng(0)
+    states = []
+    for b in blobs:
+        st = WorldState.from_bytes(b)
+        st.base = np.array([rng.uniform(1.8, 2.8), rng.uniform(-0.6, 0.2), rng.uniform(-3, 3)])
+        states.append(st.to_bytes())
+    sim.set_state(states)
+    orc = oracle(0)
+    cur = list(states)
+    for step in range(20):
+        q = np.stack([WorldState.from_bytes(s).joints[4:] for s in cur])
+        arm = q + rng.uniform(-0.05, 0.05, q.shape)
+        base = np.stack([rng.uniform(-0.5, 1.0, len(cur)), rng.uniform(-1, 1, len(cur))], axis=1)
+        sim.step_physics(torch.tensor(arm), torch.tensor(base), check=True)
+        torch.cuda.synchronize()
+        got = sim.get_state()
+        for e in range(len(cur)):
+            r = orc.step(cur[e], arm[e], base[e])
+            tr = np.array(sim.trace(e)).reshape(-1, 4)
+            np.testing.assert_array_equal(tr[:, [0, 1, 2]], r.pairs, err_msg=f"step {step} env {e}")
+            _cmp_state(WorldState.from_bytes(got[e]), WorldState.from_bytes(r.snapshot), 1e-9, 1e-7, f"step {step} env {e}")
+            cur[e] = got[e]
+    sim.close()
+
+
+def test_fixed_point_is_bit_exact_on_gpu():
+    g = golden("traj_fixed.npz")
+    sim = BatchSimulator(layouts=(1,), n_env=1)
+    sim.set_state([g["pre"][0].tobytes()])
+    q = torch.tensor(g["arm"][:1])
+    zero = torch.zeros((1, 2), dtype=torch.float64)
+    sim.step_physics(q, zero)
+    a = sim.world_state(0)
+    for _ in range(3):
+        sim.step_physics(torch.tensor(a.joints[4:][None]), zero)
+        b = sim.world_state(0)
+        for f in ("pos", "quat", "lin_vel", "ang_vel", "asleep", "sleep_counter", "joints", "base"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+        assert b.step_index == a.step_index + 1
+        a = b
+    sim.close()
+
+
+def test_render_matches_oracle_and_reference():
+    g = golden("render.npz")
+    n = len(g["cam"])
+    sim = BatchSimulator(layouts=(0,), n_env=n)
+    sim.set_state([s.tobytes() for s in g["state"]])
+    rgba, depth, ids = (t.cpu().numpy() for t in sim.render(("head", "arm")))
+    orc = oracle(0)
+    for i in range(n):
+        cam = int(g["cam"][i])
+        o_rgba, o_depth, o_ids, o_t = orc.render(g["state"][i].tobytes(), cam)
+        ref_t = g["t"][i]
+        miss = ~(np.isfinite(ref_t) & (ref_t <= 10.0))
+        np.testing.assert_array_equal(ids[i, cam], np.where(miss, -1, g["ids"][i]), err_msg=f"frame {i} vs reference")
+        np.testing.assert_array_equal(ids[i, cam], o_ids, err_msg=f"frame {i} vs oracle")
+        np.testing.assert_allclose(depth[i, cam], o_depth, rtol=1e-6, atol=1e-6)
+        assert np.abs(rgba[i, cam].astype(int) - o_rgba.astype(int)).max() <= 1
+    sim.close()
+
+
+def test_render_tiles_many_envs_consistently():
+    """Same state in 300 envs across both cameras -> identical images (no
+    cross-env interference in the batched launch)."""
+    g = golden("render.npz")
+    sim = BatchSimulator(layouts=(0,), n_env=300)
+    sim.set_state([g["state"][2].tobytes()] * 300)
+    rgba, depth, ids = sim.render()
+    assert (ids == ids[:1]).all() and (depth == depth[:1]).all() and (rgba == rgba[:1]).all()
+    sim.close()
+
+
+def test_grasp_snap_and_release():
+    g = golden("traj_held.npz")
+    # the recorded pre-state of step 0 already holds an object: release it, re-snap
+    st = WorldState.from_bytes(g["pre"][0].tobytes())
+    held = st.held
+    sim = BatchSimulator(layouts=(0,), n_env=1)
+    sim.set_state([st.to_bytes()])
+    sim.grasp(torch.tensor([-1.0]))
+    s1 = sim.world_state(0)
+    assert s1.held == -1 and not s1.asleep[held]
+    sim.grasp(torch.tensor([1.0]))
+    s2 = sim.world_state(0)
+    assert s2.held == held
+    np.testing.assert_allclose(s2.held_offset, st.held_offset, atol=1e-12)
+    sim.close()
+
+
+def test_nonfinite_state_raises_physics_fault():
+    g = golden("traj_idle.npz")
+    st = WorldState.from_bytes(g["pre"][0].tobytes())
+    st.pos[30, 1] = np.nan
+    sim = BatchSimulator(layouts=(0,), n_env=2)
+    sim.set_state([g["pre"][0].tobytes(), st.to_bytes()])
+    with pytest.raises(PhysicsFault, match="env 1: non-finite pos for body 30"):
+        sim.step_physics(torch.tensor(g["arm"][:2]), torch.tensor(g["base"][:2]), check=True)
+    sim.close()
+
+
+def test_step_host_end_to_end():
+    g = golden("traj_idle.npz")
+    n = 8
+    sim = BatchSimulator(layouts=(0,), n_env=n)
+    sim.set_state([g["pre"][0].tobytes()] * n)
+    h_arm = torch.tensor(np.tile(g["arm"][0], (n, 1))).pin_memory()
+    h_base = torch.tensor(np.tile(g["base"][0], (n, 1))).pin_memory()
+    stats = sim.step_host(h_arm, h_base)
+    ref = WorldState.from_bytes(g["post"][0].tobytes())
+    assert (stats[:, 1] == 0).all()
+    assert (stats[:, 3] == ref.asleep.sum()).all()
+    got = WorldState.from_bytes(sim.get_state([3])[0])
+    np.testing.assert_allclose(got.pos, ref.pos, atol=1e-12)
+    sim.close()
