@@ -1,0 +1,375 @@
+"""Benchmark: batched env.step = 1/30 s physics (4 x 1/120 s substeps) +
+128x128 RGBD render of the head and arm cameras (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W --envs E] [--impl reference]
+
+Workload (BASELINE.json configs[4], one GPU's share): E envs per GPU
+(default 2048) of the synthetic ReplicaCAD-style apartment (layout
+global_env_id % 3), Fetch-like robot, 20 settled clutter objects, Idle
+scenario (robot spawned in the living room, random actions: arm joint
+targets around the resting pose, base linear U(-0.5, 1) m/s, angular
+U(-1, 1) rad/s).  Env shards are disjoint per rank; no collective on the
+step path (one NCCL all_reduce of episode stats and of the timing at the
+end).  Prints ONE JSON line on rank 0.
+
+--impl reference times the reference algorithm's CPU implementation (the C
+oracle restatement, tests-only infrastructure; the Python reference cannot
+travel to the GPU box) on all host cores: each step = one env-step
+(physics + 2 renders) on every core.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulation steps/sec (128x128 RGBD + 1/30s physics) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "env-steps/s"
+H = W = 128
+N_CAMS = 2
+PAPER_8GPU_SPS = 25734.0  # PAPER.md:530 (8x RTX 2080 Ti, Idle) -- different hardware, not this metric's config
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--envs", type=int, default=2048, help="envs per GPU")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-baseline-steps", type=int, default=2, help="env-steps per core in the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- workload
+
+def settled_pool():
+    g = np.load(os.path.join(ROOT, "tests", "golden", "settled_pool.npz"))
+    by_layout = {0: [], 1: [], 2: []}
+    for blob, (v, _seed) in zip(g["snapshots"], g["tags"]):
+        by_layout[int(v)].append(blob.tobytes())
+    return by_layout
+
+
+def idle_states(global_ids, pool):
+    """Idle scenario: settled clutter, robot at the living-room centre
+    (builtin.py:358) with a per-env heading."""
+    from paper_2106_14405_b200.state import WorldState
+
+    out = []
+    for gid in global_ids:
+        v = gid % 3
+        blobs = pool[v]
+        st = WorldState.from_bytes(blobs[(gid // 3) % len(blobs)])
+        rng = np.random.default_rng(1000 + gid)
+        st.base = np.array([2.3, -0.2, rng.uniform(-math.pi, math.pi)])
+        out.append(st.to_bytes())
+    return out
+
+
+def action_table(n_env, n_steps, seed):
+    """[n_steps, n_env, 7] arm joint targets and [n_steps, n_env, 2] base commands."""
+    rest = np.array([0.0, 0.5, 0.0, -2.2, 0.0, 1.3, 0.0])
+    rng = np.random.default_rng(seed)
+    arm = rest + rng.uniform(-0.3, 0.3, (n_steps, n_env, 7))
+    base = np.stack([rng.uniform(-0.5, 1.0, (n_steps, n_env)), rng.uniform(-1.0, 1.0, (n_steps, n_env))], axis=-1)
+    return arm, base
+
+
+# ------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    QUERY = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw"
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+        return False
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16), float(parts[3])))
+            except (ValueError, IndexError):
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                 0x100: "display_clock_setting"}
+        mask = 0
+        for r in rows:
+            mask |= r[2]
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": [n for b, n in names.items() if mask & b], "samples": len(rows),
+                "power_w_max": max(r[3] for r in rows)}
+
+
+# --------------------------------------------------------------- CPU oracle
+
+def _cpu_worker(args):
+    """One process: oracle env-steps (physics + 2 camera renders)."""
+    layout, snap, arm, base, n = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle.oracle import Oracle
+    from paper_2106_14405_b200.compiler import compile_world
+    from paper_2106_14405_b200.scene import build_world, flat_clutter
+
+    orc = Oracle(compile_world(build_world(layout, flat_clutter())))
+    t0 = time.perf_counter()
+    for k in range(n):
+        r = orc.step(snap, arm[k], base[k])
+        snap = r.snapshot
+        orc.render(snap, 0)
+        orc.render(snap, 1)
+    return n, time.perf_counter() - t0
+
+
+def cpu_oracle_sps(n_steps_per_core, cores=None, seed=0):
+    import multiprocessing as mp
+
+    from oracle import oracle as orc
+
+    orc.build()
+    cores = cores or os.cpu_count() or 1
+    pool_states = settled_pool()
+    states = idle_states(range(cores), pool_states)
+    arm, base = action_table(cores, n_steps_per_core, seed)
+    jobs = [(g % 3, states[g], arm[:, g], base[:, g], n_steps_per_core) for g in range(cores)]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as p:
+        p.map(_cpu_worker, [(j[0], j[1], j[2], j[3], 1) for j in jobs])  # warm (build + import)
+        t0 = time.perf_counter()
+        res = p.map(_cpu_worker, jobs)
+        wall = time.perf_counter() - t0
+    steps = sum(r[0] for r in res)
+    return steps / wall, cores, wall, steps
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# -------------------------------------------------------------------- arms
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    per_step = []
+    for k in range(args.warmup + args.steps):
+        sps, _, wall, steps = cpu_oracle_sps(1, cores, seed=k)
+        if k >= args.warmup:
+            per_step.append((wall, steps))
+    total_steps = sum(s for _, s in per_step)
+    total_wall = sum(w for w, _ in per_step)
+    value = total_steps / total_wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "idle env.step (physics 4x1/120 s + 2 cams 128x128 RGBD), one env-step per host core "
+                               "per step", "envs_per_step": cores, "layouts": "apt_{env%3}", "clutter": 20},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{total_steps} env-steps of the C oracle restatement ({cpu_model()})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import __graft_entry__ as ge
+
+    ge.build() if rank == 0 and world == 1 else None
+    from paper_2106_14405_b200 import native
+    from paper_2106_14405_b200.sim import BatchSimulator
+
+    E = args.envs
+    gids = np.arange(rank * E, (rank + 1) * E)
+    layout_of = gids % 3
+    sim = BatchSimulator(layouts=(0, 1, 2), n_env=E, env_layout=layout_of.tolist(), device=dev)
+    sim.set_state(idle_states(gids, settled_pool()))
+    n_tab = args.warmup + args.steps
+    arm_np, base_np = action_table(E, n_tab, seed=7 + rank)
+    arm_d = torch.tensor(arm_np, device=dev)
+    base_d = torch.tensor(base_np, device=dev)
+    obs = sim.alloc_obs(("head", "arm"))
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k, ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        sim.step_physics(arm_d[k], base_d[k])
+        if ev is not None:
+            ev[1].record(stream)
+        sim.render(("head", "arm"), out=obs)
+        if ev is not None:
+            ev[2].record(stream)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize(dev)
+    sim.raise_faults()
+
+    # ---- device-resident timed region (value)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k, evs[k])
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms_total = t_start.elapsed_time(t_end)
+    ms_phys = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    ms_rend = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    sim.raise_faults()
+
+    # ---- end-to-end through the C-ABI with host buffers (e2e)
+    h_arm = torch.tensor(arm_np).pin_memory()
+    h_base = torch.tensor(base_np).pin_memory()
+    h_stats = torch.empty((E, 4), dtype=torch.float64).pin_memory()
+    for k in range(2):
+        sim.step_host(h_arm[k], h_base[k], out=obs, h_stats=h_stats)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        sim.step_host(h_arm[args.warmup + k], h_base[args.warmup + k], out=obs, h_stats=h_stats)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_e2e = e0.elapsed_time(e1)
+    acc = float(h_stats[:, 0].sum())
+
+    # ---- across ranks: max time, summed stats (the only collectives)
+    t = torch.tensor([ms_total, ms_e2e, ms_phys, ms_rend], device=dev, dtype=torch.float64)
+    stats = torch.tensor([acc, float(E)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+    ms_total, ms_e2e, ms_phys, ms_rend = (float(x) for x in t.cpu())
+    total_envs = E * world
+    value = total_envs * args.steps / (ms_total * 1e-3)
+    e2e_value = total_envs * args.steps / (ms_e2e * 1e-3)
+
+    if rank == 0:
+        # roofline: dominant kernel against the measured FMA pipe peak
+        import ctypes as C
+
+        peak64, peak32 = C.c_double(0), C.c_double(0)
+        L = native.lib()
+        L.rsim_bench_fma_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+        L.rsim_bench_fma_peak(1, C.byref(peak64))
+        L.rsim_bench_fma_peak(0, C.byref(peak32))
+        render_flop = N_CAMS * H * W * (14 * 566 + 22 * 4)  # SURVEY.md §8d W_r (brute-force proxy raycast)
+        phys_flop = 0.09e6  # SURVEY.md §8d idle W_p per env-step
+        if ms_rend >= ms_phys:
+            dom, ms_dom, flop = "render_kernel", ms_rend, render_flop
+        else:
+            dom, ms_dom, flop = "step_kernel", ms_phys, phys_flop
+        achieved = flop * E / (ms_dom * 1e-3) / 1e12
+        obs_bytes = E * N_CAMS * H * W * (4 + 4 + 4)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (settled-clutter pool from the reference recipe, random idle actions)",
+            "config": {"workload": "configs[4] full step: physics 4x1/120 s + head+arm 128x128 RGBD, Idle",
+                       "envs_per_gpu": E, "global_envs": total_envs, "layouts": "apt_{env%3}", "clutter": 20,
+                       "parallelism": f"env-shard dp{world}",
+                       "l2": "inputs > L2: 805 MB of RGBD/id writes per step at 2048 envs evict the state slabs"},
+            "kernels_ms_per_step": {"step_kernel": ms_phys, "render_kernel": ms_rend},
+            "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak64.value,
+                         "unit": "TFLOP/s", "frac": achieved / peak64.value if peak64.value else None,
+                         "traffic": None,
+                         "peak_source": "measured FP64 FMA microbenchmark (rsim_bench_fma_peak); "
+                                        "MEASURED_PEAKS.json has no FP64/FP32 entry",
+                         "fp32_peak_tflops": peak32.value,
+                         "algorithmic_flop_per_unit": flop,
+                         "hbm_gbs_obs_writes": obs_bytes / (ms_rend * 1e-3) / 1e9},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(E * (7 + 2) * 8),
+                    "d2h_bytes_per_step": int(E * 4 * 8)},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.summary(),
+            "episode_stats_allreduce": {"accumulated_contact_force_sum": float(stats[0]), "envs": int(stats[1])},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            sps, cores, wall, steps = cpu_oracle_sps(args.cpu_baseline_steps)
+            line["cpu_baseline"] = {"value": sps, "unit": UNIT, "cores": cores, "kind": "port",
+                                    "sample": f"{steps} env-steps (physics + 2 renders) of the C oracle, "
+                                              f"{args.cpu_baseline_steps} per core, {wall:.1f} s wall, {cpu_model()}"}
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

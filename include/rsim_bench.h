@@ -1,0 +1,18 @@
+/*
+ * rsim_bench.h -- measurement helpers shipped in librsim.so (not part of the
+ * reference-facing ABI in rsim.h).
+ */
+#ifndef RSIM_BENCH_H
+#define RSIM_BENCH_H
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Sustained FMA throughput of the FP64 (fp64=1) or FP32 (fp64=0) pipe on the
+ * current device, in TFLOP/s (2 flops per FMA).  Returns 0 on success. */
+int rsim_bench_fma_peak(int fp64, double *tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -23,6 +23,7 @@ UNITS = {
     "physics.cu": ["-fmad=false"],
     "render.cu": [],
     "abi.cu": [],
+    "peak.cu": [],
 }
 HEADERS = ["device.cuh", "se3.cuh"]
 
@@ -40,6 +41,7 @@ def _stale() -> bool:
     t = os.path.getmtime(LIB)
     srcs = [os.path.join(CSRC, f) for f in list(UNITS) + HEADERS]
     srcs.append(os.path.join(HERE, "..", "include", "rsim.h"))
+    srcs.append(os.path.join(HERE, "..", "include", "rsim_bench.h"))
     srcs.append(__file__)
     return any(os.path.getmtime(s) > t for s in srcs)
 

@@ -173,19 +173,35 @@ def test_render_tiles_many_envs_consistently():
 
 
 def test_grasp_snap_and_release():
-    g = golden("traj_held.npz")
-    # the recorded pre-state of step 0 already holds an object: release it, re-snap
+    """grasp_rule + apply_grasp (robot.py:323-346, physics.py:1055-1079):
+    a clutter COM 0.10 m from the end effector snaps; holding ignores +1;
+    -1 releases and wakes the body."""
+    from paper_2106_14405_b200.geom import Pose
+    from paper_2106_14405_b200.state import ee_pose
+
+    g = golden("traj_idle.npz")
     st = WorldState.from_bytes(g["pre"][0].tobytes())
-    held = st.held
-    sim = BatchSimulator(layouts=(0,), n_env=1)
-    sim.set_state([st.to_bytes()])
-    sim.grasp(torch.tensor([-1.0]))
-    s1 = sim.world_state(0)
-    assert s1.held == -1 and not s1.asleep[held]
-    sim.grasp(torch.tensor([1.0]))
-    s2 = sim.world_state(0)
-    assert s2.held == held
-    np.testing.assert_allclose(s2.held_offset, st.held_offset, atol=1e-12)
+    world = build_world(0, flat_clutter())
+    ee = ee_pose(world, st)
+    obj = world.clutter_body_ids[3]
+    com_local = world.bodies[obj].com
+    target_com = ee.pos + np.array([0.0, 0.06, -0.08])  # 0.10 m away
+    p = st.body_pose(obj)
+    st.pos[obj] = target_com - p.rot @ com_local
+    sim = BatchSimulator(layouts=(0,), n_env=2)
+    far = WorldState.from_bytes(g["pre"][0].tobytes())  # nothing within 0.15 m
+    sim.set_state([st.to_bytes(), far.to_bytes()])
+    sim.grasp(torch.tensor([1.0, 1.0]))
+    s1, f1 = (WorldState.from_bytes(b) for b in sim.get_state())
+    assert s1.held == obj and s1.held_joint == -1 and not s1.asleep[obj]
+    assert f1.held == -1
+    rel = ee.inverse().compose(st.body_pose(obj))
+    np.testing.assert_allclose(s1.held_offset, np.concatenate([rel.pos, rel.quat()]), atol=1e-12)
+    sim.grasp(torch.tensor([1.0, 0.0]))
+    assert sim.world_state(0).held == obj
+    sim.grasp(torch.tensor([-1.0, -1.0]))
+    s3 = sim.world_state(0)
+    assert s3.held == -1 and not s3.asleep[obj]
     sim.close()
 
 
