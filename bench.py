@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--envs", type=int, default=2048, help="envs per GPU")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-baseline-steps", type=int, default=2, help="env-steps per core in the cpu_baseline sample")
+    ap.add_argument("--cpu-baseline-steps", type=int, default=24, help="env-steps per core in the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -140,43 +140,66 @@ class ClockSampler:
 
 # --------------------------------------------------------------- CPU oracle
 
-def _cpu_worker(args):
-    """One process: oracle env-steps (physics + 2 camera renders)."""
-    layout, snap, arm, base, n = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+_ORC = {}
+
+
+def _cpu_init():
+    os.environ["OMP_NUM_THREADS"] = "1"
     from oracle.oracle import Oracle
     from paper_2106_14405_b200.compiler import compile_world
     from paper_2106_14405_b200.scene import build_world, flat_clutter
 
-    orc = Oracle(compile_world(build_world(layout, flat_clutter())))
+    for v in range(3):
+        _ORC[v] = Oracle(compile_world(build_world(v, flat_clutter())))
+
+
+def _cpu_worker(args):
+    """Oracle env-steps (physics + 2 camera renders) in one worker process."""
+    layout, snap, arm, base, n = args
+    orc = _ORC[layout]
     t0 = time.perf_counter()
     for k in range(n):
-        r = orc.step(snap, arm[k], base[k])
-        snap = r.snapshot
+        snap = orc.step(snap, arm[k], base[k]).snapshot
         orc.render(snap, 0)
         orc.render(snap, 1)
-    return n, time.perf_counter() - t0
+    return n, time.perf_counter() - t0, snap
+
+
+class CpuOracle:
+    """One worker process per host core, each owning one env."""
+
+    def __init__(self, cores=None):
+        import multiprocessing as mp
+
+        from oracle import oracle as orc
+
+        orc.build()
+        self.cores = cores or os.cpu_count() or 1
+        self.states = idle_states(range(self.cores), settled_pool())
+        self.pool = mp.get_context("spawn").Pool(self.cores, initializer=_cpu_init)
+
+    def run(self, steps_per_core, seed):
+        arm, base = action_table(self.cores, steps_per_core, seed)
+        jobs = [(g % 3, self.states[g], arm[:, g], base[:, g], steps_per_core) for g in range(self.cores)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_worker, jobs)
+        wall = time.perf_counter() - t0
+        self.states = [r[2] for r in res]
+        return sum(r[0] for r in res), wall
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
 
 
 def cpu_oracle_sps(n_steps_per_core, cores=None, seed=0):
-    import multiprocessing as mp
-
-    from oracle import oracle as orc
-
-    orc.build()
-    cores = cores or os.cpu_count() or 1
-    pool_states = settled_pool()
-    states = idle_states(range(cores), pool_states)
-    arm, base = action_table(cores, n_steps_per_core, seed)
-    jobs = [(g % 3, states[g], arm[:, g], base[:, g], n_steps_per_core) for g in range(cores)]
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores) as p:
-        p.map(_cpu_worker, [(j[0], j[1], j[2], j[3], 1) for j in jobs])  # warm (build + import)
-        t0 = time.perf_counter()
-        res = p.map(_cpu_worker, jobs)
-        wall = time.perf_counter() - t0
-    steps = sum(r[0] for r in res)
-    return steps / wall, cores, wall, steps
+    c = CpuOracle(cores)
+    try:
+        c.run(1, seed + 1000)  # warm
+        steps, wall = c.run(n_steps_per_core, seed)
+    finally:
+        c.close()
+    return steps / wall, c.cores, wall, steps
 
 
 def cpu_model():
@@ -195,12 +218,14 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cores = os.cpu_count() or 1
+    c = CpuOracle()
+    cores = c.cores
     per_step = []
     for k in range(args.warmup + args.steps):
-        sps, _, wall, steps = cpu_oracle_sps(1, cores, seed=k)
+        steps, wall = c.run(1, seed=k)
         if k >= args.warmup:
             per_step.append((wall, steps))
+    c.close()
     total_steps = sum(s for _, s in per_step)
     total_wall = sum(w for w, _ in per_step)
     value = total_steps / total_wall
@@ -230,9 +255,6 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    import __graft_entry__ as ge
-
-    ge.build() if rank == 0 and world == 1 else None
     from paper_2106_14405_b200 import native
     from paper_2106_14405_b200.sim import BatchSimulator
 
@@ -292,12 +314,17 @@ def run_b200(args):
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host_ms = []
     e0.record(stream)
     for k in range(args.steps):
+        h0 = time.perf_counter()
         sim.step_host(h_arm[args.warmup + k], h_base[args.warmup + k], out=obs, h_stats=h_stats)
+        host_ms.append(1e3 * (time.perf_counter() - h0))
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms_e2e = e0.elapsed_time(e1)
+    if rank == 0:
+        print(f"[bench] e2e per-step host ms: {np.round(host_ms, 3).tolist()}", file=sys.stderr)
     acc = float(h_stats[:, 0].sum())
 
     # ---- across ranks: max time, summed stats (the only collectives)
@@ -321,6 +348,11 @@ def run_b200(args):
         L.rsim_bench_fma_peak(1, C.byref(peak64))
         L.rsim_bench_fma_peak(0, C.byref(peak32))
         render_flop = N_CAMS * H * W * (14 * 566 + 22 * 4)  # SURVEY.md §8d W_r (brute-force proxy raycast)
+        L.rsim_bench_render_work.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p]
+        ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+        L.rsim_bench_render_work(sim._batch, 3, C.c_void_p(ctr.data_ptr()), C.c_void_p(stream.cuda_stream))
+        torch.cuda.synchronize(dev)
+        executed_tests = float(ctr.item()) / E  # ray-plane (+ sphere) tests per env-step actually executed
         phys_flop = 0.09e6  # SURVEY.md §8d idle W_p per env-step
         if ms_rend >= ms_phys:
             dom, ms_dom, flop = "render_kernel", ms_rend, render_flop
@@ -345,6 +377,11 @@ def run_b200(args):
                                         "MEASURED_PEAKS.json has no FP64/FP32 entry",
                          "fp32_peak_tflops": peak32.value,
                          "algorithmic_flop_per_unit": flop,
+                         "executed_flop_per_unit": 14.0 * executed_tests if dom == "render_kernel" else None,
+                         "executed_achieved": (14.0 * executed_tests * E / (ms_dom * 1e-3) / 1e12)
+                         if dom == "render_kernel" else None,
+                         "executed_frac": (14.0 * executed_tests * E / (ms_dom * 1e-3) / 1e12 / peak64.value)
+                         if dom == "render_kernel" and peak64.value else None,
                          "hbm_gbs_obs_writes": obs_bytes / (ms_rend * 1e-3) / 1e9},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(E * (7 + 2) * 8),
                     "d2h_bytes_per_step": int(E * 4 * 8)},

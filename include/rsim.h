@@ -123,8 +123,7 @@ typedef struct {
   uint32_t *fault;        /* [n_env] */
   int32_t *event_count;   /* [n_env] events of the last rs_step (may exceed cap: overflow) */
   double *events;         /* [n_env][event_cap][7]: a, b, impulse, force, point xyz */
-  int64_t *counters;      /* [n_env][3] narrowphase_tests, skipped_sleeping_pairs, wakes (cumulative) */
-  double *acc_force;      /* [n_env] accumulated_contact_force (alias into the state) */
+  int64_t *counters;      /* [n_env][3] narrowphase_tests, skipped_sleeping_pairs, wakes (since rs_set_state) */
 } rs_buffers;
 
 typedef struct rs_scene rs_scene;
@@ -151,7 +150,10 @@ int rs_set_state(rs_batch *batch, const uint8_t *snapshots, int64_t stride, cons
 int rs_get_state(rs_batch *batch, uint8_t *snapshots, int64_t stride, const int32_t *env_ids,
                  int32_t n, void *stream);
 
-/* one control step for every env (device pointers):
+/* one control step for every env (device pointers).  The batch keeps two
+ * state buffers: rs_step reads s_t and writes s_{t+1} into the other one, so
+ * an rs_render of s_t enqueued BEFORE rs_step (on another stream) may run
+ * concurrently with it (interleaved physics || render).
  *   arm_targets [n_env][n_arm] f64 joint targets (JointTargets.arm)
  *   base_cmd    [n_env][2] f64 linear, angular velocity (BaseAction)
  *   has_targets [n_env] u8, 0 = targets None (settle mode); NULL = all 1 */

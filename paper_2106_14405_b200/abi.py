@@ -61,7 +61,7 @@ class rs_render_config(C.Structure):
 class rs_buffers(C.Structure):
     _fields_ = [("n_env", C.c_int32), ("n_bodies", C.c_int32), ("n_joints", C.c_int32), ("event_cap", C.c_int32),
                 ("fault", C.c_void_p), ("event_count", C.c_void_p), ("events", C.c_void_p),
-                ("counters", C.c_void_p), ("acc_force", C.c_void_p)]
+                ("counters", C.c_void_p)]
 
 
 def _ptr(a: np.ndarray, ctype):

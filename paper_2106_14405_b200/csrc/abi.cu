@@ -9,13 +9,14 @@
 #include <vector>
 
 #include "../../include/rsim.h"
+#include "../../include/rsim_bench.h"
 #include "device.cuh"
 
 namespace rsim {
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, const uint8_t *has_targets,
                         double dt, int substeps, cudaStream_t stream);
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
-                          cudaStream_t stream);
+                          cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_grasp(const DevBatch &B, const double *gripper, cudaStream_t stream);
 cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream);
 size_t step_scratch_doubles_per_env(int row_cap);
@@ -47,6 +48,16 @@ struct rs_batch {
   int32_t *d_env_scene = nullptr;
   std::vector<void *> allocs;
   int narm = 0;
+  // ping-pong state buffers: rs_step reads buf[cur] and writes buf[cur ^ 1]
+  double *sd_buf[2] = {nullptr, nullptr};
+  int32_t *si_buf[2] = {nullptr, nullptr};
+  int cur = 0;
+  DevBatch view() const {
+    DevBatch v = d;
+    v.sd = sd_buf[cur]; v.si = si_buf[cur];
+    v.sd_out = sd_buf[cur ^ 1]; v.si_out = si_buf[cur ^ 1];
+    return v;
+  }
   // lazily allocated staging for rs_step_host
   double *h_pin = nullptr, *d_act = nullptr, *d_stats = nullptr;
 };
@@ -182,6 +193,8 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   }
   BA(sd, sizeof(double) * d.L.dbl_size * (size_t)n_env);
   BA(si, sizeof(int32_t) * d.L.int_size * (size_t)n_env);
+  BA(sd_out, sizeof(double) * d.L.dbl_size * (size_t)n_env);
+  BA(si_out, sizeof(int32_t) * d.L.int_size * (size_t)n_env);
   BA(step_index, sizeof(int64_t) * n_env);
   BA(fault, sizeof(uint32_t) * n_env);
   BA(event_count, sizeof(int32_t) * n_env);
@@ -207,6 +220,8 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   }
   d.scenes = b->d_scenes;
   d.env_scene = b->d_env_scene;
+  b->sd_buf[0] = d.sd; b->sd_buf[1] = d.sd_out;
+  b->si_buf[0] = d.si; b->si_buf[1] = d.si_out;
   *out = b;
   return RS_OK;
 }
@@ -224,7 +239,6 @@ int rs_batch_buffers(rs_batch *b, rs_buffers *o) {
   if (!b || !o) return fail(RS_ERR_ARG, "null argument");
   o->n_env = b->d.n_env; o->n_bodies = b->d.nb; o->n_joints = b->d.nj; o->event_cap = b->d.event_cap;
   o->fault = b->d.fault; o->event_count = b->d.event_count; o->events = b->d.events; o->counters = b->d.counters;
-  o->acc_force = b->d.sd + b->d.L.acc;  // stride = L.dbl_size doubles
   return RS_OK;
 }
 
@@ -276,7 +290,7 @@ static void pack_snapshot(const StateLayout &L, const double *sd, const int32_t 
 
 int rs_set_state(rs_batch *b, const uint8_t *snaps, int64_t stride, const int32_t *env_ids, int32_t n, void *stream) {
   if (!b || !snaps || n < 0) return fail(RS_ERR_ARG, "null argument");
-  const DevBatch &d = b->d;
+  const DevBatch d = b->view();
   const StateLayout &L = d.L;
   if (stride <= 0) stride = rs_snapshot_size(L.nb, L.nj);
   cudaStream_t st = (cudaStream_t)stream;
@@ -322,7 +336,7 @@ int rs_set_state(rs_batch *b, const uint8_t *snaps, int64_t stride, const int32_
 
 int rs_get_state(rs_batch *b, uint8_t *snaps, int64_t stride, const int32_t *env_ids, int32_t n, void *stream) {
   if (!b || !snaps || n < 0) return fail(RS_ERR_ARG, "null argument");
-  const DevBatch &d = b->d;
+  const DevBatch d = b->view();
   const StateLayout &L = d.L;
   if (stride <= 0) stride = rs_snapshot_size(L.nb, L.nj);
   cudaStream_t st = (cudaStream_t)stream;
@@ -350,20 +364,21 @@ int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
   if (!arm || !base_cmd) return fail(RS_ERR_ARG, "arm_targets and base_cmd are required device pointers");
-  CUDA_TRY(launch_step(b->d, arm, base_cmd, has_targets, dt, substeps, (cudaStream_t)stream));
+  CUDA_TRY(launch_step(b->view(), arm, base_cmd, has_targets, dt, substeps, (cudaStream_t)stream));
+  b->cur ^= 1;
   return RS_OK;
 }
 
 int rs_render(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream) {
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (cam_mask >> 2) return fail(RS_ERR_ARG, "camera mask selects a camera the robot does not have");
-  CUDA_TRY(launch_render(b->d, cam_mask, rgba, depth, ids, (cudaStream_t)stream));
+  CUDA_TRY(launch_render(b->view(), cam_mask, rgba, depth, ids, (cudaStream_t)stream));
   return RS_OK;
 }
 
 int rs_grasp(rs_batch *b, const double *gripper, void *stream) {
   if (!b || !gripper) return fail(RS_ERR_ARG, "null argument");
-  CUDA_TRY(launch_grasp(b->d, gripper, (cudaStream_t)stream));
+  CUDA_TRY(launch_grasp(b->view(), gripper, (cudaStream_t)stream));
   return RS_OK;
 }
 
@@ -395,9 +410,15 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
     rc = rs_render(b, cam_mask, rgba, depth, ids, stream);
     if (rc) return rc;
   }
-  CUDA_TRY(launch_stats(b->d, b->d_stats, st));
+  CUDA_TRY(launch_stats(b->view(), b->d_stats, st));
   CUDA_TRY(cudaMemcpyAsync(h_out_stats, b->d_stats, sizeof(double) * (size_t)E * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return RS_OK;
 }
 
+
+int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
+  if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");
+  CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
+  return RS_OK;
+}

@@ -87,8 +87,10 @@ struct StateLayout {
 struct DevBatch {
   int n_env, nb, nj;
   StateLayout L;
-  double *sd;          // [E][L.dbl_size]
+  double *sd;          // [E][L.dbl_size]  current state s_t (read)
   int32_t *si;         // [E][L.int_size]
+  double *sd_out;      // successor s_{t+1} written by the step kernel (ping-pong buffer)
+  int32_t *si_out;
   int64_t *step_index; // [E]
   const DevScene *scenes;  // device array
   const int32_t *env_scene;

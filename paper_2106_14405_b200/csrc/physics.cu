@@ -1231,6 +1231,17 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
   return true;
 }
 
+// a faulted env keeps its input state (the reference raises before mutating)
+__device__ void copy_through(const DevBatch &B, int env, int lane) {
+  const StateLayout &L = B.L;
+  const double *a = B.sd + (size_t)env * L.dbl_size;
+  double *b = B.sd_out + (size_t)env * L.dbl_size;
+  for (int i = lane; i < L.dbl_size; i += 32) b[i] = a[i];
+  const int32_t *x = B.si + (size_t)env * L.int_size;
+  int32_t *y = B.si_out + (size_t)env * L.int_size;
+  for (int i = lane; i < L.int_size; i += 32) y[i] = x[i];
+}
+
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, const double *arm_targets,
                                                                    const double *base_cmd, const uint8_t *has_targets,
                                                                    double dt, int substeps) {
@@ -1281,6 +1292,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, c
     }
     if (f) {
       if (lane == 0) B.fault[env] = f;
+      copy_through(B, env, lane);
       return;
     }
   }
@@ -1294,6 +1306,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, c
   for (int s = 0; s < substeps && ok; ++s) ok = substep(c, arm, bc, dts, s);
   if (!ok) {
     if (lane == 0) B.fault[env] = (uint32_t)RS_FAULT_OVERFLOW << 16;
+    copy_through(B, env, lane);
     return;
   }
   if (lane == 0) {
@@ -1303,8 +1316,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, c
     for (int i = 0; i < 3; ++i) B.counters[3 * env + i] += S.ctr[i];
   }
   __syncwarp();
-  double *wsd = B.sd + (size_t)env * L.dbl_size;
-  int32_t *wsi = B.si + (size_t)env * L.int_size;
+  double *wsd = B.sd_out + (size_t)env * L.dbl_size;
+  int32_t *wsi = B.si_out + (size_t)env * L.int_size;
   for (int i = lane; i < L.dbl_size; i += 32) wsd[i] = S.sd[i];
   for (int i = lane; i < L.int_size; i += 32) wsi[i] = S.si[i];
 }

@@ -8,22 +8,27 @@
 //
 // One CTA renders one (env, camera) image:
 //   1. stage: body poses from the env's state slab -> world part frames ->
-//      world facet planes (n, b0 = d - n.o) in shared memory (~25 KB);
-//   2. cull: per 16x16-pixel tile, a bitmask of parts whose bounding sphere
-//      meets the tile frustum; per part a range lower bound |c - o| - r;
-//   3. trace: each warp walks its tiles; per pixel it visits only the tile's
-//      candidate parts in body-id order, skipping parts whose lower bound
-//      exceeds the running t_min + tie_eps, and tracks (t_min, id, t_2nd);
-//      near-ties (t_2nd - t_min <= tie_eps) take an exact slow path;
-//   4. write rgba (u32), depth (f32), id (i32) rows, coalesced per warp.
-// Float64 arithmetic throughout (parity with the float64 oracle); the
-// plane arg-max/arg-min uses division-free cross-multiplied compares and
-// only the two winning planes are divided.
+//      world facet planes (n, b0 = d - n.o) in shared memory (~25 KB); per
+//      part a range lower bound lb = |c - o| - r from its bounding sphere;
+//   2. cull: per 16x16-pixel tile, the parts whose bounding sphere meets the
+//      tile frustum, listed in ascending lb (one sort per image);
+//   3. trace: per pixel, walk the tile list front to back; stop as soon as
+//      lb > t_min + tie_eps (every later part is farther: the early-out is
+//      exact), tracking (t_min, id) and the best other body (t_2nd); a
+//      near-tie (t_2nd - t_min <= tie_eps) re-resolves the pixel with the
+//      exact lowest-id rule in body order;
+//   4. write rgba (u32), depth (f32), id (i32), 16 consecutive pixels per
+//      half-warp.
+// Float64 arithmetic throughout (parity with the float64 oracle); boxes use
+// their 3 face normals (the -x/-y/-z planes are exact negations), and the
+// plane arg-max/arg-min uses division-free cross-multiplied compares so only
+// the two winning planes are divided.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
 
+#include "../../include/rsim_bench.h"
 #include "device.cuh"
 #include "se3.cuh"
 
@@ -32,39 +37,52 @@ namespace rsim {
 constexpr int kTile = 16;
 constexpr int kMaxParts = 128;
 constexpr int kMaskWords = kMaxParts / 32;
+constexpr int kMaxTiles = (128 / kTile) * (128 / kTile);
 constexpr int kRenderThreads = 256;
 constexpr double kParallelEps = 1e-12;  // geometry.py:731
 
 struct PartW {
-  double c[3];   // world part origin (sphere centre)
-  double r;      // bounding radius / sphere radius
-  double lb;     // lower bound of any hit range from the camera origin
+  double c[3];  // world part origin (sphere centre)
+  double r;     // bounding radius / sphere radius
+  double lb;    // lower bound of any hit range from the camera origin
   int f0, nf, kind, body;
 };
 
 struct RenderSmem {
   double plane[4 * 1024];  // n.xyz, b0 per facet (world)
   PartW part[kMaxParts];
-  uint32_t mask[(128 / kTile) * (128 / kTile)][kMaskWords];
+  uint32_t mask[kMaxTiles][kMaskWords];
+  uint8_t list[kMaxTiles][kMaxParts];  // per tile: candidate parts in ascending lb
+  int nlist[kMaxTiles];
+  uint8_t order[kMaxParts];
   Pose cam;
 };
 
-// ray vs one convex: reference _ray_halfspaces, one ray
+// ray vs one convex (reference _ray_halfspaces, one ray); face = entering plane
+template <bool kBox>
 __device__ __forceinline__ double ray_convex(const double *pl, int nf, const double *d, int &face) {
-  int fe = -1, fx = -1, bad = 0;
+  int fe = -1, fx = -1;
+  bool bad = false;
   double se = 0, be = 0, sx = 0, bx = 0;
-  for (int f = 0; f < nf; ++f) {
+  double sb[3];
+  if (kBox) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) sb[k] = d[0] * pl[4 * k] + d[1] * pl[4 * k + 1] + d[2] * pl[4 * k + 2];
+  }
+  const int n = kBox ? 6 : nf;
+#pragma unroll 6
+  for (int f = 0; f < n; ++f) {
     const double *P = pl + 4 * f;
-    double s = d[0] * P[0] + d[1] * P[1] + d[2] * P[2];
+    double s = kBox ? (f < 3 ? sb[f] : -sb[f - 3]) : d[0] * P[0] + d[1] * P[1] + d[2] * P[2];
     double b = P[3];
     if (s < -kParallelEps) {
-      // ratio b/s > be/se  (s, se < 0)  <=>  b*se > be*s
+      // b/s > be/se with s, se < 0  <=>  b*se > be*s
       if (fe < 0 || b * se > be * s) { fe = f; se = s; be = b; }
     } else if (s > kParallelEps) {
-      // ratio b/s < bx/sx  (s, sx > 0)  <=>  b*sx < bx*s
+      // b/s < bx/sx with s, sx > 0  <=>  b*sx < bx*s
       if (fx < 0 || b * sx < bx * s) { fx = f; sx = s; bx = b; }
     } else if (b < 0) {
-      bad = 1;
+      bad = true;
     }
   }
   double te = fe >= 0 ? be / se : -INFINITY;
@@ -75,7 +93,7 @@ __device__ __forceinline__ double ray_convex(const double *pl, int nf, const dou
   return 0.0;
 }
 
-// reference _ray_sphere, one ray (oc = o - c precomputed per part)
+// reference _ray_sphere, one ray
 __device__ __forceinline__ double ray_sphere(const PartW &p, const double *o, const double *d) {
   double oc[3] = {o[0] - p.c[0], o[1] - p.c[1], o[2] - p.c[2]};
   double b = oc[0] * d[0] + oc[1] * d[1] + oc[2] * d[2];
@@ -88,16 +106,20 @@ __device__ __forceinline__ double ray_sphere(const PartW &p, const double *o, co
 
 __device__ __forceinline__ double part_hit(const RenderSmem &S, int p, const double *o, const double *d, int &face) {
   const PartW &P = S.part[p];
+  double t;
   if (P.kind == RS_SPHERE) {
     face = -1;
     return ray_sphere(P, o, d);
+  } else if (P.kind == RS_BOX) {
+    t = ray_convex<true>(S.plane + 4 * P.f0, 6, d, face);
+  } else {
+    t = ray_convex<false>(S.plane + 4 * P.f0, P.nf, d, face);
   }
-  double t = ray_convex(S.plane + 4 * P.f0, P.nf, d, face);
   if (face >= 0) face += P.f0;
   return t;
 }
 
-// exact lowest-id rule for near-tie pixels
+// exact lowest-id rule for near-tie pixels: bodies in id order, parts in order
 __device__ __noinline__ void resolve_tie(const RenderSmem &S, const uint32_t *mask, const double *o, const double *d,
                                          double tmin, double eps, int &id, int &wpart, int &wface) {
   int cur_b = -1, cur_p = -1, cur_f = -1;
@@ -110,7 +132,8 @@ __device__ __noinline__ void resolve_tie(const RenderSmem &S, const uint32_t *ma
       int b = S.part[p].body;
       if (b != cur_b) {
         if (cur_b >= 0 && cur_t <= tmin + eps) { id = cur_b; wpart = cur_p; wface = cur_f; return; }
-        cur_b = b; cur_t = INFINITY;
+        cur_b = b;
+        cur_t = INFINITY;
       }
       int f;
       double t = part_hit(S, p, o, d, f);
@@ -121,17 +144,21 @@ __device__ __noinline__ void resolve_tie(const RenderSmem &S, const uint32_t *ma
 }
 
 __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out,
-                                                                uint32_t *rgba, float *depth, int32_t *ids) {
+                                                                uint32_t *rgba, float *depth, int32_t *ids,
+                                                                unsigned long long *work) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RenderSmem &S = *reinterpret_cast<RenderSmem *>(smem_raw);
   const int env = blockIdx.x / n_cam_out, slot = blockIdx.x % n_cam_out;
   int cam = -1;
   for (int c = 0, k = 0; c < 32; ++c)
-    if (cam_mask & (1u << c)) { if (k == slot) { cam = c; break; } ++k; }
+    if (cam_mask & (1u << c)) {
+      if (k == slot) { cam = c; break; }
+      ++k;
+    }
   const DevScene &sc = B.scenes[B.env_scene[env]];
   const StateLayout &L = B.L;
   const double *sd = B.sd + (size_t)env * L.dbl_size;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, np = sc.np;
 
   // -- camera pose (robot.py:43-47 mounts; tools_make_robot_json.py:12-19 axes)
   if (tid == 0) {
@@ -158,8 +185,8 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
   __syncthreads();
   const double *o = S.cam.p;
 
-  // -- world part frames + bounds
-  for (int p = tid; p < sc.np; p += blockDim.x) {
+  // -- world part frames, bounds, world planes (geometry.py:554-557), b0 = d - n.o
+  for (int p = tid; p < np; p += blockDim.x) {
     int b = sc.part_body[p];
     Pose bp, lp, wp;
     quat_to_mat(sd + L.quat + 4 * b, bp.R);
@@ -172,11 +199,10 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
     P.body = b;
     P.f0 = sc.part_facet_begin[p];
     P.nf = sc.part_facet_begin[p + 1] - P.f0;
-    P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : (double)sc.part_bound[p];
+    P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : sc.part_bound[p];
     double v[3] = {wp.p[0] - o[0], wp.p[1] - o[1], wp.p[2] - o[2]};
     double dist = sqrt(dot3(v, v)) - P.r * (1.0 + 1e-9) - 1e-9;
     P.lb = dist > 0.0 ? dist : 0.0;
-    // world planes of this part (geometry.py:554-557), then b0 = d - n.o
     for (int f = P.f0; f < P.f0 + P.nf; ++f) {
       const double *F = sc.facet + 4 * f;
       double n[3];
@@ -187,16 +213,25 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
       Q[3] = dw - dot3(o, n);
     }
   }
-  __syncthreads();
-
-  // -- tile culling: sphere vs the 4 side planes of the tile frustum (camera frame)
   const int W = B.rcfg.width, H = B.rcfg.height;
   const int tx_n = W / kTile, ty_n = H / kTile, ntiles = tx_n * ty_n;
-  const double f = (W / 2.0) / tan(B.rcfg.fov / 2.0);
   for (int i = tid; i < ntiles * kMaskWords; i += blockDim.x) S.mask[i / kMaskWords][i % kMaskWords] = 0u;
   __syncthreads();
-  for (int i = tid; i < ntiles * sc.np; i += blockDim.x) {
-    int tile = i / sc.np, p = i % sc.np;
+
+  // -- front-to-back order of parts (rank by (lb, index))
+  for (int p = tid; p < np; p += blockDim.x) {
+    const double lb = S.part[p].lb;
+    int rank = 0;
+    for (int q = 0; q < np; ++q) {
+      double lq = S.part[q].lb;
+      rank += (lq < lb) || (lq == lb && q < p);
+    }
+    S.order[rank] = (uint8_t)p;
+  }
+  // -- tile culling: sphere vs the 4 side planes of the tile frustum (camera frame)
+  const double f = (W / 2.0) / tan(B.rcfg.fov / 2.0);
+  for (int i = tid; i < ntiles * np; i += blockDim.x) {
+    int tile = i / np, p = i % np;
     const PartW &P = S.part[p];
     double v[3] = {P.c[0] - o[0], P.c[1] - o[1], P.c[2] - o[2]}, c[3];
     mattvec(S.cam.R, v, c);  // camera frame: x right, y down, z view
@@ -205,7 +240,6 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
     if (in) {
       double u0 = ((tile % tx_n) * kTile - W / 2.0) / f, u1 = ((tile % tx_n) * kTile + kTile - W / 2.0) / f;
       double v0 = ((tile / tx_n) * kTile - H / 2.0) / f, v1 = ((tile / tx_n) * kTile + kTile - H / 2.0) / f;
-      // plane x - u z >= 0 (left), -x + u1 z >= 0 (right), same in y; signed distances
       double nl = sqrt(1.0 + u0 * u0), nr = sqrt(1.0 + u1 * u1), nt = sqrt(1.0 + v0 * v0), nbm = sqrt(1.0 + v1 * v1);
       in = (c[0] - u0 * c[2]) / nl >= -r && (-c[0] + u1 * c[2]) / nr >= -r && (c[1] - v0 * c[2]) / nt >= -r &&
            (-c[1] + v1 * c[2]) / nbm >= -r;
@@ -213,13 +247,29 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
     if (in) atomicOr(&S.mask[tile][p >> 5], 1u << (p & 31));
   }
   __syncthreads();
+  // -- per tile candidate lists in front-to-back order (warp per tile, ballot compaction)
+  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  for (int tile = warp; tile < ntiles; tile += nwarps) {
+    int n = 0;
+    for (int i0 = 0; i0 < np; i0 += 32) {
+      int i = i0 + lane;
+      int p = i < np ? S.order[i] : 0;
+      bool in = i < np && ((S.mask[tile][p >> 5] >> (p & 31)) & 1u);
+      unsigned m = __ballot_sync(0xffffffffu, in);
+      if (in) S.list[tile][n + __popc(m & ((1u << lane) - 1))] = (uint8_t)p;
+      n += __popc(m);
+    }
+    if (lane == 0) S.nlist[tile] = n;
+  }
+  __syncthreads();
 
   // -- trace
-  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   const double eps = B.rcfg.tie_eps, zfar = B.rcfg.zfar, znear = B.rcfg.znear;
   const size_t img = (size_t)(env * n_cam_out + slot) * H * W;
+  unsigned long long tests = 0;
   for (int tile = warp; tile < ntiles; tile += nwarps) {
-    const uint32_t *mask = S.mask[tile];
+    const uint8_t *list = S.list[tile];
+    const int nl = S.nlist[tile];
     const int ux = (tile % tx_n) * kTile, vy = (tile / tx_n) * kTile;
     for (int k = lane; k < kTile * kTile; k += 32) {
       const int u = ux + (k % kTile), v = vy + (k / kTile);
@@ -228,28 +278,27 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
       dc[0] /= l; dc[1] /= l; dc[2] /= l;
       double d[3];
       matvec(S.cam.R, dc, d);
-      double tmin = INFINITY, t2 = INFINITY, cur_t = INFINITY;
-      int id = -1, wpart = -1, wface = -1, cur_b = -1, cur_p = -1, cur_f = -1;
-      for (int w = 0; w < kMaskWords; ++w) {
-        uint32_t m = mask[w];
-        while (m) {
-          int p = w * 32 + __ffs(m) - 1;
-          m &= m - 1;
-          const int b = S.part[p].body;
-          if (b != cur_b) {
-            if (cur_t < tmin) { t2 = tmin; tmin = cur_t; id = cur_b; wpart = cur_p; wface = cur_f; }
-            else if (cur_t < t2) t2 = cur_t;
-            cur_b = b; cur_t = INFINITY;
-          }
-          if (S.part[p].lb > tmin + eps) continue;
-          int fc;
-          double t = part_hit(S, p, o, d, fc);
-          if (t < cur_t) { cur_t = t; cur_p = p; cur_f = fc; }
+      double tmin = INFINITY, t2 = INFINITY;
+      int id = -1, wpart = -1, wface = -1;
+      for (int j = 0; j < nl; ++j) {
+        const int p = list[j];
+        const PartW &P = S.part[p];
+        if (P.lb > tmin + eps) break;  // sorted: nothing later can be nearer or tie
+        int fc;
+        const double t = part_hit(S, p, o, d, fc);
+        if (work) tests += P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf);
+        if (!(t < INFINITY)) continue;
+        const int b = P.body;
+        if (b == id) {
+          if (t < tmin || (t == tmin && p < wpart)) { tmin = t; wpart = p; wface = fc; }
+        } else if (t < tmin) {
+          t2 = tmin;
+          tmin = t; id = b; wpart = p; wface = fc;
+        } else if (t < t2) {
+          t2 = t;
         }
       }
-      if (cur_t < tmin) { t2 = tmin; tmin = cur_t; id = cur_b; wpart = cur_p; wface = cur_f; }
-      else if (cur_t < t2) t2 = cur_t;
-      if (isfinite(tmin) && t2 - tmin <= eps) resolve_tie(S, mask, o, d, tmin, eps, id, wpart, wface);
+      if (tmin < INFINITY && t2 - tmin <= eps) resolve_tie(S, S.mask[tile], o, d, tmin, eps, id, wpart, wface);
 
       const size_t px = img + (size_t)v * W + u;
       if (!(tmin <= zfar)) {
@@ -270,7 +319,8 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
             cosv = -dot3(n, d);
           }
         } else if (wface >= 0) {
-          cosv = -dot3(S.plane + 4 * wface, d);
+          const double *Q = S.plane + 4 * wface;
+          cosv = -(d[0] * Q[0] + d[1] * Q[1] + d[2] * Q[2]);
         }
         float shade = __fadd_rn(0.3f, __fmul_rn(0.7f, (float)(cosv > 0.0 ? cosv : 0.0)));
         const float *col = sc.color + 3 * id;
@@ -283,12 +333,13 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
       }
     }
   }
+  if (work) atomicAdd(work, tests);
 }
 
 size_t render_smem_bytes() { return sizeof(RenderSmem); }
 
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, unsigned long long *work) {
   int n_cam_out = __builtin_popcount(cam_mask);
   if (n_cam_out == 0) return cudaSuccess;
   static bool configured = false;
@@ -300,7 +351,7 @@ cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, f
   }
   dim3 grid(B.n_env * n_cam_out);
   render_kernel<<<grid, kRenderThreads, smem, stream>>>(B, cam_mask, n_cam_out, reinterpret_cast<uint32_t *>(rgba),
-                                                        depth, ids);
+                                                        depth, ids, work);
   return cudaGetLastError();
 }
 
