@@ -51,7 +51,15 @@ enum {
   RA = 35, RB = 36, RPT = 37, RDEPTH = 40, RGRP = 41
 };
 // ---- pair (group) field offsets --------------------------------------------
-enum { PIA = 0, PIB = 9, PCA = 18, PCB = 21, PIMA = 24, PIMB = 25, PMU = 26, PE = 27, PKOFF = 28, PHASK = 29 };
+enum { PIA = 0, PIB = 9, PCA = 18, PCB = 21, PIMA = 24, PIMB = 25, PMU = 26, PE = 27, PKOFF = 28, PHASK = 29, PMASK = 30 };
+
+// block workspace in shared memory (per warp), m <= kMaxBlockRows
+struct BlockWS {
+  double cur[kMaxBlockRows], q[kMaxBlockRows], lam[kMaxBlockRows], wv[kMaxBlockRows], rhs[kMaxBlockRows],
+      sol[kMaxBlockRows], ck[kMaxBlockRows];
+  int active[kMaxBlockRows];
+  int na, worst, converged;
+};
 
 struct WarpSmem {
   double sd[1024];
@@ -73,6 +81,7 @@ struct WarpSmem {
   unsigned long long awake_dyn;
   int moved_mask;
   int64_t ctr[3];
+  BlockWS ws;
 };
 
 struct Ctx {
@@ -82,7 +91,10 @@ struct Ctx {
   WarpSmem *S;
   double *rows;   // [row_cap][kRowD]
   double *pairs;  // [kMaxGroups][kPairD]
-  double *K;      // [kKCap]
+  double *K;      // [kKCap] block matrices
+  double *Vc;     // [kKCap] cached eigenvectors per block
+  double *evc;    // [kMaxContacts] cached eigenvalues per block
+  double *W;      // [kMaxBlockRows^2] eigensolver workspace
   int env, lane;
   const StateLayout *L;
 };
@@ -582,10 +594,25 @@ __device__ void row_solve(Ctx &c, double *r) {
   row_friction(c, r);
 }
 
-// cyclic Jacobi eigen-decomposition (same sweep order / stopping rule as the oracle)
-__device__ void sym_eig(int m, double *A, double *V, double *ev) {
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < m; ++j) V[i * m + j] = (i == j);
+// ---------------------------------------------------------------------------
+// Block LCP (physics.py:760-816), warp-cooperative.
+//
+// The reference solves each active sub-block with np.linalg.lstsq(rcond=1e-8)
+// (min-norm); for the symmetric PSD K the same solution comes from a
+// Jacobi eigendecomposition with the gelsd cutoff s <= rcond * s_max.  The
+// oracle runs a serial cyclic Jacobi; here every rotation is still applied
+// in the same (p, q) order, but the row / column / eigenvector updates of a
+// rotation are spread over the lanes (one element per lane), and every
+// reduction keeps the oracle's summation order -- the results are
+// bit-identical to the serial code.  K is fixed for the whole substep, so
+// the decomposition of K[A, A] is cached per block and active set A: across
+// the 16 Gauss-Seidel sweeps the active set repeats and the eigensolve runs
+// once per distinct set.
+
+// A (m x m, row-major, destroyed) -> V (eigenvectors in columns), ev. warp-collective.
+__device__ void sym_eig_warp(int m, double *A, double *V, double *ev, int lane) {
+  for (int e = lane; e < m * m; e += 32) V[e] = (e / m == e % m);
+  __syncwarp();
   for (int sweep = 0; sweep < 64; ++sweep) {
     double off = 0.0, tot = 0.0;
     for (int i = 0; i < m; ++i)
@@ -597,122 +624,168 @@ __device__ void sym_eig(int m, double *A, double *V, double *ev) {
     if (off <= 1e-32 * tot || off == 0.0) break;
     for (int p = 0; p < m - 1; ++p)
       for (int q = p + 1; q < m; ++q) {
-        double apq = A[p * m + q];
+        const double apq = A[p * m + q];
         if (apq == 0.0) continue;
-        double app = A[p * m + p], aqq = A[q * m + q];
-        double theta = (aqq - app) / (2.0 * apq);
-        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        double cs = 1.0 / sqrt(t * t + 1.0), s = t * cs;
-        for (int k = 0; k < m; ++k) {
+        const double app = A[p * m + p], aqq = A[q * m + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+        __syncwarp();
+        if (lane < m) {
+          const int k = lane;
           double akp = A[k * m + p], akq = A[k * m + q];
-          A[k * m + p] = cs * akp - s * akq;
-          A[k * m + q] = s * akp + cs * akq;
-        }
-        for (int k = 0; k < m; ++k) {
-          double apk = A[p * m + k], aqk = A[q * m + k];
-          A[p * m + k] = cs * apk - s * aqk;
-          A[q * m + k] = s * apk + cs * aqk;
-        }
-        for (int k = 0; k < m; ++k) {
+          A[k * m + p] = cs * akp - sn * akq;
+          A[k * m + q] = sn * akp + cs * akq;
           double vkp = V[k * m + p], vkq = V[k * m + q];
-          V[k * m + p] = cs * vkp - s * vkq;
-          V[k * m + q] = s * vkp + cs * vkq;
+          V[k * m + p] = cs * vkp - sn * vkq;
+          V[k * m + q] = sn * vkp + cs * vkq;
         }
+        __syncwarp();
+        if (lane < m) {
+          const int k = lane;
+          double apk = A[p * m + k], aqk = A[q * m + k];
+          A[p * m + k] = cs * apk - sn * aqk;
+          A[q * m + k] = sn * apk + cs * aqk;
+        }
+        __syncwarp();
       }
   }
-  for (int i = 0; i < m; ++i) ev[i] = A[i * m + i];
+  if (lane < m) ev[lane] = A[lane * m + lane];
+  __syncwarp();
 }
 
-// min-norm solve with lstsq's rcond cutoff (physics.py:782), scratch in global memory
-__device__ void pinv_solve(int m, const double *A, const double *b, double rcond, double *x, double *W, double *V) {
-  double ev[kMaxBlockRows];
-  for (int i = 0; i < m * m; ++i) W[i] = A[i];
-  sym_eig(m, W, V, ev);
-  double smax = 0.0;
-  for (int i = 0; i < m; ++i) smax = fmax(smax, fabs(ev[i]));
-  for (int i = 0; i < m; ++i) x[i] = 0.0;
-  for (int k = 0; k < m; ++k) {
-    if (fabs(ev[k]) <= rcond * smax) continue;
-    double cc = 0.0;
-    for (int i = 0; i < m; ++i) cc += V[i * m + k] * b[i];
-    cc /= ev[k];
-    for (int i = 0; i < m; ++i) x[i] += cc * V[i * m + k];
-  }
-}
 
-// physics.py:760-816 (lane 0)
-__device__ void solve_block(Ctx &c, int first, int m, const double *K, double *scratch) {
-  double cur[kMaxBlockRows], q[kMaxBlockRows], lam[kMaxBlockRows], wv[kMaxBlockRows], rhs[kMaxBlockRows],
-      sol[kMaxBlockRows];
-  int active[kMaxBlockRows], na = 0;
-  double *sub = scratch, *W = scratch + kMaxBlockRows * kMaxBlockRows, *V = W + kMaxBlockRows * kMaxBlockRows;
-  for (int i = 0; i < m; ++i) {
-    double *r = c.rows + kRowD * (first + i);
-    cur[i] = r[RLAM];
-    wv[i] = row_vn(c, r) - r[RTGT];
+// physics.py:760-816; warp-collective.  Kc/evc: this block's eigen cache.
+__device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, BlockWS &ws, double *W, double *Vc,
+                            double *evc) {
+  const int lane = c.lane;
+  double *P = c.pairs + kPairD * g;
+  if (lane < m) {
+    double *r = c.rows + kRowD * (first + lane);
+    ws.cur[lane] = r[RLAM];
+    ws.wv[lane] = row_vn(c, r) - r[RTGT];
   }
-  for (int i = 0; i < m; ++i) {
+  __syncwarp();
+  if (lane < m) {
+    const int i = lane;
     double s = 0.0;
-    for (int j = 0; j < m; ++j) s += K[i * m + j] * cur[j];
-    q[i] = wv[i] - s;
+    for (int j = 0; j < m; ++j) s += K[i * m + j] * ws.cur[j];
+    ws.q[i] = ws.wv[i] - s;
   }
-  for (int i = 0; i < m; ++i)
-    if (cur[i] > 0.0 || wv[i] < 0.0) active[na++] = i;
-  bool converged = false;
+  if (lane == 0) {
+    int na = 0;
+    for (int i = 0; i < m; ++i)
+      if (ws.cur[i] > 0.0 || ws.wv[i] < 0.0) ws.active[na++] = i;
+    ws.na = na;
+    ws.converged = 0;
+  }
+  __syncwarp();
   for (int it = 0; it < 4 * m + 4; ++it) {
-    for (int i = 0; i < m; ++i) lam[i] = 0.0;
+    const int na = ws.na;
+    if (lane < m) ws.lam[lane] = 0.0;
     if (na) {
-      for (int i = 0; i < na; ++i) {
-        for (int j = 0; j < na; ++j) sub[i * na + j] = K[active[i] * m + active[j]];
-        rhs[i] = -q[active[i]];
+      unsigned mask = 0u;
+      for (int i = 0; i < na; ++i) mask |= 1u << ws.active[i];
+      if (lane < na) ws.rhs[lane] = -ws.q[ws.active[lane]];
+      if ((double)mask != P[PMASK]) {
+        // eigendecomposition of K[A, A] (cache miss)
+        for (int e = lane; e < na * na; e += 32) W[e] = K[ws.active[e / na] * m + ws.active[e % na]];
+        __syncwarp();
+        sym_eig_warp(na, W, Vc, evc, lane);
+        if (lane == 0) P[PMASK] = (double)mask;
       }
-      pinv_solve(na, sub, rhs, 1e-8, sol, W, V);
-      for (int i = 0; i < na; ++i) lam[active[i]] = sol[i];
+      __syncwarp();
+      // x = sum_k (V_k . b / ev_k) V_k over ev_k > rcond * max|ev| (oracle pinv_solve order)
+      double smax = 0.0;
+      for (int i = 0; i < na; ++i) smax = fmax(smax, fabs(evc[i]));
+      if (lane < na) {
+        const int k = lane;
+        double cc = 0.0;
+        for (int i = 0; i < na; ++i) cc += Vc[i * na + k] * ws.rhs[i];
+        ws.ck[k] = cc / evc[k];
+      }
+      __syncwarp();
+      if (lane < na) {
+        const int i = lane;
+        double x = 0.0;
+        for (int k = 0; k < na; ++k) {
+          if (fabs(evc[k]) <= 1e-8 * smax) continue;
+          x += ws.ck[k] * Vc[i * na + k];
+        }
+        ws.lam[ws.active[i]] = x;
+      }
     }
-    int worst = -1;
-    for (int i = 0; i < na; ++i) {
-      int ii = active[i];
-      if (lam[ii] < -1e-10 && (worst < 0 || lam[ii] < lam[worst] || (lam[ii] == lam[worst] && ii < worst))) worst = ii;
+    __syncwarp();
+    if (lane == 0) {
+      int worst = -1;
+      for (int i = 0; i < na; ++i) {
+        int ii = ws.active[i];
+        double l = ws.lam[ii];
+        if (l < -1e-10 && (worst < 0 || l < ws.lam[worst] || (l == ws.lam[worst] && ii < worst))) worst = ii;
+      }
+      ws.worst = worst;
     }
-    if (worst >= 0) {
-      int k = 0;
-      for (int i = 0; i < na; ++i) if (active[i] != worst) active[k++] = active[i];
-      na = k;
+    __syncwarp();
+    if (ws.worst >= 0) {
+      if (lane == 0) {
+        int k = 0;
+        for (int i = 0; i < na; ++i)
+          if (ws.active[i] != ws.worst) ws.active[k++] = ws.active[i];
+        ws.na = k;
+      }
+      __syncwarp();
       continue;
     }
-    worst = -1;
-    for (int i = 0; i < m; ++i) {
+    // w = K lam + q on the inactive rows (lane i, oracle order)
+    if (lane < m) {
+      const int i = lane;
       bool in = false;
-      for (int j = 0; j < na; ++j) in |= (active[j] == i);
-      if (in) continue;
-      double wi = 0.0;
-      for (int j = 0; j < m; ++j) wi += K[i * m + j] * lam[j];
-      wi += q[i];
-      wv[i] = wi;
-      if (wi < -1e-10 && (worst < 0 || wi < wv[worst] || (wi == wv[worst] && i < worst))) worst = i;
+      for (int j = 0; j < na; ++j) in |= (ws.active[j] == i);
+      if (!in) {
+        double wi = 0.0;
+        for (int j = 0; j < m; ++j) wi += K[i * m + j] * ws.lam[j];
+        wi += ws.q[i];
+        ws.wv[i] = wi;
+      }
     }
-    if (worst >= 0) {
-      int k = na;
-      while (k > 0 && active[k - 1] > worst) { active[k] = active[k - 1]; --k; }
-      active[k] = worst;
-      ++na;
-      continue;
+    __syncwarp();
+    if (lane == 0) {
+      int worst = -1;
+      for (int i = 0; i < m; ++i) {
+        bool in = false;
+        for (int j = 0; j < na; ++j) in |= (ws.active[j] == i);
+        if (in) continue;
+        double wi = ws.wv[i];
+        if (wi < -1e-10 && (worst < 0 || wi < ws.wv[worst] || (wi == ws.wv[worst] && i < worst))) worst = i;
+      }
+      if (worst >= 0) {
+        int k = na;
+        while (k > 0 && ws.active[k - 1] > worst) { ws.active[k] = ws.active[k - 1]; --k; }
+        ws.active[k] = worst;
+        ws.na = na + 1;
+      } else {
+        ws.converged = 1;
+      }
+      ws.worst = worst;
     }
-    converged = true;
-    break;
+    __syncwarp();
+    if (ws.converged) break;
   }
-  if (!converged) {
-    for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
-    return;
+  if (lane == 0) {
+    if (!ws.converged) {
+      for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
+    } else {
+      for (int i = 0; i < m; ++i) {
+        double *r = c.rows + kRowD * (first + i);
+        double l = ws.lam[i] > 0.0 ? ws.lam[i] : 0.0;
+        double d = l - r[RLAM];
+        r[RLAM] = l;
+        if (d != 0.0) row_apply(c, r, r[RN] * d, r[RN + 1] * d, r[RN + 2] * d);
+      }
+      for (int i = 0; i < m; ++i) row_friction(c, c.rows + kRowD * (first + i));
+    }
   }
-  for (int i = 0; i < m; ++i) {
-    double *r = c.rows + kRowD * (first + i);
-    double l = lam[i] > 0.0 ? lam[i] : 0.0;
-    double d = l - r[RLAM];
-    r[RLAM] = l;
-    if (d != 0.0) row_apply(c, r, r[RN] * d, r[RN + 1] * d, r[RN + 2] * d);
-  }
-  for (int i = 0; i < m; ++i) row_friction(c, c.rows + kRowD * (first + i));
+  __syncwarp();
 }
 
 __device__ __forceinline__ bool solver_dynamic(Ctx &c, int b) {
@@ -1078,7 +1151,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
       bool hask = m > 1 && c.rows[kRowD * first + RK] > 0.0;
       if (hask && m > kMaxBlockRows) return false;
       if (hask && koff + m * m > kKCap) return false;
-      if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; }
+      if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; P[PMASK] = -1.0; }
       if (hask) {
         double *K = c.K + koff;
         const double *r0 = c.rows + kRowD * first;
@@ -1111,17 +1184,24 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
       }
     }
     __syncwarp();
-    // Gauss-Seidel sweeps: lane 0, blocks in sorted pair order
-    if (lane == 0) {
-      double *scratch = c.K + kKCap;  // 3 * 32 * 32 doubles
+    // Gauss-Seidel sweeps, blocks in sorted pair order (physics.py:931-937).
+    // Rows with k <= 0 are no-ops in the reference (physics.py:1294): when
+    // every row is such, the sweeps change nothing and are skipped.
+    bool any_k = false;
+    for (int i = lane; i < nc; i += 32) any_k |= c.rows[kRowD * i + RK] > 0.0;
+    any_k = __any_sync(0xffffffffu, any_k);
+    if (any_k) {
       for (int it = 0; it < cfg.solver_iterations; ++it)
         for (int g = 0; g < ng; ++g) {
           const int first = S.g_first[g], m = S.g_n[g];
           const double *P = c.pairs + kPairD * g;
           if (P[PHASK] == 0.0) {
-            for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
+            if (lane == 0)
+              for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
+            __syncwarp();
           } else {
-            solve_block(c, first, m, c.K + (int)P[PKOFF], scratch);
+            const int koff = (int)P[PKOFF];
+            solve_block(c, g, first, m, c.K + koff, S.ws, c.W, c.Vc + koff, c.evc + first);
           }
         }
     }
@@ -1231,6 +1311,8 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
   return true;
 }
 
+__host__ __device__ size_t step_scratch_doubles_per_env(int row_cap);
+
 // a faulted env keeps its input state (the reference raises before mutating)
 __device__ void copy_through(const DevBatch &B, int env, int lane) {
   const StateLayout &L = B.L;
@@ -1260,10 +1342,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, c
   c.env = env;
   c.lane = lane;
   c.L = &L;
-  const size_t per_env = (size_t)B.row_cap * kRowD + kMaxGroups * kPairD + kKCap + 3 * kMaxBlockRows * kMaxBlockRows;
+  const size_t per_env = step_scratch_doubles_per_env(B.row_cap);
   c.rows = B.row_scratch + per_env * env;
   c.pairs = c.rows + (size_t)B.row_cap * kRowD;
   c.K = c.pairs + kMaxGroups * kPairD;
+  c.Vc = c.K + kKCap;
+  c.evc = c.Vc + kKCap;
+  c.W = c.evc + kMaxContacts;
 
   // stage the state slab (coalesced)
   const double *gsd = B.sd + (size_t)env * L.dbl_size;
@@ -1322,8 +1407,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, c
   for (int i = lane; i < L.int_size; i += 32) wsi[i] = S.si[i];
 }
 
-size_t step_scratch_doubles_per_env(int row_cap) {
-  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + kKCap + 3 * kMaxBlockRows * kMaxBlockRows;
+__host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
+  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 2 * kKCap + kMaxContacts + kMaxBlockRows * kMaxBlockRows;
 }
 int step_row_cap() { return kMaxContacts; }
 

@@ -70,7 +70,7 @@ __device__ __forceinline__ double ray_convex(const double *pl, int nf, const dou
     for (int k = 0; k < 3; ++k) sb[k] = d[0] * pl[4 * k] + d[1] * pl[4 * k + 1] + d[2] * pl[4 * k + 2];
   }
   const int n = kBox ? 6 : nf;
-#pragma unroll 6
+#pragma unroll(kBox ? 6 : 1)
   for (int f = 0; f < n; ++f) {
     const double *P = pl + 4 * f;
     double s = kBox ? (f < 3 ? sb[f] : -sb[f - 3]) : d[0] * P[0] + d[1] * P[1] + d[2] * P[2];
@@ -267,10 +267,12 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
   const double eps = B.rcfg.tie_eps, zfar = B.rcfg.zfar, znear = B.rcfg.znear;
   const size_t img = (size_t)(env * n_cam_out + slot) * H * W;
   unsigned long long tests = 0;
+#pragma unroll 1
   for (int tile = warp; tile < ntiles; tile += nwarps) {
     const uint8_t *list = S.list[tile];
     const int nl = S.nlist[tile];
     const int ux = (tile % tx_n) * kTile, vy = (tile / tx_n) * kTile;
+#pragma unroll 1
     for (int k = lane; k < kTile * kTile; k += 32) {
       const int u = ux + (k % kTile), v = vy + (k / kTile);
       double dc[3] = {(u + 0.5 - W / 2.0) / f, (v + 0.5 - H / 2.0) / f, 1.0};
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
       matvec(S.cam.R, dc, d);
       double tmin = INFINITY, t2 = INFINITY;
       int id = -1, wpart = -1, wface = -1;
+#pragma unroll 1
       for (int j = 0; j < nl; ++j) {
         const int p = list[j];
         const PartW &P = S.part[p];
