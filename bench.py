@@ -258,11 +258,13 @@ def run_b200(args):
     from paper_2106_14405_b200 import native
     from paper_2106_14405_b200.sim import BatchSimulator
 
+    from paper_2106_14405_b200.shard import layout_of, reduce_window, shard_env_ids
+
     E = args.envs
-    gids = np.arange(rank * E, (rank + 1) * E)
-    layout_of = gids % 3
-    sim = BatchSimulator(layouts=(0, 1, 2), n_env=E, env_layout=layout_of.tolist(), device=dev)
-    sim.set_state(idle_states(gids, settled_pool()))
+    gids = shard_env_ids(rank, world, E)
+    sim = BatchSimulator(layouts=(0, 1, 2), n_env=E, env_layout=layout_of(gids).tolist(), device=dev)
+    init_states = idle_states(gids, settled_pool())
+    sim.set_state(init_states)
     n_tab = args.warmup + args.steps
     arm_np, base_np = action_table(E, n_tab, seed=7 + rank)
     arm_d = torch.tensor(arm_np, device=dev)
@@ -304,12 +306,15 @@ def run_b200(args):
     ms_rend = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
     sim.raise_faults()
 
-    # ---- end-to-end through the C-ABI with host buffers (e2e)
+    # ---- end-to-end through the C-ABI with host buffers (e2e): replay the
+    # same trajectory (same initial states, same actions) as the timed region
+    sim.set_state(init_states)
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize(dev)
     h_arm = torch.tensor(arm_np).pin_memory()
     h_base = torch.tensor(base_np).pin_memory()
     h_stats = torch.empty((E, 4), dtype=torch.float64).pin_memory()
-    for k in range(2):
-        sim.step_host(h_arm[k], h_base[k], out=obs, h_stats=h_stats)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -324,16 +329,17 @@ def run_b200(args):
     torch.cuda.synchronize(dev)
     ms_e2e = e0.elapsed_time(e1)
     if rank == 0:
+        st = h_stats.numpy()
         print(f"[bench] e2e per-step host ms: {np.round(host_ms, 3).tolist()}", file=sys.stderr)
+        print(f"[bench] envs with awake clutter: {int((st[:, 3] < 20).sum())}, "
+              f"envs with contact events: {int((st[:, 2] > 0).sum())}, faults: {int((st[:, 1] != 0).sum())}",
+              file=sys.stderr)
     acc = float(h_stats[:, 0].sum())
 
     # ---- across ranks: max time, summed stats (the only collectives)
-    t = torch.tensor([ms_total, ms_e2e, ms_phys, ms_rend], device=dev, dtype=torch.float64)
-    stats = torch.tensor([acc, float(E)], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM)
-    ms_total, ms_e2e, ms_phys, ms_rend = (float(x) for x in t.cpu())
+    stats, tms = reduce_window({"acc": acc, "envs": float(E)},
+                               {"total": ms_total, "e2e": ms_e2e, "phys": ms_phys, "rend": ms_rend}, device=dev)
+    ms_total, ms_e2e, ms_phys, ms_rend = tms["total"], tms["e2e"], tms["phys"], tms["rend"]
     total_envs = E * world
     value = total_envs * args.steps / (ms_total * 1e-3)
     e2e_value = total_envs * args.steps / (ms_e2e * 1e-3)
@@ -387,7 +393,7 @@ def run_b200(args):
                     "d2h_bytes_per_step": int(E * 4 * 8)},
             "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
-            "episode_stats_allreduce": {"accumulated_contact_force_sum": float(stats[0]), "envs": int(stats[1])},
+            "episode_stats_allreduce": {"accumulated_contact_force_sum": stats["acc"], "envs": int(stats["envs"])},
         }
         if world == 1 and not args.no_cpu_baseline:
             sps, cores, wall, steps = cpu_oracle_sps(args.cpu_baseline_steps)

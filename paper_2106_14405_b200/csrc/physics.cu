@@ -64,12 +64,13 @@ struct BlockWS {
 struct WarpSmem {
   double sd[1024];
   int32_t si[160];
-  double R[kMaxBodies][9];
-  double lo[kMaxBodies][3], hi[kMaxBodies][3];
-  double vel[kMaxBodies][6];
+  // phase-scoped scratch: broadphase AABBs | narrowphase planes | solver velocities
+  union {
+    struct { double lo[kMaxBodies][3], hi[kMaxBodies][3]; } bp;
+    double planes[2][kMaxFacetsPerPart * 4];
+    struct { double vel[kMaxBodies][6]; BlockWS ws; } sol;
+  } u;
   double jdv[kMaxJoints];
-  double cp[kMaxContacts][3], cn[kMaxContacts][3], cd[kMaxContacts];
-  double planes[2][kMaxFacetsPerPart * 4];
   double links[kMaxArm][12];
   double ee[12];
   double raa[kMaxArm][9];
@@ -81,7 +82,6 @@ struct WarpSmem {
   unsigned long long awake_dyn;
   int moved_mask;
   int64_t ctr[3];
-  BlockWS ws;
 };
 
 struct Ctx {
@@ -119,13 +119,7 @@ __device__ __forceinline__ void body_pose(Ctx &c, int b, Pose &o) {
   const double *p = POS(c, b);
   o.p[0] = p[0]; o.p[1] = p[1]; o.p[2] = p[2];
 }
-// pose from the rotation cache (valid between refresh_rot calls)
-__device__ __forceinline__ void body_pose_cached(Ctx &c, int b, Pose &o) {
-#pragma unroll
-  for (int i = 0; i < 9; ++i) o.R[i] = c.S->R[b][i];
-  const double *p = POS(c, b);
-  o.p[0] = p[0]; o.p[1] = p[1]; o.p[2] = p[2];
-}
+__device__ __forceinline__ void body_pose_cached(Ctx &c, int b, Pose &o) { body_pose(c, b, o); }
 
 // write a kinematic pose; 1 if it changed (physics.py:419-433, :441-453)
 __device__ int set_kinematic(Ctx &c, int b, const Pose &p, double dt, bool zero_if_same) {
@@ -308,7 +302,7 @@ __device__ void planes_world(Ctx &c, int p, const Pose &wp, int slot) {
   int f0 = sc.part_facet_begin[p], nf = sc.part_facet_begin[p + 1] - f0;
   for (int f = c.lane; f < nf; f += 32) {
     const double *F = sc.facet + 4 * (f0 + f);
-    double *o = c.S->planes[slot] + 4 * f;
+    double *o = c.S->u.planes[slot] + 4 * f;
     double n[3];
     matvec(wp.R, F, n);
     o[0] = n[0]; o[1] = n[1]; o[2] = n[2];
@@ -316,10 +310,12 @@ __device__ void planes_world(Ctx &c, int p, const Pose &wp, int slot) {
   }
 }
 
+// contacts are written straight into their solver rows (global scratch)
 __device__ __forceinline__ int add_contact(Ctx &c, int idx, const double *p, const double *n, double depth) {
   if (idx >= kMaxContacts) return 0;
-  for (int i = 0; i < 3; ++i) { c.S->cp[idx][i] = p[i]; c.S->cn[idx][i] = n[i]; }
-  c.S->cd[idx] = depth;
+  double *r = c.rows + kRowD * idx;
+  for (int i = 0; i < 3; ++i) { r[RPT + i] = p[i]; r[RN + i] = n[i]; }
+  r[RDEPTH] = depth;
   return 1;
 }
 
@@ -330,7 +326,7 @@ __device__ int vertices_vs_planes(Ctx &c, int pv, const Pose &wv, int pf, int sl
   const DevScene &sc = *c.sc;
   int v0 = sc.part_vert_begin[pv], nv = sc.part_vert_begin[pv + 1] - v0;
   int nf = sc.part_facet_begin[pf + 1] - sc.part_facet_begin[pf];
-  const double *pl = c.S->planes[slot];
+  const double *pl = c.S->u.planes[slot];
   int total = 0;
   for (int k0 = 0; k0 < nv; k0 += 32) {
     int v = k0 + c.lane;
@@ -400,7 +396,7 @@ __device__ int sphere_convex(Ctx &c, int ps, const Pose &ws, int pc, const Pose 
   const DevScene &sc = *c.sc;
   double r = sc.part_param[3 * ps];
   const double *ctr = ws.p;
-  const double *pl = c.S->planes[slot];
+  const double *pl = c.S->u.planes[slot];
   int nf = sc.part_facet_begin[pc + 1] - sc.part_facet_begin[pc];
   bool inside = true;
   int f = 0;
@@ -513,7 +509,7 @@ __device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
 // ------------------------------------------------------------------ solver
 
 __device__ __forceinline__ void row_rel_vel(Ctx &c, const double *r, double *o) {
-  const double *va = c.S->vel[(int)r[RA]], *vb = c.S->vel[(int)r[RB]];
+  const double *va = c.S->u.sol.vel[(int)r[RA]], *vb = c.S->u.sol.vel[(int)r[RB]];
   const double *ra = r + RRA, *rb = r + RRB;
   double ax = va[0] + va[4] * ra[2] - va[5] * ra[1];
   double ay = va[1] + va[5] * ra[0] - va[3] * ra[2];
@@ -541,7 +537,7 @@ __device__ __forceinline__ double row_vn(Ctx &c, const double *r) {
 __device__ void row_apply(Ctx &c, const double *r, double ix, double iy, double iz) {
   const double *pg = c.pairs + kPairD * (int)r[RGRP];
   if (r[RIMA] > 0.0) {
-    double *va = c.S->vel[(int)r[RA]], m = r[RIMA];
+    double *va = c.S->u.sol.vel[(int)r[RA]], m = r[RIMA];
     va[0] += ix * m; va[1] += iy * m; va[2] += iz * m;
     const double *ra = r + RRA;
     double tx = ra[1] * iz - ra[2] * iy, ty = ra[2] * ix - ra[0] * iz, tz = ra[0] * iy - ra[1] * ix;
@@ -551,7 +547,7 @@ __device__ void row_apply(Ctx &c, const double *r, double ix, double iy, double 
     va[5] += I[6] * tx + I[7] * ty + I[8] * tz;
   }
   if (r[RIMB] > 0.0) {
-    double *vb = c.S->vel[(int)r[RB]], m = r[RIMB];
+    double *vb = c.S->u.sol.vel[(int)r[RB]], m = r[RIMB];
     vb[0] -= ix * m; vb[1] -= iy * m; vb[2] -= iz * m;
     const double *rb = r + RRB;
     double tx = rb[1] * iz - rb[2] * iy, ty = rb[2] * ix - rb[0] * iz, tz = rb[0] * iy - rb[1] * ix;
@@ -814,11 +810,6 @@ __device__ int joint_jacobian(Ctx &c, int b, const double *pt, double *jac, doub
   return ji;
 }
 
-// rotation cache refresh (lanes per body)
-__device__ __forceinline__ void refresh_rot(Ctx &c) {
-  for (int b = c.lane; b < c.sc->nb; b += 32) quat_to_mat(QUAT(c, b), c.S->R[b]);
-  __syncwarp();
-}
 
 __device__ __forceinline__ void wake(Ctx &c, int b) {
   if (c.sc->body_kind[b] != RS_DYNAMIC) return;
@@ -950,7 +941,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
     unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(mine >> 32));
     S.awake_dyn = ((unsigned long long)hi32 << 32) | lo32;
   }
-  refresh_rot(c);
+  __syncwarp();
 
   // ---- broadphase: AABBs (lanes per body)
   for (int b = lane; b < nb; b += 32) {
@@ -965,7 +956,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
     }
     if (sc.body_kind[b] == RS_KINEMATIC)
       for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
-    for (int i = 0; i < 3; ++i) { S.lo[b][i] = lo[i]; S.hi[b][i] = hi[i]; }
+    for (int i = 0; i < 3; ++i) { S.u.bp.lo[b][i] = lo[i]; S.u.bp.hi[b][i] = hi[i]; }
   }
   __syncwarp();
   // ---- overlap candidates in sorted (a, b) order (lanes per pair, ballot compaction)
@@ -979,8 +970,8 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
       if (b < nb) {
         const int kb = sc.body_kind[b];
         ov = !(ka == RS_STATIC && kb == RS_STATIC) && !(ga != RS_NO_GROUP && ga == sc.body_group[b]) &&
-             S.lo[a][0] <= S.hi[b][0] && S.lo[b][0] <= S.hi[a][0] && S.lo[b][1] <= S.hi[a][1] &&
-             S.lo[a][1] <= S.hi[b][1] && S.lo[b][2] <= S.hi[a][2] && S.lo[a][2] <= S.hi[b][2];
+             S.u.bp.lo[a][0] <= S.u.bp.hi[b][0] && S.u.bp.lo[b][0] <= S.u.bp.hi[a][0] && S.u.bp.lo[b][1] <= S.u.bp.hi[a][1] &&
+             S.u.bp.lo[a][1] <= S.u.bp.hi[b][1] && S.u.bp.lo[b][2] <= S.u.bp.hi[a][2] && S.u.bp.lo[a][2] <= S.u.bp.hi[b][2];
       }
       unsigned m = __ballot_sync(0xffffffffu, ov);
       if (ov) {
@@ -1063,7 +1054,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
   // ---- solver (physics.py:846-960)
   for (int b = lane; b < nb; b += 32) {
     const double *lv = LV(c, b), *av = AV(c, b);
-    for (int i = 0; i < 3; ++i) { S.vel[b][i] = lv[i]; S.vel[b][3 + i] = av[i]; }
+    for (int i = 0; i < 3; ++i) { S.u.sol.vel[b][i] = lv[i]; S.u.sol.vel[b][3 + i] = av[i]; }
   }
   for (int j = lane; j < kMaxJoints; j += 32) S.jdv[j] = 0.0;
   // per-pair solver data (lanes per group)
@@ -1099,13 +1090,11 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
     for (int i = lane; i < m; i += 32) {
       const int ci = first + i;
       double *r = c.rows + kRowD * ci;
-      const double *n = S.cn[ci], *pt = S.cp[ci];
+      const double *n = r + RN, *pt = r + RPT;
       r[RA] = S.g_a[g]; r[RB] = S.g_b[g]; r[RGRP] = g;
       for (int k = 0; k < 3; ++k) {
-        r[RN + k] = n[k];
         r[RRA + k] = pt[k] - P[PCA + k];
         r[RRB + k] = pt[k] - P[PCB + k];
-        r[RPT + k] = pt[k];
       }
       double kk = P[PIMA] + P[PIMB], t[3], u[3], v[3];
       cross3(r + RRA, n, t); matvec(P + PIA, t, u); cross3(u, r + RRA, v); kk += dot3(n, v);
@@ -1128,10 +1117,9 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
       for (int k = 0; k < 3; ++k) t2[k] /= l;
       r[RK] = kk; r[RMU] = P[PMU]; r[RIMA] = P[PIMA]; r[RIMB] = P[PIMB];
       r[RLAM] = r[RLT1] = r[RLT2] = 0.0;
-      r[RDEPTH] = S.cd[ci];
       double vn = row_vn(c, r);
       r[RVN] = vn;
-      double sep = -S.cd[ci] > 0.0 ? -S.cd[ci] : 0.0;
+      double sep = -r[RDEPTH] > 0.0 ? -r[RDEPTH] : 0.0;
       if (sep > 0.0) {
         r[RTGT] = -sep / dt;
         r[RFRIC] = 0.0;
@@ -1201,7 +1189,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
             __syncwarp();
           } else {
             const int koff = (int)P[PKOFF];
-            solve_block(c, g, first, m, c.K + koff, S.ws, c.W, c.Vc + koff, c.evc + first);
+            solve_block(c, g, first, m, c.K + koff, S.u.sol.ws, c.W, c.Vc + koff, c.evc + first);
           }
         }
     }
@@ -1209,7 +1197,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
     for (int b = lane; b < nb; b += 32)
       if (solver_dynamic(c, b)) {
         double *lv = LV(c, b), *av = AV(c, b);
-        for (int i = 0; i < 3; ++i) { lv[i] = S.vel[b][i]; av[i] = S.vel[b][3 + i]; }
+        for (int i = 0; i < 3; ++i) { lv[i] = S.u.sol.vel[b][i]; av[i] = S.u.sol.vel[b][3 + i]; }
       }
     // events + force tally in row order (lane 0)
     if (lane == 0) {
@@ -1245,16 +1233,17 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
         double tot = ima + imb;
         if (tot <= 0.0) continue;
         for (int i = S.g_first[g]; i < S.g_first[g] + S.g_n[g]; ++i) {
-          double push = cfg.correction_factor * fmax(S.cd[i] - cfg.slop, 0.0);
+          const double *r = c.rows + kRowD * i;
+          double push = cfg.correction_factor * fmax(r[RDEPTH] - cfg.slop, 0.0);
           if (push <= 0.0) continue;
           if (a == b && ima > 0.0) {
             double s = push * ima / tot;
-            for (int k = 0; k < 3; ++k) corr[k] += S.cn[i][k] * s;
+            for (int k = 0; k < 3; ++k) corr[k] += r[RN + k] * s;
             cnt++;
           }
           if (bb == b && imb > 0.0) {
             double s = push * imb / tot;
-            for (int k = 0; k < 3; ++k) corr[k] -= S.cn[i][k] * s;
+            for (int k = 0; k < 3; ++k) corr[k] -= r[RN + k] * s;
             cnt++;
           }
         }
