@@ -170,10 +170,12 @@ int rs_render(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, i
  * < 0 releases. */
 int rs_grasp(rs_batch *batch, const double *gripper, void *stream);
 
-/* End-to-end env step with HOST buffers (pipeline.step restated):
- * copies arm_targets/base_cmd (host) to the device, runs rs_step then rs_render
- * (cam_mask) into the device observation tensors, and copies per-env step
- * results back to host: out_stats [n_env][4] = accumulated_contact_force,
+/* End-to-end env step with HOST buffers (pipeline.step restated, SPEC.md:316,
+ * default StepConfig: observation_delay = 1, interleave = true):
+ * renders o_t = render(s_t) (cam_mask) into the device observation tensors on
+ * an internal side stream WHILE copying arm_targets/base_cmd (host) to the
+ * device and running rs_step s_t -> s_{t+1} on `stream`; then copies per-env
+ * step results back to host: out_stats [n_env][4] = accumulated_contact_force,
  * fault word, event count, sleeping-body count.  Synchronises `stream`. */
 int rs_step_host(rs_batch *batch, const double *h_arm_targets, const double *h_base_cmd, double dt,
                  int32_t substeps, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,

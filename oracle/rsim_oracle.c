@@ -776,11 +776,29 @@ static void solve_row(row_t *r, velset_t *vs) {
   solve_friction(r, vs);
 }
 
-/* cyclic Jacobi eigensolver for a symmetric m x m matrix (row-major, m <= 32) */
+/* Jacobi eigensolver for a symmetric m x m matrix (row-major, m <= 32) in
+ * round-robin ("parallel") ordering: each sweep is m'-1 rounds (m' = m
+ * rounded up to even) of m'/2 disjoint rotations, all computed from the
+ * matrix at the start of the round, then applied as one column pass and one
+ * row pass.  The CUDA block solver executes exactly these per-element
+ * operations one element per lane, so the two agree bit for bit.  The pair
+ * schedule is the circle method: in round r, (n-1, r) and
+ * ((r+k) mod (n-1), (r-k+n-1) mod (n-1)) for k = 1..n/2-1. */
+void orc_jacobi_pair(int n, int r, int k, int *p, int *q) {
+  int a, b;
+  if (k == 0) { a = n - 1; b = r; }
+  else { a = (r + k) % (n - 1); b = (r - k + n - 1) % (n - 1); }
+  *p = a < b ? a : b;
+  *q = a < b ? b : a;
+}
+
 static void sym_eig(int m, double *A, double *V, double *ev) {
+  const int n = m + (m & 1);
+  double cs[16], sn[16];
+  int pp[16], qq[16];
   for (int i = 0; i < m; ++i)
     for (int j = 0; j < m; ++j) V[i * m + j] = (i == j);
-  for (int sweep = 0; sweep < 64; ++sweep) {
+  for (int sweep = 0; sweep < 64 && m > 1; ++sweep) {
     double off = 0.0, tot = 0.0;
     for (int i = 0; i < m; ++i)
       for (int j = 0; j < m; ++j) {
@@ -789,30 +807,45 @@ static void sym_eig(int m, double *A, double *V, double *ev) {
         if (i != j) off += a2;
       }
     if (off <= 1e-32 * tot || off == 0.0) break;
-    for (int p = 0; p < m - 1; ++p)
-      for (int q = p + 1; q < m; ++q) {
+    for (int r = 0; r < n - 1; ++r) {
+      for (int k = 0; k < n / 2; ++k) {
+        int p, q;
+        orc_jacobi_pair(n, r, k, &p, &q);
+        pp[k] = p; qq[k] = q;
+        cs[k] = 1.0; sn[k] = 0.0;
+        if (q >= m) continue; /* padding index */
         double apq = A[p * m + q];
         if (apq == 0.0) continue;
         double app = A[p * m + p], aqq = A[q * m + q];
         double theta = (aqq - app) / (2.0 * apq);
         double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < m; ++k) {
-          double akp = A[k * m + p], akq = A[k * m + q];
-          A[k * m + p] = c * akp - s * akq;
-          A[k * m + q] = s * akp + c * akq;
-        }
-        for (int k = 0; k < m; ++k) {
-          double apk = A[p * m + k], aqk = A[q * m + k];
-          A[p * m + k] = c * apk - s * aqk;
-          A[q * m + k] = s * apk + c * aqk;
-        }
-        for (int k = 0; k < m; ++k) {
-          double vkp = V[k * m + p], vkq = V[k * m + q];
-          V[k * m + p] = c * vkp - s * vkq;
-          V[k * m + q] = s * vkp + c * vkq;
+        cs[k] = 1.0 / sqrt(t * t + 1.0);
+        sn[k] = t * cs[k];
+      }
+      /* column pass (A and V) */
+      for (int k = 0; k < n / 2; ++k) {
+        int p = pp[k], q = qq[k];
+        if (q >= m || sn[k] == 0.0) continue;
+        for (int i = 0; i < m; ++i) {
+          double aip = A[i * m + p], aiq = A[i * m + q];
+          A[i * m + p] = cs[k] * aip - sn[k] * aiq;
+          A[i * m + q] = sn[k] * aip + cs[k] * aiq;
+          double vip = V[i * m + p], viq = V[i * m + q];
+          V[i * m + p] = cs[k] * vip - sn[k] * viq;
+          V[i * m + q] = sn[k] * vip + cs[k] * viq;
         }
       }
+      /* row pass */
+      for (int k = 0; k < n / 2; ++k) {
+        int p = pp[k], q = qq[k];
+        if (q >= m || sn[k] == 0.0) continue;
+        for (int j = 0; j < m; ++j) {
+          double apj = A[p * m + j], aqj = A[q * m + j];
+          A[p * m + j] = cs[k] * apj - sn[k] * aqj;
+          A[q * m + j] = sn[k] * apj + cs[k] * aqj;
+        }
+      }
+    }
   }
   for (int i = 0; i < m; ++i) ev[i] = A[i * m + i];
 }

@@ -60,6 +60,8 @@ struct rs_batch {
   }
   // lazily allocated staging for rs_step_host
   double *h_pin = nullptr, *d_act = nullptr, *d_stats = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // exported functions take C linkage from their declarations in rsim.h
@@ -232,6 +234,9 @@ void rs_batch_destroy(rs_batch *b) {
   if (b->h_pin) cudaFreeHost(b->h_pin);
   if (b->d_act) cudaFree(b->d_act);
   if (b->d_stats) cudaFree(b->d_stats);
+  if (b->side) cudaStreamDestroy(b->side);
+  if (b->ev_fork) cudaEventDestroy(b->ev_fork);
+  if (b->ev_join) cudaEventDestroy(b->ev_join);
   delete b;
 }
 
@@ -400,22 +405,30 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
   if (!b->d_act) {
     CUDA_TRY(cudaMalloc(&b->d_act, sizeof(double) * (size_t)E * (na + 2)));
     CUDA_TRY(cudaMalloc(&b->d_stats, sizeof(double) * (size_t)E * 4));
+    CUDA_TRY(cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
+  }
+  // render o_t = render(s_t) on the side stream, concurrently with the physics
+  // s_t -> s_{t+1} on `stream` (ping-pong state buffers)
+  if (cam_mask) {
+    CUDA_TRY(cudaEventRecord(b->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(b->side, b->ev_fork, 0));
+    int rc = rs_render(b, cam_mask, rgba, depth, ids, b->side);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(b->ev_join, b->side));
   }
   double *d_arm = b->d_act, *d_base = b->d_act + (size_t)E * na;
   CUDA_TRY(cudaMemcpyAsync(d_arm, h_arm, sizeof(double) * (size_t)E * na, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(d_base, h_base, sizeof(double) * (size_t)E * 2, cudaMemcpyHostToDevice, st));
   int rc = rs_step(b, d_arm, d_base, nullptr, dt, substeps, stream);
   if (rc) return rc;
-  if (cam_mask) {
-    rc = rs_render(b, cam_mask, rgba, depth, ids, stream);
-    if (rc) return rc;
-  }
   CUDA_TRY(launch_stats(b->view(), b->d_stats, st));
   CUDA_TRY(cudaMemcpyAsync(h_out_stats, b->d_stats, sizeof(double) * (size_t)E * 4, cudaMemcpyDeviceToHost, st));
+  if (cam_mask) CUDA_TRY(cudaStreamWaitEvent(st, b->ev_join, 0));
   CUDA_TRY(cudaStreamSynchronize(st));
   return RS_OK;
 }
-
 
 int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
   if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");

@@ -41,7 +41,7 @@ constexpr int kMaxContacts = 128;
 constexpr int kMaxGroups = 96;
 constexpr int kMaxBlockRows = 32;
 constexpr int kRowD = 44;  // doubles per solver row in global scratch
-constexpr int kPairD = 32; // doubles per contact group (pair) in global scratch
+constexpr int kPairD = 34; // doubles per contact group (pair) in global scratch
 constexpr int kKCap = kMaxContacts * kMaxBlockRows;  // Sigma m^2 <= 32 * 128
 
 // ---- row field offsets (doubles) ------------------------------------------
@@ -51,14 +51,18 @@ enum {
   RA = 35, RB = 36, RPT = 37, RDEPTH = 40, RGRP = 41
 };
 // ---- pair (group) field offsets --------------------------------------------
-enum { PIA = 0, PIB = 9, PCA = 18, PCB = 21, PIMA = 24, PIMB = 25, PMU = 26, PE = 27, PKOFF = 28, PHASK = 29, PMASK = 30 };
+enum { PIA = 0, PIB = 9, PCA = 18, PCB = 21, PIMA = 24, PIMB = 25, PMU = 26, PE = 27, PKOFF = 28, PHASK = 29, PMASK = 30, PREPL = 32 };  // PMASK, PMASK+1: cached active sets
 
 // block workspace in shared memory (per warp), m <= kMaxBlockRows
+constexpr int kSmemEig = 12;  // eigensolver matrices live in shared memory up to this size
 struct BlockWS {
   double cur[kMaxBlockRows], q[kMaxBlockRows], lam[kMaxBlockRows], wv[kMaxBlockRows], rhs[kMaxBlockRows],
-      sol[kMaxBlockRows], ck[kMaxBlockRows];
+      ck[kMaxBlockRows];
+  double cs[kMaxBlockRows / 2], sn[kMaxBlockRows / 2];
+  int pp[kMaxBlockRows / 2], qq[kMaxBlockRows / 2];
+  double A[kSmemEig * kSmemEig], V[kSmemEig * kSmemEig];
   int active[kMaxBlockRows];
-  int na, worst, converged;
+  int na, worst, converged, slot;
 };
 
 struct WarpSmem {
@@ -605,11 +609,25 @@ __device__ void row_solve(Ctx &c, double *r) {
 // the 16 Gauss-Seidel sweeps the active set repeats and the eigensolve runs
 // once per distinct set.
 
-// A (m x m, row-major, destroyed) -> V (eigenvectors in columns), ev. warp-collective.
-__device__ void sym_eig_warp(int m, double *A, double *V, double *ev, int lane) {
+__device__ __forceinline__ void jacobi_pair(int n, int r, int k, int &p, int &q) {
+  int a, b;
+  if (k == 0) { a = n - 1; b = r; }
+  else { a = (r + k) % (n - 1); b = (r - k + n - 1) % (n - 1); }
+  p = a < b ? a : b;
+  q = a < b ? b : a;
+}
+
+// A (m x m, row-major, destroyed) -> V (eigenvectors in columns), ev; warp-collective.
+// Round-robin Jacobi: m'-1 rounds of m'/2 disjoint rotations per sweep, rotation
+// parameters from the matrix at the start of the round (one pair per lane),
+// then a column pass and a row pass (one element pair per lane).  Identical
+// per-element arithmetic to oracle/rsim_oracle.c sym_eig.
+__device__ void sym_eig_warp(int m, double *A, double *V, double *ev, double *cs, double *sn, int *pp, int *qq,
+                             int lane) {
+  const int n = m + (m & 1), half = n / 2;
   for (int e = lane; e < m * m; e += 32) V[e] = (e / m == e % m);
   __syncwarp();
-  for (int sweep = 0; sweep < 64; ++sweep) {
+  for (int sweep = 0; sweep < 64 && m > 1; ++sweep) {
     double off = 0.0, tot = 0.0;
     for (int i = 0; i < m; ++i)
       for (int j = 0; j < m; ++j) {
@@ -618,38 +636,51 @@ __device__ void sym_eig_warp(int m, double *A, double *V, double *ev, int lane) 
         if (i != j) off += a2;
       }
     if (off <= 1e-32 * tot || off == 0.0) break;
-    for (int p = 0; p < m - 1; ++p)
-      for (int q = p + 1; q < m; ++q) {
-        const double apq = A[p * m + q];
-        if (apq == 0.0) continue;
-        const double app = A[p * m + p], aqq = A[q * m + q];
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
-        __syncwarp();
-        if (lane < m) {
-          const int k = lane;
-          double akp = A[k * m + p], akq = A[k * m + q];
-          A[k * m + p] = cs * akp - sn * akq;
-          A[k * m + q] = sn * akp + cs * akq;
-          double vkp = V[k * m + p], vkq = V[k * m + q];
-          V[k * m + p] = cs * vkp - sn * vkq;
-          V[k * m + q] = sn * vkp + cs * vkq;
+    for (int r = 0; r < n - 1; ++r) {
+      __syncwarp();
+      if (lane < half) {
+        int p, q;
+        jacobi_pair(n, r, lane, p, q);
+        double c = 1.0, sv = 0.0;
+        if (q < m) {
+          const double apq = A[p * m + q];
+          if (apq != 0.0) {
+            const double app = A[p * m + p], aqq = A[q * m + q];
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            sv = t * c;
+          }
         }
-        __syncwarp();
-        if (lane < m) {
-          const int k = lane;
-          double apk = A[p * m + k], aqk = A[q * m + k];
-          A[p * m + k] = cs * apk - sn * aqk;
-          A[q * m + k] = sn * apk + cs * aqk;
-        }
-        __syncwarp();
+        pp[lane] = p; qq[lane] = q; cs[lane] = c; sn[lane] = sv;
       }
+      __syncwarp();
+      for (int it = lane; it < half * m; it += 32) {  // column pass
+        const int k = it / m, i = it % m, p = pp[k], q = qq[k];
+        if (q >= m || sn[k] == 0.0) continue;
+        const double c = cs[k], sv = sn[k];
+        double aip = A[i * m + p], aiq = A[i * m + q];
+        A[i * m + p] = c * aip - sv * aiq;
+        A[i * m + q] = sv * aip + c * aiq;
+        double vip = V[i * m + p], viq = V[i * m + q];
+        V[i * m + p] = c * vip - sv * viq;
+        V[i * m + q] = sv * vip + c * viq;
+      }
+      __syncwarp();
+      for (int it = lane; it < half * m; it += 32) {  // row pass
+        const int k = it / m, j = it % m, p = pp[k], q = qq[k];
+        if (q >= m || sn[k] == 0.0) continue;
+        const double c = cs[k], sv = sn[k];
+        double apj = A[p * m + j], aqj = A[q * m + j];
+        A[p * m + j] = c * apj - sv * aqj;
+        A[q * m + j] = sv * apj + c * aqj;
+      }
+      __syncwarp();
+    }
   }
   if (lane < m) ev[lane] = A[lane * m + lane];
   __syncwarp();
 }
-
 
 // physics.py:760-816; warp-collective.  Kc/evc: this block's eigen cache.
 __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, BlockWS &ws, double *W, double *Vc,
@@ -683,30 +714,37 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
       unsigned mask = 0u;
       for (int i = 0; i < na; ++i) mask |= 1u << ws.active[i];
       if (lane < na) ws.rhs[lane] = -ws.q[ws.active[lane]];
-      if ((double)mask != P[PMASK]) {
-        // eigendecomposition of K[A, A] (cache miss)
-        for (int e = lane; e < na * na; e += 32) W[e] = K[ws.active[e / na] * m + ws.active[e % na]];
+      // two cached decompositions per block, keyed by the active set
+      int slot = (double)mask == P[PMASK] ? 0 : ((double)mask == P[PMASK + 1] ? 1 : -1);
+      if (slot < 0) {
+        slot = (int)P[PREPL];
+        double *A = na <= kSmemEig ? ws.A : W;
+        double *Vt = na <= kSmemEig ? ws.V : Vc + slot * m * m;
+        for (int e = lane; e < na * na; e += 32) A[e] = K[ws.active[e / na] * m + ws.active[e % na]];
         __syncwarp();
-        sym_eig_warp(na, W, Vc, evc, lane);
-        if (lane == 0) P[PMASK] = (double)mask;
+        sym_eig_warp(na, A, Vt, evc + slot * m, ws.cs, ws.sn, ws.pp, ws.qq, lane);
+        if (na <= kSmemEig)
+          for (int e = lane; e < na * na; e += 32) Vc[slot * m * m + e] = Vt[e];
+        if (lane == 0) { P[PMASK + slot] = (double)mask; P[PREPL] = (double)(slot ^ 1); }
       }
       __syncwarp();
+      const double *Vs = Vc + slot * m * m, *es = evc + slot * m;
       // x = sum_k (V_k . b / ev_k) V_k over ev_k > rcond * max|ev| (oracle pinv_solve order)
       double smax = 0.0;
-      for (int i = 0; i < na; ++i) smax = fmax(smax, fabs(evc[i]));
+      for (int i = 0; i < na; ++i) smax = fmax(smax, fabs(es[i]));
       if (lane < na) {
         const int k = lane;
         double cc = 0.0;
-        for (int i = 0; i < na; ++i) cc += Vc[i * na + k] * ws.rhs[i];
-        ws.ck[k] = cc / evc[k];
+        for (int i = 0; i < na; ++i) cc += Vs[i * na + k] * ws.rhs[i];
+        ws.ck[k] = cc / es[k];
       }
       __syncwarp();
       if (lane < na) {
         const int i = lane;
         double x = 0.0;
         for (int k = 0; k < na; ++k) {
-          if (fabs(evc[k]) <= 1e-8 * smax) continue;
-          x += ws.ck[k] * Vc[i * na + k];
+          if (fabs(es[k]) <= 1e-8 * smax) continue;
+          x += ws.ck[k] * Vs[i * na + k];
         }
         ws.lam[ws.active[i]] = x;
       }
@@ -1139,7 +1177,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
       bool hask = m > 1 && c.rows[kRowD * first + RK] > 0.0;
       if (hask && m > kMaxBlockRows) return false;
       if (hask && koff + m * m > kKCap) return false;
-      if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; P[PMASK] = -1.0; }
+      if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; P[PMASK] = P[PMASK + 1] = -1.0; P[PREPL] = 0.0; }
       if (hask) {
         double *K = c.K + koff;
         const double *r0 = c.rows + kRowD * first;
@@ -1189,7 +1227,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
             __syncwarp();
           } else {
             const int koff = (int)P[PKOFF];
-            solve_block(c, g, first, m, c.K + koff, S.u.sol.ws, c.W, c.Vc + koff, c.evc + first);
+            solve_block(c, g, first, m, c.K + koff, S.u.sol.ws, c.W, c.Vc + 2 * koff, c.evc + 2 * first);
           }
         }
     }
@@ -1336,8 +1374,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, c
   c.pairs = c.rows + (size_t)B.row_cap * kRowD;
   c.K = c.pairs + kMaxGroups * kPairD;
   c.Vc = c.K + kKCap;
-  c.evc = c.Vc + kKCap;
-  c.W = c.evc + kMaxContacts;
+  c.evc = c.Vc + 2 * kKCap;
+  c.W = c.evc + 2 * kMaxContacts;
 
   // stage the state slab (coalesced)
   const double *gsd = B.sd + (size_t)env * L.dbl_size;
@@ -1397,7 +1435,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, c
 }
 
 __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
-  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 2 * kKCap + kMaxContacts + kMaxBlockRows * kMaxBlockRows;
+  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + kMaxBlockRows * kMaxBlockRows;
 }
 int step_row_cap() { return kMaxContacts; }
 
