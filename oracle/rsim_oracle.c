@@ -799,14 +799,20 @@ static void sym_eig(int m, double *A, double *V, double *ev) {
   for (int i = 0; i < m; ++i)
     for (int j = 0; j < m; ++j) V[i * m + j] = (i == j);
   for (int sweep = 0; sweep < 64 && m > 1; ++sweep) {
+    /* Frobenius norms as per-row partial sums, rows added in order (the GPU
+       computes one row per lane) */
     double off = 0.0, tot = 0.0;
-    for (int i = 0; i < m; ++i)
+    for (int i = 0; i < m; ++i) {
+      double ro = 0.0, rt = 0.0;
       for (int j = 0; j < m; ++j) {
         double a2 = A[i * m + j] * A[i * m + j];
-        tot += a2;
-        if (i != j) off += a2;
+        rt += a2;
+        if (i != j) ro += a2;
       }
-    if (off <= 1e-32 * tot || off == 0.0) break;
+      off += ro;
+      tot += rt;
+    }
+    if (off <= 1e-30 * tot || off == 0.0) break; /* off-diagonal <= 1e-15 of the Frobenius norm */
     for (int r = 0; r < n - 1; ++r) {
       for (int k = 0; k < n / 2; ++k) {
         int p, q;

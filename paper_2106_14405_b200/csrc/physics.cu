@@ -58,7 +58,7 @@ constexpr int kSmemEig = 12;  // eigensolver matrices live in shared memory up t
 struct BlockWS {
   double cur[kMaxBlockRows], q[kMaxBlockRows], lam[kMaxBlockRows], wv[kMaxBlockRows], rhs[kMaxBlockRows],
       ck[kMaxBlockRows];
-  double cs[kMaxBlockRows / 2], sn[kMaxBlockRows / 2];
+  double cs[kMaxBlockRows], sn[kMaxBlockRows];  // rotations (m/2) / row-norm scratch (m)
   int pp[kMaxBlockRows / 2], qq[kMaxBlockRows / 2];
   double A[kSmemEig * kSmemEig], V[kSmemEig * kSmemEig];
   int active[kMaxBlockRows];
@@ -628,14 +628,22 @@ __device__ void sym_eig_warp(int m, double *A, double *V, double *ev, double *cs
   for (int e = lane; e < m * m; e += 32) V[e] = (e / m == e % m);
   __syncwarp();
   for (int sweep = 0; sweep < 64 && m > 1; ++sweep) {
-    double off = 0.0, tot = 0.0;
-    for (int i = 0; i < m; ++i)
+    // Frobenius norms: row partial sums (lane per row), rows added in order
+    if (lane < m) {
+      double ro = 0.0, rt = 0.0;
       for (int j = 0; j < m; ++j) {
-        double a2 = A[i * m + j] * A[i * m + j];
-        tot += a2;
-        if (i != j) off += a2;
+        double a2 = A[lane * m + j] * A[lane * m + j];
+        rt += a2;
+        if (lane != j) ro += a2;
       }
-    if (off <= 1e-32 * tot || off == 0.0) break;
+      cs[lane] = ro;  // cs/sn double as row-sum scratch
+      sn[lane] = rt;
+    }
+    __syncwarp();
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < m; ++i) { off += cs[i]; tot += sn[i]; }
+    __syncwarp();
+    if (off <= 1e-30 * tot || off == 0.0) break;  // off-diagonal <= 1e-15 of the Frobenius norm
     for (int r = 0; r < n - 1; ++r) {
       __syncwarp();
       if (lane < half) {
