@@ -58,9 +58,12 @@ struct RenderSmem {
   Pose cam;
 };
 
-// ray vs one convex (reference _ray_halfspaces, one ray); face = entering plane
+// ray vs one convex (reference _ray_halfspaces, one ray); face = entering plane.
+// Division-free: the hit test te <= tx && tx >= 0 is evaluated as
+// be*sx >= bx*se && bx >= 0 (se < 0 < sx), and te = be/se is divided only when
+// the hit can matter (te < tcut, the caller's t_min + tie_eps).
 template <bool kBox>
-__device__ __forceinline__ double ray_convex(const double *pl, int nf, const double *d, int &face) {
+__device__ __forceinline__ double ray_convex(const double *pl, int nf, const double *d, double tcut, int &face) {
   int fe = -1, fx = -1;
   bool bad = false;
   double se = 0, be = 0, sx = 0, bx = 0;
@@ -85,12 +88,15 @@ __device__ __forceinline__ double ray_convex(const double *pl, int nf, const dou
       bad = true;
     }
   }
-  double te = fe >= 0 ? be / se : -INFINITY;
-  double tx = fx >= 0 ? bx / sx : INFINITY;
   face = -1;
-  if (!(te <= tx && tx >= 0.0) || bad) return INFINITY;
-  if (te >= 0.0) { face = fe; return te; }
-  return 0.0;
+  if (bad) return INFINITY;
+  if (fx >= 0 && bx < 0) return INFINITY;            // tx < 0
+  if (fe < 0) return 0.0;                             // no entering plane: origin inside (te = -inf)
+  if (fx >= 0 && be * sx < bx * se) return INFINITY;  // te > tx
+  if (be >= 0) return 0.0;                            // te <= 0: origin inside
+  if (be <= tcut * se) return INFINITY;               // te >= tcut: cannot matter
+  face = fe;
+  return be / se;
 }
 
 // reference _ray_sphere, one ray
@@ -104,16 +110,17 @@ __device__ __forceinline__ double ray_sphere(const PartW &p, const double *o, co
   return t0 >= 0.0 ? t0 : (t1 >= 0.0 ? 0.0 : INFINITY);
 }
 
-__device__ __forceinline__ double part_hit(const RenderSmem &S, int p, const double *o, const double *d, int &face) {
+__device__ __forceinline__ double part_hit(const RenderSmem &S, int p, const double *o, const double *d, int &face,
+                                           double tcut = INFINITY) {
   const PartW &P = S.part[p];
   double t;
   if (P.kind == RS_SPHERE) {
     face = -1;
     return ray_sphere(P, o, d);
   } else if (P.kind == RS_BOX) {
-    t = ray_convex<true>(S.plane + 4 * P.f0, 6, d, face);
+    t = ray_convex<true>(S.plane + 4 * P.f0, 6, d, tcut, face);
   } else {
-    t = ray_convex<false>(S.plane + 4 * P.f0, P.nf, d, face);
+    t = ray_convex<false>(S.plane + 4 * P.f0, P.nf, d, tcut, face);
   }
   if (face >= 0) face += P.f0;
   return t;
@@ -277,7 +284,8 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
       const int u = ux + (k % kTile), v = vy + (k / kTile);
       double dc[3] = {(u + 0.5 - W / 2.0) / f, (v + 0.5 - H / 2.0) / f, 1.0};
       double l = sqrt(dot3(dc, dc));
-      dc[0] /= l; dc[1] /= l; dc[2] /= l;
+      const double rl = 1.0 / l;
+      dc[0] *= rl; dc[1] *= rl; dc[2] *= rl;
       double d[3];
       matvec(S.cam.R, dc, d);
       double tmin = INFINITY, t2 = INFINITY;
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
         const PartW &P = S.part[p];
         if (P.lb > tmin + eps) break;  // sorted: nothing later can be nearer or tie
         int fc;
-        const double t = part_hit(S, p, o, d, fc);
+        const double t = part_hit(S, p, o, d, fc, tmin + eps);
         if (work) tests += P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf);
         if (!(t < INFINITY)) continue;
         const int b = P.body;
