@@ -181,6 +181,23 @@ int rs_step_host(rs_batch *batch, const double *h_arm_targets, const double *h_b
                  int32_t substeps, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                  double *h_out_stats, void *stream);
 
+/* Triangle-soup scene representation (AssetDef.visual_mesh scene.py:63-76,
+ * SURVEY.md §8a R3): per part a triangle list in the part frame with a BVH
+ * (paper_2106_14405_b200/mesh.py).  Must be attached before rs_batch_create. */
+typedef struct {
+  int32_t n_parts, n_tris, n_nodes;
+  const double *tri;             /* [n_tris][9]: v0, e1 = v1 - v0, e2 = v2 - v0 */
+  const float *node_lo, *node_hi; /* [n_nodes][3], rounded outward */
+  const int32_t *node_meta;      /* [n_nodes][2]: leaf (first_tri, count) | internal (right child, -1) */
+  const int32_t *part_node_begin; /* [n_parts + 1]: BVH root of each part */
+  const double *part_bound;      /* [n_parts]: bounding radius of the part mesh about its origin */
+} rs_mesh_desc;
+int rs_scene_set_mesh(rs_scene *scene, const rs_mesh_desc *mesh);
+
+/* RGBD render against the triangle soups (same outputs and conventions as
+ * rs_render; a camera inside a closed mesh sees its exit faces). */
+int rs_render_mesh(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream);
+
 /* Debug trace for parity tests (not on the hot path): when set, every rs_step
  * records per env and substep the admitted broadphase pairs in sorted order
  * with their narrowphase contact counts:

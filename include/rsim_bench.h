@@ -18,6 +18,9 @@ int rsim_bench_fma_peak(int fp64, double *tflops);
 struct rs_batch;
 int rsim_bench_render_work(struct rs_batch *batch, unsigned int cam_mask, unsigned long long *d_counter,
                            void *stream);
+/* same for rs_render_mesh: counts candidate-part BVH traversals */
+int rsim_bench_render_mesh_work(struct rs_batch *batch, unsigned int cam_mask, unsigned long long *d_counter,
+                                void *stream);
 
 #ifdef __cplusplus
 }

@@ -41,6 +41,38 @@ class rs_scene_desc(C.Structure):
     ]
 
 
+class rs_mesh_desc(C.Structure):
+    _fields_ = [("n_parts", C.c_int32), ("n_tris", C.c_int32), ("n_nodes", C.c_int32), ("tri", F64P),
+                ("node_lo", F32P), ("node_hi", F32P), ("node_meta", I32P), ("part_node_begin", I32P),
+                ("part_bound", F64P)]
+
+
+class MeshDesc:
+    """Owns the mesh arrays (paper_2106_14405_b200.mesh.compile_mesh) and the rs_mesh_desc view."""
+
+    def __init__(self, m: dict):
+        self.arrays = {
+            "tri": np.ascontiguousarray(m["tri"], np.float64),
+            "node_lo": np.ascontiguousarray(m["node_lo"], np.float32),
+            "node_hi": np.ascontiguousarray(m["node_hi"], np.float32),
+            "node_meta": np.ascontiguousarray(m["node_meta"], np.int32),
+            "part_node_begin": np.ascontiguousarray(m["part_node_begin"], np.int32),
+            "part_bound": np.ascontiguousarray(m["part_bound"], np.float64),
+        }
+        a = self.arrays
+        d = rs_mesh_desc()
+        d.n_parts = len(a["part_bound"])
+        d.n_tris = len(a["tri"])
+        d.n_nodes = len(a["node_meta"])
+        d.tri = _ptr(a["tri"], C.c_double)
+        d.node_lo = _ptr(a["node_lo"], C.c_float)
+        d.node_hi = _ptr(a["node_hi"], C.c_float)
+        d.node_meta = _ptr(a["node_meta"], C.c_int32)
+        d.part_node_begin = _ptr(a["part_node_begin"], C.c_int32)
+        d.part_bound = _ptr(a["part_bound"], C.c_double)
+        self.desc = d
+
+
 class rs_physics_config(C.Structure):
     _fields_ = [
         ("gravity", C.c_double), ("solver_iterations", C.c_int32),

@@ -17,6 +17,8 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
                         double dt, int substeps, cudaStream_t stream);
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                           cudaStream_t stream, unsigned long long *work = nullptr);
+cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                               cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_grasp(const DevBatch &B, const double *gripper, cudaStream_t stream);
 cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream);
 size_t step_scratch_doubles_per_env(int row_cap);
@@ -48,6 +50,7 @@ struct rs_batch {
   int32_t *d_env_scene = nullptr;
   std::vector<void *> allocs;
   int narm = 0;
+  bool has_mesh = false;
   // ping-pong state buffers: rs_step reads buf[cur] and writes buf[cur ^ 1]
   double *sd_buf[2] = {nullptr, nullptr};
   int32_t *si_buf[2] = {nullptr, nullptr};
@@ -150,6 +153,23 @@ int rs_scene_create(const rs_scene_desc *D, rs_scene **out) {
   return RS_OK;
 }
 
+int rs_scene_set_mesh(rs_scene *s, const rs_mesh_desc *M) {
+  if (!s || !M) return fail(RS_ERR_ARG, "null argument");
+  DevScene &d = s->d;
+  if (M->n_parts != d.np) return fail(RS_ERR_ARG, "mesh part count differs from the scene's");
+  int rc = 0;
+  if (!rc) rc = upload(s, M->tri, (size_t)9 * M->n_tris, &d.mtri);
+  if (!rc) rc = upload(s, M->node_lo, (size_t)3 * M->n_nodes, &d.node_lo);
+  if (!rc) rc = upload(s, M->node_hi, (size_t)3 * M->n_nodes, &d.node_hi);
+  if (!rc) rc = upload(s, M->node_meta, (size_t)2 * M->n_nodes, &d.node_meta);
+  if (!rc) rc = upload(s, M->part_node_begin, (size_t)M->n_parts + 1, &d.part_node_begin);
+  if (!rc) rc = upload(s, M->part_bound, (size_t)M->n_parts, &d.mesh_bound);
+  if (rc) return rc;
+  d.n_tri = M->n_tris;
+  d.n_nodes = M->n_nodes;
+  return RS_OK;
+}
+
 void rs_scene_destroy(rs_scene *s) {
   if (!s) return;
   for (void *p : s->allocs) cudaFree(p);
@@ -211,7 +231,11 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
     return rc;
   }
   std::vector<DevScene> hs(n_scenes);
-  for (int i = 0; i < n_scenes; ++i) hs[i] = scenes[i]->d;
+  b->has_mesh = true;
+  for (int i = 0; i < n_scenes; ++i) {
+    hs[i] = scenes[i]->d;
+    b->has_mesh = b->has_mesh && hs[i].mtri != nullptr;
+  }
   std::vector<int32_t> es(n_env, 0);
   if (env_scene) memcpy(es.data(), env_scene, sizeof(int32_t) * n_env);
   cudaError_t e1 = cudaMemcpy(b->d_scenes, hs.data(), sizeof(DevScene) * n_scenes, cudaMemcpyHostToDevice);
@@ -381,6 +405,15 @@ int rs_render(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32
   return RS_OK;
 }
 
+int rs_render_mesh(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream) {
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  if (cam_mask >> 2) return fail(RS_ERR_ARG, "camera mask selects a camera the robot does not have");
+  DevBatch v = b->view();
+  if (!b->has_mesh) return fail(RS_ERR_ARG, "scene has no mesh (rs_scene_set_mesh before rs_batch_create)");
+  CUDA_TRY(launch_render_mesh(v, cam_mask, rgba, depth, ids, (cudaStream_t)stream));
+  return RS_OK;
+}
+
 int rs_grasp(rs_batch *b, const double *gripper, void *stream) {
   if (!b || !gripper) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_grasp(b->view(), gripper, (cudaStream_t)stream));
@@ -433,5 +466,11 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
 int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
   if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
+  return RS_OK;
+}
+
+int rsim_bench_render_mesh_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
+  if (!b || !d_counter || !b->has_mesh) return fail(RS_ERR_ARG, "null argument or no mesh");
+  CUDA_TRY(launch_render_mesh(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
   return RS_OK;
 }

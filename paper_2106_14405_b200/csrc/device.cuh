@@ -45,6 +45,13 @@ struct DevScene {
   double nav_origin[2], nav_cell;
   const uint8_t *nav;
   const int32_t *clutter;  // clutter body ids (dynamic, after the robot)
+  // optional triangle-soup representation (rs_scene_set_mesh)
+  int n_tri, n_nodes;
+  const double *mtri;            // [n_tri][9]: v0, e1, e2 in the part frame
+  const float *node_lo, *node_hi;  // [n_nodes][3]
+  const int32_t *node_meta;      // [n_nodes][2]: leaf (first, count) | internal (right, -1)
+  const int32_t *part_node_begin;  // [np + 1] BVH root per part
+  const double *mesh_bound;      // [np] bounding radius of the part's mesh
 };
 
 // offsets (in doubles / int32s) inside one env's slabs

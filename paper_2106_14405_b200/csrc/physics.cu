@@ -1359,7 +1359,7 @@ __device__ void copy_through(const DevBatch &B, int env, int lane) {
   for (int i = lane; i < L.int_size; i += 32) y[i] = x[i];
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock) step_kernel(DevBatch B, const double *arm_targets,
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B, const double *arm_targets,
                                                                    const double *base_cmd, const uint8_t *has_targets,
                                                                    double dt, int substeps) {
   extern __shared__ __align__(16) unsigned char dsm[];

@@ -126,9 +126,73 @@ __device__ __forceinline__ double part_hit(const RenderSmem &S, int p, const dou
   return t;
 }
 
+
+// ---- triangle-soup path (AssetDef.visual_mesh, scene.py:63-76)
+// Part-local BVH traversal; two-sided Moller-Trumbore in scaled form so only
+// accepted hits are divided.  Triangles are stored as (v0, e1 = v1 - v0,
+// e2 = v2 - v0).  `face` returns the triangle index (for shading).
+__device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem &S, int p, const double *o,
+                                           const double *d, double tcut, int &face) {
+  const PartW &P = S.part[p];
+  const double *R = S.plane + 9 * p;  // mesh mode keeps part rotations here
+  double v[3] = {o[0] - P.c[0], o[1] - P.c[1], o[2] - P.c[2]}, ol[3], dl[3];
+  mattvec(R, v, ol);
+  mattvec(R, d, dl);
+  const double inv[3] = {1.0 / dl[0], 1.0 / dl[1], 1.0 / dl[2]};
+  double best = tcut;
+  face = -1;
+  int stack[40], sp = 0;
+  int node = sc.part_node_begin[p];
+  for (;;) {
+    const float *lo = sc.node_lo + 3 * node, *hi = sc.node_hi + 3 * node;
+    double tn = 0.0, tf = best;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double t0 = ((double)lo[a] - ol[a]) * inv[a], t1 = ((double)hi[a] - ol[a]) * inv[a];
+      if (t0 > t1) { double x = t0; t0 = t1; t1 = x; }
+      tn = t0 > tn ? t0 : tn;
+      tf = t1 < tf ? t1 : tf;
+    }
+    bool visit = tn <= tf;
+    const int2 meta = reinterpret_cast<const int2 *>(sc.node_meta)[node];
+    if (visit && meta.y >= 0) {  // leaf
+      for (int t = meta.x; t < meta.x + meta.y; ++t) {
+        const double *T = sc.mtri + 9 * t;
+        const double *v0 = T, *e1 = T + 3, *e2 = T + 6;
+        double pv[3];
+        cross3(dl, e2, pv);
+        const double det = dot3(e1, pv);
+        if (det == 0.0) continue;
+        const double sgn = det > 0 ? 1.0 : -1.0, adet = fabs(det);
+        double sv[3] = {ol[0] - v0[0], ol[1] - v0[1], ol[2] - v0[2]};
+        const double u = sgn * dot3(sv, pv);
+        if (u < 0.0 || u > adet) continue;
+        double qv[3];
+        cross3(sv, e1, qv);
+        const double w = sgn * dot3(dl, qv);
+        if (w < 0.0 || u + w > adet) continue;
+        const double tt = sgn * dot3(e2, qv);
+        if (tt < 0.0 || tt >= best * adet) continue;
+        best = tt / adet;
+        face = t;
+      }
+      visit = false;
+    }
+    if (visit) {  // internal: left child follows the node
+      stack[sp++] = meta.x;
+      node = node + 1;
+      continue;
+    }
+    if (sp == 0) break;
+    node = stack[--sp];
+  }
+  return face >= 0 ? best : INFINITY;
+}
+
 // exact lowest-id rule for near-tie pixels: bodies in id order, parts in order
-__device__ __noinline__ void resolve_tie(const RenderSmem &S, const uint32_t *mask, const double *o, const double *d,
-                                         double tmin, double eps, int &id, int &wpart, int &wface) {
+template <bool kMesh>
+__device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S, const uint32_t *mask, const double *o,
+                                         const double *d, double tmin, double eps, int &id, int &wpart, int &wface) {
   int cur_b = -1, cur_p = -1, cur_f = -1;
   double cur_t = INFINITY;
   for (int w = 0; w < kMaskWords; ++w) {
@@ -143,14 +207,15 @@ __device__ __noinline__ void resolve_tie(const RenderSmem &S, const uint32_t *ma
         cur_t = INFINITY;
       }
       int f;
-      double t = part_hit(S, p, o, d, f);
+      double t = kMesh ? mesh_hit(sc, S, p, o, d, INFINITY, f) : part_hit(S, p, o, d, f);
       if (t < cur_t) { cur_t = t; cur_p = p; cur_f = f; }
     }
   }
   if (cur_b >= 0 && cur_t <= tmin + eps) { id = cur_b; wpart = cur_p; wface = cur_f; }
 }
 
-__global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out,
+template <bool kMesh>
+__global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out,
                                                                 uint32_t *rgba, float *depth, int32_t *ids,
                                                                 unsigned long long *work) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -206,11 +271,16 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
     P.body = b;
     P.f0 = sc.part_facet_begin[p];
     P.nf = sc.part_facet_begin[p + 1] - P.f0;
-    P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : sc.part_bound[p];
+    if (kMesh) {
+      P.r = sc.mesh_bound[p];
+      for (int k = 0; k < 9; ++k) S.plane[9 * p + k] = wp.R[k];
+    } else {
+      P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : sc.part_bound[p];
+    }
     double v[3] = {wp.p[0] - o[0], wp.p[1] - o[1], wp.p[2] - o[2]};
     double dist = sqrt(dot3(v, v)) - P.r * (1.0 + 1e-9) - 1e-9;
     P.lb = dist > 0.0 ? dist : 0.0;
-    for (int f = P.f0; f < P.f0 + P.nf; ++f) {
+    for (int f = P.f0; f < P.f0 + (kMesh ? 0 : P.nf); ++f) {
       const double *F = sc.facet + 4 * f;
       double n[3];
       matvec(wp.R, F, n);
@@ -296,8 +366,8 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
         const PartW &P = S.part[p];
         if (P.lb > tmin + eps) break;  // sorted: nothing later can be nearer or tie
         int fc;
-        const double t = part_hit(S, p, o, d, fc, tmin + eps);
-        if (work) tests += P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf);
+        const double t = kMesh ? mesh_hit(sc, S, p, o, d, tmin + eps, fc) : part_hit(S, p, o, d, fc, tmin + eps);
+        if (work) tests += kMesh ? 1 : (P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf));
         if (!(t < INFINITY)) continue;
         const int b = P.body;
         if (b == id) {
@@ -309,7 +379,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
           t2 = t;
         }
       }
-      if (tmin < INFINITY && t2 - tmin <= eps) resolve_tie(S, S.mask[tile], o, d, tmin, eps, id, wpart, wface);
+      if (tmin < INFINITY && t2 - tmin <= eps) resolve_tie<kMesh>(sc, S, S.mask[tile], o, d, tmin, eps, id, wpart, wface);
 
       const size_t px = img + (size_t)v * W + u;
       if (!(tmin <= zfar)) {
@@ -323,7 +393,15 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
       if (rgba) {
         double cosv = 0.0;
         const PartW &P = S.part[wpart];
-        if (P.kind == RS_SPHERE) {
+        if (kMesh) {
+          if (wface >= 0) {  // |n.d| of the hit triangle (two-sided)
+            const double *T = sc.mtri + 9 * wface, *R = S.plane + 9 * wpart;
+            double nl[3], nw[3];
+            cross3(T + 3, T + 6, nl);
+            matvec(R, nl, nw);
+            cosv = fabs(dot3(nw, d)) / sqrt(dot3(nw, nw));
+          }
+        } else if (P.kind == RS_SPHERE) {
           if (tmin > 0.0) {
             double n[3];
             for (int i = 0; i < 3; ++i) n[i] = (o[i] + tmin * d[i] - P.c[i]) / P.r;
@@ -349,21 +427,32 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(DevBatch B, uint
 
 size_t render_smem_bytes() { return sizeof(RenderSmem); }
 
-cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
-                          cudaStream_t stream, unsigned long long *work) {
+template <bool kMesh>
+static cudaError_t launch_render_t(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                                   cudaStream_t stream, unsigned long long *work) {
   int n_cam_out = __builtin_popcount(cam_mask);
   if (n_cam_out == 0) return cudaSuccess;
   static bool configured = false;
   size_t smem = sizeof(RenderSmem);
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(render_kernel<kMesh>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   dim3 grid(B.n_env * n_cam_out);
-  render_kernel<<<grid, kRenderThreads, smem, stream>>>(B, cam_mask, n_cam_out, reinterpret_cast<uint32_t *>(rgba),
-                                                        depth, ids, work);
+  render_kernel<kMesh><<<grid, kRenderThreads, smem, stream>>>(B, cam_mask, n_cam_out,
+                                                              reinterpret_cast<uint32_t *>(rgba), depth, ids, work);
   return cudaGetLastError();
+}
+
+cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                          cudaStream_t stream, unsigned long long *work) {
+  return launch_render_t<false>(B, cam_mask, rgba, depth, ids, stream, work);
+}
+
+cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                               cudaStream_t stream, unsigned long long *work) {
+  return launch_render_t<true>(B, cam_mask, rgba, depth, ids, stream, work);
 }
 
 }  // namespace rsim

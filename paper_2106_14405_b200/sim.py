@@ -53,7 +53,7 @@ def _dptr(t: torch.Tensor | None):
 class BatchSimulator:
     def __init__(self, layouts=(0,), n_env: int = 1, clutter: list[str] | None = None, env_layout=None,
                  config: dict | None = None, render: dict | None = None, event_cap: int = 256,
-                 device: str | torch.device = "cuda"):
+                 device: str | torch.device = "cuda", mesh_k: int | None = None):
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise native.NativeLibraryError("BatchSimulator runs on CUDA devices only (no CPU fallback)")
@@ -77,10 +77,18 @@ class BatchSimulator:
         with torch.cuda.device(self.device):
             self._descs = [abi.SceneDesc(t) for t in self.tables]
             self._scenes = []
-            for d in self._descs:
+            self._meshes = []
+            for w, d in zip(self.worlds, self._descs):
                 h = C.c_void_p()
                 native.check(self.L.rs_scene_create(C.byref(d.desc), C.byref(h)), "rs_scene_create")
                 self._scenes.append(h)
+                if mesh_k is not None:
+                    from .mesh import compile_mesh
+
+                    md = abi.MeshDesc(compile_mesh(w, mesh_k))
+                    self._meshes.append(md)
+                    native.check(self.L.rs_scene_set_mesh(h, C.byref(md.desc)), "rs_scene_set_mesh")
+            self.n_triangles = len(self._meshes[0].arrays["tri"]) if self._meshes else None
             arr = (C.c_void_p * len(self._scenes))(*[h.value for h in self._scenes])
             b = C.c_void_p()
             native.check(self.L.rs_batch_create(arr, len(self._scenes), env_scene.ctypes.data, self.n_env,
@@ -222,6 +230,14 @@ class BatchSimulator:
         rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
         native.check(self.L.rs_render(self._batch, self.cam_mask(cams), _dptr(rgba), _dptr(depth), _dptr(ids),
                                       _stream_ptr()), "rs_render")
+        return rgba, depth, ids
+
+    def render_mesh(self, cams=("head", "arm"), out=None):
+        """Same as ``render`` against the triangle soups (``mesh_k`` at construction)."""
+        cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
+        rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
+        native.check(self.L.rs_render_mesh(self._batch, self.cam_mask(cams), _dptr(rgba), _dptr(depth), _dptr(ids),
+                                           _stream_ptr()), "rs_render_mesh")
         return rgba, depth, ids
 
     # ------------------------------------------------------- end-to-end (host)
