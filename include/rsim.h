@@ -18,6 +18,8 @@
  *   rs_step_host      <- pipeline.step (SPEC only)
  *                        physics + render with host buffers
  *   rs_grasp          <- grasp_rule + apply_grasp              robot.py:323-346, physics.py:1039-1079
+ *   rs_arm_action     <- apply_arm_action / solve_ik           robot.py:185-313
+ *   rs_render_mesh    <- render over AssetDef.visual_mesh      scene.py:63-76
  *
  * Conventions:
  *   - every call is stream-ordered on the cudaStream_t passed as `stream`
@@ -164,6 +166,13 @@ int rs_step(rs_batch *batch, const double *arm_targets, const double *base_cmd, 
  *   rgba [n_env][n_cam_out][H][W][4] u8, depth [..][H][W] f32, ids [..][H][W] i32;
  * n_cam_out = popcount(cam_mask); any output pointer may be NULL. */
 int rs_render(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream);
+
+/* End-effector action -> joint targets per env (robot.py:293-313
+ * apply_arm_action: clamp |delta| to 1.5 cm, damped-least-squares IK with the
+ * reference's deterministic restarts, robot.py:199-279).  Device pointers:
+ *   delta_ee [n_env][3] f64 (robot base frame), arm_targets [n_env][n_arm] f64 out,
+ *   ik_failed [n_env] i32 out (nullable; 1 = NoSolution -> targets = current joints). */
+int rs_arm_action(rs_batch *batch, const double *delta_ee, double *arm_targets, int32_t *ik_failed, void *stream);
 
 /* grasp transition per env between steps (robot.py:323-346 + physics.py:1055-1079):
  * gripper [n_env] f64 device; scalar > 0 snaps the nearest candidate within 0.15 m,

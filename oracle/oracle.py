@@ -54,6 +54,10 @@ def lib():
         L.orc_nearest_walkable.restype = C.c_int
         L.orc_nearest_walkable.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_void_p]
         L.orc_link_poses.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_solve_ik.restype = C.c_int
+        L.orc_solve_ik.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_apply_arm_action.restype = C.c_int
+        L.orc_apply_arm_action.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_snapshot_size.restype = C.c_int64
         L.orc_snapshot_size.argtypes = [C.c_int, C.c_int]
         _lib = L
@@ -138,6 +142,22 @@ class Oracle:
         out = np.zeros(2)
         lib().orc_nearest_walkable(self.h, x, y, out.ctypes.data)
         return out
+
+    def solve_ik(self, target, seed):
+        """(attempt index or -1, q) -- robot.solve_ik restated."""
+        t = np.ascontiguousarray(target, dtype=np.float64)
+        sd = np.ascontiguousarray(seed, dtype=np.float64)
+        out = np.zeros(len(sd))
+        r = lib().orc_solve_ik(self.h, t.ctypes.data, sd.ctypes.data, out.ctypes.data)
+        return r, (out if r >= 0 else sd.copy())
+
+    def apply_arm_action(self, q, delta):
+        """(joint targets, ik_failed) -- robot.apply_arm_action restated."""
+        qa = np.ascontiguousarray(q, dtype=np.float64)
+        d = np.ascontiguousarray(delta, dtype=np.float64)
+        out = np.zeros(len(qa))
+        f = lib().orc_apply_arm_action(self.h, qa.ctypes.data, d.ctypes.data, out.ctypes.data)
+        return out, bool(f)
 
     def link_poses(self, q, base):
         q = np.ascontiguousarray(q, dtype=np.float64)

@@ -1577,3 +1577,146 @@ int orc_render(const orc_world *w, const uint8_t *snap, int cam, const rs_render
   free(nw); free(dw); free(sc);
   return 0;
 }
+
+/* ------------------------------------------------------------------ IK */
+
+/* LAPACK dgesv-style solve (partial pivoting, first max) of the 3x3 system
+ * A X = B with nrhs columns (B row-major [3][nrhs]); np.linalg.solve. */
+static void solve3(const double *A_in, double *B, int nrhs) {
+  double A[9];
+  int piv[3];
+  memcpy(A, A_in, sizeof A);
+  for (int j = 0; j < 3; ++j) {
+    int p = j;
+    for (int i = j + 1; i < 3; ++i) if (fabs(A[3 * i + j]) > fabs(A[3 * p + j])) p = i;
+    piv[j] = p;
+    if (p != j) for (int k = 0; k < 3; ++k) { double t = A[3 * j + k]; A[3 * j + k] = A[3 * p + k]; A[3 * p + k] = t; }
+    double r = 1.0 / A[3 * j + j];
+    for (int i = j + 1; i < 3; ++i) A[3 * i + j] *= r;
+    for (int i = j + 1; i < 3; ++i)
+      for (int k = j + 1; k < 3; ++k) A[3 * i + k] -= A[3 * i + j] * A[3 * j + k];
+  }
+  for (int c = 0; c < nrhs; ++c) {
+    double x[3];
+    for (int i = 0; i < 3; ++i) x[i] = B[i * nrhs + c];
+    for (int j = 0; j < 3; ++j) if (piv[j] != j) { double t = x[j]; x[j] = x[piv[j]]; x[piv[j]] = t; }
+    for (int i = 1; i < 3; ++i) for (int k = 0; k < i; ++k) x[i] -= A[3 * i + k] * x[k];
+    for (int i = 2; i >= 0; --i) {
+      for (int k = i + 1; k < 3; ++k) x[i] -= A[3 * i + k] * x[k];
+      x[i] /= A[3 * i + i];
+    }
+    for (int i = 0; i < 3; ++i) B[i * nrhs + c] = x[i];
+  }
+}
+
+/* robot.py:199-221 one damped-least-squares attempt; returns 1 on success */
+static int dls_attempt(const orc_world *w, const double *target, const double *seed, double *q_out) {
+  const int n = w->narm;
+  const double tol = 5e-3, lam2 = 0.05 * 0.05, zero3[3] = {0, 0, 0};
+  double q[16], lo[16], hi[16], mid[16];
+  for (int i = 0; i < n; ++i) {
+    lo[i] = w->arm_limits[2 * i]; hi[i] = w->arm_limits[2 * i + 1];
+    mid[i] = 0.5 * (lo[i] + hi[i]);
+    q[i] = seed[i] < lo[i] ? lo[i] : (seed[i] > hi[i] ? hi[i] : seed[i]);
+  }
+  pose_t links[16], ee;
+  for (int it = 0; it <= 100; ++it) {
+    link_poses(w, q, zero3, links, &ee);
+    double err[3] = {target[0] - ee.p[0], target[1] - ee.p[1], target[2] - ee.p[2]};
+    if (sqrt(dot3(err, err)) < tol) { memcpy(q_out, q, 8 * n); return 1; }
+    if (it == 100) break;
+    double J[3 * 16], JT_sol[3 * 16], jjt[9];
+    for (int i = 0; i < n; ++i) {
+      double ax[3], d[3], c[3];
+      matvec(links[i].R, w->arm_axis + 3 * i, ax);
+      for (int k = 0; k < 3; ++k) d[k] = ee.p[k] - links[i].p[k];
+      cross(ax, d, c);
+      for (int k = 0; k < 3; ++k) J[k * n + i] = c[k];
+    }
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += J[a * n + i] * J[b * n + i];
+        jjt[3 * a + b] = s + (a == b ? lam2 : 0.0);
+      }
+    double y[3] = {err[0], err[1], err[2]};
+    solve3(jjt, y, 1);
+    memcpy(JT_sol, J, sizeof(double) * 3 * n);
+    solve3(jjt, JT_sol, n);  /* solve(jjt, J): [3][n] */
+    double dq[16], r[16];
+    for (int i = 0; i < n; ++i) dq[i] = J[0 * n + i] * y[0] + J[1 * n + i] * y[1] + J[2 * n + i] * y[2];
+    for (int i = 0; i < n; ++i) r[i] = mid[i] - q[i];
+    for (int i = 0; i < n; ++i) {
+      /* (I - J^T solve(jjt, J)) (mid - q), row i */
+      double s = 0.0;
+      for (int j = 0; j < n; ++j) {
+        double pij = J[0 * n + i] * JT_sol[0 * n + j] + J[1 * n + i] * JT_sol[1 * n + j] + J[2 * n + i] * JT_sol[2 * n + j];
+        s += ((i == j ? 1.0 : 0.0) - pij) * r[j];
+      }
+      dq[i] += 0.1 * s;
+    }
+    double step = 0.0;
+    for (int i = 0; i < n; ++i) step += dq[i] * dq[i];
+    step = sqrt(step);
+    if (step > 0.5) for (int i = 0; i < n; ++i) dq[i] *= 0.5 / step;
+    for (int i = 0; i < n; ++i) {
+      double v = q[i] + dq[i];
+      q[i] = v < lo[i] ? lo[i] : (v > hi[i] ? hi[i] : v);
+    }
+  }
+  return 0;
+}
+
+static const double RESTART[11][7] = {
+    {0.0, 0.25, 0.0, -0.35, 0.0, 0.3, 0.0},       {0.3, -0.2, 0.2, 0.3, -0.2, -0.3, 0.2},
+    {-0.3, 0.3, -0.25, -0.3, 0.25, 0.35, -0.2},   {0.15, 0.4, 0.3, 0.4, 0.3, -0.4, 0.3},
+    {-0.15, -0.35, -0.3, 0.45, -0.35, 0.4, -0.3}, {0.45, 0.1, 0.45, -0.45, 0.4, -0.1, 0.45},
+    {-0.45, -0.1, -0.45, 0.2, 0.45, 0.15, -0.45}, {0.6, 0.85, -0.8, -0.2, 0.7, 0.0, -0.3},
+    {-0.6, 0.85, 0.8, -0.2, -0.7, 0.0, 0.3},      {0.85, 0.9, -0.55, 0.3, 0.75, -0.25, 0.0},
+    {-0.85, 0.9, 0.55, 0.3, -0.75, 0.25, 0.0}};
+static const double WEYL[7] = {0.618034, 0.754878, 0.569840, 0.380110, 0.245122, 0.119409, 0.059683};
+
+/* robot.py:240-279 solve_ik; returns the attempt index that succeeded
+ * (0 = seed, 1..11 restarts, 12..35 Weyl spray) or -1 (NoSolution). */
+int orc_solve_ik(const orc_world *w, const double *target, const double *seed, double *q_out) {
+  const int n = w->narm;
+  /* reach check: shoulder = joint 0 offset; max reach = sum |offset_1..| + |gripper| */
+  double reach = 0.0;
+  for (int i = 1; i < n; ++i) reach += sqrt(dot3(w->arm_offset + 3 * i, w->arm_offset + 3 * i));
+  reach += sqrt(dot3(w->gripper, w->gripper));
+  double d[3] = {target[0] - w->arm_offset[0], target[1] - w->arm_offset[1], target[2] - w->arm_offset[2]};
+  if (sqrt(dot3(d, d)) > reach + 5e-3) return -1;
+  if (dls_attempt(w, target, seed, q_out)) return 0;
+  double lo[16], hi[16], mid[16], span[16], s[16];
+  for (int i = 0; i < n; ++i) {
+    lo[i] = w->arm_limits[2 * i]; hi[i] = w->arm_limits[2 * i + 1];
+    mid[i] = 0.5 * (lo[i] + hi[i]); span[i] = hi[i] - lo[i];
+  }
+  for (int r = 0; r < 11; ++r) {
+    for (int i = 0; i < n; ++i) s[i] = mid[i] + RESTART[r][i] * span[i] * 0.5;
+    if (dls_attempt(w, target, s, q_out)) return 1 + r;
+  }
+  double u[16];
+  for (int i = 0; i < n; ++i) u[i] = 0.5;
+  for (int r = 0; r < 24; ++r) {
+    for (int i = 0; i < n; ++i) { u[i] = fmod(u[i] + WEYL[i], 1.0); s[i] = lo[i] + u[i] * span[i]; }
+    if (dls_attempt(w, target, s, q_out)) return 12 + r;
+  }
+  return -1;
+}
+
+/* robot.py:293-313 apply_arm_action: clamp, FK (base frame), IK; on failure
+ * the targets are the current joints.  Returns 1 on IK failure. */
+int orc_apply_arm_action(const orc_world *w, const double *q, const double *delta, double *targets) {
+  const int n = w->narm;
+  double dl[3] = {delta[0], delta[1], delta[2]};
+  double nd = sqrt(dot3(dl, dl));
+  if (nd > 0.015) for (int k = 0; k < 3; ++k) dl[k] = dl[k] * (0.015 / nd);
+  const double zero3[3] = {0, 0, 0};
+  pose_t ee;
+  link_poses(w, q, zero3, NULL, &ee);
+  double target[3] = {ee.p[0] + dl[0], ee.p[1] + dl[1], ee.p[2] + dl[2]};
+  if (orc_solve_ik(w, target, q, targets) >= 0) return 0;
+  memcpy(targets, q, 8 * n);
+  return 1;
+}

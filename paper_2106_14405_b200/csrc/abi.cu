@@ -20,6 +20,7 @@ cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, f
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_grasp(const DevBatch &B, const double *gripper, cudaStream_t stream);
+cudaError_t launch_ik(const DevBatch &B, const double *delta, double *targets, int32_t *failed, cudaStream_t stream);
 cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream);
 size_t step_scratch_doubles_per_env(int row_cap);
 int step_row_cap();
@@ -411,6 +412,12 @@ int rs_render_mesh(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, 
   DevBatch v = b->view();
   if (!b->has_mesh) return fail(RS_ERR_ARG, "scene has no mesh (rs_scene_set_mesh before rs_batch_create)");
   CUDA_TRY(launch_render_mesh(v, cam_mask, rgba, depth, ids, (cudaStream_t)stream));
+  return RS_OK;
+}
+
+int rs_arm_action(rs_batch *b, const double *delta_ee, double *arm_targets, int32_t *ik_failed, void *stream) {
+  if (!b || !delta_ee || !arm_targets) return fail(RS_ERR_ARG, "null argument");
+  CUDA_TRY(launch_ik(b->view(), delta_ee, arm_targets, ik_failed, (cudaStream_t)stream));
   return RS_OK;
 }
 

@@ -1583,4 +1583,199 @@ cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ IK
+// robot.py:185-313 apply_arm_action -> solve_ik -> _dls_attempt, batched.
+// One warp per env: lane 0 runs the attempt from the current joints; if it
+// fails, the 11 restart seeds and the 24 Weyl-spray seeds run one per lane
+// and the lowest-index success wins (= the reference's sequential order).
+// Same operation order as oracle/rsim_oracle.c (this unit is -fmad=false).
+
+__device__ void ik_link_poses(const DevScene &sc, const double *q, Pose *links, Pose &ee) {
+  Pose t, off, rot;
+  const double zero3[3] = {0.0, 0.0, 0.0};
+  base3(zero3, t);
+  rot_z(0.0, off.R);
+  rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
+  for (int i = 0; i < sc.narm; ++i) {
+    off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
+    compose(t, off, t);
+    axis_angle_mat(sc.arm_axis + 3 * i, q[i], rot.R);
+    compose(t, rot, t);
+    if (links) links[i] = t;
+  }
+  Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}};
+  compose(t, g, ee);
+}
+
+__device__ void ik_solve3(const double *A_in, double *B, int nrhs) {
+  double A[9];
+  int piv[3];
+  for (int i = 0; i < 9; ++i) A[i] = A_in[i];
+  for (int j = 0; j < 3; ++j) {
+    int p = j;
+    for (int i = j + 1; i < 3; ++i) if (fabs(A[3 * i + j]) > fabs(A[3 * p + j])) p = i;
+    piv[j] = p;
+    if (p != j) for (int k = 0; k < 3; ++k) { double t = A[3 * j + k]; A[3 * j + k] = A[3 * p + k]; A[3 * p + k] = t; }
+    double r = 1.0 / A[3 * j + j];
+    for (int i = j + 1; i < 3; ++i) A[3 * i + j] *= r;
+    for (int i = j + 1; i < 3; ++i)
+      for (int k = j + 1; k < 3; ++k) A[3 * i + k] -= A[3 * i + j] * A[3 * j + k];
+  }
+  for (int c = 0; c < nrhs; ++c) {
+    double x[3];
+    for (int i = 0; i < 3; ++i) x[i] = B[i * nrhs + c];
+    for (int j = 0; j < 3; ++j) if (piv[j] != j) { double t = x[j]; x[j] = x[piv[j]]; x[piv[j]] = t; }
+    for (int i = 1; i < 3; ++i) for (int k = 0; k < i; ++k) x[i] -= A[3 * i + k] * x[k];
+    for (int i = 2; i >= 0; --i) {
+      for (int k = i + 1; k < 3; ++k) x[i] -= A[3 * i + k] * x[k];
+      x[i] /= A[3 * i + i];
+    }
+    for (int i = 0; i < 3; ++i) B[i * nrhs + c] = x[i];
+  }
+}
+
+// robot.py:199-221; one lane
+__device__ bool ik_dls_attempt(const DevScene &sc, const double *target, const double *seed, double *q_out) {
+  const int n = sc.narm;
+  const double tol = 5e-3, lam2 = 0.05 * 0.05;
+  double q[kMaxArm], lo[kMaxArm], hi[kMaxArm], mid[kMaxArm];
+  for (int i = 0; i < n; ++i) {
+    lo[i] = sc.arm_limits[2 * i]; hi[i] = sc.arm_limits[2 * i + 1];
+    mid[i] = 0.5 * (lo[i] + hi[i]);
+    q[i] = seed[i] < lo[i] ? lo[i] : (seed[i] > hi[i] ? hi[i] : seed[i]);
+  }
+  Pose links[kMaxArm], ee;
+  for (int it = 0; it <= 100; ++it) {
+    ik_link_poses(sc, q, links, ee);
+    double err[3] = {target[0] - ee.p[0], target[1] - ee.p[1], target[2] - ee.p[2]};
+    if (sqrt(dot3(err, err)) < tol) {
+      for (int i = 0; i < n; ++i) q_out[i] = q[i];
+      return true;
+    }
+    if (it == 100) break;
+    double J[3 * kMaxArm], JS[3 * kMaxArm], jjt[9];
+    for (int i = 0; i < n; ++i) {
+      double ax[3], d[3], cc[3];
+      matvec(links[i].R, sc.arm_axis + 3 * i, ax);
+      for (int k = 0; k < 3; ++k) d[k] = ee.p[k] - links[i].p[k];
+      cross3(ax, d, cc);
+      for (int k = 0; k < 3; ++k) J[k * n + i] = cc[k];
+    }
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double sacc = 0.0;
+        for (int i = 0; i < n; ++i) sacc += J[a * n + i] * J[b * n + i];
+        jjt[3 * a + b] = sacc + (a == b ? lam2 : 0.0);
+      }
+    double y[3] = {err[0], err[1], err[2]};
+    ik_solve3(jjt, y, 1);
+    for (int i = 0; i < 3 * n; ++i) JS[i] = J[i];
+    ik_solve3(jjt, JS, n);
+    double dq[kMaxArm], r[kMaxArm];
+    for (int i = 0; i < n; ++i) dq[i] = J[0 * n + i] * y[0] + J[1 * n + i] * y[1] + J[2 * n + i] * y[2];
+    for (int i = 0; i < n; ++i) r[i] = mid[i] - q[i];
+    for (int i = 0; i < n; ++i) {
+      double sacc = 0.0;
+      for (int j = 0; j < n; ++j) {
+        double pij = J[0 * n + i] * JS[0 * n + j] + J[1 * n + i] * JS[1 * n + j] + J[2 * n + i] * JS[2 * n + j];
+        sacc += ((i == j ? 1.0 : 0.0) - pij) * r[j];
+      }
+      dq[i] += 0.1 * sacc;
+    }
+    double step = 0.0;
+    for (int i = 0; i < n; ++i) step += dq[i] * dq[i];
+    step = sqrt(step);
+    if (step > 0.5) for (int i = 0; i < n; ++i) dq[i] *= 0.5 / step;
+    for (int i = 0; i < n; ++i) {
+      double v = q[i] + dq[i];
+      q[i] = v < lo[i] ? lo[i] : (v > hi[i] ? hi[i] : v);
+    }
+  }
+  return false;
+}
+
+__constant__ double kRestart[11][7] = {
+    {0.0, 0.25, 0.0, -0.35, 0.0, 0.3, 0.0},       {0.3, -0.2, 0.2, 0.3, -0.2, -0.3, 0.2},
+    {-0.3, 0.3, -0.25, -0.3, 0.25, 0.35, -0.2},   {0.15, 0.4, 0.3, 0.4, 0.3, -0.4, 0.3},
+    {-0.15, -0.35, -0.3, 0.45, -0.35, 0.4, -0.3}, {0.45, 0.1, 0.45, -0.45, 0.4, -0.1, 0.45},
+    {-0.45, -0.1, -0.45, 0.2, 0.45, 0.15, -0.45}, {0.6, 0.85, -0.8, -0.2, 0.7, 0.0, -0.3},
+    {-0.6, 0.85, 0.8, -0.2, -0.7, 0.0, 0.3},      {0.85, 0.9, -0.55, 0.3, 0.75, -0.25, 0.0},
+    {-0.85, 0.9, 0.55, 0.3, -0.75, 0.25, 0.0}};
+__constant__ double kWeyl[7] = {0.618034, 0.754878, 0.569840, 0.380110, 0.245122, 0.119409, 0.059683};
+
+// seed of attempt a (0 = current joints, 1..11 restarts, 12..35 Weyl spray)
+__device__ void ik_seed(const DevScene &sc, int a, const double *q0, double *seed) {
+  const int n = sc.narm;
+  if (a == 0) { for (int i = 0; i < n; ++i) seed[i] = q0[i]; return; }
+  for (int i = 0; i < n; ++i) {
+    const double lo = sc.arm_limits[2 * i], hi = sc.arm_limits[2 * i + 1];
+    const double mid = 0.5 * (lo + hi), span = hi - lo;
+    if (a <= 11) {
+      seed[i] = mid + kRestart[a - 1][i] * span * 0.5;
+    } else {
+      double u = 0.5;
+      for (int r = 0; r <= a - 12; ++r) u = fmod(u + kWeyl[i], 1.0);
+      seed[i] = lo + u * span;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) ik_kernel(DevBatch B, const double *delta, double *targets, int32_t *failed) {
+  const int env = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (env >= B.n_env) return;
+  const DevScene &sc = B.scenes[B.env_scene[env]];
+  const StateLayout &L = B.L;
+  const double *sd = B.sd + (size_t)env * L.dbl_size;
+  const int n = sc.narm;
+  double q0[kMaxArm], target[3];
+  for (int i = 0; i < n; ++i) q0[i] = sd[L.joints + sc.nsj + i];
+  // clamp to 1.5 cm (robot.py:88-93) and form the base-frame target
+  {
+    double dl[3] = {delta[3 * env], delta[3 * env + 1], delta[3 * env + 2]};
+    double nd = sqrt(dot3(dl, dl));
+    if (nd > 0.015) for (int k = 0; k < 3; ++k) dl[k] = dl[k] * (0.015 / nd);
+    Pose ee;
+    ik_link_poses(sc, q0, nullptr, ee);
+    for (int k = 0; k < 3; ++k) target[k] = ee.p[k] + dl[k];
+  }
+  // reach check (robot.py:256-258)
+  double reach = 0.0;
+  for (int i = 1; i < n; ++i) reach += sqrt(dot3(sc.arm_offset + 3 * i, sc.arm_offset + 3 * i));
+  reach += sqrt(dot3(sc.gripper, sc.gripper));
+  double dd[3] = {target[0] - sc.arm_offset[0], target[1] - sc.arm_offset[1], target[2] - sc.arm_offset[2]};
+  const bool reachable = !(sqrt(dot3(dd, dd)) > reach + 5e-3);
+  double q[kMaxArm], seed[kMaxArm];
+  int win = -1;
+  if (reachable) {
+    bool ok = false;
+    if (lane == 0) ok = ik_dls_attempt(sc, target, q0, q);
+    if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
+      win = 0;
+    } else {
+      for (int base = 1; base < 36 && win < 0; base += 32) {
+        const int a = base + lane;
+        bool oka = false;
+        if (a < 36) {
+          ik_seed(sc, a, q0, seed);
+          oka = ik_dls_attempt(sc, target, seed, q);
+        }
+        unsigned m = __ballot_sync(0xffffffffu, oka);
+        if (m) win = base + __ffs(m) - 1;
+      }
+    }
+  }
+  const int src = win < 0 ? -1 : (win == 0 ? 0 : (win - 1) % 32);
+  for (int i = 0; i < n; ++i) {
+    double v = __shfl_sync(0xffffffffu, q[i], src < 0 ? 0 : src);
+    if (lane == 0) targets[(size_t)env * n + i] = win < 0 ? q0[i] : v;
+  }
+  if (lane == 0 && failed) failed[env] = win < 0 ? 1 : 0;
+}
+
+cudaError_t launch_ik(const DevBatch &B, const double *delta, double *targets, int32_t *failed, cudaStream_t stream) {
+  const int threads = 128, per_block = threads / 32;
+  ik_kernel<<<(B.n_env + per_block - 1) / per_block, threads, 0, stream>>>(B, delta, targets, failed);
+  return cudaGetLastError();
+}
+
 }  // namespace rsim

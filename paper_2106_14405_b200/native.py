@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 # every symbol include/rsim.h declares
 EXPORTS = ("rs_abi_version", "rs_last_error", "rs_snapshot_size", "rs_scene_create", "rs_scene_destroy",
            "rs_batch_create", "rs_batch_destroy", "rs_batch_buffers", "rs_set_state", "rs_get_state", "rs_step",
-           "rs_render", "rs_grasp", "rs_step_host", "rs_set_trace", "rs_scene_set_mesh", "rs_render_mesh")
+           "rs_render", "rs_grasp", "rs_step_host", "rs_set_trace", "rs_scene_set_mesh", "rs_render_mesh", "rs_arm_action")
 
 
 class NativeLibraryError(RuntimeError):
@@ -60,6 +60,7 @@ def lib():
     L.rs_set_trace.argtypes = [vp, vp, vp, i32, i32]
     L.rs_scene_set_mesh.argtypes = [vp, C.POINTER(abi.rs_mesh_desc)]
     L.rs_render_mesh.argtypes = [vp, u32, vp, vp, vp, vp]
+    L.rs_arm_action.argtypes = [vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("rs_abi_version", "rs_last_error", "rs_snapshot_size", "rs_scene_destroy",
                         "rs_batch_destroy"):

@@ -203,6 +203,17 @@ class BatchSimulator:
             out.extend((s, *map(int, p)) for p in pairs[env, s, :n])
         return out
 
+    # ------------------------------------------------------------- arm action
+    def arm_action(self, delta_ee: torch.Tensor, out: torch.Tensor | None = None, failed: torch.Tensor | None = None):
+        """EE displacement [E, 3] (robot base frame) -> joint targets [E, 7]
+        via the batched IK (robot.py:293-313 apply_arm_action)."""
+        d = self._dev(delta_ee, (self.n_env, 3), torch.float64)
+        out = out if out is not None else torch.empty((self.n_env, self.n_arm), dtype=torch.float64, device=self.device)
+        failed = failed if failed is not None else torch.empty(self.n_env, dtype=torch.int32, device=self.device)
+        native.check(self.L.rs_arm_action(self._batch, _dptr(d), _dptr(out), _dptr(failed), _stream_ptr()),
+                     "rs_arm_action")
+        return out, failed
+
     # ------------------------------------------------------------------ grasp
     def grasp(self, gripper: torch.Tensor):
         g = self._dev(gripper, (self.n_env,), torch.float64)

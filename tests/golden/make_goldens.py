@@ -504,9 +504,48 @@ def gen_kat():
     np.savez_compressed(os.path.join(OUT, "kat.npz"), **out)
 
 
+# --------------------------------------------------------------------------
+# IK / arm actions (robot.py:185-313)
+# --------------------------------------------------------------------------
+
+def gen_ik():
+    m = rb.default_model()
+    rng = np.random.default_rng(21)
+    lo, hi = m.limits_lo(), m.limits_hi()
+    qs, deltas, targets, fails = [], [], [], []
+    # (1) the action space: random joint states near rest, 1.5 cm-clamped EE deltas
+    for _ in range(150):
+        q = np.clip(m.resting_joints + rng.uniform(-0.6, 0.6, 7), lo, hi)
+        d = rng.uniform(-0.03, 0.03, 3)
+        st = {}
+        tg = rb.apply_arm_action(m, q, rb.ArmAction(d, 0.0), st)
+        qs.append(q); deltas.append(d); targets.append(tg.arm); fails.append(st.get("ik_failures", 0))
+    # (2) hard seeds: joints at limits / random over the box (restarts, Weyl spray, failures)
+    for _ in range(50):
+        q = rng.uniform(lo, hi)
+        d = rng.uniform(-0.015, 0.015, 3)
+        st = {}
+        tg = rb.apply_arm_action(m, q, rb.ArmAction(d, 0.0), st)
+        qs.append(q); deltas.append(d); targets.append(tg.arm); fails.append(st.get("ik_failures", 0))
+    # (3) direct solve_ik on far targets (reach failures and restarts)
+    sq, st_t, sres, sok = [], [], [], []
+    for _ in range(40):
+        seed = np.clip(m.resting_joints + rng.uniform(-1, 1, 7), lo, hi)
+        tgt = np.array([0.12, 0.0, 0.96]) + rng.uniform(-1.1, 1.1, 3)
+        try:
+            res, ok = rb.solve_ik(m, tgt, seed), True
+        except rb.NoSolution:
+            res, ok = seed, False
+        sq.append(seed); st_t.append(tgt); sres.append(res); sok.append(ok)
+    np.savez_compressed(os.path.join(OUT, "ik.npz"), meta=meta(), q=np.array(qs), delta=np.array(deltas),
+                        targets=np.array(targets), fails=np.array(fails), solve_seed=np.array(sq),
+                        solve_target=np.array(st_t), solve_q=np.array(sres), solve_ok=np.array(sok))
+    print(f"  ik: {len(qs)} actions ({sum(fails)} failures), {len(sq)} solves ({sum(sok)} ok)")
+
+
 if __name__ == "__main__":
     t0 = time.time()
-    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat"]
+    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
     blobs = tags = None
@@ -521,3 +560,5 @@ if __name__ == "__main__":
         gen_render(); print("render", time.time() - t0)
     if "kat" in what:
         gen_kat(); print("kat", time.time() - t0)
+    if "ik" in what:
+        gen_ik(); print("ik", time.time() - t0)

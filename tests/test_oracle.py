@@ -136,3 +136,19 @@ def test_nonfinite_state_faults_naming_body():
     st.pos[30, 1] = np.nan
     r = oracle_for(0).step(st.to_bytes(), g["arm"][0], g["base"][0])
     assert r.snapshot is None and r.fault == (1 << 16) | 30
+
+
+def test_ik_matches_reference():
+    """apply_arm_action / solve_ik (robot.py:185-313) vs the reference: same
+    success/failure, joint targets within 1e-9 rad (iterative DLS; the
+    reference's 3x3 solves go through LAPACK)."""
+    k = golden("ik.npz")
+    orc = oracle_for(0)
+    for q, d, tg, f in zip(k["q"], k["delta"], k["targets"], k["fails"]):
+        out, failed = orc.apply_arm_action(q, d)
+        assert failed == bool(f)
+        np.testing.assert_allclose(out, tg, rtol=0, atol=1e-9)
+    for seed, tgt, res, ok in zip(k["solve_seed"], k["solve_target"], k["solve_q"], k["solve_ok"]):
+        r, q = orc.solve_ik(tgt, seed)
+        assert (r >= 0) == bool(ok)
+        np.testing.assert_allclose(q, res, rtol=0, atol=1e-9)
