@@ -79,12 +79,16 @@ def idle_states(global_ids, pool):
 
 
 def action_table(n_env, n_steps, seed):
-    """[n_steps, n_env, 7] arm joint targets and [n_steps, n_env, 2] base commands."""
-    rest = np.array([0.0, 0.5, 0.0, -2.2, 0.0, 1.3, 0.0])
+    """[n_steps, n_env, 6] Idle random actions in the paper's action space
+    (§5.1): EE displacement U(-0.02, 0.02)^3 m (clamped
+    to 1.5 cm by the IK front end), gripper 0, base linear U(-0.5, 1) m/s,
+    angular U(-1, 1) rad/s."""
     rng = np.random.default_rng(seed)
-    arm = rest + rng.uniform(-0.3, 0.3, (n_steps, n_env, 7))
-    base = np.stack([rng.uniform(-0.5, 1.0, (n_steps, n_env)), rng.uniform(-1.0, 1.0, (n_steps, n_env))], axis=-1)
-    return arm, base
+    a = np.zeros((n_steps, n_env, 6))
+    a[..., :3] = rng.uniform(-0.02, 0.02, (n_steps, n_env, 3))
+    a[..., 4] = rng.uniform(-0.5, 1.0, (n_steps, n_env))
+    a[..., 5] = rng.uniform(-1.0, 1.0, (n_steps, n_env))
+    return a
 
 
 # ------------------------------------------------------------------- clocks
@@ -154,12 +158,16 @@ def _cpu_init():
 
 
 def _cpu_worker(args):
-    """Oracle env-steps (physics + 2 camera renders) in one worker process."""
-    layout, snap, arm, base, n = args
+    """Oracle env-steps (IK + physics + 2 camera renders) in one worker process."""
+    from paper_2106_14405_b200.state import WorldState
+
+    layout, snap, act, n = args
     orc = _ORC[layout]
     t0 = time.perf_counter()
     for k in range(n):
-        snap = orc.step(snap, arm[k], base[k]).snapshot
+        q = WorldState.from_bytes(snap).joints[4:]
+        tg, _ = orc.apply_arm_action(q, act[k, :3])
+        snap = orc.step(snap, tg, act[k, 4:]).snapshot
         orc.render(snap, 0)
         orc.render(snap, 1)
     return n, time.perf_counter() - t0, snap
@@ -179,8 +187,8 @@ class CpuOracle:
         self.pool = mp.get_context("spawn").Pool(self.cores, initializer=_cpu_init)
 
     def run(self, steps_per_core, seed):
-        arm, base = action_table(self.cores, steps_per_core, seed)
-        jobs = [(g % 3, self.states[g], arm[:, g], base[:, g], steps_per_core) for g in range(self.cores)]
+        act = action_table(self.cores, steps_per_core, seed)
+        jobs = [(g % 3, self.states[g], act[:, g], steps_per_core) for g in range(self.cores)]
         t0 = time.perf_counter()
         res = self.pool.map(_cpu_worker, jobs)
         wall = time.perf_counter() - t0
@@ -233,10 +241,12 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "idle env.step (physics 4x1/120 s + 2 cams 128x128 RGBD), one env-step per host core "
-                               "per step", "envs_per_step": cores, "layouts": "apt_{env%3}", "clutter": 20},
+        "config": {"workload": "idle env.step (dEE action -> IK, physics 4x1/120 s, 2 cams 128x128 RGBD), one "
+                               "env-step per host core per step", "envs_per_step": cores, "layouts": "apt_{env%3}",
+                   "clutter": 20},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{total_steps} env-steps of the C oracle restatement ({cpu_model()})"},
+                         "sample": f"{total_steps} env-steps (IK + physics + 2 renders) of the C oracle "
+                                   f"restatement ({cpu_model()})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -266,9 +276,8 @@ def run_b200(args):
     init_states = idle_states(gids, settled_pool())
     sim.set_state(init_states)
     n_tab = args.warmup + args.steps
-    arm_np, base_np = action_table(E, n_tab, seed=7 + rank)
-    arm_d = torch.tensor(arm_np, device=dev)
-    base_d = torch.tensor(base_np, device=dev)
+    act_np = action_table(E, n_tab, seed=7 + rank)
+    act_d = torch.tensor(act_np, device=dev)
     obs = sim.alloc_obs(("head", "arm"))
     stream = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)
@@ -286,7 +295,7 @@ def run_b200(args):
                 ev[3].record(side)
         if ev is not None:
             ev[0].record(stream)
-        sim.step_physics(arm_d[k], base_d[k])
+        sim.env_step(act_d[k])  # IK -> physics -> grasp rule
         if ev is not None:
             ev[1].record(stream)
         stream.wait_stream(side)
@@ -321,8 +330,7 @@ def run_b200(args):
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize(dev)
-    h_arm = torch.tensor(arm_np).pin_memory()
-    h_base = torch.tensor(base_np).pin_memory()
+    h_act = torch.tensor(act_np).pin_memory()
     h_stats = torch.empty((E, 4), dtype=torch.float64).pin_memory()
     if world > 1:
         dist.barrier()
@@ -332,7 +340,7 @@ def run_b200(args):
     e0.record(stream)
     for k in range(args.steps):
         h0 = time.perf_counter()
-        sim.step_host(h_arm[args.warmup + k], h_base[args.warmup + k], out=obs, h_stats=h_stats)
+        sim.env_step_host(h_act[args.warmup + k], out=obs, h_stats=h_stats)
         host_ms.append(1e3 * (time.perf_counter() - h0))
     e1.record(stream)
     torch.cuda.synchronize(dev)
@@ -380,12 +388,13 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (settled-clutter pool from the reference recipe, random idle actions)",
-            "config": {"workload": "configs[4] full step: physics 4x1/120 s + head+arm 128x128 RGBD, Idle; "
-                                   "render(s_t) interleaved with physics(s_t->s_t+1) (obs delay 1)",
+            "config": {"workload": "configs[4] full env step: dEE action -> IK, physics 4x1/120 s, grasp rule, "
+                                   "head+arm 128x128 RGBD; Idle; render(s_t) interleaved with "
+                                   "physics(s_t->s_t+1) (obs delay 1)",
                        "envs_per_gpu": E, "global_envs": total_envs, "layouts": "apt_{env%3}", "clutter": 20,
                        "parallelism": f"env-shard dp{world}",
                        "l2": "inputs > L2: 805 MB of RGBD/id writes per step at 2048 envs evict the state slabs"},
-            "kernels_ms_per_step": {"step_kernel": ms_phys, "render_kernel": ms_rend},
+            "kernels_ms_per_step": {"ik+step+grasp": ms_phys, "render_kernel": ms_rend},
             "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak64.value,
                          "unit": "TFLOP/s", "frac": achieved / peak64.value if peak64.value else None,
                          "traffic": None,
@@ -399,16 +408,16 @@ def run_b200(args):
                          "executed_frac": (14.0 * executed_tests * E / (ms_dom * 1e-3) / 1e12 / peak64.value)
                          if dom == "render_kernel" and peak64.value else None,
                          "hbm_gbs_obs_writes": obs_bytes / (ms_rend * 1e-3) / 1e9},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(E * (7 + 2) * 8),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(E * 6 * 8),
                     "d2h_bytes_per_step": int(E * 4 * 8)},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 4 * args.steps,  # ik, step, grasp, render per env step
             "clocks": clk.summary(),
             "episode_stats_allreduce": {"accumulated_contact_force_sum": stats["acc"], "envs": int(stats["envs"])},
         }
         if world == 1 and not args.no_cpu_baseline:
             sps, cores, wall, steps = cpu_oracle_sps(args.cpu_baseline_steps)
             line["cpu_baseline"] = {"value": sps, "unit": UNIT, "cores": cores, "kind": "port",
-                                    "sample": f"{steps} env-steps (physics + 2 renders) of the C oracle, "
+                                    "sample": f"{steps} env-steps (IK + physics + 2 renders) of the C oracle, "
                                               f"{args.cpu_baseline_steps} per core, {wall:.1f} s wall, {cpu_model()}"}
         print(json.dumps(line), flush=True)
     sim.close()

@@ -17,6 +17,7 @@
  *                        restated over geometry.parts_ray_hits geometry.py:772-776
  *   rs_step_host      <- pipeline.step (SPEC only)
  *                        physics + render with host buffers
+ *   rs_env_step[_host]<- pipeline.step with ArmAction/BaseAction SPEC.md:316, robot.py:84-104
  *   rs_grasp          <- grasp_rule + apply_grasp              robot.py:323-346, physics.py:1039-1079
  *   rs_arm_action     <- apply_arm_action / solve_ik           robot.py:185-313
  *   rs_render_mesh    <- render over AssetDef.visual_mesh      scene.py:63-76
@@ -173,6 +174,18 @@ int rs_render(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, i
  *   delta_ee [n_env][3] f64 (robot base frame), arm_targets [n_env][n_arm] f64 out,
  *   ik_failed [n_env] i32 out (nullable; 1 = NoSolution -> targets = current joints). */
 int rs_arm_action(rs_batch *batch, const double *delta_ee, double *arm_targets, int32_t *ik_failed, void *stream);
+
+/* The SPEC env step with the paper's action space (SPEC.md:316-324,
+ * PAPER.md §5.1): action [n_env][6] f64 device = (dx, dy, dz EE displacement
+ * in the robot base frame, gripper scalar, base linear m/s, base angular
+ * rad/s).  Runs rs_arm_action -> rs_step -> rs_grasp on `stream`. */
+int rs_env_step(rs_batch *batch, const double *action, double dt, int32_t substeps, void *stream);
+
+/* rs_env_step with a HOST action buffer, the observation o_t = render(s_t)
+ * rendered concurrently on an internal stream (observation delay 1,
+ * interleaved), and the per-env results of rs_step_host copied back. */
+int rs_env_step_host(rs_batch *batch, const double *h_action, double dt, int32_t substeps, uint32_t cam_mask,
+                     uint8_t *rgba, float *depth, int32_t *ids, double *h_out_stats, void *stream);
 
 /* grasp transition per env between steps (robot.py:323-346 + physics.py:1055-1079):
  * gripper [n_env] f64 device; scalar > 0 snaps the nearest candidate within 0.15 m,

@@ -19,8 +19,9 @@ cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, f
                           cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work = nullptr);
-cudaError_t launch_grasp(const DevBatch &B, const double *gripper, cudaStream_t stream);
-cudaError_t launch_ik(const DevBatch &B, const double *delta, double *targets, int32_t *failed, cudaStream_t stream);
+cudaError_t launch_grasp(const DevBatch &B, const double *gripper, int stride, cudaStream_t stream);
+cudaError_t launch_ik(const DevBatch &B, const double *delta, int stride, double *targets, int32_t *failed,
+                      cudaStream_t stream);
 cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream);
 size_t step_scratch_doubles_per_env(int row_cap);
 int step_row_cap();
@@ -63,7 +64,8 @@ struct rs_batch {
     return v;
   }
   // lazily allocated staging for rs_step_host
-  double *h_pin = nullptr, *d_act = nullptr, *d_stats = nullptr;
+  double *h_pin = nullptr, *d_act = nullptr, *d_stats = nullptr, *d_env_act = nullptr, *d_targets = nullptr;
+  int32_t *d_ik_failed = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -259,6 +261,9 @@ void rs_batch_destroy(rs_batch *b) {
   if (b->h_pin) cudaFreeHost(b->h_pin);
   if (b->d_act) cudaFree(b->d_act);
   if (b->d_stats) cudaFree(b->d_stats);
+  if (b->d_env_act) cudaFree(b->d_env_act);
+  if (b->d_targets) cudaFree(b->d_targets);
+  if (b->d_ik_failed) cudaFree(b->d_ik_failed);
   if (b->side) cudaStreamDestroy(b->side);
   if (b->ev_fork) cudaEventDestroy(b->ev_fork);
   if (b->ev_join) cudaEventDestroy(b->ev_join);
@@ -417,13 +422,13 @@ int rs_render_mesh(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, 
 
 int rs_arm_action(rs_batch *b, const double *delta_ee, double *arm_targets, int32_t *ik_failed, void *stream) {
   if (!b || !delta_ee || !arm_targets) return fail(RS_ERR_ARG, "null argument");
-  CUDA_TRY(launch_ik(b->view(), delta_ee, arm_targets, ik_failed, (cudaStream_t)stream));
+  CUDA_TRY(launch_ik(b->view(), delta_ee, 3, arm_targets, ik_failed, (cudaStream_t)stream));
   return RS_OK;
 }
 
 int rs_grasp(rs_batch *b, const double *gripper, void *stream) {
   if (!b || !gripper) return fail(RS_ERR_ARG, "null argument");
-  CUDA_TRY(launch_grasp(b->view(), gripper, (cudaStream_t)stream));
+  CUDA_TRY(launch_grasp(b->view(), gripper, 1, (cudaStream_t)stream));
   return RS_OK;
 }
 
@@ -479,5 +484,59 @@ int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d
 int rsim_bench_render_mesh_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
   if (!b || !d_counter || !b->has_mesh) return fail(RS_ERR_ARG, "null argument or no mesh");
   CUDA_TRY(launch_render_mesh(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
+  return RS_OK;
+}
+
+// ---- the SPEC env step with the paper's action space (§5.1)
+static int ensure_env_buffers(rs_batch *b) {
+  const int E = b->d.n_env;
+  if (!b->d_targets) {
+    CUDA_TRY(cudaMalloc(&b->d_targets, sizeof(double) * (size_t)E * b->narm));
+    CUDA_TRY(cudaMalloc(&b->d_ik_failed, sizeof(int32_t) * (size_t)E));
+    CUDA_TRY(cudaMalloc(&b->d_env_act, sizeof(double) * (size_t)E * 6));
+  }
+  if (!b->d_stats) {
+    CUDA_TRY(cudaMalloc(&b->d_stats, sizeof(double) * (size_t)E * 4));
+    CUDA_TRY(cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
+  }
+  return RS_OK;
+}
+
+int rs_env_step(rs_batch *b, const double *action, double dt, int32_t substeps, void *stream) {
+  if (!b || !action) return fail(RS_ERR_ARG, "null argument");
+  if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
+  int rc = ensure_env_buffers(b);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(launch_ik(b->view(), action, 6, b->d_targets, b->d_ik_failed, st));           // robot.py:293
+  CUDA_TRY(launch_step(b->view(), b->d_targets, action + 4, nullptr, dt, substeps, st));  // physics.py:575
+  b->cur ^= 1;
+  CUDA_TRY(launch_grasp(b->view(), action + 3, 6, st));                                   // robot.py:323
+  return RS_OK;
+}
+
+int rs_env_step_host(rs_batch *b, const double *h_action, double dt, int32_t substeps, uint32_t cam_mask,
+                     uint8_t *rgba, float *depth, int32_t *ids, double *h_out_stats, void *stream) {
+  if (!b || !h_action || !h_out_stats) return fail(RS_ERR_ARG, "null argument");
+  int rc = ensure_env_buffers(b);
+  if (rc) return rc;
+  const int E = b->d.n_env;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cam_mask) {  // o_t = render(s_t) on the side stream, concurrently with the step
+    CUDA_TRY(cudaEventRecord(b->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(b->side, b->ev_fork, 0));
+    rc = rs_render(b, cam_mask, rgba, depth, ids, b->side);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(b->ev_join, b->side));
+  }
+  CUDA_TRY(cudaMemcpyAsync(b->d_env_act, h_action, sizeof(double) * (size_t)E * 6, cudaMemcpyHostToDevice, st));
+  rc = rs_env_step(b, b->d_env_act, dt, substeps, stream);
+  if (rc) return rc;
+  CUDA_TRY(launch_stats(b->view(), b->d_stats, st));
+  CUDA_TRY(cudaMemcpyAsync(h_out_stats, b->d_stats, sizeof(double) * (size_t)E * 4, cudaMemcpyDeviceToHost, st));
+  if (cam_mask) CUDA_TRY(cudaStreamWaitEvent(st, b->ev_join, 0));
+  CUDA_TRY(cudaStreamSynchronize(st));
   return RS_OK;
 }

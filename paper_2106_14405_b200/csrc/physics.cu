@@ -1464,14 +1464,14 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
 // ------------------------------------------------------------------ grasp
 // robot.py:323-346 grasp_rule + physics.py:1039-1079 grasp_candidates /
 // apply_grasp; one thread per env, between control steps.
-__global__ void grasp_kernel(DevBatch B, const double *gripper) {
+__global__ void grasp_kernel(DevBatch B, const double *gripper, int stride) {
   const int env = blockIdx.x * blockDim.x + threadIdx.x;
   if (env >= B.n_env) return;
   const DevScene &sc = B.scenes[B.env_scene[env]];
   const StateLayout &L = B.L;
   double *sd = B.sd + (size_t)env * L.dbl_size;
   int32_t *si = B.si + (size_t)env * L.int_size;
-  const double g = gripper[env];
+  const double g = gripper[(size_t)stride * env];
   const bool holding = si[L.held] >= 0;
   if (g < 0 && holding) {
     int h = si[L.held];
@@ -1573,8 +1573,8 @@ __global__ void stats_kernel(DevBatch B, double *out) {
   out[4 * env + 3] = (double)asleep;
 }
 
-cudaError_t launch_grasp(const DevBatch &B, const double *gripper, cudaStream_t stream) {
-  grasp_kernel<<<(B.n_env + 127) / 128, 128, 0, stream>>>(B, gripper);
+cudaError_t launch_grasp(const DevBatch &B, const double *gripper, int stride, cudaStream_t stream) {
+  grasp_kernel<<<(B.n_env + 127) / 128, 128, 0, stream>>>(B, gripper, stride);
   return cudaGetLastError();
 }
 
@@ -1720,7 +1720,8 @@ __device__ void ik_seed(const DevScene &sc, int a, const double *q0, double *see
   }
 }
 
-__global__ void __launch_bounds__(128) ik_kernel(DevBatch B, const double *delta, double *targets, int32_t *failed) {
+__global__ void __launch_bounds__(128) ik_kernel(DevBatch B, const double *delta, int stride, double *targets,
+                                                 int32_t *failed) {
   const int env = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (env >= B.n_env) return;
   const DevScene &sc = B.scenes[B.env_scene[env]];
@@ -1731,7 +1732,7 @@ __global__ void __launch_bounds__(128) ik_kernel(DevBatch B, const double *delta
   for (int i = 0; i < n; ++i) q0[i] = sd[L.joints + sc.nsj + i];
   // clamp to 1.5 cm (robot.py:88-93) and form the base-frame target
   {
-    double dl[3] = {delta[3 * env], delta[3 * env + 1], delta[3 * env + 2]};
+    double dl[3] = {delta[(size_t)stride * env], delta[(size_t)stride * env + 1], delta[(size_t)stride * env + 2]};
     double nd = sqrt(dot3(dl, dl));
     if (nd > 0.015) for (int k = 0; k < 3; ++k) dl[k] = dl[k] * (0.015 / nd);
     Pose ee;
@@ -1772,9 +1773,10 @@ __global__ void __launch_bounds__(128) ik_kernel(DevBatch B, const double *delta
   if (lane == 0 && failed) failed[env] = win < 0 ? 1 : 0;
 }
 
-cudaError_t launch_ik(const DevBatch &B, const double *delta, double *targets, int32_t *failed, cudaStream_t stream) {
+cudaError_t launch_ik(const DevBatch &B, const double *delta, int stride, double *targets, int32_t *failed,
+                      cudaStream_t stream) {
   const int threads = 128, per_block = threads / 32;
-  ik_kernel<<<(B.n_env + per_block - 1) / per_block, threads, 0, stream>>>(B, delta, targets, failed);
+  ik_kernel<<<(B.n_env + per_block - 1) / per_block, threads, 0, stream>>>(B, delta, stride, targets, failed);
   return cudaGetLastError();
 }
 

@@ -50,18 +50,13 @@ struct PartW {
 
 struct RenderSmem {
   double plane[4 * 1024];  // n.xyz, b0 per facet (world)
-  float4 plane32[1024];    // the same rounded to float32 (pass-1 prefilter)
   PartW part[kMaxParts];
   uint32_t mask[kMaxTiles][kMaskWords];
   uint8_t list[kMaxTiles][kMaxParts];  // per tile: candidate parts in ascending lb
   int nlist[kMaxTiles];
   uint8_t order[kMaxParts];
   Pose cam;
-  float camR32[9];
 };
-
-// camera-frame ray component of pixel index i (float32 pass)
-__device__ __forceinline__ float dcf(int i, int n, double f) { return (float)((i + 0.5 - n / 2.0) / f); }
 
 // ray vs one convex (reference _ray_halfspaces, one ray); face = entering plane.
 // Division-free: the hit test te <= tx && tx >= 0 is evaluated as
@@ -104,6 +99,38 @@ __device__ __forceinline__ double ray_convex(const double *pl, int nf, const dou
   return be / se;
 }
 
+// ray vs one box part (6 planes stored +x +y +z -x -y -z): the same rule
+// per axis and branch-free.  For axis k with s = d.n_k, the entering plane is
+// +k when s < 0 (else -k) and the exiting plane the other one; both ratios
+// have denominator |s|, so the arg-max / arg-min over the 3 axes compares
+// cross products, and te = -b_e / |s_e| is divided only for hits that matter.
+__device__ __forceinline__ double ray_box(const double *pl, const double *d, double tcut, int &face) {
+  bool bad = false, has = false;
+  double aE = 0, bE = 0, aX = 0, bX = 0;
+  int fE = -1;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double sv = d[0] * pl[4 * k] + d[1] * pl[4 * k + 1] + d[2] * pl[4 * k + 2];
+    const double bp = pl[4 * k + 3], bm = pl[4 * (k + 3) + 3];
+    const bool par = !(sv < -kParallelEps) && !(sv > kParallelEps);
+    bad |= par && (bp < 0 || bm < 0);
+    if (par) continue;
+    const double a = fabs(sv), be = sv < 0 ? bp : bm, bx = sv < 0 ? bm : bp;
+    if (!has || be * aE < bE * a) { aE = a; bE = be; fE = sv < 0 ? k : k + 3; }  // -be/a > -bE/aE
+    if (!has || bx * aX < bX * a) { aX = a; bX = bx; }                           //  bx/a <  bX/aX
+    has = true;
+  }
+  face = -1;
+  if (bad) return INFINITY;
+  if (!has) return 0.0;                        // every slab parallel and containing the origin
+  if (bX < 0) return INFINITY;                 // tx < 0
+  if (-bE * aX > bX * aE) return INFINITY;     // te > tx
+  if (bE >= 0) return 0.0;                     // te <= 0: origin inside
+  if (-bE >= tcut * aE) return INFINITY;       // te >= tcut: cannot matter
+  face = fE;
+  return -bE / aE;
+}
+
 // reference _ray_sphere, one ray
 __device__ __forceinline__ double ray_sphere(const PartW &p, const double *o, const double *d) {
   double oc[3] = {o[0] - p.c[0], o[1] - p.c[1], o[2] - p.c[2]};
@@ -123,7 +150,7 @@ __device__ __forceinline__ double part_hit(const RenderSmem &S, int p, const dou
     face = -1;
     return ray_sphere(P, o, d);
   } else if (P.kind == RS_BOX) {
-    t = ray_convex<true>(S.plane + 4 * P.f0, 6, d, tcut, face);
+    t = ray_box(S.plane + 4 * P.f0, d, tcut, face);
   } else {
     t = ray_convex<false>(S.plane + 4 * P.f0, P.nf, d, tcut, face);
   }
@@ -194,55 +221,6 @@ __device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem 
   return face >= 0 ? best : INFINITY;
 }
 
-
-// ---- float32 prefilter (pass 1).  Returns 0 = certainly no hit, 1 = certain
-// hit with the float64 range t inside [tlo, thi], 2 = undecided (possible hit,
-// t >= tlo).  Error model: |ds| <= 6e-7 (float ray and normals), |db| <=
-// 2e-7 |b| (b0 rounding), so a plane ratio r = b/s is within
-// 1e-6 (1 + |b| + |r|) / |s| of its float64 value (>= 2x margin); planes
-// with |s| <= 1e-6 (float64 parallel test undecidable) make the part undecided.
-template <bool kBox>
-__device__ __forceinline__ int ray_convex32(const float4 *pl, int nf, const float *d, float &tlo, float &thi) {
-  float te = -INFINITY, tx = INFINITY, ee = 0.f, ex = 0.f;
-  bool has_e = false, has_x = false;
-  if (kBox) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float4 P = pl[k], M = pl[k + 3];
-      const float sv = d[0] * P.x + d[1] * P.y + d[2] * P.z;
-      const float a = fabsf(sv);
-      if (a <= 1e-6f) { tlo = 0.f; return 2; }
-      const float be = sv < 0.f ? P.w : M.w, bx = sv < 0.f ? M.w : P.w;
-      const float inv = __frcp_rn(a);
-      const float re = -be * inv, rx = bx * inv;
-      te = fmaxf(te, re); ee = fmaxf(ee, 1e-6f * (1.f + fabsf(be) + fabsf(re)) * inv);
-      tx = fminf(tx, rx); ex = fmaxf(ex, 1e-6f * (1.f + fabsf(bx) + fabsf(rx)) * inv);
-    }
-    has_e = has_x = true;
-  } else {
-#pragma unroll 1
-    for (int f = 0; f < nf; ++f) {
-      const float4 P = pl[f];
-      const float sv = d[0] * P.x + d[1] * P.y + d[2] * P.z;
-      const float a = fabsf(sv);
-      if (a <= 1e-6f) { tlo = 0.f; return 2; }
-      const float inv = __frcp_rn(a);
-      const float r = P.w * (sv < 0.f ? -inv : inv);
-      const float er = 1e-6f * (1.f + fabsf(P.w) + fabsf(r)) * inv;
-      if (sv < 0.f) { te = fmaxf(te, r); ee = fmaxf(ee, er); has_e = true; }
-      else { tx = fminf(tx, r); ex = fmaxf(ex, er); has_x = true; }
-    }
-  }
-  // reference hit rule: te <= tx && tx >= 0; t = max(te, 0)
-  if (has_x && tx + ex < 0.f) return 0;
-  if (has_e && has_x && te - ee > tx + ex) return 0;
-  tlo = has_e ? fmaxf(te - ee, 0.f) : 0.f;
-  const bool sure = (!has_x || tx - ex >= 0.f) && (!has_e || !has_x || te + ee < tx - ex);
-  if (!sure) return 2;
-  thi = has_e ? fmaxf(te + ee, 0.f) : 0.f;
-  return 1;
-}
-
 // exact lowest-id rule for near-tie pixels: bodies in id order, parts in order
 template <bool kMesh>
 __device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S, const uint32_t *mask, const double *o,
@@ -307,7 +285,6 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(DevBatch B, u
     }
     pose_load12(sc.cam_mount + 12 * cam, mount);
     compose(parent, mount, S.cam);
-    for (int k = 0; k < 9; ++k) S.camR32[k] = (float)S.cam.R[k];
   }
   __syncthreads();
   const double *o = S.cam.p;
@@ -343,7 +320,6 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(DevBatch B, u
       double *Q = S.plane + 4 * f;
       Q[0] = n[0]; Q[1] = n[1]; Q[2] = n[2];
       Q[3] = dw - dot3(o, n);
-      S.plane32[f] = make_float4((float)Q[0], (float)Q[1], (float)Q[2], (float)Q[3]);
     }
   }
   const int W = B.rcfg.width, H = B.rcfg.height;
@@ -416,48 +392,8 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(DevBatch B, u
       matvec(S.cam.R, dc, d);
       double tmin = INFINITY, t2 = INFINITY;
       int id = -1, wpart = -1, wface = -1;
-      // pass 1 (proxy path): float32 prefilter -> contender set (bitmask over list slots)
-      uint32_t cmask[kMaskWords] = {0u, 0u, 0u, 0u};
-      if (!kMesh) {
-        const float d32[3] = {(float)(S.camR32[0] * dcf(u, W, f) + S.camR32[1] * dcf(v, H, f) + S.camR32[2]),
-                              (float)(S.camR32[3] * dcf(u, W, f) + S.camR32[4] * dcf(v, H, f) + S.camR32[5]),
-                              (float)(S.camR32[6] * dcf(u, W, f) + S.camR32[7] * dcf(v, H, f) + S.camR32[8])};
-        const float nrm = rsqrtf(d32[0] * d32[0] + d32[1] * d32[1] + d32[2] * d32[2]);
-        const float dn[3] = {d32[0] * nrm, d32[1] * nrm, d32[2] * nrm};
-        double thi_min = INFINITY;
-#pragma unroll 1
-        for (int j = 0; j < nl; ++j) {
-          const int p = list[j];
-          const PartW &P = S.part[p];
-          if (P.lb > thi_min + eps) break;
-          float tlo = 0.f, thi = INFINITY;
-          int r;
-          if (P.kind == RS_SPHERE) {
-            r = 2;
-            tlo = (float)P.lb;
-          } else if (P.kind == RS_BOX) {
-            r = ray_convex32<true>(S.plane32 + P.f0, 6, dn, tlo, thi);
-          } else {
-            r = ray_convex32<false>(S.plane32 + P.f0, P.nf, dn, tlo, thi);
-          }
-          if (work) tests += P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 3 : P.nf);
-          if (r == 0) continue;
-          if (r == 1 && (double)thi < thi_min) thi_min = (double)thi;
-          if ((double)tlo <= thi_min + eps) cmask[j >> 5] |= 1u << (j & 31);
-        }
-      }
-      // pass 2: float64 exact walk (over the contenders on the proxy path)
 #pragma unroll 1
       for (int j = 0; j < nl; ++j) {
-        if (!kMesh) {
-          // jump to the next contender slot
-          int w = j >> 5;
-          uint32_t m = cmask[w] & (0xffffffffu << (j & 31));
-          while (!m && ++w < kMaskWords) m = cmask[w];
-          if (!m) break;
-          j = (w << 5) + __ffs(m) - 1;
-          if (j >= nl) break;
-        }
         const int p = list[j];
         const PartW &P = S.part[p];
         if (P.lb > tmin + eps) break;  // sorted: nothing later can be nearer or tie

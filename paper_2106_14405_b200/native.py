@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "lib
 # every symbol include/rsim.h declares
 EXPORTS = ("rs_abi_version", "rs_last_error", "rs_snapshot_size", "rs_scene_create", "rs_scene_destroy",
            "rs_batch_create", "rs_batch_destroy", "rs_batch_buffers", "rs_set_state", "rs_get_state", "rs_step",
-           "rs_render", "rs_grasp", "rs_step_host", "rs_set_trace", "rs_scene_set_mesh", "rs_render_mesh", "rs_arm_action")
+           "rs_render", "rs_grasp", "rs_step_host", "rs_set_trace", "rs_scene_set_mesh", "rs_render_mesh", "rs_arm_action", "rs_env_step", "rs_env_step_host")
 
 
 class NativeLibraryError(RuntimeError):
@@ -61,6 +61,8 @@ def lib():
     L.rs_scene_set_mesh.argtypes = [vp, C.POINTER(abi.rs_mesh_desc)]
     L.rs_render_mesh.argtypes = [vp, u32, vp, vp, vp, vp]
     L.rs_arm_action.argtypes = [vp, vp, vp, vp, vp]
+    L.rs_env_step.argtypes = [vp, vp, dbl, i32, vp]
+    L.rs_env_step_host.argtypes = [vp, vp, dbl, i32, u32, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("rs_abi_version", "rs_last_error", "rs_snapshot_size", "rs_scene_destroy",
                         "rs_batch_destroy"):

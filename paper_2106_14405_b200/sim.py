@@ -214,6 +214,26 @@ class BatchSimulator:
                      "rs_arm_action")
         return out, failed
 
+    # ------------------------------------------------------------- env step
+    def env_step(self, action: torch.Tensor, dt: float = 1.0 / 30.0, substeps: int = 4):
+        """Paper action space [E, 6] = (dEE xyz, gripper, base lin, base ang) on
+        device: IK -> physics -> grasp rule (rs_env_step)."""
+        a = self._dev(action, (self.n_env, 6), torch.float64)
+        native.check(self.L.rs_env_step(self._batch, _dptr(a), float(dt), int(substeps), _stream_ptr()),
+                     "rs_env_step")
+
+    def env_step_host(self, h_action: torch.Tensor, cams=("head", "arm"), out=None, h_stats=None,
+                      dt: float = 1.0 / 30.0, substeps: int = 4):
+        """rs_env_step_host: host [E, 6] actions, o_t rendered concurrently, host stats back."""
+        cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
+        rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
+        if h_stats is None:
+            h_stats = torch.empty((self.n_env, 4), dtype=torch.float64).pin_memory()
+        native.check(self.L.rs_env_step_host(self._batch, C.c_void_p(h_action.data_ptr()), float(dt), int(substeps),
+                                             self.cam_mask(cams), _dptr(rgba), _dptr(depth), _dptr(ids),
+                                             C.c_void_p(h_stats.data_ptr()), _stream_ptr()), "rs_env_step_host")
+        return h_stats
+
     # ------------------------------------------------------------------ grasp
     def grasp(self, gripper: torch.Tensor):
         g = self._dev(gripper, (self.n_env,), torch.float64)
