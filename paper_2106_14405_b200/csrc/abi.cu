@@ -13,15 +13,15 @@
 #include "device.cuh"
 
 namespace rsim {
-cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, const uint8_t *has_targets,
-                        double dt, int substeps, cudaStream_t stream);
+cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
+                        const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream);
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                           cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_grasp(const DevBatch &B, const double *gripper, int stride, cudaStream_t stream);
 cudaError_t launch_ik(const DevBatch &B, const double *delta, int stride, double *targets, int32_t *failed,
-                      cudaStream_t stream);
+                      double *scratch, cudaStream_t stream);
 cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream);
 size_t step_scratch_doubles_per_env(int row_cap);
 int step_row_cap();
@@ -66,6 +66,7 @@ struct rs_batch {
   // lazily allocated staging for rs_step_host
   double *h_pin = nullptr, *d_act = nullptr, *d_stats = nullptr, *d_env_act = nullptr, *d_targets = nullptr;
   int32_t *d_ik_failed = nullptr;
+  double *d_ik_scratch = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -264,6 +265,7 @@ void rs_batch_destroy(rs_batch *b) {
   if (b->d_env_act) cudaFree(b->d_env_act);
   if (b->d_targets) cudaFree(b->d_targets);
   if (b->d_ik_failed) cudaFree(b->d_ik_failed);
+  if (b->d_ik_scratch) cudaFree(b->d_ik_scratch);
   if (b->side) cudaStreamDestroy(b->side);
   if (b->ev_fork) cudaEventDestroy(b->ev_fork);
   if (b->ev_join) cudaEventDestroy(b->ev_join);
@@ -399,7 +401,7 @@ int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
   if (!arm || !base_cmd) return fail(RS_ERR_ARG, "arm_targets and base_cmd are required device pointers");
-  CUDA_TRY(launch_step(b->view(), arm, base_cmd, has_targets, dt, substeps, (cudaStream_t)stream));
+  CUDA_TRY(launch_step(b->view(), arm, base_cmd, 2, has_targets, dt, substeps, (cudaStream_t)stream));
   b->cur ^= 1;
   return RS_OK;
 }
@@ -420,9 +422,16 @@ int rs_render_mesh(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, 
   return RS_OK;
 }
 
+static int ensure_ik_scratch(rs_batch *b) {
+  if (!b->d_ik_scratch) CUDA_TRY(cudaMalloc(&b->d_ik_scratch, sizeof(double) * ((size_t)b->d.n_env * 4 + 2)));
+  return RS_OK;
+}
+
 int rs_arm_action(rs_batch *b, const double *delta_ee, double *arm_targets, int32_t *ik_failed, void *stream) {
   if (!b || !delta_ee || !arm_targets) return fail(RS_ERR_ARG, "null argument");
-  CUDA_TRY(launch_ik(b->view(), delta_ee, 3, arm_targets, ik_failed, (cudaStream_t)stream));
+  int rc = ensure_ik_scratch(b);
+  if (rc) return rc;
+  CUDA_TRY(launch_ik(b->view(), delta_ee, 3, arm_targets, ik_failed, b->d_ik_scratch, (cudaStream_t)stream));
   return RS_OK;
 }
 
@@ -508,10 +517,11 @@ int rs_env_step(rs_batch *b, const double *action, double dt, int32_t substeps, 
   if (!b || !action) return fail(RS_ERR_ARG, "null argument");
   if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
   int rc = ensure_env_buffers(b);
+  if (!rc) rc = ensure_ik_scratch(b);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  CUDA_TRY(launch_ik(b->view(), action, 6, b->d_targets, b->d_ik_failed, st));           // robot.py:293
-  CUDA_TRY(launch_step(b->view(), b->d_targets, action + 4, nullptr, dt, substeps, st));  // physics.py:575
+  CUDA_TRY(launch_ik(b->view(), action, 6, b->d_targets, b->d_ik_failed, b->d_ik_scratch, st));  // robot.py:293
+  CUDA_TRY(launch_step(b->view(), b->d_targets, action + 4, 6, nullptr, dt, substeps, st));  // physics.py:575
   b->cur ^= 1;
   CUDA_TRY(launch_grasp(b->view(), action + 3, 6, st));                                   // robot.py:323
   return RS_OK;

@@ -1360,8 +1360,9 @@ __device__ void copy_through(const DevBatch &B, int env, int lane) {
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B, const double *arm_targets,
-                                                                   const double *base_cmd, const uint8_t *has_targets,
-                                                                   double dt, int substeps) {
+                                                                   const double *base_cmd, int base_stride,
+                                                                   const uint8_t *has_targets, double dt,
+                                                                   int substeps) {
   extern __shared__ __align__(16) unsigned char dsm[];
   WarpSmem *smem = reinterpret_cast<WarpSmem *>(dsm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1418,7 +1419,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   }
   const bool ht = has_targets == nullptr || has_targets[env];
   const double *arm = ht ? arm_targets + (size_t)env * sc.narm : nullptr;
-  const double *bc = base_cmd + (size_t)env * 2;
+  const double *bc = base_cmd + (size_t)env * base_stride;
   if (lane < kMaxArm) S.budget[lane] = B.cfg.motor_impulse_cap;
   __syncwarp();
   const double dts = dt / substeps;
@@ -1447,8 +1448,8 @@ __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
 }
 int step_row_cap() { return kMaxContacts; }
 
-cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, const uint8_t *has_targets,
-                        double dt, int substeps, cudaStream_t stream) {
+cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
+                        const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream) {
   static bool configured = false;
   const size_t smem = sizeof(WarpSmem) * kWarpsPerBlock;
   if (!configured) {
@@ -1457,7 +1458,7 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
     configured = true;
   }
   dim3 grid((B.n_env + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  step_kernel<<<grid, 32 * kWarpsPerBlock, smem, stream>>>(B, arm, base_cmd, has_targets, dt, substeps);
+  step_kernel<<<grid, 32 * kWarpsPerBlock, smem, stream>>>(B, arm, base_cmd, base_stride, has_targets, dt, substeps);
   return cudaGetLastError();
 }
 
@@ -1634,7 +1635,30 @@ __device__ void ik_solve3(const double *A_in, double *B, int nrhs) {
   }
 }
 
-// robot.py:199-221; one lane
+// FK for the IK loop: rotated joint axes, link origins and the EE position
+// (the values arm_jacobian reads, robot.py:185-192), without storing poses.
+__device__ void ik_fk(const DevScene &sc, const double *q, double (*ax)[3], double (*lp)[3], double *ee) {
+  Pose t, off, rot;
+  const double zero3[3] = {0.0, 0.0, 0.0};
+  base3(zero3, t);
+  rot_z(0.0, off.R);
+  rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
+  for (int i = 0; i < sc.narm; ++i) {
+    off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
+    compose(t, off, t);
+    axis_angle_mat(sc.arm_axis + 3 * i, q[i], rot.R);
+    compose(t, rot, t);
+    if (ax) {
+      matvec(t.R, sc.arm_axis + 3 * i, ax[i]);
+      lp[i][0] = t.p[0]; lp[i][1] = t.p[1]; lp[i][2] = t.p[2];
+    }
+  }
+  Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}}, e;
+  compose(t, g, e);
+  ee[0] = e.p[0]; ee[1] = e.p[1]; ee[2] = e.p[2];
+}
+
+// robot.py:199-221; one thread
 __device__ bool ik_dls_attempt(const DevScene &sc, const double *target, const double *seed, double *q_out) {
   const int n = sc.narm;
   const double tol = 5e-3, lam2 = 0.05 * 0.05;
@@ -1644,10 +1668,10 @@ __device__ bool ik_dls_attempt(const DevScene &sc, const double *target, const d
     mid[i] = 0.5 * (lo[i] + hi[i]);
     q[i] = seed[i] < lo[i] ? lo[i] : (seed[i] > hi[i] ? hi[i] : seed[i]);
   }
-  Pose links[kMaxArm], ee;
+  double ax[kMaxArm][3], lp[kMaxArm][3], ee[3];
   for (int it = 0; it <= 100; ++it) {
-    ik_link_poses(sc, q, links, ee);
-    double err[3] = {target[0] - ee.p[0], target[1] - ee.p[1], target[2] - ee.p[2]};
+    ik_fk(sc, q, ax, lp, ee);
+    double err[3] = {target[0] - ee[0], target[1] - ee[1], target[2] - ee[2]};
     if (sqrt(dot3(err, err)) < tol) {
       for (int i = 0; i < n; ++i) q_out[i] = q[i];
       return true;
@@ -1655,10 +1679,9 @@ __device__ bool ik_dls_attempt(const DevScene &sc, const double *target, const d
     if (it == 100) break;
     double J[3 * kMaxArm], JS[3 * kMaxArm], jjt[9];
     for (int i = 0; i < n; ++i) {
-      double ax[3], d[3], cc[3];
-      matvec(links[i].R, sc.arm_axis + 3 * i, ax);
-      for (int k = 0; k < 3; ++k) d[k] = ee.p[k] - links[i].p[k];
-      cross3(ax, d, cc);
+      double d[3], cc[3];
+      for (int k = 0; k < 3; ++k) d[k] = ee[k] - lp[i][k];
+      cross3(ax[i], d, cc);
       for (int k = 0; k < 3; ++k) J[k * n + i] = cc[k];
     }
     for (int a = 0; a < 3; ++a)
@@ -1676,9 +1699,9 @@ __device__ bool ik_dls_attempt(const DevScene &sc, const double *target, const d
     for (int i = 0; i < n; ++i) r[i] = mid[i] - q[i];
     for (int i = 0; i < n; ++i) {
       double sacc = 0.0;
-      for (int j = 0; j < n; ++j) {
-        double pij = J[0 * n + i] * JS[0 * n + j] + J[1 * n + i] * JS[1 * n + j] + J[2 * n + i] * JS[2 * n + j];
-        sacc += ((i == j ? 1.0 : 0.0) - pij) * r[j];
+      for (int jj = 0; jj < n; ++jj) {
+        double pij = J[0 * n + i] * JS[0 * n + jj] + J[1 * n + i] * JS[1 * n + jj] + J[2 * n + i] * JS[2 * n + jj];
+        sacc += ((i == jj ? 1.0 : 0.0) - pij) * r[jj];
       }
       dq[i] += 0.1 * sacc;
     }
@@ -1720,63 +1743,80 @@ __device__ void ik_seed(const DevScene &sc, int a, const double *q0, double *see
   }
 }
 
-__global__ void __launch_bounds__(128) ik_kernel(DevBatch B, const double *delta, int stride, double *targets,
-                                                 int32_t *failed) {
-  const int env = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+// phase 1: one thread per env -- clamp, target, reach check, attempt 0 from the
+// current joints (robot.py:293-313, :256-262).  status: 0 done, 1 IK failure
+// (targets = current joints), 2 attempt 0 failed -> phase 2.
+__global__ void __launch_bounds__(128) ik_first_kernel(DevBatch B, const double *delta, int stride, double *targets,
+                                                       double *tgt_scratch, int32_t *status) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
   if (env >= B.n_env) return;
   const DevScene &sc = B.scenes[B.env_scene[env]];
   const StateLayout &L = B.L;
   const double *sd = B.sd + (size_t)env * L.dbl_size;
   const int n = sc.narm;
-  double q0[kMaxArm], target[3];
+  double q0[kMaxArm], target[3], ee[3];
   for (int i = 0; i < n; ++i) q0[i] = sd[L.joints + sc.nsj + i];
-  // clamp to 1.5 cm (robot.py:88-93) and form the base-frame target
-  {
-    double dl[3] = {delta[(size_t)stride * env], delta[(size_t)stride * env + 1], delta[(size_t)stride * env + 2]};
-    double nd = sqrt(dot3(dl, dl));
-    if (nd > 0.015) for (int k = 0; k < 3; ++k) dl[k] = dl[k] * (0.015 / nd);
-    Pose ee;
-    ik_link_poses(sc, q0, nullptr, ee);
-    for (int k = 0; k < 3; ++k) target[k] = ee.p[k] + dl[k];
-  }
-  // reach check (robot.py:256-258)
+  double dl[3] = {delta[(size_t)stride * env], delta[(size_t)stride * env + 1], delta[(size_t)stride * env + 2]};
+  double nd = sqrt(dot3(dl, dl));
+  if (nd > 0.015) for (int k = 0; k < 3; ++k) dl[k] = dl[k] * (0.015 / nd);
+  ik_fk(sc, q0, nullptr, nullptr, ee);
+  for (int k = 0; k < 3; ++k) target[k] = ee[k] + dl[k];
+  for (int k = 0; k < 3; ++k) tgt_scratch[3 * env + k] = target[k];
   double reach = 0.0;
   for (int i = 1; i < n; ++i) reach += sqrt(dot3(sc.arm_offset + 3 * i, sc.arm_offset + 3 * i));
   reach += sqrt(dot3(sc.gripper, sc.gripper));
   double dd[3] = {target[0] - sc.arm_offset[0], target[1] - sc.arm_offset[1], target[2] - sc.arm_offset[2]};
-  const bool reachable = !(sqrt(dot3(dd, dd)) > reach + 5e-3);
-  double q[kMaxArm], seed[kMaxArm];
-  int win = -1;
-  if (reachable) {
-    bool ok = false;
-    if (lane == 0) ok = ik_dls_attempt(sc, target, q0, q);
-    if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
-      win = 0;
-    } else {
-      for (int base = 1; base < 36 && win < 0; base += 32) {
-        const int a = base + lane;
-        bool oka = false;
-        if (a < 36) {
-          ik_seed(sc, a, q0, seed);
-          oka = ik_dls_attempt(sc, target, seed, q);
-        }
-        unsigned m = __ballot_sync(0xffffffffu, oka);
-        if (m) win = base + __ffs(m) - 1;
-      }
-    }
+  double q[kMaxArm];
+  int st = 1;
+  if (!(sqrt(dot3(dd, dd)) > reach + 5e-3)) st = ik_dls_attempt(sc, target, q0, q) ? 0 : 2;
+  for (int i = 0; i < n; ++i) targets[(size_t)env * n + i] = st == 0 ? q[i] : q0[i];
+  status[env] = st;
+}
+
+// phase 2 (rare): one warp per env whose first attempt failed -- the 11 restart
+// seeds and 24 Weyl-spray seeds one per lane, lowest-index success wins.
+__global__ void __launch_bounds__(128) ik_fallback_kernel(DevBatch B, double *targets, const double *tgt_scratch,
+                                                          int32_t *status, int32_t *failed) {
+  const int env = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (env >= B.n_env) return;
+  const int st = status[env];
+  if (st != 2) {
+    if (lane == 0 && failed) failed[env] = st;
+    return;
   }
-  const int src = win < 0 ? -1 : (win == 0 ? 0 : (win - 1) % 32);
+  const DevScene &sc = B.scenes[B.env_scene[env]];
+  const StateLayout &L = B.L;
+  const double *sd = B.sd + (size_t)env * L.dbl_size;
+  const int n = sc.narm;
+  double q0[kMaxArm], q[kMaxArm], seed[kMaxArm];
+  for (int i = 0; i < n; ++i) q0[i] = sd[L.joints + sc.nsj + i];
+  const double target[3] = {tgt_scratch[3 * env], tgt_scratch[3 * env + 1], tgt_scratch[3 * env + 2]};
+  int win = -1;
+  for (int base = 1; base < 36 && win < 0; base += 32) {
+    const int a = base + lane;
+    bool oka = false;
+    if (a < 36) {
+      ik_seed(sc, a, q0, seed);
+      oka = ik_dls_attempt(sc, target, seed, q);
+    }
+    unsigned m = __ballot_sync(0xffffffffu, oka);
+    if (m) win = base + __ffs(m) - 1;
+  }
+  const int src = win < 0 ? 0 : (win - 1) % 32;
   for (int i = 0; i < n; ++i) {
-    double v = __shfl_sync(0xffffffffu, q[i], src < 0 ? 0 : src);
+    double v = __shfl_sync(0xffffffffu, q[i], src);
     if (lane == 0) targets[(size_t)env * n + i] = win < 0 ? q0[i] : v;
   }
   if (lane == 0 && failed) failed[env] = win < 0 ? 1 : 0;
 }
 
 cudaError_t launch_ik(const DevBatch &B, const double *delta, int stride, double *targets, int32_t *failed,
-                      cudaStream_t stream) {
-  const int threads = 128, per_block = threads / 32;
-  ik_kernel<<<(B.n_env + per_block - 1) / per_block, threads, 0, stream>>>(B, delta, stride, targets, failed);
+                      double *scratch, cudaStream_t stream) {
+  // scratch: [n_env] status (int32, stored in doubles) + [n_env][3] targets
+  int32_t *status = reinterpret_cast<int32_t *>(scratch);
+  double *tgt = scratch + (B.n_env + 1) / 2 + 1;
+  ik_first_kernel<<<(B.n_env + 127) / 128, 128, 0, stream>>>(B, delta, stride, targets, tgt, status);
+  ik_fallback_kernel<<<(B.n_env + 3) / 4, 128, 0, stream>>>(B, targets, tgt, status, failed);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,7 @@ import os
 
 from . import abi
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "librsim.so")
+LIB_PATH = os.environ.get("RSIM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "librsim.so")
 
 # every symbol include/rsim.h declares
 EXPORTS = ("rs_abi_version", "rs_last_error", "rs_snapshot_size", "rs_scene_create", "rs_scene_destroy",
