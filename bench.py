@@ -260,10 +260,17 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; RSIM_DIST_BACKEND=gloo lets several ranks share one
+    # device for host-path testing (NCCL refuses duplicate GPUs)
+    backend = os.environ.get("RSIM_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2106_14405_b200 import native
     from paper_2106_14405_b200.sim import BatchSimulator
@@ -355,7 +362,8 @@ def run_b200(args):
 
     # ---- across ranks: max time, summed stats (the only collectives)
     stats, tms = reduce_window({"acc": acc, "envs": float(E)},
-                               {"total": ms_total, "e2e": ms_e2e, "phys": ms_phys, "rend": ms_rend}, device=dev)
+                               {"total": ms_total, "e2e": ms_e2e, "phys": ms_phys, "rend": ms_rend},
+                               device=dev if backend == "nccl" else "cpu")
     ms_total, ms_e2e, ms_phys, ms_rend = tms["total"], tms["e2e"], tms["phys"], tms["rend"]
     total_envs = E * world
     value = total_envs * args.steps / (ms_total * 1e-3)

@@ -98,6 +98,9 @@ int rs_scene_create(const rs_scene_desc *D, rs_scene **out) {
   for (int p = 0; p < np; ++p)
     if (D->part_facet_begin[p + 1] - D->part_facet_begin[p] > kMaxFacetsPerPart)
       return fail(RS_ERR_CAPACITY, "part with more than 48 facets");
+  for (int b = 0; b < nb; ++b)
+    if (D->body_part_begin[b + 1] - D->body_part_begin[b] > 8)
+      return fail(RS_ERR_CAPACITY, "body with more than 8 parts");
   if (D->robot_base < 0 || D->robot_base + D->n_arm >= nb) return fail(RS_ERR_ARG, "robot bodies out of range");
   rs_scene *s = new rs_scene();
   DevScene &d = s->d;

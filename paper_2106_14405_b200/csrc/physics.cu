@@ -38,6 +38,7 @@ constexpr int kWarpsPerBlock = 2;
 constexpr int kMaxCand = 512;
 constexpr int kMaxAdm = 256;
 constexpr int kMaxContacts = 128;
+constexpr int kMaxPartsPerBody = 8;
 constexpr int kMaxGroups = 96;
 constexpr int kMaxBlockRows = 32;
 constexpr int kRowD = 44;  // doubles per solver row in global scratch
@@ -71,9 +72,14 @@ struct WarpSmem {
   // phase-scoped scratch: broadphase AABBs | narrowphase planes | solver velocities
   union {
     struct { double lo[kMaxBodies][3], hi[kMaxBodies][3]; } bp;
-    double planes[2][kMaxFacetsPerPart * 4];
+    struct {
+      double planes[2][kMaxFacetsPerPart * 4];
+      double pw[2][kMaxPartsPerBody][12];  // world frames of the pair's parts
+      double pab[2][kMaxPartsPerBody][6];  // their AABBs (lo, hi)
+    } np;
     struct { double vel[kMaxBodies][6]; BlockWS ws; } sol;
   } u;
+  DevScene sc;  // this env's scene table header (pointers), staged from global
   double jdv[kMaxJoints];
   double links[kMaxArm][12];
   double ee[12];
@@ -99,6 +105,7 @@ struct Ctx {
   double *Vc;     // [kKCap] cached eigenvectors per block
   double *evc;    // [kMaxContacts] cached eigenvalues per block
   double *W;      // [kMaxBlockRows^2] eigensolver workspace
+  double *saabb;  // [kMaxBodies][6] AABBs of the static bodies for this control step
   int env, lane;
   const StateLayout *L;
 };
@@ -300,13 +307,27 @@ __device__ void prim_aabb(Ctx &c, int p, const Pose &wp, double *lo, double *hi)
   }
 }
 
+// union of the part AABBs of body b (geometry.py:289-296)
+__device__ void body_aabb(Ctx &c, int b, double *lo, double *hi) {
+  const DevScene &sc = *c.sc;
+  Pose bp, wp;
+  body_pose(c, b, bp);
+  for (int i = 0; i < 3; ++i) { lo[i] = INFINITY; hi[i] = -INFINITY; }
+  for (int p = sc.body_part_begin[b]; p < sc.body_part_begin[b + 1]; ++p) {
+    double l[3], h[3];
+    part_world(c, bp, p, wp);
+    prim_aabb(c, p, wp, l, h);
+    for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], l[i]); hi[i] = fmax(hi[i], h[i]); }
+  }
+}
+
 // world planes of part p into S->planes[slot] (lanes per facet)
 __device__ void planes_world(Ctx &c, int p, const Pose &wp, int slot) {
   const DevScene &sc = *c.sc;
   int f0 = sc.part_facet_begin[p], nf = sc.part_facet_begin[p + 1] - f0;
   for (int f = c.lane; f < nf; f += 32) {
     const double *F = sc.facet + 4 * (f0 + f);
-    double *o = c.S->u.planes[slot] + 4 * f;
+    double *o = c.S->u.np.planes[slot] + 4 * f;
     double n[3];
     matvec(wp.R, F, n);
     o[0] = n[0]; o[1] = n[1]; o[2] = n[2];
@@ -330,7 +351,7 @@ __device__ int vertices_vs_planes(Ctx &c, int pv, const Pose &wv, int pf, int sl
   const DevScene &sc = *c.sc;
   int v0 = sc.part_vert_begin[pv], nv = sc.part_vert_begin[pv + 1] - v0;
   int nf = sc.part_facet_begin[pf + 1] - sc.part_facet_begin[pf];
-  const double *pl = c.S->u.planes[slot];
+  const double *pl = c.S->u.np.planes[slot];
   int total = 0;
   for (int k0 = 0; k0 < nv; k0 += 32) {
     int v = k0 + c.lane;
@@ -400,7 +421,7 @@ __device__ int sphere_convex(Ctx &c, int ps, const Pose &ws, int pc, const Pose 
   const DevScene &sc = *c.sc;
   double r = sc.part_param[3 * ps];
   const double *ctr = ws.p;
-  const double *pl = c.S->u.planes[slot];
+  const double *pl = c.S->u.np.planes[slot];
   int nf = sc.part_facet_begin[pc + 1] - sc.part_facet_begin[pc];
   bool inside = true;
   int f = 0;
@@ -465,23 +486,42 @@ __device__ int sphere_sphere(Ctx &c, int pa, const Pose &wa, int pb, const Pose 
 }
 
 // geometry.py:701-716: contacts of body pair (a, b), appended at S->nc. warp-collective.
+// The world frame and AABB of every part of a and b are computed once per
+// pair (lanes per part) into shared memory; the part-pair loop then culls
+// from there (the reference's margin test) and generates contacts in the
+// reference's part order.
 __device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
   const DevScene &sc = *c.sc;
-  Pose pa, pb, wa, wb;
-  body_pose_cached(c, a, pa);
-  body_pose_cached(c, b, pb);
+  const int a0 = sc.body_part_begin[a], na = sc.body_part_begin[a + 1] - a0;
+  const int b0 = sc.body_part_begin[b], nbp = sc.body_part_begin[b + 1] - b0;
+  auto &NP = c.S->u.np;
+  if (c.lane < na + nbp) {
+    const int side = c.lane < na ? 0 : 1, k = side ? c.lane - na : c.lane, p = side ? b0 + k : a0 + k;
+    Pose bp, wp;
+    body_pose(c, side ? b : a, bp);
+    part_world(c, bp, p, wp);
+    double lo[3], hi[3];
+    prim_aabb(c, p, wp, lo, hi);
+    for (int q = 0; q < 9; ++q) NP.pw[side][k][q] = wp.R[q];
+    for (int q = 0; q < 3; ++q) {
+      NP.pw[side][k][9 + q] = wp.p[q];
+      NP.pab[side][k][q] = lo[q];
+      NP.pab[side][k][3 + q] = hi[q];
+    }
+  }
+  __syncwarp();
   int base = c.S->nc, n = 0;
-  for (int i = sc.body_part_begin[a]; i < sc.body_part_begin[a + 1]; ++i) {
-    double loa[3], hia[3];
-    part_world(c, pa, i, wa);
-    prim_aabb(c, i, wa, loa, hia);
-    for (int j = sc.body_part_begin[b]; j < sc.body_part_begin[b + 1]; ++j) {
-      double lob[3], hib[3];
-      part_world(c, pb, j, wb);
-      prim_aabb(c, j, wb, lob, hib);
+  for (int ii = 0; ii < na; ++ii) {
+    const double *la = NP.pab[0][ii], *ha = NP.pab[0][ii] + 3;
+    for (int jj = 0; jj < nbp; ++jj) {
+      const double *lb = NP.pab[1][jj], *hb = NP.pab[1][jj] + 3;
       bool sep = false;
-      for (int k = 0; k < 3; ++k) sep |= (loa[k] > hib[k] + margin) || (lob[k] > hia[k] + margin);
+      for (int k = 0; k < 3; ++k) sep |= (la[k] > hb[k] + margin) || (lb[k] > ha[k] + margin);
       if (sep) continue;
+      const int i = a0 + ii, j = b0 + jj;
+      Pose wa, wb;
+      pose_load12(NP.pw[0][ii], wa);
+      pose_load12(NP.pw[1][jj], wb);
       int ka = sc.part_kind[i], kb = sc.part_kind[j];
       if (ka == RS_SPHERE && kb == RS_SPHERE) {
         int r = 0;
@@ -989,19 +1029,17 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
   }
   __syncwarp();
 
-  // ---- broadphase: AABBs (lanes per body)
+  // ---- broadphase: AABBs (lanes per body); static bodies never move during
+  // a control step: theirs come from the per-step cache (c.saabb)
   for (int b = lane; b < nb; b += 32) {
-    Pose bp, wp;
-    body_pose_cached(c, b, bp);
-    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int p = sc.body_part_begin[b]; p < sc.body_part_begin[b + 1]; ++p) {
-      double l[3], h[3];
-      part_world(c, bp, p, wp);
-      prim_aabb(c, p, wp, l, h);
-      for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], l[i]); hi[i] = fmax(hi[i], h[i]); }
+    double lo[3], hi[3];
+    if (sc.body_kind[b] == RS_STATIC) {
+      for (int i = 0; i < 3; ++i) { lo[i] = c.saabb[6 * b + i]; hi[i] = c.saabb[6 * b + 3 + i]; }
+    } else {
+      body_aabb(c, b, lo, hi);
+      if (sc.body_kind[b] == RS_KINEMATIC)
+        for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
     }
-    if (sc.body_kind[b] == RS_KINEMATIC)
-      for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
     for (int i = 0; i < 3; ++i) { S.u.bp.lo[b][i] = lo[i]; S.u.bp.hi[b][i] = hi[i]; }
   }
   __syncwarp();
@@ -1371,7 +1409,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   WarpSmem &S = smem[warp];
   const StateLayout &L = B.L;
   Ctx c;
-  c.sc = &B.scenes[B.env_scene[env]];
+  {  // stage the scene header (table pointers + scalars) into shared memory
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(&B.scenes[B.env_scene[env]]);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(&S.sc);
+    for (int i = lane; i < (int)(sizeof(DevScene) / 4); i += 32) dst[i] = src[i];
+    __syncwarp();
+  }
+  c.sc = &S.sc;
   c.B = &B;
   c.cfg = &B.cfg;
   c.S = &S;
@@ -1385,6 +1429,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   c.Vc = c.K + kKCap;
   c.evc = c.Vc + 2 * kKCap;
   c.W = c.evc + 2 * kMaxContacts;
+  c.saabb = c.W + kMaxBlockRows * kMaxBlockRows;
 
   // stage the state slab (coalesced)
   const double *gsd = B.sd + (size_t)env * L.dbl_size;
@@ -1421,6 +1466,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   const double *arm = ht ? arm_targets + (size_t)env * sc.narm : nullptr;
   const double *bc = base_cmd + (size_t)env * base_stride;
   if (lane < kMaxArm) S.budget[lane] = B.cfg.motor_impulse_cap;
+  for (int b = lane; b < sc.nb; b += 32)
+    if (sc.body_kind[b] == RS_STATIC) body_aabb(c, b, c.saabb + 6 * b, c.saabb + 6 * b + 3);
   __syncwarp();
   const double dts = dt / substeps;
   bool ok = true;
@@ -1444,7 +1491,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
 }
 
 __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
-  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + kMaxBlockRows * kMaxBlockRows;
+  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + kMaxBlockRows * kMaxBlockRows +
+         6 * kMaxBodies;
 }
 int step_row_cap() { return kMaxContacts; }
 

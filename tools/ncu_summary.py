@@ -42,6 +42,26 @@ def report(path):
             print(f"    {n:40s} {s:8d} {100.0 * s / tot:5.1f}%")
 
 
+def hot_lines(path, top=30):
+    """Top CUDA source lines by warp-stall samples (needs -lineinfo + --import-source)."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = next(r for r in rows if "# Samples" in r)
+    si, ie = hdr.index("# Samples"), hdr.index("Instructions Executed")
+    res = []
+    for r in rows[rows.index(hdr) + 1:]:
+        if len(r) > si and r[2] == "-":
+            try:
+                res.append((int(r[si]), int(r[0]), int(r[ie] or 0), r[1].strip()[:90]))
+            except ValueError:
+                pass
+    tot = sum(x[0] for x in res) or 1
+    print(f"  hot source lines (of {tot} samples):")
+    for n, line, inst, src in sorted(res, reverse=True)[:top]:
+        print(f"    {100.0 * n / tot:5.1f}%  L{line:<5d} inst {inst:>11d}  {src}")
+
+
 def launches(path):
     text = open(path).read()
     text = text[text.index('"ID"'):]
@@ -59,5 +79,8 @@ def launches(path):
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "--lines":
+        report(sys.argv[2])
+        hot_lines(sys.argv[2])
     else:
         report(sys.argv[1])
