@@ -758,9 +758,9 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
   for (int it = 0; it < 4 * m + 4; ++it) {
     const int na = ws.na;
     if (lane < m) ws.lam[lane] = 0.0;
+    unsigned mask = 0u;  // active set as a bitmask over the block's rows
+    for (int i = 0; i < na; ++i) mask |= 1u << ws.active[i];
     if (na) {
-      unsigned mask = 0u;
-      for (int i = 0; i < na; ++i) mask |= 1u << ws.active[i];
       if (lane < na) ws.rhs[lane] = -ws.q[ws.active[lane]];
       // two cached decompositions per block, keyed by the active set
       int slot = (double)mask == P[PMASK] ? 0 : ((double)mask == P[PMASK + 1] ? 1 : -1);
@@ -821,9 +821,7 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     // w = K lam + q on the inactive rows (lane i, oracle order)
     if (lane < m) {
       const int i = lane;
-      bool in = false;
-      for (int j = 0; j < na; ++j) in |= (ws.active[j] == i);
-      if (!in) {
+      if (!((mask >> i) & 1u)) {
         double wi = 0.0;
         for (int j = 0; j < m; ++j) wi += K[i * m + j] * ws.lam[j];
         wi += ws.q[i];
@@ -834,9 +832,7 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     if (lane == 0) {
       int worst = -1;
       for (int i = 0; i < m; ++i) {
-        bool in = false;
-        for (int j = 0; j < na; ++j) in |= (ws.active[j] == i);
-        if (in) continue;
+        if ((mask >> i) & 1u) continue;
         double wi = ws.wv[i];
         if (wi < -1e-10 && (worst < 0 || wi < ws.wv[worst] || (wi == ws.wv[worst] && i < worst))) worst = i;
       }
