@@ -14,7 +14,9 @@
 
 namespace rsim {
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
-                        const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream);
+                        const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream,
+                        const uint8_t *heavy_in, uint8_t *heavy_out, cudaStream_t side, cudaEvent_t fork,
+                        cudaEvent_t join);
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                           cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
@@ -69,6 +71,10 @@ struct rs_batch {
   double *d_ik_scratch = nullptr;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // contact-heavy scheduling: per-env flags (ping-pong like the state) and a physics side stream
+  uint8_t *heavy[2] = {nullptr, nullptr};
+  cudaStream_t phys_side = nullptr;
+  cudaEvent_t ph_fork = nullptr, ph_join = nullptr;
 };
 
 // exported functions take C linkage from their declarations in rsim.h
@@ -230,6 +236,7 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   BA(events, sizeof(double) * 7 * (size_t)(event_cap ? event_cap : 1) * n_env);
   BA(counters, sizeof(int64_t) * 3 * n_env);
   BA(row_scratch, sizeof(double) * step_scratch_doubles_per_env(d.row_cap) * (size_t)n_env);
+  if (!rc) rc = balloc(b, &p, 2 * (size_t)n_env), b->heavy[0] = (uint8_t *)p, b->heavy[1] = (uint8_t *)p + n_env;
 #undef BA
   if (!rc) rc = balloc(b, &p, sizeof(DevScene) * n_scenes), b->d_scenes = (DevScene *)p;
   if (!rc) rc = balloc(b, &p, sizeof(int32_t) * n_env), b->d_env_scene = (int32_t *)p;
@@ -270,6 +277,9 @@ void rs_batch_destroy(rs_batch *b) {
   if (b->d_ik_failed) cudaFree(b->d_ik_failed);
   if (b->d_ik_scratch) cudaFree(b->d_ik_scratch);
   if (b->side) cudaStreamDestroy(b->side);
+  if (b->phys_side) cudaStreamDestroy(b->phys_side);
+  if (b->ph_fork) cudaEventDestroy(b->ph_fork);
+  if (b->ph_join) cudaEventDestroy(b->ph_join);
   if (b->ev_fork) cudaEventDestroy(b->ev_fork);
   if (b->ev_join) cudaEventDestroy(b->ev_join);
   delete b;
@@ -399,12 +409,24 @@ int rs_get_state(rs_batch *b, uint8_t *snaps, int64_t stride, const int32_t *env
   return RS_OK;
 }
 
+static cudaError_t launch_step_b(rs_batch *b, const double *arm, const double *base_cmd, int base_stride,
+                                 const uint8_t *has_targets, double dt, int substeps, cudaStream_t st) {
+  if (!b->phys_side) {
+    cudaError_t e = cudaStreamCreateWithFlags(&b->phys_side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_join, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_step(b->view(), arm, base_cmd, base_stride, has_targets, dt, substeps, st, b->heavy[b->cur],
+                     b->heavy[b->cur ^ 1], b->phys_side, b->ph_fork, b->ph_join);
+}
+
 int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_t *has_targets, double dt,
             int32_t substeps, void *stream) {
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
   if (!arm || !base_cmd) return fail(RS_ERR_ARG, "arm_targets and base_cmd are required device pointers");
-  CUDA_TRY(launch_step(b->view(), arm, base_cmd, 2, has_targets, dt, substeps, (cudaStream_t)stream));
+  CUDA_TRY(launch_step_b(b, arm, base_cmd, 2, has_targets, dt, substeps, (cudaStream_t)stream));
   b->cur ^= 1;
   return RS_OK;
 }
@@ -524,7 +546,7 @@ int rs_env_step(rs_batch *b, const double *action, double dt, int32_t substeps, 
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(launch_ik(b->view(), action, 6, b->d_targets, b->d_ik_failed, b->d_ik_scratch, st));  // robot.py:293
-  CUDA_TRY(launch_step(b->view(), b->d_targets, action + 4, 6, nullptr, dt, substeps, st));  // physics.py:575
+  CUDA_TRY(launch_step_b(b, b->d_targets, action + 4, 6, nullptr, dt, substeps, st));  // physics.py:575
   b->cur ^= 1;
   CUDA_TRY(launch_grasp(b->view(), action + 3, 6, st));                                   // robot.py:323
   return RS_OK;

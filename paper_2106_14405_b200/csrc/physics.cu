@@ -90,7 +90,7 @@ struct WarpSmem {
   int16_t g_a[kMaxGroups], g_b[kMaxGroups], g_first[kMaxGroups], g_n[kMaxGroups];
   int ncand, nadm, nc, ng, fault;
   unsigned long long awake_dyn;
-  int moved_mask;
+  int moved_mask, dragged, n_active, max_active;
   int64_t ctr[3];
 };
 
@@ -913,7 +913,8 @@ __device__ void emit_event(Ctx &c, const double *r, double lam, double force) {
 }
 
 // physics.py:657-701; returns false on capacity overflow
-__device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double dt, int sub) {
+// physics.py:657-699 up to the solver set-up (rows, blocks); false on capacity overflow
+__device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, double dt, int sub) {
   const DevScene &sc = *c.sc;
   const rs_physics_config &cfg = *c.cfg;
   WarpSmem &S = *c.S;
@@ -951,6 +952,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
     __syncwarp();
   }
   int dragged = HELDJ(c);
+  if (lane == 0) S.dragged = dragged;
   if (dragged >= 0) {
     if (lane == 0) {  // physics.py:623-655
       int ji = dragged;
@@ -1210,6 +1212,16 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
     }
   }
   __syncwarp();
+  {  // groups with a row of k > 0 (the only ones the sweeps change): load metric for scheduling
+    int act = 0;
+    for (int g = lane; g < ng; g += 32) {
+      bool a = false;
+      for (int i = S.g_first[g]; i < S.g_first[g] + S.g_n[g]; ++i) a |= c.rows[kRowD * i + RK] > 0.0;
+      act += a;
+    }
+    act = __reduce_add_sync(0xffffffffu, act);
+    if (lane == 0) S.n_active = act;
+  }
   if (nc) {
     // block matrices (physics.py:721-758): lanes per entry
     int koff = 0;
@@ -1252,7 +1264,18 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
       }
     }
     __syncwarp();
-    // Gauss-Seidel sweeps, blocks in sorted pair order (physics.py:931-937).
+  }
+  __syncwarp();
+  return true;
+}
+
+// Gauss-Seidel sweeps, single warp (physics.py:915-937)
+__device__ void substep_sweeps(Ctx &c) {
+  const rs_physics_config &cfg = *c.cfg;
+  WarpSmem &S = *c.S;
+  const int lane = c.lane, nc = S.nc, ng = S.ng;
+  if (!nc) return;
+    // blocks in sorted pair order (physics.py:931-937).
     // Rows with k <= 0 are no-ops in the reference (physics.py:1294): when
     // every row is such, the sweeps change nothing and are skipped.
     bool any_k = false;
@@ -1274,6 +1297,15 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
         }
     }
     __syncwarp();
+}
+
+// physics.py:939-1035: velocity write-back, events, integration, joints
+__device__ void substep_back(Ctx &c, double dt) {
+  const DevScene &sc = *c.sc;
+  const rs_physics_config &cfg = *c.cfg;
+  WarpSmem &S = *c.S;
+  const int lane = c.lane, nb = sc.nb, nsj = sc.nsj, nc = S.nc, ng = S.ng, dragged = S.dragged;
+  if (nc) {
     for (int b = lane; b < nb; b += 32)
       if (solver_dynamic(c, b)) {
         double *lv = LV(c, b), *av = AV(c, b);
@@ -1377,7 +1409,90 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
   __syncwarp();
   int moved = S.moved_mask;
   if (moved) update_scene_joint_poses(c, moved, dt);
+}
+
+__device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double dt, int sub) {
+  if (!substep_front(c, arm, basecmd, dt, sub)) return false;
+  substep_sweeps(c);
+  substep_back(c, dt);
   return true;
+}
+
+// ---------------------------------------------------------------------------
+// Contact-heavy envs: one CTA of kHeavyWarps warps per env.  Warp 0 runs every
+// phase as in the warp-per-env kernel; the Gauss-Seidel sweeps are run by all
+// warps over a wavefront schedule of the contact groups.  Group g depends on
+// every earlier group h < g that shares a velocity it writes (a body with
+// non-zero solver inverse mass, or a scene joint's joint_dv); groups of one
+// level touch disjoint state, so solving them concurrently gives bit-identical
+// results to the reference's sequential order (physics.py:931-937).
+constexpr int kHeavyWarps = 4;
+constexpr int kHeavyGroups = 4;  // envs with >= this many active groups go to the CTA kernel
+
+struct HeavyShared {
+  BlockWS ws[kHeavyWarps - 1];  // block-solver workspaces of warps 1..
+  int16_t lvl_order[kMaxGroups];
+  int16_t lvl_start[kMaxGroups + 1];
+  int nlev, ok;
+};
+
+// wavefront levels of the active groups (warp 0, lane 0)
+__device__ void build_levels(Ctx &c, HeavyShared &H) {
+  WarpSmem &S = *c.S;
+  const int ng = S.ng, nb = c.sc->nb;
+  int16_t level[kMaxGroups];
+  unsigned long long res[kMaxGroups];
+  int count[kMaxGroups + 1];
+  int nlev = 0;
+  for (int g = 0; g < ng; ++g) {
+    const int first = S.g_first[g], m = S.g_n[g];
+    bool act = false;
+    for (int i = first; i < first + m; ++i) act |= c.rows[kRowD * i + RK] > 0.0;
+    level[g] = -1;
+    if (!act) continue;
+    const double *r0 = c.rows + kRowD * first;
+    unsigned long long rs = 0ull;
+    if (r0[RIMA] > 0.0) rs |= 1ull << (int)r0[RA];
+    if (r0[RIMB] > 0.0) rs |= 1ull << (int)r0[RB];
+    if (r0[RJA] >= 0.0) rs |= 1ull << (nb + (int)r0[RJA]);
+    if (r0[RJB] >= 0.0) rs |= 1ull << (nb + (int)r0[RJB]);
+    res[g] = rs;
+    int lv = 0;
+    for (int h = 0; h < g; ++h)
+      if (level[h] >= 0 && (res[h] & rs) && level[h] + 1 > lv) lv = level[h] + 1;
+    level[g] = (int16_t)lv;
+    if (lv + 1 > nlev) nlev = lv + 1;
+  }
+  for (int l = 0; l <= nlev; ++l) count[l] = 0;
+  for (int g = 0; g < ng; ++g)
+    if (level[g] >= 0) count[level[g] + 1]++;
+  for (int l = 0; l < nlev; ++l) count[l + 1] += count[l];
+  for (int l = 0; l <= nlev; ++l) H.lvl_start[l] = (int16_t)count[l];
+  for (int g = 0; g < ng; ++g)
+    if (level[g] >= 0) H.lvl_order[count[level[g]]++] = (int16_t)g;
+  H.nlev = nlev;
+}
+
+// all warps of the CTA; ends with a CTA barrier
+__device__ void sweeps_cta(Ctx &c, HeavyShared &H, int warp, BlockWS &ws, double *W) {
+  const int iters = c.cfg->solver_iterations, nlev = H.nlev;
+  for (int it = 0; it < iters; ++it)
+    for (int l = 0; l < nlev; ++l) {
+      for (int idx = H.lvl_start[l] + warp; idx < H.lvl_start[l + 1]; idx += kHeavyWarps) {
+        const int g = H.lvl_order[idx];
+        const int first = c.S->g_first[g], m = c.S->g_n[g];
+        const double *P = c.pairs + kPairD * g;
+        if (P[PHASK] == 0.0) {
+          if (c.lane == 0)
+            for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
+          __syncwarp();
+        } else {
+          const int koff = (int)P[PKOFF];
+          solve_block(c, g, first, m, c.K + koff, ws, W, c.Vc + 2 * koff, c.evc + 2 * first);
+        }
+      }
+      __syncthreads();
+    }
 }
 
 __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap);
@@ -1393,81 +1508,76 @@ __device__ void copy_through(const DevBatch &B, int env, int lane) {
   for (int i = lane; i < L.int_size; i += 32) y[i] = x[i];
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B, const double *arm_targets,
-                                                                   const double *base_cmd, int base_stride,
-                                                                   const uint8_t *has_targets, double dt,
-                                                                   int substeps) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  WarpSmem *smem = reinterpret_cast<WarpSmem *>(dsm);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int env = blockIdx.x * kWarpsPerBlock + warp;
-  if (env >= B.n_env) return;
-  WarpSmem &S = smem[warp];
-  const StateLayout &L = B.L;
-  Ctx c;
-  {  // stage the scene header (table pointers + scalars) into shared memory
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(&B.scenes[B.env_scene[env]]);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(&S.sc);
-    for (int i = lane; i < (int)(sizeof(DevScene) / 4); i += 32) dst[i] = src[i];
-    __syncwarp();
-  }
+// per-env context over the batch scratch (any warp of the env's CTA)
+__device__ void make_ctx(Ctx &c, const DevBatch &B, WarpSmem &S, int env, int lane, int warp) {
   c.sc = &S.sc;
   c.B = &B;
   c.cfg = &B.cfg;
   c.S = &S;
   c.env = env;
   c.lane = lane;
-  c.L = &L;
+  c.L = &B.L;
   const size_t per_env = step_scratch_doubles_per_env(B.row_cap);
   c.rows = B.row_scratch + per_env * env;
   c.pairs = c.rows + (size_t)B.row_cap * kRowD;
   c.K = c.pairs + kMaxGroups * kPairD;
   c.Vc = c.K + kKCap;
   c.evc = c.Vc + 2 * kKCap;
-  c.W = c.evc + 2 * kMaxContacts;
-  c.saabb = c.W + kMaxBlockRows * kMaxBlockRows;
+  c.saabb = c.evc + 2 * kMaxContacts;
+  c.W = c.saabb + 6 * kMaxBodies + (size_t)warp * kMaxBlockRows * kMaxBlockRows;
+}
 
-  // stage the state slab (coalesced)
+// stage scene header + state slab, _check_finite (physics.py:596-606), per-step
+// set-up; false if the env faulted (its input state is copied through).  One warp.
+__device__ bool env_begin(Ctx &c, const DevBatch &B, int env) {
+  WarpSmem &S = *c.S;
+  const StateLayout &L = B.L;
+  const int lane = c.lane;
+  {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(&B.scenes[B.env_scene[env]]);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(&S.sc);
+    for (int i = lane; i < (int)(sizeof(DevScene) / 4); i += 32) dst[i] = src[i];
+  }
   const double *gsd = B.sd + (size_t)env * L.dbl_size;
   const int32_t *gsi = B.si + (size_t)env * L.int_size;
   for (int i = lane; i < L.dbl_size; i += 32) S.sd[i] = gsd[i];
   for (int i = lane; i < L.int_size; i += 32) S.si[i] = gsi[i];
   if (lane < 3) S.ctr[lane] = 0;
-  if (lane == 0) { B.event_count[env] = 0; S.fault = 0; }
+  if (lane == 0) { B.event_count[env] = 0; S.fault = 0; S.max_active = 0; }
   __syncwarp();
   const DevScene &sc = *c.sc;
-  // _check_finite (physics.py:596-606): first offending body per field class
-  {
-    uint32_t f = 0;
-    for (int cls = 0; cls < 4 && !f; ++cls) {
-      int n = cls == 3 ? L.nj : sc.nb, best = 1 << 30;
-      for (int i = lane; i < n; i += 32) {
-        bool bad = false;
-        if (cls == 0) { const double *p = POS(c, i); bad = !isfinite(p[0]) || !isfinite(p[1]) || !isfinite(p[2]); }
-        if (cls == 1) { const double *q = QUAT(c, i); bad = !isfinite(q[0]) || !isfinite(q[1]) || !isfinite(q[2]) || !isfinite(q[3]); }
-        if (cls == 2) { const double *v = LV(c, i); bad = !isfinite(v[0]) || !isfinite(v[1]) || !isfinite(v[2]); }
-        if (cls == 3) bad = !isfinite(JOINTS(c)[i]);
-        if (bad && i < best) best = i;
-      }
-      best = __reduce_min_sync(0xffffffffu, best);
-      if (best < (1 << 30)) f = ((uint32_t)(cls + 1) << 16) | (uint32_t)best;
+  uint32_t f = 0;
+  for (int cls = 0; cls < 4 && !f; ++cls) {
+    int n = cls == 3 ? L.nj : sc.nb, best = 1 << 30;
+    for (int i = lane; i < n; i += 32) {
+      bool bad = false;
+      if (cls == 0) { const double *p = POS(c, i); bad = !isfinite(p[0]) || !isfinite(p[1]) || !isfinite(p[2]); }
+      if (cls == 1) { const double *q = QUAT(c, i); bad = !isfinite(q[0]) || !isfinite(q[1]) || !isfinite(q[2]) || !isfinite(q[3]); }
+      if (cls == 2) { const double *v = LV(c, i); bad = !isfinite(v[0]) || !isfinite(v[1]) || !isfinite(v[2]); }
+      if (cls == 3) bad = !isfinite(JOINTS(c)[i]);
+      if (bad && i < best) best = i;
     }
-    if (f) {
-      if (lane == 0) B.fault[env] = f;
-      copy_through(B, env, lane);
-      return;
-    }
+    best = __reduce_min_sync(0xffffffffu, best);
+    if (best < (1 << 30)) f = ((uint32_t)(cls + 1) << 16) | (uint32_t)best;
   }
-  const bool ht = has_targets == nullptr || has_targets[env];
-  const double *arm = ht ? arm_targets + (size_t)env * sc.narm : nullptr;
-  const double *bc = base_cmd + (size_t)env * base_stride;
+  if (f) {
+    if (lane == 0) B.fault[env] = f;
+    copy_through(B, env, lane);
+    return false;
+  }
   if (lane < kMaxArm) S.budget[lane] = B.cfg.motor_impulse_cap;
   for (int b = lane; b < sc.nb; b += 32)
     if (sc.body_kind[b] == RS_STATIC) body_aabb(c, b, c.saabb + 6 * b, c.saabb + 6 * b + 3);
   __syncwarp();
-  const double dts = dt / substeps;
-  bool ok = true;
-  for (int s = 0; s < substeps && ok; ++s) ok = substep(c, arm, bc, dts, s);
+  return true;
+}
+
+// time / step index / counters, write the successor slab (physics.py:592-594). One warp.
+__device__ void env_end(Ctx &c, const DevBatch &B, int env, double dt, bool ok, uint8_t *heavy_out) {
+  WarpSmem &S = *c.S;
+  const StateLayout &L = B.L;
+  const int lane = c.lane;
+  if (lane == 0 && heavy_out) heavy_out[env] = S.max_active >= kHeavyGroups ? 1 : 0;
   if (!ok) {
     if (lane == 0) B.fault[env] = (uint32_t)RS_FAULT_OVERFLOW << 16;
     copy_through(B, env, lane);
@@ -1486,23 +1596,113 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   for (int i = lane; i < L.int_size; i += 32) wsi[i] = S.si[i];
 }
 
+// warp per env (envs not flagged heavy by the previous step)
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B, const double *arm_targets,
+                                                                   const double *base_cmd, int base_stride,
+                                                                   const uint8_t *has_targets, double dt,
+                                                                   int substeps, const uint8_t *heavy_in,
+                                                                   uint8_t *heavy_out) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  WarpSmem *smem = reinterpret_cast<WarpSmem *>(dsm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int env = blockIdx.x * kWarpsPerBlock + warp;
+  if (env >= B.n_env) return;
+  if (heavy_in && heavy_in[env]) return;
+  WarpSmem &S = smem[warp];
+  Ctx c;
+  make_ctx(c, B, S, env, lane, 0);
+  if (!env_begin(c, B, env)) return;
+  const DevScene &sc = *c.sc;
+  const bool ht = has_targets == nullptr || has_targets[env];
+  const double *arm = ht ? arm_targets + (size_t)env * sc.narm : nullptr;
+  const double *bc = base_cmd + (size_t)env * base_stride;
+  const double dts = dt / substeps;
+  bool ok = true;
+  for (int s = 0; s < substeps && ok; ++s) {
+    ok = substep(c, arm, bc, dts, s);
+    if (lane == 0 && S.n_active > S.max_active) S.max_active = S.n_active;
+  }
+  __syncwarp();
+  env_end(c, B, env, dt, ok, heavy_out);
+}
+
+// CTA of kHeavyWarps warps per env (envs flagged heavy by the previous step)
+__global__ void __launch_bounds__(32 * kHeavyWarps) step_kernel_cta(DevBatch B, const double *arm_targets,
+                                                                   const double *base_cmd, int base_stride,
+                                                                   const uint8_t *has_targets, double dt,
+                                                                   int substeps, const uint8_t *heavy_in,
+                                                                   uint8_t *heavy_out) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  WarpSmem &S = *reinterpret_cast<WarpSmem *>(dsm);
+  HeavyShared &H = *reinterpret_cast<HeavyShared *>(dsm + ((sizeof(WarpSmem) + 15) & ~(size_t)15));
+  const int env = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!heavy_in[env]) return;
+  Ctx c;
+  make_ctx(c, B, S, env, lane, warp);
+  if (warp == 0) {
+    bool ok = env_begin(c, B, env);
+    if (lane == 0) H.ok = ok;
+  }
+  __syncthreads();
+  if (!H.ok) return;
+  const DevScene &sc = *c.sc;
+  const bool ht = has_targets == nullptr || has_targets[env];
+  const double *arm = ht ? arm_targets + (size_t)env * sc.narm : nullptr;
+  const double *bc = base_cmd + (size_t)env * base_stride;
+  const double dts = dt / substeps;
+  BlockWS &ws = warp == 0 ? S.u.sol.ws : H.ws[warp - 1];
+  bool ok = true;
+  for (int s = 0; s < substeps; ++s) {
+    if (warp == 0) {
+      bool f = substep_front(c, arm, bc, dts, s);
+      if (lane == 0) {
+        H.ok = f;
+        if (S.n_active > S.max_active) S.max_active = S.n_active;
+        if (f) build_levels(c, H);
+      }
+    }
+    __syncthreads();
+    ok = H.ok;
+    if (!ok) break;
+    sweeps_cta(c, H, warp, ws, c.W);
+    if (warp == 0) substep_back(c, dts);
+    __syncthreads();
+  }
+  if (warp == 0) env_end(c, B, env, dt, ok, heavy_out);
+}
+
 __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
-  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + kMaxBlockRows * kMaxBlockRows +
-         6 * kMaxBodies;
+  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + 6 * kMaxBodies +
+         (size_t)kHeavyWarps * kMaxBlockRows * kMaxBlockRows;
 }
 int step_row_cap() { return kMaxContacts; }
 
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
-                        const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream) {
+                        const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream,
+                        const uint8_t *heavy_in, uint8_t *heavy_out, cudaStream_t side, cudaEvent_t fork,
+                        cudaEvent_t join) {
   static bool configured = false;
   const size_t smem = sizeof(WarpSmem) * kWarpsPerBlock;
+  const size_t smem_cta = ((sizeof(WarpSmem) + 15) & ~(size_t)15) + sizeof(HeavyShared);
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(step_kernel_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cta);
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  if (heavy_in && side) {
+    // contact-heavy envs (flagged by the previous step) on a second stream, first
+    cudaEventRecord(fork, stream);
+    cudaStreamWaitEvent(side, fork, 0);
+    step_kernel_cta<<<B.n_env, 32 * kHeavyWarps, smem_cta, side>>>(B, arm, base_cmd, base_stride, has_targets, dt,
+                                                                     substeps, heavy_in, heavy_out);
+    cudaEventRecord(join, side);
+  }
   dim3 grid((B.n_env + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  step_kernel<<<grid, 32 * kWarpsPerBlock, smem, stream>>>(B, arm, base_cmd, base_stride, has_targets, dt, substeps);
+  step_kernel<<<grid, 32 * kWarpsPerBlock, smem, stream>>>(B, arm, base_cmd, base_stride, has_targets, dt, substeps,
+                                                           heavy_in && side ? heavy_in : nullptr, heavy_out);
+  if (heavy_in && side) cudaStreamWaitEvent(stream, join, 0);
   return cudaGetLastError();
 }
 

@@ -39,9 +39,9 @@ constexpr int kMaxParts = 128;
 constexpr int kMaskWords = kMaxParts / 32;
 constexpr int kMaxTiles = (128 / kTile) * (128 / kTile);
 constexpr int kRenderThreads = 256;
-// CTAs per SM the register budget is sized for (80 registers: the two-ray
-// proxy walk spills heavily at 64; the mesh walk spills its BVH stack at 64)
-constexpr int kMinBlocksProxy = 3, kMinBlocksMesh = 3;
+// CTAs per SM the register budget is sized for (measured: proxy 4 -> 64
+// registers, 4% faster than 3; mesh 3 -> 80 registers, 4 spills its BVH stack)
+constexpr int kMinBlocksProxy = 4, kMinBlocksMesh = 3;
 constexpr double kParallelEps = 1e-12;  // geometry.py:731
 
 struct PartW {
@@ -249,79 +249,6 @@ __device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S
   if (cur_b >= 0 && cur_t <= tmin + eps) { id = cur_b; wpart = cur_p; wface = cur_f; }
 }
 
-
-struct RayState {
-  double tmin, t2;
-  int id, wpart, wface;
-  __device__ __forceinline__ void init() { tmin = INFINITY; t2 = INFINITY; id = -1; wpart = -1; wface = -1; }
-  // nearest hit per body with the lowest-part tie-break; t2 = best other body
-  __device__ __forceinline__ void update(double t, int b, int p, int fc) {
-    if (!(t < INFINITY)) return;
-    if (b == id) {
-      if (t < tmin || (t == tmin && p < wpart)) { tmin = t; wpart = p; wface = fc; }
-    } else if (t < tmin) {
-      t2 = tmin;
-      tmin = t; id = b; wpart = p; wface = fc;
-    } else if (t < t2) {
-      t2 = t;
-    }
-  }
-};
-
-// unit ray of pixel (u, v): camera frame (x right, y down, z view), normalised, rotated
-__device__ __forceinline__ void pixel_dir(const RenderSmem &S, int u, int v, int W, int H, double f, double *d) {
-  double dc[3] = {(u + 0.5 - W / 2.0) / f, (v + 0.5 - H / 2.0) / f, 1.0};
-  const double rl = 1.0 / sqrt(dot3(dc, dc));
-  dc[0] *= rl; dc[1] *= rl; dc[2] *= rl;
-  matvec(S.cam.R, dc, d);
-}
-
-// pinned output conventions: far/miss sentinel, near clamp, shading
-template <bool kMesh>
-__device__ __forceinline__ void write_pixel(const DevScene &sc, const RenderSmem &S, size_t px, const double *d,
-                                            const double *o, const RayState &A, double zfar, double znear,
-                                            uint32_t *rgba, float *depth, int32_t *ids) {
-  const double tmin = A.tmin;
-  if (!(tmin <= zfar)) {
-    if (rgba) rgba[px] = 0u;
-    if (depth) depth[px] = 0.0f;
-    if (ids) ids[px] = -1;
-    return;
-  }
-  if (depth) depth[px] = (float)(tmin < znear ? znear : tmin);
-  if (ids) ids[px] = A.id;
-  if (!rgba) return;
-  double cosv = 0.0;
-  const PartW &P = S.part[A.wpart];
-  const int wface = A.wface;
-  if (kMesh) {
-    if (wface >= 0) {  // |n.d| of the hit triangle (two-sided)
-      const double *T = sc.mtri + 9 * wface, *R = S.plane + 9 * A.wpart;
-      double nl[3], nw[3];
-      cross3(T + 3, T + 6, nl);
-      matvec(R, nl, nw);
-      cosv = fabs(dot3(nw, d)) / sqrt(dot3(nw, nw));
-    }
-  } else if (P.kind == RS_SPHERE) {
-    if (tmin > 0.0) {
-      double n[3];
-      for (int i = 0; i < 3; ++i) n[i] = (o[i] + tmin * d[i] - P.c[i]) / P.r;
-      cosv = -dot3(n, d);
-    }
-  } else if (wface >= 0) {
-    const double *Q = S.plane + 4 * wface;
-    cosv = -(d[0] * Q[0] + d[1] * Q[1] + d[2] * Q[2]);
-  }
-  float shade = __fadd_rn(0.3f, __fmul_rn(0.7f, (float)(cosv > 0.0 ? cosv : 0.0)));
-  const float *col = sc.color + 3 * A.id;
-  uint32_t px4 = 0xff000000u;
-  for (int i = 0; i < 3; ++i) {
-    float cv = __fadd_rn(__fmul_rn(__fmul_rn(255.0f, col[i]), shade), 0.5f);
-    px4 |= (uint32_t)(cv > 255.0f ? 255.0f : cv) << (8 * i);
-  }
-  rgba[px] = px4;
-}
-
 template <bool kMesh>
 __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinBlocksProxy) render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out,
                                                                 uint32_t *rgba, float *depth, int32_t *ids,
@@ -457,50 +384,6 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
     const uint8_t *list = S.list[tile];
     const int nl = S.nlist[tile];
     const int ux = (tile % tx_n) * kTile, vy = (tile / tx_n) * kTile;
-    if constexpr (!kMesh) {
-      // proxy path: two pixels per thread (k, k + 32) walked together over the
-      // tile list -- two independent ray tests per part give the scheduler
-      // instruction-level parallelism (float64 latency-bound otherwise)
-#pragma unroll 1
-      for (int k = lane; k < kTile * kTile; k += 64) {
-        RayState R2[2];
-        double dd[2][3];
-        int uu[2], vv[2];
-        for (int r = 0; r < 2; ++r) {
-          uu[r] = ux + ((k + 32 * r) % kTile);
-          vv[r] = vy + ((k + 32 * r) / kTile);
-          pixel_dir(S, uu[r], vv[r], W, H, f, dd[r]);
-          R2[r].init();
-        }
-#pragma unroll 1
-        for (int j = 0; j < nl; ++j) {
-          const int p = list[j];
-          const PartW &P = S.part[p];
-          const bool g0 = !(P.lb > R2[0].tmin + eps), g1 = !(P.lb > R2[1].tmin + eps);
-          if (!g0 && !g1) break;  // sorted: nothing later can be nearer or tie (for either ray)
-          int f0, f1;
-          double t0, t1;
-          if (P.kind == RS_BOX) {
-            t0 = ray_box(S.plane + 4 * P.f0, dd[0], R2[0].tmin + eps, f0);
-            t1 = ray_box(S.plane + 4 * P.f0, dd[1], R2[1].tmin + eps, f1);
-            if (f0 >= 0) f0 += P.f0;
-            if (f1 >= 0) f1 += P.f0;
-          } else {
-            t0 = part_hit(S, p, o, dd[0], f0, R2[0].tmin + eps);
-            t1 = part_hit(S, p, o, dd[1], f1, R2[1].tmin + eps);
-          }
-          if (work) tests += 2 * (P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf));
-          R2[0].update(t0, P.body, p, f0);
-          R2[1].update(t1, P.body, p, f1);
-        }
-        for (int r = 0; r < 2; ++r) {
-          RayState &A = R2[r];
-          if (A.tmin < INFINITY && A.t2 - A.tmin <= eps)
-            resolve_tie<kMesh>(sc, S, S.mask[tile], o, dd[r], A.tmin, eps, A.id, A.wpart, A.wface);
-          write_pixel<kMesh>(sc, S, img + (size_t)vv[r] * W + uu[r], dd[r], o, A, zfar, znear, rgba, depth, ids);
-        }
-      }
-    } else {
 #pragma unroll 1
     for (int k = lane; k < kTile * kTile; k += 32) {
       const int u = ux + (k % kTile), v = vy + (k / kTile);
@@ -533,10 +416,45 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
       }
       if (tmin < INFINITY && t2 - tmin <= eps) resolve_tie<kMesh>(sc, S, S.mask[tile], o, d, tmin, eps, id, wpart, wface);
 
-      RayState A;
-      A.tmin = tmin; A.t2 = t2; A.id = id; A.wpart = wpart; A.wface = wface;
-      write_pixel<kMesh>(sc, S, img + (size_t)v * W + u, d, o, A, zfar, znear, rgba, depth, ids);
-    }
+      const size_t px = img + (size_t)v * W + u;
+      if (!(tmin <= zfar)) {
+        if (rgba) rgba[px] = 0u;
+        if (depth) depth[px] = 0.0f;
+        if (ids) ids[px] = -1;
+        continue;
+      }
+      if (depth) depth[px] = (float)(tmin < znear ? znear : tmin);
+      if (ids) ids[px] = id;
+      if (rgba) {
+        double cosv = 0.0;
+        const PartW &P = S.part[wpart];
+        if (kMesh) {
+          if (wface >= 0) {  // |n.d| of the hit triangle (two-sided)
+            const double *T = sc.mtri + 9 * wface, *R = S.plane + 9 * wpart;
+            double nl[3], nw[3];
+            cross3(T + 3, T + 6, nl);
+            matvec(R, nl, nw);
+            cosv = fabs(dot3(nw, d)) / sqrt(dot3(nw, nw));
+          }
+        } else if (P.kind == RS_SPHERE) {
+          if (tmin > 0.0) {
+            double n[3];
+            for (int i = 0; i < 3; ++i) n[i] = (o[i] + tmin * d[i] - P.c[i]) / P.r;
+            cosv = -dot3(n, d);
+          }
+        } else if (wface >= 0) {
+          const double *Q = S.plane + 4 * wface;
+          cosv = -(d[0] * Q[0] + d[1] * Q[1] + d[2] * Q[2]);
+        }
+        float shade = __fadd_rn(0.3f, __fmul_rn(0.7f, (float)(cosv > 0.0 ? cosv : 0.0)));
+        const float *col = sc.color + 3 * id;
+        uint32_t px4 = 0xff000000u;
+        for (int i = 0; i < 3; ++i) {
+          float cv = __fadd_rn(__fmul_rn(__fmul_rn(255.0f, col[i]), shade), 0.5f);
+          px4 |= (uint32_t)(cv > 255.0f ? 255.0f : cv) << (8 * i);
+        }
+        rgba[px] = px4;
+      }
     }
   }
   if (work) atomicAdd(work, tests);

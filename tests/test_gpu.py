@@ -59,13 +59,24 @@ def test_teacher_forced_vs_oracle_and_reference(name):
     arm = torch.tensor(g["arm"], dtype=torch.float64)
     base = torch.tensor(g["base"], dtype=torch.float64)
     ht = torch.tensor(g["has_targets"].astype(np.uint8))
-    sim.step_physics(arm, base, ht, check=True)
-    torch.cuda.synchronize()
+    orc = oracle(LAYOUT[name], **cfg)
+    # pass 0: warp-per-env kernel (no heavy flags yet); pass 1: the same inputs
+    # again -- envs the first pass flagged contact-heavy now take the CTA
+    # (wavefront Gauss-Seidel) kernel; both must match bit for bit.
+    for pass_ in range(2):
+        if pass_:
+            sim.set_state([g["pre"][s].tobytes() for s in range(n)])
+        sim.step_physics(arm, base, ht, check=True)
+        torch.cuda.synchronize()
+        _check_pass(sim, g, orc, name, n)
+    sim.close()
+
+
+def _check_pass(sim, g, orc, name, n):
     out = sim.get_state()
     counters = sim.counters().cpu().numpy()
     ev_cnt = sim.event_counts().cpu().numpy()
     events = sim.events().cpu().numpy()
-    orc = oracle(LAYOUT[name], **cfg)
     for s in range(n):
         arm_s = g["arm"][s] if g["has_targets"][s] else None
         r = orc.step(g["pre"][s].tobytes(), arm_s, g["base"][s])
@@ -87,7 +98,6 @@ def test_teacher_forced_vs_oracle_and_reference(name):
         ev_o = r.events[r.events[:, 2] > EV_NOISE]
         np.testing.assert_array_equal(ev[:, :2], ev_o[:, :2])
         np.testing.assert_allclose(ev[:, 2:], ev_o[:, 2:], rtol=1e-9, atol=1e-9)
-    sim.close()
 
 
 def test_free_running_matches_oracle():
