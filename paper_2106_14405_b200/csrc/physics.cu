@@ -1427,7 +1427,7 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
 // level touch disjoint state, so solving them concurrently gives bit-identical
 // results to the reference's sequential order (physics.py:931-937).
 constexpr int kHeavyWarps = 4;
-constexpr int kHeavyGroups = 4;  // envs with >= this many active groups go to the CTA kernel
+constexpr int kHeavyGroups = 2;  // envs with >= this many active groups go to the CTA kernel
 
 struct HeavyShared {
   BlockWS ws[kHeavyWarps - 1];  // block-solver workspaces of warps 1..
