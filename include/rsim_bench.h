@@ -18,6 +18,16 @@ int rsim_bench_fma_peak(int fp64, double *tflops);
 struct rs_batch;
 int rsim_bench_render_work(struct rs_batch *batch, unsigned int cam_mask, unsigned long long *d_counter,
                            void *stream);
+/* rs_render with every ray test in FP64 (rs_render selects candidates with
+ * bounded-error FP32 box tests and resolves them in FP64; this variant is its
+ * parity reference). Same arguments and outputs as rs_render. */
+int rsim_bench_render_exact(struct rs_batch *batch, unsigned int cam_mask, unsigned char *rgba, float *depth,
+                            int *ids, void *stream);
+/* Per-env step latency probe: when d_cycles (device int64[E]) is set, every
+ * step writes each env's SM clock cycles from kernel entry to its state
+ * write-back (negated for envs run by the contact-heavy CTA kernel); NULL
+ * turns the probe off. */
+int rsim_bench_env_cycles(struct rs_batch *batch, long long *d_cycles);
 /* same for rs_render_mesh: counts candidate-part BVH traversals */
 int rsim_bench_render_mesh_work(struct rs_batch *batch, unsigned int cam_mask, unsigned long long *d_counter,
                                 void *stream);

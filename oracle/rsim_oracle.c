@@ -792,6 +792,22 @@ void orc_jacobi_pair(int n, int r, int k, int *p, int *q) {
   *q = a < b ? b : a;
 }
 
+#ifdef ORC_PROFILE
+/* solver work log for tools/solver_profile.py (not built by default) */
+typedef struct { int sub, it, g, m, na, mask, sweeps, asi; } orc_prof_rec;
+static orc_prof_rec g_prof[1 << 20];
+static int g_nprof, g_prof_sub, g_prof_it, g_prof_g, g_prof_m, g_prof_mask, g_prof_asi, g_last_sweeps;
+int orc_profile_take(int *out, int cap) {
+  int n = g_nprof < cap ? g_nprof : cap;
+  memcpy(out, g_prof, sizeof(orc_prof_rec) * n);
+  g_nprof = 0;
+  return n;
+}
+#define PROF_SWEEPS(s) (g_last_sweeps = (s))
+#else
+#define PROF_SWEEPS(s) ((void)0)
+#endif
+
 static void sym_eig(int m, double *A, double *V, double *ev) {
   const int n = m + (m & 1);
   double cs[16], sn[16];
@@ -812,7 +828,9 @@ static void sym_eig(int m, double *A, double *V, double *ev) {
       off += ro;
       tot += rt;
     }
+    PROF_SWEEPS(sweep);
     if (off <= 1e-30 * tot || off == 0.0) break; /* off-diagonal <= 1e-15 of the Frobenius norm */
+    PROF_SWEEPS(sweep + 1);
     for (int r = 0; r < n - 1; ++r) {
       for (int k = 0; k < n / 2; ++k) {
         int p, q;
@@ -901,6 +919,14 @@ static void solve_block(row_t *rows, int first, int m, const double *K, velset_t
       }
       pinv_solve(na, sub, rhs, 1e-8, sol);
       for (int i = 0; i < na; ++i) lam[active[i]] = sol[i];
+#ifdef ORC_PROFILE
+      if (g_nprof < (1 << 20)) {
+        int mask = 0;
+        for (int i = 0; i < na; ++i) mask |= 1 << active[i];
+        orc_prof_rec r = {g_prof_sub, g_prof_it, g_prof_g, m, na, mask, g_last_sweeps, it};
+        g_prof[g_nprof++] = r;
+      }
+#endif
     }
     int worst = -1;
     for (int i = 0; i < na; ++i) {
@@ -1114,6 +1140,9 @@ static int substep(const orc_world *w, ostate *st, const double *arm, const doub
                    scratch_t *S, orc_trace *tr, int sub) {
   const rs_physics_config *cfg = &w->cfg;
   int nb = w->nb, nsj = w->nsj;
+#ifdef ORC_PROFILE
+  g_prof_sub = sub;
+#endif
   if (!cfg->sleeping_enabled)
     for (int b = 0; b < nb; ++b)
       if (w->body_kind[b] == RS_DYNAMIC && st->asleep[b]) {
@@ -1293,6 +1322,9 @@ static int substep(const orc_world *w, ostate *st, const double *arm, const doub
     }
     for (int it = 0; it < cfg->solver_iterations; ++it)
       for (int g = 0; g < npc; ++g) {
+#ifdef ORC_PROFILE
+        g_prof_it = it; g_prof_g = g;
+#endif
         if (!hasK[g])
           for (int i = pair_first[g]; i < pair_first[g] + pair_n[g]; ++i) solve_row(&S->rows[i], &vs);
         else

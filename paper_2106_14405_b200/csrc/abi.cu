@@ -21,6 +21,9 @@ cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, f
                           cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work = nullptr);
+cudaError_t launch_render_tables(const DevBatch &B, cudaStream_t stream);
+cudaError_t launch_render_exact(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                                cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_grasp(const DevBatch &B, const double *gripper, int stride, cudaStream_t stream);
 cudaError_t launch_ik(const DevBatch &B, const double *delta, int stride, double *targets, int32_t *failed,
                       double *scratch, cudaStream_t stream);
@@ -235,6 +238,8 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   BA(event_count, sizeof(int32_t) * n_env);
   BA(events, sizeof(double) * 7 * (size_t)(event_cap ? event_cap : 1) * n_env);
   BA(counters, sizeof(int64_t) * 3 * n_env);
+  BA(ray_dir, sizeof(double) * 3 * (size_t)rcfg->width * rcfg->height);
+  BA(tile_frustum, sizeof(double) * 8 * (size_t)(rcfg->width / 16) * (rcfg->height / 16));
   BA(row_scratch, sizeof(double) * step_scratch_doubles_per_env(d.row_cap) * (size_t)n_env);
   if (!rc) rc = balloc(b, &p, 2 * (size_t)n_env), b->heavy[0] = (uint8_t *)p, b->heavy[1] = (uint8_t *)p + n_env;
 #undef BA
@@ -248,6 +253,7 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   b->has_mesh = true;
   for (int i = 0; i < n_scenes; ++i) {
     hs[i] = scenes[i]->d;
+    d.max_nf = hs[i].nf > d.max_nf ? hs[i].nf : d.max_nf;
     b->has_mesh = b->has_mesh && hs[i].mtri != nullptr;
   }
   std::vector<int32_t> es(n_env, 0);
@@ -260,6 +266,10 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   }
   d.scenes = b->d_scenes;
   d.env_scene = b->d_env_scene;
+  if (launch_render_tables(d, 0) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
+    rs_batch_destroy(b);
+    return fail(RS_ERR_CUDA, "render table setup failed");
+  }
   b->sd_buf[0] = d.sd; b->sd_buf[1] = d.sd_out;
   b->si_buf[0] = d.si; b->si_buf[1] = d.si_out;
   *out = b;
@@ -512,6 +522,19 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
 int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
   if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
+  return RS_OK;
+}
+
+int rsim_bench_env_cycles(rs_batch *b, long long *d_cycles) {
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  b->d.env_cycles = d_cycles;
+  return RS_OK;
+}
+
+int rsim_bench_render_exact(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                            void *stream) {
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  CUDA_TRY(launch_render_exact(b->view(), cam_mask, rgba, depth, ids, (cudaStream_t)stream));
   return RS_OK;
 }
 

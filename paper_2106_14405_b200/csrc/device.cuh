@@ -93,6 +93,7 @@ struct StateLayout {
 
 struct DevBatch {
   int n_env, nb, nj;
+  int max_nf;          // most facets of any scene in the batch (render smem sizing)
   StateLayout L;
   double *sd;          // [E][L.dbl_size]  current state s_t (read)
   int32_t *si;         // [E][L.int_size]
@@ -114,6 +115,10 @@ struct DevBatch {
   // optional parity trace (rs_set_trace)
   int32_t *trace_pairs, *trace_count;
   int trace_cap, trace_sub;
+  // render tables (render_tables_kernel): unit camera-frame ray per pixel, tile frustum planes
+  const double *ray_dir, *tile_frustum;
+  // optional per-env step latency probe (rsim_bench_env_cycles): SM clock cycles of the last step
+  long long *env_cycles;
 };
 
 }  // namespace rsim

@@ -1608,6 +1608,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   const int env = blockIdx.x * kWarpsPerBlock + warp;
   if (env >= B.n_env) return;
   if (heavy_in && heavy_in[env]) return;
+  const long long t_begin = B.env_cycles ? clock64() : 0;
   WarpSmem &S = smem[warp];
   Ctx c;
   make_ctx(c, B, S, env, lane, 0);
@@ -1624,6 +1625,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   }
   __syncwarp();
   env_end(c, B, env, dt, ok, heavy_out);
+  if (B.env_cycles && lane == 0) B.env_cycles[env] = clock64() - t_begin;
 }
 
 // CTA of kHeavyWarps warps per env (envs flagged heavy by the previous step)
@@ -1637,6 +1639,7 @@ __global__ void __launch_bounds__(32 * kHeavyWarps) step_kernel_cta(DevBatch B, 
   HeavyShared &H = *reinterpret_cast<HeavyShared *>(dsm + ((sizeof(WarpSmem) + 15) & ~(size_t)15));
   const int env = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!heavy_in[env]) return;
+  const long long t_begin = B.env_cycles ? clock64() : 0;
   Ctx c;
   make_ctx(c, B, S, env, lane, warp);
   if (warp == 0) {
@@ -1669,6 +1672,7 @@ __global__ void __launch_bounds__(32 * kHeavyWarps) step_kernel_cta(DevBatch B, 
     __syncthreads();
   }
   if (warp == 0) env_end(c, B, env, dt, ok, heavy_out);
+  if (B.env_cycles && threadIdx.x == 0) B.env_cycles[env] = -(clock64() - t_begin);  // negative: CTA kernel
 }
 
 __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {

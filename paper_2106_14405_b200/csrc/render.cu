@@ -51,15 +51,26 @@ struct PartW {
   int f0, nf, kind, body;
 };
 
+// render variants
+constexpr int kProxyMixed = 0;  // FP32 box tests select candidates, FP64 resolves them (default)
+constexpr int kMeshExact = 1;   // triangle soup, FP64
+constexpr int kProxyExact = 2;  // every test in FP64 (the parity reference for kProxyMixed)
+
 struct RenderSmem {
-  double plane[4 * 1024];  // n.xyz, b0 per facet (world)
   PartW part[kMaxParts];
+  float4 box32[kMaxParts][4];  // FP32 box data: (u_k, b0 of +k) k = 0..2, (b0 of -0, -1, -2, 0)
+  float2 trace[kMaxParts];     // (lb rounded down, kind << 8 | body as int bits)
   uint32_t mask[kMaxTiles][kMaskWords];
-  uint8_t list[kMaxTiles][kMaxParts];  // per tile: candidate parts in ascending lb
+  union {
+    double R[kMaxParts][9];               // staging: world part rotations (proxy variants)
+    uint8_t list[kMaxTiles][kMaxParts];  // per tile: candidate parts in ascending lb
+  } u;
   int nlist[kMaxTiles];
   uint8_t order[kMaxParts];
   Pose cam;
 };
+// world planes (n.xyz, b0 per facet; mesh variant: part rotations) follow the struct
+constexpr size_t kPlaneOff = (sizeof(RenderSmem) + 15) & ~(size_t)15;
 
 // ray vs one convex (reference _ray_halfspaces, one ray); face = entering plane.
 // Division-free: the hit test te <= tx && tx >= 0 is evaluated as
@@ -145,31 +156,30 @@ __device__ __forceinline__ double ray_sphere(const PartW &p, const double *o, co
   return t0 >= 0.0 ? t0 : (t1 >= 0.0 ? 0.0 : INFINITY);
 }
 
-__device__ __forceinline__ double part_hit(const RenderSmem &S, int p, const double *o, const double *d, int &face,
-                                           double tcut = INFINITY) {
+__device__ __forceinline__ double part_hit(const RenderSmem &S, const double *plane, int p, const double *o,
+                                           const double *d, int &face, double tcut = INFINITY) {
   const PartW &P = S.part[p];
   double t;
   if (P.kind == RS_SPHERE) {
     face = -1;
     return ray_sphere(P, o, d);
   } else if (P.kind == RS_BOX) {
-    t = ray_box(S.plane + 4 * P.f0, d, tcut, face);
+    t = ray_box(plane + 4 * P.f0, d, tcut, face);
   } else {
-    t = ray_convex<false>(S.plane + 4 * P.f0, P.nf, d, tcut, face);
+    t = ray_convex<false>(plane + 4 * P.f0, P.nf, d, tcut, face);
   }
   if (face >= 0) face += P.f0;
   return t;
 }
 
-
 // ---- triangle-soup path (AssetDef.visual_mesh, scene.py:63-76)
 // Part-local BVH traversal; two-sided Moller-Trumbore in scaled form so only
 // accepted hits are divided.  Triangles are stored as (v0, e1 = v1 - v0,
 // e2 = v2 - v0).  `face` returns the triangle index (for shading).
-__device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem &S, int p, const double *o,
-                                           const double *d, double tcut, int &face) {
+__device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem &S, const double *plane, int p,
+                                           const double *o, const double *d, double tcut, int &face) {
   const PartW &P = S.part[p];
-  const double *R = S.plane + 9 * p;  // mesh mode keeps part rotations here
+  const double *R = plane + 9 * p;  // mesh mode keeps part rotations here
   double v[3] = {o[0] - P.c[0], o[1] - P.c[1], o[2] - P.c[2]}, ol[3], dl[3];
   mattvec(R, v, ol);
   mattvec(R, d, dl);
@@ -226,8 +236,9 @@ __device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem 
 
 // exact lowest-id rule for near-tie pixels: bodies in id order, parts in order
 template <bool kMesh>
-__device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S, const uint32_t *mask, const double *o,
-                                         const double *d, double tmin, double eps, int &id, int &wpart, int &wface) {
+__device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S, const double *plane,
+                                         const uint32_t *mask, const double *o, const double *d, double tmin,
+                                         double eps, int &id, int &wpart, int &wface) {
   int cur_b = -1, cur_p = -1, cur_f = -1;
   double cur_t = INFINITY;
   for (int w = 0; w < kMaskWords; ++w) {
@@ -242,19 +253,153 @@ __device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S
         cur_t = INFINITY;
       }
       int f;
-      double t = kMesh ? mesh_hit(sc, S, p, o, d, INFINITY, f) : part_hit(S, p, o, d, f);
+      double t = kMesh ? mesh_hit(sc, S, plane, p, o, d, INFINITY, f) : part_hit(S, plane, p, o, d, f);
       if (t < cur_t) { cur_t = t; cur_p = p; cur_f = f; }
     }
   }
   if (cur_b >= 0 && cur_t <= tmin + eps) { id = cur_b; wpart = cur_p; wface = cur_f; }
 }
 
+// All-FP64 walk of one pixel's tile list (front to back, exact early-out,
+// near-tie re-resolution).  The mesh and exact variants use it for every
+// pixel; the mixed variant only for a pixel whose candidate set overflows.
 template <bool kMesh>
-__global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinBlocksProxy) render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out,
-                                                                uint32_t *rgba, float *depth, int32_t *ids,
-                                                                unsigned long long *work) {
+__device__ __forceinline__ double trace_exact(const DevScene &sc, const RenderSmem &S, const double *plane,
+                                              const uint8_t *list, int nl, const uint32_t *mask, const double *o,
+                                              const double *d, double eps, int &id, int &wpart, int &wface,
+                                              unsigned long long &tests, bool count) {
+  double tmin = INFINITY, t2 = INFINITY;
+  id = -1; wpart = -1; wface = -1;
+#pragma unroll 1
+  for (int j = 0; j < nl; ++j) {
+    const int p = list[j];
+    const PartW &P = S.part[p];
+    if (P.lb > tmin + eps) break;  // sorted: nothing later can be nearer or tie
+    int fc;
+    const double t = kMesh ? mesh_hit(sc, S, plane, p, o, d, tmin + eps, fc) : part_hit(S, plane, p, o, d, fc, tmin + eps);
+    if (count) tests += kMesh ? 1 : (P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf));
+    if (!(t < INFINITY)) continue;
+    const int b = P.body;
+    if (b == id) {
+      if (t < tmin || (t == tmin && p < wpart)) { tmin = t; wpart = p; wface = fc; }
+    } else if (t < tmin) {
+      t2 = tmin;
+      tmin = t; id = b; wpart = p; wface = fc;
+    } else if (t < t2) {
+      t2 = t;
+    }
+  }
+  if (tmin < INFINITY && t2 - tmin <= eps) resolve_tie<kMesh>(sc, S, plane, mask, o, d, tmin, eps, id, wpart, wface);
+  return tmin;
+}
+
+// ---- mixed-precision walk (kProxyMixed) --------------------------------
+//
+// FP32 box test with a rigorous error bound.  With d a unit vector and u_k
+// unit normals rounded to float, |s32 - s| <= ~5u (u = 2^-24) for
+// s = d.u_k; b32 = float(b0) has relative error u; t = b/|s| through the
+// approximate reciprocal adds ~3u.  So every ratio carries a relative error
+// <= kEs/|s| + 4u, and max/min over the three axes keep that bound.  The
+// margin e = (|te| + |tx|)(kEs/amin + kRel) (kEs, kRel carry >= 2x slack)
+// bounds |t32 - t64|.  Results:
+//   0  certain miss  (tx < -e or te - tx > e: the FP64 test misses too)
+//   1  certain hit   t in [t32 - e, t32 + e] (t = 0, e = 0: origin strictly inside)
+//   2  uncertain     (a near-parallel axis |s| < kAmin, exit near the origin,
+//                     grazing edge te ~ tx, or entry near the origin):
+//                     the caller evaluates the part in FP64.
+constexpr float kEs = 2e-6f;
+constexpr float kRel = 16.0f * 5.9604645e-8f;
+constexpr float kAmin = 1e-3f;
+
+__device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float dz, float &t, float &e) {
+  const float4 A = bx[0], Bv = bx[1], C = bx[2], M = bx[3];
+  const float s0 = fmaf(dx, A.x, fmaf(dy, A.y, dz * A.z));
+  const float s1 = fmaf(dx, Bv.x, fmaf(dy, Bv.y, dz * Bv.z));
+  const float s2 = fmaf(dx, C.x, fmaf(dy, C.y, dz * C.z));
+  const float a0 = fabsf(s0), a1 = fabsf(s1), a2 = fabsf(s2);
+  const float amin = fminf(a0, fminf(a1, a2));
+  if (amin < kAmin) return 2;
+  const float r0 = __fdividef(1.0f, a0), r1 = __fdividef(1.0f, a1), r2 = __fdividef(1.0f, a2);
+  const float te = fmaxf(-(s0 < 0.f ? A.w : M.x) * r0, fmaxf(-(s1 < 0.f ? Bv.w : M.y) * r1, -(s2 < 0.f ? C.w : M.z) * r2));
+  const float tx = fminf((s0 < 0.f ? M.x : A.w) * r0, fminf((s1 < 0.f ? M.y : Bv.w) * r1, (s2 < 0.f ? M.z : C.w) * r2));
+  const float rmax = fmaxf(r0, fmaxf(r1, r2));
+  e = (fabsf(te) + fabsf(tx)) * fmaf(kEs, rmax, kRel);
+  if (tx < -e || te - tx > e) return 0;
+  if (tx <= e || tx - te <= e) return 2;
+  if (te < -e) { t = 0.0f; e = 0.0f; return 1; }
+  if (te <= e) return 2;
+  t = te;
+  return 1;
+}
+
+// Walk one pixel's tile list with FP32 box tests (spheres and hulls, and
+// uncertain boxes, in FP64), keeping every part whose lower bound can still
+// be within tie_eps of the nearest hit (at most two: coplanar ties); then
+// resolve them in FP64 with the exact nearest / lowest-id rule.  Returns
+// false if a third candidate was live (the caller falls back to trace_exact).
+__device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *plane, const uint8_t *list, int nl,
+                                            const double *o, const double *d, double eps, double &tmin, int &id,
+                                            int &wpart, int &wface, unsigned long long &tests, bool count) {
+  const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
+  const float eps32 = __double2float_ru(eps);
+  float tup = INFINITY, bound = INFINITY;  // upper bound of the nearest hit range; + tie_eps
+  int p1 = -1, p2 = -1;
+  float l1 = INFINITY, l2 = INFINITY;  // candidates' lower bounds
+#pragma unroll 1
+  for (int j = 0; j < nl; ++j) {
+    const int p = list[j];
+    const float2 tr = S.trace[p];
+    if (tr.x > bound) break;  // sorted by lb: nothing later can be nearer or tie
+    const int kind = __float_as_int(tr.y) >> 8;
+    float tl, tu;
+    int st = 2;
+    if (kind == RS_BOX) {
+      float t, e;
+      st = box32(S.box32[p], dx, dy, dz, t, e);
+      if (count) tests += 6;
+      if (st == 0) continue;
+      if (st == 1) { tl = __fsub_rd(t, e); tu = __fadd_ru(t, e); }
+    }
+    if (st == 2) {
+      int fc;
+      const double t = part_hit(S, plane, p, o, d, fc);
+      if (count) tests += kind == RS_BOX ? 6 : (kind == RS_SPHERE ? 1 : S.part[p].nf);
+      if (!(t < INFINITY)) continue;
+      tl = __double2float_rd(t);
+      tu = __double2float_ru(t);
+    }
+    if (tu < tup) { tup = tu; bound = __fadd_ru(tup, eps32); }
+    if (tl > bound) continue;
+    if (l1 > bound) { p1 = p; l1 = tl; }       // slot 1 free or stale
+    else if (l2 > bound) { p2 = p; l2 = tl; }  // slot 2 free or stale
+    else return false;
+  }
+  // exact resolution: t* = min over candidates; id = lowest body within tie_eps
+  int f1 = -1, f2 = -1;
+  double t1 = INFINITY, t2 = INFINITY;
+  if (p1 >= 0 && l1 <= bound) t1 = part_hit(S, plane, p1, o, d, f1);
+  if (p2 >= 0 && l2 <= bound) t2 = part_hit(S, plane, p2, o, d, f2);
+  if (count) tests += 12;
+  tmin = fmin(t1, t2);
+  id = -1; wpart = -1; wface = -1;
+  if (!(tmin < INFINITY)) return true;
+  const bool in1 = t1 <= tmin + eps, in2 = t2 <= tmin + eps;
+  const int b1 = in1 ? S.part[p1].body : 0x7fffffff, b2 = in2 ? S.part[p2].body : 0x7fffffff;
+  // lowest body wins; within a body its nearest part, the lower part index on equal range
+  const bool take2 = b2 < b1 || (b2 == b1 && (t2 < t1 || (t2 == t1 && p2 < p1)));
+  if (take2) { id = b2; wpart = p2; wface = f2; }
+  else { id = b1; wpart = p1; wface = f1; }
+  return true;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBlocksMesh : kMinBlocksProxy)
+    render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out, uint32_t *rgba, float *depth, int32_t *ids,
+                  unsigned long long *work) {
+  constexpr bool kMesh = kMode == kMeshExact;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RenderSmem &S = *reinterpret_cast<RenderSmem *>(smem_raw);
+  double *plane = reinterpret_cast<double *>(smem_raw + kPlaneOff);
   const int env = blockIdx.x / n_cam_out, slot = blockIdx.x % n_cam_out;
   int cam = -1;
   for (int c = 0, k = 0; c < 32; ++c)
@@ -292,7 +437,8 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
   __syncthreads();
   const double *o = S.cam.p;
 
-  // -- world part frames, bounds, world planes (geometry.py:554-557), b0 = d - n.o
+  // -- world part frames and bounds (lanes per part), then world planes
+  //    (geometry.py:554-557), b0 = d - n.o (lanes per facet)
   for (int p = tid; p < np; p += blockDim.x) {
     int b = sc.part_body[p];
     Pose bp, lp, wp;
@@ -308,59 +454,87 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
     P.nf = sc.part_facet_begin[p + 1] - P.f0;
     if (kMesh) {
       P.r = sc.mesh_bound[p];
-      for (int k = 0; k < 9; ++k) S.plane[9 * p + k] = wp.R[k];
+      for (int k = 0; k < 9; ++k) plane[9 * p + k] = wp.R[k];
     } else {
       P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : sc.part_bound[p];
+      for (int k = 0; k < 9; ++k) S.u.R[p][k] = wp.R[k];
     }
     double v[3] = {wp.p[0] - o[0], wp.p[1] - o[1], wp.p[2] - o[2]};
     double dist = sqrt(dot3(v, v)) - P.r * (1.0 + 1e-9) - 1e-9;
     P.lb = dist > 0.0 ? dist : 0.0;
-    for (int f = P.f0; f < P.f0 + (kMesh ? 0 : P.nf); ++f) {
-      const double *F = sc.facet + 4 * f;
+    S.trace[p] = make_float2(__double2float_rd(P.lb), __int_as_float((P.kind << 8) | b));
+  }
+  __syncthreads();
+  if (!kMesh) {
+    const int nf = sc.nf;
+    for (int f = tid; f < nf; f += blockDim.x) {
+      int lo = 0, hi = np - 1;  // owning part: last p with f0 <= f
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (S.part[mid].f0 <= f) lo = mid; else hi = mid - 1;
+      }
+      const double *F = sc.facet + 4 * f, *R = S.u.R[lo], *wpp = S.part[lo].c;
       double n[3];
-      matvec(wp.R, F, n);
-      double dw = F[3] + dot3(n, wp.p);
-      double *Q = S.plane + 4 * f;
+      matvec(R, F, n);
+      double dw = F[3] + dot3(n, wpp);
+      double *Q = plane + 4 * f;
       Q[0] = n[0]; Q[1] = n[1]; Q[2] = n[2];
       Q[3] = dw - dot3(o, n);
     }
+    __syncthreads();
+    if (kMode == kProxyMixed)
+      for (int p = tid; p < np; p += blockDim.x) {
+        const PartW &P = S.part[p];
+        if (P.kind != RS_BOX) continue;
+        const double *Q = plane + 4 * P.f0;
+        for (int k = 0; k < 3; ++k)
+          S.box32[p][k] = make_float4((float)Q[4 * k], (float)Q[4 * k + 1], (float)Q[4 * k + 2], (float)Q[4 * k + 3]);
+        S.box32[p][3] = make_float4((float)Q[15], (float)Q[19], (float)Q[23], 0.0f);
+      }
   }
   const int W = B.rcfg.width, H = B.rcfg.height;
   const int tx_n = W / kTile, ty_n = H / kTile, ntiles = tx_n * ty_n;
-  for (int i = tid; i < ntiles * kMaskWords; i += blockDim.x) S.mask[i / kMaskWords][i % kMaskWords] = 0u;
-  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  if (kMesh) __syncthreads();
 
-  // -- front-to-back order of parts (rank by (lb, index))
-  for (int p = tid; p < np; p += blockDim.x) {
-    const double lb = S.part[p].lb;
-    int rank = 0;
-    for (int q = 0; q < np; ++q) {
-      double lq = S.part[q].lb;
-      rank += (lq < lb) || (lq == lb && q < p);
+  // -- warps 0..3: tile culling, lane = part (sphere vs the 4 side planes of
+  //    each tile frustum, camera frame; inward normals from B.tile_frustum),
+  //    one ballot per (tile, 32 parts) = one mask word.  Warps 4..7: the
+  //    front-to-back order of parts (rank by (lb, index)).
+  if (warp < kMaskWords) {
+    const int p = warp * 32 + lane;
+    double c[3] = {0.0, 0.0, 0.0}, r = 0.0;
+    const bool live = p < np;
+    if (live) {
+      const PartW &P = S.part[p];
+      double v[3] = {P.c[0] - o[0], P.c[1] - o[1], P.c[2] - o[2]};
+      mattvec(S.cam.R, v, c);  // camera frame: x right, y down, z view
+      r = P.r * (1.0 + 1e-9) + 1e-9;
     }
-    S.order[rank] = (uint8_t)p;
-  }
-  // -- tile culling: sphere vs the 4 side planes of the tile frustum (camera frame)
-  const double f = (W / 2.0) / tan(B.rcfg.fov / 2.0);
-  for (int i = tid; i < ntiles * np; i += blockDim.x) {
-    int tile = i / np, p = i % np;
-    const PartW &P = S.part[p];
-    double v[3] = {P.c[0] - o[0], P.c[1] - o[1], P.c[2] - o[2]}, c[3];
-    mattvec(S.cam.R, v, c);  // camera frame: x right, y down, z view
-    double r = P.r * (1.0 + 1e-9) + 1e-9;
-    bool in = c[2] > -r;
-    if (in) {
-      double u0 = ((tile % tx_n) * kTile - W / 2.0) / f, u1 = ((tile % tx_n) * kTile + kTile - W / 2.0) / f;
-      double v0 = ((tile / tx_n) * kTile - H / 2.0) / f, v1 = ((tile / tx_n) * kTile + kTile - H / 2.0) / f;
-      double nl = sqrt(1.0 + u0 * u0), nr = sqrt(1.0 + u1 * u1), nt = sqrt(1.0 + v0 * v0), nbm = sqrt(1.0 + v1 * v1);
-      in = (c[0] - u0 * c[2]) / nl >= -r && (-c[0] + u1 * c[2]) / nr >= -r && (c[1] - v0 * c[2]) / nt >= -r &&
-           (-c[1] + v1 * c[2]) / nbm >= -r;
+    const bool front = live && c[2] > -r;
+    for (int tile = 0; tile < ntiles; ++tile) {
+      bool in = false;
+      if (front) {
+        const double *T = B.tile_frustum + 8 * tile;  // u0, u1, v0, v1, |(1,u0)|, |(1,u1)|, |(1,v0)|, |(1,v1)|
+        in = c[0] - T[0] * c[2] >= -r * T[4] && -c[0] + T[1] * c[2] >= -r * T[5] &&
+             c[1] - T[2] * c[2] >= -r * T[6] && -c[1] + T[3] * c[2] >= -r * T[7];
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (lane == 0) S.mask[tile][warp] = m;
     }
-    if (in) atomicOr(&S.mask[tile][p >> 5], 1u << (p & 31));
+  } else {
+    for (int p = tid - 32 * kMaskWords; p < np; p += blockDim.x - 32 * kMaskWords) {
+      const double lb = S.part[p].lb;
+      int rank = 0;
+      for (int q = 0; q < np; ++q) {
+        double lq = S.part[q].lb;
+        rank += (lq < lb) || (lq == lb && q < p);
+      }
+      S.order[rank] = (uint8_t)p;
+    }
   }
   __syncthreads();
   // -- per tile candidate lists in front-to-back order (warp per tile, ballot compaction)
-  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   for (int tile = warp; tile < ntiles; tile += nwarps) {
     int n = 0;
     for (int i0 = 0; i0 < np; i0 += 32) {
@@ -368,7 +542,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
       int p = i < np ? S.order[i] : 0;
       bool in = i < np && ((S.mask[tile][p >> 5] >> (p & 31)) & 1u);
       unsigned m = __ballot_sync(0xffffffffu, in);
-      if (in) S.list[tile][n + __popc(m & ((1u << lane) - 1))] = (uint8_t)p;
+      if (in) S.u.list[tile][n + __popc(m & ((1u << lane) - 1))] = (uint8_t)p;
       n += __popc(m);
     }
     if (lane == 0) S.nlist[tile] = n;
@@ -379,42 +553,23 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
   const double eps = B.rcfg.tie_eps, zfar = B.rcfg.zfar, znear = B.rcfg.znear;
   const size_t img = (size_t)(env * n_cam_out + slot) * H * W;
   unsigned long long tests = 0;
+  const bool count = work != nullptr;
 #pragma unroll 1
   for (int tile = warp; tile < ntiles; tile += nwarps) {
-    const uint8_t *list = S.list[tile];
+    const uint8_t *list = S.u.list[tile];
     const int nl = S.nlist[tile];
     const int ux = (tile % tx_n) * kTile, vy = (tile / tx_n) * kTile;
 #pragma unroll 1
     for (int k = lane; k < kTile * kTile; k += 32) {
       const int u = ux + (k % kTile), v = vy + (k / kTile);
-      double dc[3] = {(u + 0.5 - W / 2.0) / f, (v + 0.5 - H / 2.0) / f, 1.0};
-      double l = sqrt(dot3(dc, dc));
-      const double rl = 1.0 / l;
-      dc[0] *= rl; dc[1] *= rl; dc[2] *= rl;
+      const double *dc = B.ray_dir + 3 * ((size_t)v * W + u);  // unit camera-frame ray (render_tables_kernel)
       double d[3];
       matvec(S.cam.R, dc, d);
-      double tmin = INFINITY, t2 = INFINITY;
-      int id = -1, wpart = -1, wface = -1;
-#pragma unroll 1
-      for (int j = 0; j < nl; ++j) {
-        const int p = list[j];
-        const PartW &P = S.part[p];
-        if (P.lb > tmin + eps) break;  // sorted: nothing later can be nearer or tie
-        int fc;
-        const double t = kMesh ? mesh_hit(sc, S, p, o, d, tmin + eps, fc) : part_hit(S, p, o, d, fc, tmin + eps);
-        if (work) tests += kMesh ? 1 : (P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf));
-        if (!(t < INFINITY)) continue;
-        const int b = P.body;
-        if (b == id) {
-          if (t < tmin || (t == tmin && p < wpart)) { tmin = t; wpart = p; wface = fc; }
-        } else if (t < tmin) {
-          t2 = tmin;
-          tmin = t; id = b; wpart = p; wface = fc;
-        } else if (t < t2) {
-          t2 = t;
-        }
-      }
-      if (tmin < INFINITY && t2 - tmin <= eps) resolve_tie<kMesh>(sc, S, S.mask[tile], o, d, tmin, eps, id, wpart, wface);
+      double tmin;
+      int id, wpart, wface;
+      if (kMode != kProxyMixed ||
+          !trace_mixed(S, plane, list, nl, o, d, eps, tmin, id, wpart, wface, tests, count))
+        tmin = trace_exact<kMesh>(sc, S, plane, list, nl, S.mask[tile], o, d, eps, id, wpart, wface, tests, count);
 
       const size_t px = img + (size_t)v * W + u;
       if (!(tmin <= zfar)) {
@@ -430,7 +585,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
         const PartW &P = S.part[wpart];
         if (kMesh) {
           if (wface >= 0) {  // |n.d| of the hit triangle (two-sided)
-            const double *T = sc.mtri + 9 * wface, *R = S.plane + 9 * wpart;
+            const double *T = sc.mtri + 9 * wface, *R = plane + 9 * wpart;
             double nl[3], nw[3];
             cross3(T + 3, T + 6, nl);
             matvec(R, nl, nw);
@@ -443,7 +598,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
             cosv = -dot3(n, d);
           }
         } else if (wface >= 0) {
-          const double *Q = S.plane + 4 * wface;
+          const double *Q = plane + 4 * wface;
           cosv = -(d[0] * Q[0] + d[1] * Q[1] + d[2] * Q[2]);
         }
         float shade = __fadd_rn(0.3f, __fmul_rn(0.7f, (float)(cosv > 0.0 ? cosv : 0.0)));
@@ -460,34 +615,72 @@ __global__ void __launch_bounds__(kRenderThreads, kMesh ? kMinBlocksMesh : kMinB
   if (work) atomicAdd(work, tests);
 }
 
-size_t render_smem_bytes() { return sizeof(RenderSmem); }
+// Per-batch constant tables: unit camera-frame ray per pixel centre
+// (u + 1/2, v + 1/2; f = (W/2)/tan(fov/2); normalise) and the inward side
+// planes of every 16x16 tile frustum.
+__global__ void render_tables_kernel(int W, int H, double fov, double *ray_dir, double *tile_frustum) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double f = (W / 2.0) / tan(fov / 2.0);
+  if (i < W * H) {
+    const int u = i % W, v = i / W;
+    double dc[3] = {(u + 0.5 - W / 2.0) / f, (v + 0.5 - H / 2.0) / f, 1.0};
+    double l = sqrt(dot3(dc, dc));
+    const double rl = 1.0 / l;
+    ray_dir[3 * i] = dc[0] * rl; ray_dir[3 * i + 1] = dc[1] * rl; ray_dir[3 * i + 2] = dc[2] * rl;
+  }
+  const int tx_n = W / kTile;
+  if (i < tx_n * (H / kTile)) {
+    double *T = tile_frustum + 8 * i;
+    T[0] = ((i % tx_n) * kTile - W / 2.0) / f; T[1] = ((i % tx_n) * kTile + kTile - W / 2.0) / f;
+    T[2] = ((i / tx_n) * kTile - H / 2.0) / f; T[3] = ((i / tx_n) * kTile + kTile - H / 2.0) / f;
+    for (int k = 0; k < 4; ++k) T[4 + k] = sqrt(1.0 + T[k] * T[k]);
+  }
+}
 
-template <bool kMesh>
+cudaError_t launch_render_tables(const DevBatch &B, cudaStream_t stream) {
+  const int n = B.rcfg.width * B.rcfg.height;
+  render_tables_kernel<<<(n + 255) / 256, 256, 0, stream>>>(B.rcfg.width, B.rcfg.height, B.rcfg.fov,
+                                                            const_cast<double *>(B.ray_dir),
+                                                            const_cast<double *>(B.tile_frustum));
+  return cudaGetLastError();
+}
+
+static size_t render_smem(const DevBatch &B, int mode) {
+  const size_t planes = mode == kMeshExact ? 9 * (size_t)kMaxParts : 4 * (size_t)(B.max_nf > 0 ? B.max_nf : 1024);
+  return kPlaneOff + sizeof(double) * planes;
+}
+
+template <int kMode>
 static cudaError_t launch_render_t(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                    cudaStream_t stream, unsigned long long *work) {
   int n_cam_out = __builtin_popcount(cam_mask);
   if (n_cam_out == 0) return cudaSuccess;
   static bool configured = false;
-  size_t smem = sizeof(RenderSmem);
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(render_kernel<kMesh>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!configured) {  // the largest any batch can ask for: 1024 facets
+    const size_t cap = kPlaneOff + sizeof(double) * (kMode == kMeshExact ? 9 * kMaxParts : 4 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(render_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   dim3 grid(B.n_env * n_cam_out);
-  render_kernel<kMesh><<<grid, kRenderThreads, smem, stream>>>(B, cam_mask, n_cam_out,
-                                                              reinterpret_cast<uint32_t *>(rgba), depth, ids, work);
+  render_kernel<kMode><<<grid, kRenderThreads, render_smem(B, kMode), stream>>>(
+      B, cam_mask, n_cam_out, reinterpret_cast<uint32_t *>(rgba), depth, ids, work);
   return cudaGetLastError();
 }
 
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                           cudaStream_t stream, unsigned long long *work) {
-  return launch_render_t<false>(B, cam_mask, rgba, depth, ids, stream, work);
+  return launch_render_t<kProxyMixed>(B, cam_mask, rgba, depth, ids, stream, work);
+}
+
+cudaError_t launch_render_exact(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                                cudaStream_t stream, unsigned long long *work) {
+  return launch_render_t<kProxyExact>(B, cam_mask, rgba, depth, ids, stream, work);
 }
 
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work) {
-  return launch_render_t<true>(B, cam_mask, rgba, depth, ids, stream, work);
+  return launch_render_t<kMeshExact>(B, cam_mask, rgba, depth, ids, stream, work);
 }
 
 }  // namespace rsim

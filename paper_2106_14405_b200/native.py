@@ -60,6 +60,8 @@ def lib():
     L.rs_set_trace.argtypes = [vp, vp, vp, i32, i32]
     L.rs_scene_set_mesh.argtypes = [vp, C.POINTER(abi.rs_mesh_desc)]
     L.rs_render_mesh.argtypes = [vp, u32, vp, vp, vp, vp]
+    L.rsim_bench_render_exact.argtypes = [vp, u32, vp, vp, vp, vp]
+    L.rsim_bench_env_cycles.argtypes = [vp, vp]
     L.rs_arm_action.argtypes = [vp, vp, vp, vp, vp]
     L.rs_env_step.argtypes = [vp, vp, dbl, i32, vp]
     L.rs_env_step_host.argtypes = [vp, vp, dbl, i32, u32, vp, vp, vp, vp, vp]

@@ -263,6 +263,15 @@ class BatchSimulator:
                                       _stream_ptr()), "rs_render")
         return rgba, depth, ids
 
+    def render_exact(self, cams=("head", "arm"), out=None):
+        """``render`` with every ray test in FP64 (rsim_bench_render_exact): the
+        parity reference of the mixed-precision default; not a serving path."""
+        cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
+        rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
+        native.check(self.L.rsim_bench_render_exact(self._batch, self.cam_mask(cams), _dptr(rgba), _dptr(depth),
+                                                    _dptr(ids), _stream_ptr()), "rsim_bench_render_exact")
+        return rgba, depth, ids
+
     def render_mesh(self, cams=("head", "arm"), out=None):
         """Same as ``render`` against the triangle soups (``mesh_k`` at construction)."""
         cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))

@@ -1,0 +1,92 @@
+"""GPU parity of the mixed-precision renderer (rs_render: bounded-error FP32
+box tests select candidates, FP64 resolves them) against the all-FP64 variant
+(rsim_bench_render_exact) and the C oracle.  The FP64 resolution makes the
+two variants' outputs identical bit for bit: same nearest part, same range,
+same entering face, same lowest-id tie rule."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from conftest import golden  # noqa: E402
+from paper_2106_14405_b200 import native  # noqa: E402
+from paper_2106_14405_b200.geom import base_pose  # noqa: E402
+from paper_2106_14405_b200.scene import build_world, flat_clutter  # noqa: E402
+from paper_2106_14405_b200.sim import BatchSimulator  # noqa: E402
+from paper_2106_14405_b200.state import WorldState, link_poses  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    native.lib()
+
+
+def random_views(n, seed):
+    """Settled-pool states with the robot at random walkable cells, random
+    headings and random arm configurations (link bodies moved along), so the
+    head and arm cameras look everywhere in the three layouts."""
+    pool = golden("settled_pool.npz")
+    worlds = {v: build_world(v, flat_clutter()) for v in range(3)}
+    by_layout = {0: [], 1: [], 2: []}
+    for blob, (v, _s) in zip(pool["snapshots"], pool["tags"]):
+        by_layout[int(v)].append(blob.tobytes())
+    rng = np.random.default_rng(seed)
+    states, layouts = [], []
+    for i in range(n):
+        v = i % 3
+        w = worlds[v]
+        st = WorldState.from_bytes(by_layout[v][rng.integers(len(by_layout[v]))])
+        g = w.layout.grid
+        cells = np.argwhere(g.walkable)
+        ci, cj = cells[rng.integers(len(cells))]
+        x = g.origin[0] + (ci + rng.uniform()) * g.cell
+        y = g.origin[1] + (cj + rng.uniform()) * g.cell
+        st.base = np.array([x, y, rng.uniform(-math.pi, math.pi)])
+        lo, hi = w.robot.limits_lo(), w.robot.limits_hi()
+        q = lo + rng.uniform(size=len(lo)) * (hi - lo)
+        st.joints[w.arm_slice] = q
+        links, _ = link_poses(w.robot, q, st.base)
+        for bid, p in zip(w.robot_body_ids, [base_pose(st.base)] + links):
+            st.pos[bid] = p.pos
+            st.quat[bid] = p.quat()
+        states.append(st.to_bytes())
+        layouts.append(v)
+    return states, layouts
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_mixed_equals_exact_bitwise(seed):
+    n = 768
+    states, layouts = random_views(n, seed)
+    sim = BatchSimulator(layouts=(0, 1, 2), n_env=n, env_layout=layouts)
+    sim.set_state(states)
+    a = sim.render(("head", "arm"))
+    b = sim.render_exact(("head", "arm"))
+    torch.cuda.synchronize()
+    ids_a, ids_b = a[2].cpu().numpy(), b[2].cpu().numpy()
+    bad = np.argwhere(ids_a != ids_b)
+    assert len(bad) == 0, f"{len(bad)} id mismatches, first at {bad[:5].tolist()}"
+    da, db = a[1].cpu().numpy(), b[1].cpu().numpy()
+    np.testing.assert_array_equal(da.view(np.uint32), db.view(np.uint32))
+    assert torch.equal(a[0], b[0])
+    # the views are not degenerate: many bodies visible, some misses, both cameras
+    assert len(np.unique(ids_a)) > 30 and (ids_a == -1).any() and (ids_a >= 0).mean() > 0.5
+    sim.close()
+
+
+def test_mixed_matches_golden_render_frames():
+    """Same images as the all-FP64 variant on the reference-pinned frames."""
+    g = golden("render.npz")
+    n = len(g["cam"])
+    sim = BatchSimulator(layouts=(0,), n_env=n)
+    sim.set_state([s.tobytes() for s in g["state"]])
+    a = [t.cpu().numpy() for t in sim.render()]
+    b = [t.cpu().numpy() for t in sim.render_exact()]
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    sim.close()

@@ -76,9 +76,31 @@ def launches(path):
         print(f"  {k:40s} n={len(v):4d} mean {sum(v) / len(v) / 1e3:9.1f} us  share {100 * sum(v) / tot:5.1f}%")
 
 
+def kernel_json(path):
+    """Per-kernel mean time and DRAM bytes per launch (read by bench.py as roofline.traffic)."""
+    import json
+
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    agg = {}
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("rsim::", "")
+        v = lambda k: float(r[hdr.index(k)])  # noqa: E731
+        a = agg.setdefault(name, {"launches": 0, "gpu_time_ms": 0.0, "dram_bytes": 0.0, "grid": int(v("launch__grid_size"))})
+        a["launches"] += 1
+        a["gpu_time_ms"] += v("gpu__time_duration.sum")
+        a["dram_bytes"] += (v("dram__bytes_read.sum") + v("dram__bytes_write.sum")) * 1e6
+    out = {k: {"launches": a["launches"], "grid": a["grid"], "gpu_time_ms": a["gpu_time_ms"] / a["launches"],
+               "dram_bytes_per_launch": a["dram_bytes"] / a["launches"]} for k, a in agg.items()}
+    print(json.dumps({"source": path.split("/")[-1], "kernels": out}, indent=1))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "--json":
+        kernel_json(sys.argv[2])
     elif sys.argv[1] == "--lines":
         report(sys.argv[2])
         hot_lines(sys.argv[2])
