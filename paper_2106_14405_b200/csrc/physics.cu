@@ -44,6 +44,7 @@ constexpr int kMaxBlockRows = 32;
 constexpr int kRowD = 44;  // doubles per solver row in global scratch
 constexpr int kPairD = 34; // doubles per contact group (pair) in global scratch
 constexpr int kKCap = kMaxContacts * kMaxBlockRows;  // Sigma m^2 <= 32 * 128
+constexpr int kMaxPartsCache = 128;
 
 // ---- row field offsets (doubles) ------------------------------------------
 enum {
@@ -105,7 +106,8 @@ struct Ctx {
   double *Vc;     // [kKCap] cached eigenvectors per block
   double *evc;    // [kMaxContacts] cached eigenvalues per block
   double *W;      // [kMaxBlockRows^2] eigensolver workspace
-  double *saabb;  // [kMaxBodies][6] AABBs of the static bodies for this control step
+  double *bcache; // [kMaxBodies][14]: pose key (pos bits, quat bits, valid) + body AABB
+  double *pcache; // [kMaxPartsCache][18]: world frame (R, p) + AABB of every part, valid for the key pose
   int env, lane;
   const StateLayout *L;
 };
@@ -321,6 +323,40 @@ __device__ void body_aabb(Ctx &c, int b, double *lo, double *hi) {
   }
 }
 
+// body_aabb with a pose-keyed cache in the env's global scratch: the part
+// world frames and AABBs of body b are recomputed only when its position or
+// quaternion bits changed (static and sleeping bodies: once), and stay in
+// c.pcache for the narrowphase of the same substep.  The cached values are
+// the ones the computation would produce (same inputs, same code).
+__device__ void body_aabb_cached(Ctx &c, int b, double *lo, double *hi) {
+  const DevScene &sc = *c.sc;
+  const double *pos = POS(c, b), *q = QUAT(c, b);
+  double *K = c.bcache + 14 * b;
+  const long long *kb = reinterpret_cast<const long long *>(K);
+  bool hit = K[7] == 1.0;
+  for (int i = 0; i < 3 && hit; ++i) hit = kb[i] == __double_as_longlong(pos[i]);
+  for (int i = 0; i < 4 && hit; ++i) hit = kb[3 + i] == __double_as_longlong(q[i]);
+  if (hit) {
+    for (int i = 0; i < 3; ++i) { lo[i] = K[8 + i]; hi[i] = K[11 + i]; }
+    return;
+  }
+  Pose bp, wp;
+  body_pose(c, b, bp);
+  for (int i = 0; i < 3; ++i) { lo[i] = INFINITY; hi[i] = -INFINITY; }
+  for (int p = sc.body_part_begin[b]; p < sc.body_part_begin[b + 1]; ++p) {
+    double l[3], h[3];
+    part_world(c, bp, p, wp);
+    prim_aabb(c, p, wp, l, h);
+    double *P = c.pcache + 18 * p;
+    for (int k = 0; k < 9; ++k) P[k] = wp.R[k];
+    for (int i = 0; i < 3; ++i) { P[9 + i] = wp.p[i]; P[12 + i] = l[i]; P[15 + i] = h[i]; }
+    for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], l[i]); hi[i] = fmax(hi[i], h[i]); }
+  }
+  for (int i = 0; i < 3; ++i) { K[i] = pos[i]; K[8 + i] = lo[i]; K[11 + i] = hi[i]; }
+  for (int i = 0; i < 4; ++i) K[3 + i] = q[i];
+  K[7] = 1.0;
+}
+
 // world planes of part p into S->planes[slot] (lanes per facet)
 __device__ void planes_world(Ctx &c, int p, const Pose &wp, int slot) {
   const DevScene &sc = *c.sc;
@@ -495,29 +531,28 @@ __device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
   const int a0 = sc.body_part_begin[a], na = sc.body_part_begin[a + 1] - a0;
   const int b0 = sc.body_part_begin[b], nbp = sc.body_part_begin[b + 1] - b0;
   auto &NP = c.S->u.np;
-  if (c.lane < na + nbp) {
-    const int side = c.lane < na ? 0 : 1, k = side ? c.lane - na : c.lane, p = side ? b0 + k : a0 + k;
-    Pose bp, wp;
-    body_pose(c, side ? b : a, bp);
-    part_world(c, bp, p, wp);
-    double lo[3], hi[3];
-    prim_aabb(c, p, wp, lo, hi);
-    for (int q = 0; q < 9; ++q) NP.pw[side][k][q] = wp.R[q];
-    for (int q = 0; q < 3; ++q) {
-      NP.pw[side][k][9 + q] = wp.p[q];
-      NP.pab[side][k][q] = lo[q];
-      NP.pab[side][k][3 + q] = hi[q];
-    }
+  for (int e = c.lane; e < 18 * (na + nbp); e += 32) {  // this substep's part frames + AABBs (body_aabb_cached)
+    const int k = e / 18, q = e % 18, side = k < na ? 0 : 1, kk = side ? k - na : k;
+    const double v = c.pcache[18 * ((side ? b0 : a0) + kk) + q];
+    if (q < 12) NP.pw[side][kk][q] = v; else NP.pab[side][kk][q - 12] = v;
   }
   __syncwarp();
   int base = c.S->nc, n = 0;
   for (int ii = 0; ii < na; ++ii) {
-    const double *la = NP.pab[0][ii], *ha = NP.pab[0][ii] + 3;
-    for (int jj = 0; jj < nbp; ++jj) {
-      const double *lb = NP.pab[1][jj], *hb = NP.pab[1][jj] + 3;
-      bool sep = false;
-      for (int k = 0; k < 3; ++k) sep |= (la[k] > hb[k] + margin) || (lb[k] > ha[k] + margin);
-      if (sep) continue;
+    unsigned live = 0u;  // parts of b whose AABB meets part ii of a (lanes per part of b)
+    {
+      bool ok = false;
+      if (c.lane < nbp) {
+        const double *la = NP.pab[0][ii], *ha = NP.pab[0][ii] + 3, *lb = NP.pab[1][c.lane], *hb = NP.pab[1][c.lane] + 3;
+        bool sep = false;
+        for (int k = 0; k < 3; ++k) sep |= (la[k] > hb[k] + margin) || (lb[k] > ha[k] + margin);
+        ok = !sep;
+      }
+      live = __ballot_sync(0xffffffffu, ok);
+    }
+    while (live) {
+      const int jj = __ffs(live) - 1;
+      live &= live - 1;
       const int i = a0 + ii, j = b0 + jj;
       Pose wa, wb;
       pose_load12(NP.pw[0][ii], wa);
@@ -1027,17 +1062,13 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   }
   __syncwarp();
 
-  // ---- broadphase: AABBs (lanes per body); static bodies never move during
-  // a control step: theirs come from the per-step cache (c.saabb)
+  // ---- broadphase: AABBs (lanes per body) through the pose-keyed cache: only
+  // bodies that moved are recomputed (body_aabb_cached)
   for (int b = lane; b < nb; b += 32) {
     double lo[3], hi[3];
-    if (sc.body_kind[b] == RS_STATIC) {
-      for (int i = 0; i < 3; ++i) { lo[i] = c.saabb[6 * b + i]; hi[i] = c.saabb[6 * b + 3 + i]; }
-    } else {
-      body_aabb(c, b, lo, hi);
-      if (sc.body_kind[b] == RS_KINEMATIC)
-        for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
-    }
+    body_aabb_cached(c, b, lo, hi);
+    if (sc.body_kind[b] == RS_KINEMATIC)
+      for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
     for (int i = 0; i < 3; ++i) { S.u.bp.lo[b][i] = lo[i]; S.u.bp.hi[b][i] = hi[i]; }
   }
   __syncwarp();
@@ -1523,8 +1554,9 @@ __device__ void make_ctx(Ctx &c, const DevBatch &B, WarpSmem &S, int env, int la
   c.K = c.pairs + kMaxGroups * kPairD;
   c.Vc = c.K + kKCap;
   c.evc = c.Vc + 2 * kKCap;
-  c.saabb = c.evc + 2 * kMaxContacts;
-  c.W = c.saabb + 6 * kMaxBodies + (size_t)warp * kMaxBlockRows * kMaxBlockRows;
+  c.bcache = c.evc + 2 * kMaxContacts;
+  c.pcache = c.bcache + 14 * kMaxBodies;
+  c.W = c.pcache + 18 * kMaxPartsCache + (size_t)warp * kMaxBlockRows * kMaxBlockRows;
 }
 
 // stage scene header + state slab, _check_finite (physics.py:596-606), per-step
@@ -1566,8 +1598,6 @@ __device__ bool env_begin(Ctx &c, const DevBatch &B, int env) {
     return false;
   }
   if (lane < kMaxArm) S.budget[lane] = B.cfg.motor_impulse_cap;
-  for (int b = lane; b < sc.nb; b += 32)
-    if (sc.body_kind[b] == RS_STATIC) body_aabb(c, b, c.saabb + 6 * b, c.saabb + 6 * b + 3);
   __syncwarp();
   return true;
 }
@@ -1676,7 +1706,8 @@ __global__ void __launch_bounds__(32 * kHeavyWarps) step_kernel_cta(DevBatch B, 
 }
 
 __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
-  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + 6 * kMaxBodies +
+  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + 14 * kMaxBodies +
+         18 * kMaxPartsCache +
          (size_t)kHeavyWarps * kMaxBlockRows * kMaxBlockRows;
 }
 int step_row_cap() { return kMaxContacts; }
