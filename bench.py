@@ -456,6 +456,28 @@ def run_b200(args):
             "clocks": clk.summary(),
             "episode_stats_allreduce": {"accumulated_contact_force_sum": stats["acc"], "envs": int(stats["envs"])},
         }
+        # widened rows: geodesic fields for one goal per env and the
+        # per-step geodesic reward query from every robot base
+        goals = torch.tensor(np.random.default_rng(5).uniform([-4.5, -2.5], [4.5, 2.5], (E, 2)), device=dev)
+        fields, _ = sim.distance_fields(goals, layouts=layout_of(gids).tolist())
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        fields, _ = sim.distance_fields(goals, layouts=layout_of(gids).tolist())
+        ev[1].record(stream)
+        idx = torch.arange(E, device=dev, dtype=torch.int32)
+        sim.geodesic_distance(fields, idx)
+        ev[2].record(stream)
+        for _ in range(10):
+            sim.geodesic_distance(fields, idx)
+        ev[3].record(stream)
+        torch.cuda.synchronize(dev)
+        nx_, ny_ = sim.nav_shape()
+        line["geodesics"] = {"distance_fields_per_s": E / (ev[0].elapsed_time(ev[1]) * 1e-3),
+                             "grid": [nx_, ny_], "fields": E,
+                             "geodesic_queries_per_s": 10 * E / (ev[2].elapsed_time(ev[3]) * 1e-3),
+                             "note": "rs_nav_fields (one CTA per goal, bit-exact vs the reference Dijkstra) and "
+                                     "rs_nav_geodesic from every robot base"}
+        del fields
         if world == 1 and not args.no_cpu_baseline:
             sps, cores, wall, steps = cpu_oracle_sps(args.cpu_baseline_steps)
             line["cpu_baseline"] = {"value": sps, "unit": UNIT, "cores": cores, "kind": "port",

@@ -220,6 +220,33 @@ int rs_scene_set_mesh(rs_scene *scene, const rs_mesh_desc *mesh);
  * rs_render; a camera inside a closed mesh sees its exit faces). */
 int rs_render_mesh(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream);
 
+/* ---- geodesics on the walk grid (navgrid.py:109-172).
+ * Every scene of the batch must share the walk-grid shape (rs_nav_shape).
+ * Fields are float64 [nx][ny] (x-major, the reference's NavGrid layout),
+ * +inf where unreachable; all pointers are device pointers. */
+/* grid shape of the batch's scenes; RS_ERR_ARG if they differ */
+int rs_nav_shape(rs_batch *batch, int32_t *nx, int32_t *ny);
+/* NavGrid.distance_field (navgrid.py:109-143): for goal g (scene
+ * scene_of_goal[g], NULL = scene 0) the geodesic distance from every cell to
+ * the cell of nearest_walkable(goal_xy[g]) -> fields[g]; goal_cell[g]
+ * (optional) = i*ny + j of that cell.  Bit-identical to the reference's
+ * Dijkstra (unique fixed point of the relaxation). */
+int rs_nav_fields(rs_batch *batch, const int32_t *scene_of_goal, const double *goal_xy, int32_t n_goals,
+                  double *fields, int32_t *goal_cell, void *stream);
+/* NavGrid.geodesic_distance (navgrid.py:145-148) against precomputed fields:
+ * out[q] = fields[field_of_query[q]] at the cell of nearest_walkable(from_xy[q]).
+ * from_xy = NULL: query q is env q's robot base (n_queries = n_env, the env's
+ * scene); else scene_of_query (NULL = scene 0). */
+int rs_nav_geodesic(rs_batch *batch, const double *fields, const int32_t *field_of_query,
+                    const int32_t *scene_of_query, const double *from_xy, int32_t n_queries, double *out,
+                    void *stream);
+/* NavGrid.shortest_path (navgrid.py:150-172): steepest-descent waypoints
+ * (cell centres) [n_queries][cap][2] and their count (0 = unreachable,
+ * truncated at cap). */
+int rs_nav_path(rs_batch *batch, const double *fields, const int32_t *field_of_query, const int32_t *scene_of_query,
+                const double *from_xy, int32_t n_queries, int32_t cap, double *waypoints, int32_t *count,
+                void *stream);
+
 /* Debug trace for parity tests (not on the hot path): when set, every rs_step
  * records per env and substep the admitted broadphase pairs in sorted order
  * with their narrowphase contact counts:

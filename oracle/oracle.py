@@ -58,6 +58,12 @@ def lib():
         L.orc_solve_ik.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_apply_arm_action.restype = C.c_int
         L.orc_apply_arm_action.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_nav_field.restype = C.c_long
+        L.orc_nav_field.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_void_p]
+        L.orc_nav_geodesic.restype = C.c_double
+        L.orc_nav_geodesic.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double]
+        L.orc_nav_path.restype = C.c_int
+        L.orc_nav_path.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_int]
         L.orc_snapshot_size.restype = C.c_int64
         L.orc_snapshot_size.argtypes = [C.c_int, C.c_int]
         _lib = L
@@ -150,6 +156,22 @@ class Oracle:
         out = np.zeros(len(sd))
         r = lib().orc_solve_ik(self.h, t.ctypes.data, sd.ctypes.data, out.ctypes.data)
         return r, (out if r >= 0 else sd.copy())
+
+    def nav_field(self, goal_xy):
+        """navgrid.distance_field restated: [nx, ny] geodesic distances to the goal."""
+        out = np.zeros((self.desc.desc.nav_nx, self.desc.desc.nav_ny))
+        lib().orc_nav_field(self.h, float(goal_xy[0]), float(goal_xy[1]), out.ctypes.data)
+        return out
+
+    def nav_geodesic(self, field, from_xy):
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        return lib().orc_nav_geodesic(self.h, f.ctypes.data, float(from_xy[0]), float(from_xy[1]))
+
+    def nav_path(self, field, from_xy, cap=4096):
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        out = np.zeros((cap, 2))
+        n = lib().orc_nav_path(self.h, f.ctypes.data, float(from_xy[0]), float(from_xy[1]), out.ctypes.data, cap)
+        return out[:n]
 
     def apply_arm_action(self, q, delta):
         """(joint targets, ik_failed) -- robot.apply_arm_action restated."""

@@ -450,6 +450,117 @@ void orc_move_base(const orc_world *w, const double *base, double lin, double an
   out[0] = nx; out[1] = ny; out[2] = nyaw;
 }
 
+/* ------------------------------------------------------------- geodesics */
+
+/* navgrid.py:109-143 distance_field: Dijkstra from the goal's cell (after
+ * nearest_walkable) over walkable 8-neighbours, step cost cell (straight) or
+ * cell*sqrt(2) (diagonal), heap ordered by (d, i, j) like heapq on tuples.
+ * out: [nx][ny] (x-major), +inf where unreachable. Returns the goal cell
+ * index i*ny+j. */
+typedef struct { double d; long i, j; } heap_e;
+static int heap_less(const heap_e *a, const heap_e *b) {
+  return a->d < b->d || (a->d == b->d && (a->i < b->i || (a->i == b->i && a->j < b->j)));
+}
+static void heap_push(heap_e *h, long *n, heap_e e) {
+  long k = (*n)++;
+  while (k > 0) {
+    long p = (k - 1) / 2;
+    if (!heap_less(&e, &h[p])) break;
+    h[k] = h[p];
+    k = p;
+  }
+  h[k] = e;
+}
+static heap_e heap_pop(heap_e *h, long *n) {
+  heap_e top = h[0], last = h[--(*n)];
+  long k = 0;
+  for (;;) {
+    long c = 2 * k + 1;
+    if (c >= *n) break;
+    if (c + 1 < *n && heap_less(&h[c + 1], &h[c])) ++c;
+    if (!heap_less(&h[c], &last)) break;
+    h[k] = h[c];
+    k = c;
+  }
+  if (*n > 0) h[k] = last;
+  return top;
+}
+long orc_nav_field(const orc_world *w, double gx, double gy, double *out) {
+  const long nx = w->nav_nx, ny = w->nav_ny;
+  double g[2];
+  if (orc_nearest_walkable(w, gx, gy, g) < 0) return -1;
+  long gi, gj;
+  nav_cell_of(w, g[0], g[1], &gi, &gj);
+  for (long k = 0; k < nx * ny; ++k) out[k] = INFINITY;
+  out[gi * ny + gj] = 0.0;
+  const double straight = w->nav_cell, diag = w->nav_cell * sqrt(2.0);
+  long cap = 8 * nx * ny + 16, n = 0;
+  heap_e *h = (heap_e *)malloc(sizeof(heap_e) * cap);
+  heap_e e0 = {0.0, gi, gj};
+  heap_push(h, &n, e0);
+  while (n > 0) {
+    heap_e e = heap_pop(h, &n);
+    if (e.d > out[e.i * ny + e.j]) continue;
+    for (int di = -1; di <= 1; ++di)
+      for (int dj = -1; dj <= 1; ++dj) {
+        if (!di && !dj) continue;
+        long ni = e.i + di, nj = e.j + dj;
+        if (ni < 0 || ni >= nx || nj < 0 || nj >= ny || !w->nav[ni * ny + nj]) continue;
+        double nd = e.d + ((di && dj) ? diag : straight);
+        if (nd < out[ni * ny + nj]) {
+          out[ni * ny + nj] = nd;
+          if (n >= cap) { cap *= 2; h = (heap_e *)realloc(h, sizeof(heap_e) * cap); }
+          heap_e f = {nd, ni, nj};
+          heap_push(h, &n, f);
+        }
+      }
+  }
+  free(h);
+  return gi * ny + gj;
+}
+/* navgrid.py:145-148 geodesic_distance against a field from orc_nav_field */
+double orc_nav_geodesic(const orc_world *w, const double *field, double fx, double fy) {
+  double p[2];
+  if (orc_nearest_walkable(w, fx, fy, p) < 0) return INFINITY;
+  long i, j;
+  nav_cell_of(w, p[0], p[1], &i, &j);
+  return field[i * w->nav_ny + j];
+}
+/* navgrid.py:150-172 shortest_path: steepest descent on the field from the
+ * start cell; waypoints (cell centres) into out[cap][2]; returns the count
+ * (0 when unreachable; the path is truncated at cap). */
+int orc_nav_path(const orc_world *w, const double *field, double fx, double fy, double *out, int cap) {
+  const long nx = w->nav_nx, ny = w->nav_ny;
+  double p[2];
+  if (orc_nearest_walkable(w, fx, fy, p) < 0) return 0;
+  long ci, cj;
+  nav_cell_of(w, p[0], p[1], &ci, &cj);
+  if (!isfinite(field[ci * ny + cj])) return 0;
+  int n = 0;
+  if (n < cap) { nav_centre(w, ci, cj, out + 2 * n); }
+  ++n;
+  long guard = nx * ny;
+  while (field[ci * ny + cj] > 0.0 && guard > 0) {
+    --guard;
+    int found = 0;
+    double bv = 0.0;
+    long bi = 0, bj = 0;
+    for (int di = -1; di <= 1; ++di)
+      for (int dj = -1; dj <= 1; ++dj) {
+        if (!di && !dj) continue;
+        long ni = ci + di, nj = cj + dj;
+        if (ni < 0 || ni >= nx || nj < 0 || nj >= ny || !isfinite(field[ni * ny + nj])) continue;
+        double v = field[ni * ny + nj];
+        if (!found || v < bv || (v == bv && (ni < bi || (ni == bi && nj < bj)))) { found = 1; bv = v; bi = ni; bj = nj; }
+      }
+    if (!found || bv >= field[ci * ny + cj]) break;
+    ci = bi; cj = bj;
+    if (n < cap) nav_centre(w, ci, cj, out + 2 * n);
+    ++n;
+  }
+  return n < cap ? n : cap;
+}
+
 /* -------------------------------------------------------------- primitives */
 
 static void part_world(const orc_world *w, const pose_t *bp, int p, pose_t *o) {

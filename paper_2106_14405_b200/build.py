@@ -24,8 +24,9 @@ UNITS = {
     "render.cu": [],
     "abi.cu": [],
     "peak.cu": [],
+    "nav.cu": ["-fmad=false"],
 }
-HEADERS = ["device.cuh", "se3.cuh"]
+HEADERS = ["device.cuh", "se3.cuh", "navgrid.cuh"]
 
 
 def _nvcc() -> str:

@@ -22,6 +22,14 @@ cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, f
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_tables(const DevBatch &B, cudaStream_t stream);
+cudaError_t launch_nav_fields(const DevBatch &B, int nx, int ny, const int32_t *scene_of_goal, const double *goal_xy,
+                              int n_goals, double *fields, int32_t *goal_cell, cudaStream_t stream);
+cudaError_t launch_nav_geodesic(const DevBatch &B, int nx, int ny, const double *fields, const int32_t *field_of_query,
+                                const int32_t *scene_of_query, const double *from_xy, int nq, double *out,
+                                cudaStream_t stream);
+cudaError_t launch_nav_path(const DevBatch &B, int nx, int ny, const double *fields, const int32_t *field_of_query,
+                            const int32_t *scene_of_query, const double *from_xy, int nq, int cap, double *waypoints,
+                            int32_t *count, cudaStream_t stream);
 cudaError_t launch_render_exact(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                 cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_grasp(const DevBatch &B, const double *gripper, int stride, cudaStream_t stream);
@@ -58,6 +66,8 @@ struct rs_batch {
   std::vector<void *> allocs;
   int narm = 0;
   bool has_mesh = false;
+  int nav_nx = -1, nav_ny = -1;  // shared walk-grid shape (-1: scenes differ)
+  int n_scenes = 0;
   // ping-pong state buffers: rs_step reads buf[cur] and writes buf[cur ^ 1]
   double *sd_buf[2] = {nullptr, nullptr};
   int32_t *si_buf[2] = {nullptr, nullptr};
@@ -251,8 +261,11 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   }
   std::vector<DevScene> hs(n_scenes);
   b->has_mesh = true;
+  b->n_scenes = n_scenes;
+  b->nav_nx = s0.nav_nx; b->nav_ny = s0.nav_ny;
   for (int i = 0; i < n_scenes; ++i) {
     hs[i] = scenes[i]->d;
+    if (hs[i].nav_nx != s0.nav_nx || hs[i].nav_ny != s0.nav_ny) b->nav_nx = b->nav_ny = -1;
     d.max_nf = hs[i].nf > d.max_nf ? hs[i].nf : d.max_nf;
     b->has_mesh = b->has_mesh && hs[i].mtri != nullptr;
   }
@@ -522,6 +535,45 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
 int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
   if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
+  return RS_OK;
+}
+
+// ---- geodesics (navgrid.py:109-172)
+int rs_nav_shape(rs_batch *b, int32_t *nx, int32_t *ny) {
+  if (!b || !nx || !ny) return fail(RS_ERR_ARG, "null argument");
+  if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
+  *nx = b->nav_nx; *ny = b->nav_ny;
+  return RS_OK;
+}
+
+int rs_nav_fields(rs_batch *b, const int32_t *scene_of_goal, const double *goal_xy, int32_t n_goals, double *fields,
+                  int32_t *goal_cell, void *stream) {
+  if (!b || !goal_xy || !fields || n_goals < 0) return fail(RS_ERR_ARG, "bad nav field arguments");
+  if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
+  if ((size_t)b->nav_nx * b->nav_ny * 9 > 227 * 1024) return fail(RS_ERR_ARG, "walk grid too large for one CTA");
+  CUDA_TRY(launch_nav_fields(b->view(), b->nav_nx, b->nav_ny, scene_of_goal, goal_xy, n_goals, fields, goal_cell,
+                             (cudaStream_t)stream));
+  return RS_OK;
+}
+
+int rs_nav_geodesic(rs_batch *b, const double *fields, const int32_t *field_of_query, const int32_t *scene_of_query,
+                    const double *from_xy, int32_t n_queries, double *out, void *stream) {
+  if (!b || !fields || !field_of_query || !out || n_queries < 0) return fail(RS_ERR_ARG, "bad geodesic arguments");
+  if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
+  if (!from_xy && n_queries != b->d.n_env) return fail(RS_ERR_ARG, "robot-base queries need n_queries == n_env");
+  CUDA_TRY(launch_nav_geodesic(b->view(), b->nav_nx, b->nav_ny, fields, field_of_query, scene_of_query, from_xy,
+                               n_queries, out, (cudaStream_t)stream));
+  return RS_OK;
+}
+
+int rs_nav_path(rs_batch *b, const double *fields, const int32_t *field_of_query, const int32_t *scene_of_query,
+                const double *from_xy, int32_t n_queries, int32_t cap, double *waypoints, int32_t *count,
+                void *stream) {
+  if (!b || !fields || !field_of_query || !from_xy || !waypoints || !count || n_queries < 0 || cap < 1)
+    return fail(RS_ERR_ARG, "bad path arguments");
+  if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
+  CUDA_TRY(launch_nav_path(b->view(), b->nav_nx, b->nav_ny, fields, field_of_query, scene_of_query, from_xy,
+                           n_queries, cap, waypoints, count, (cudaStream_t)stream));
   return RS_OK;
 }
 

@@ -30,6 +30,7 @@
 #include <cstdint>
 
 #include "device.cuh"
+#include "navgrid.cuh"
 #include "se3.cuh"
 
 namespace rsim {
@@ -189,43 +190,14 @@ __device__ void forward_kinematics(Ctx &c) {
   __syncwarp();
 }
 
-__device__ __forceinline__ bool nav_ok(const DevScene &sc, long i, long j) {
-  return i >= 0 && i < sc.nav_nx && j >= 0 && j < sc.nav_ny && sc.nav[i * sc.nav_ny + j];
-}
-__device__ bool nav_ring(const DevScene &sc, long ci, long cj, long r, double x, double y, double &bd, long &bi,
-                         long &bj) {
-  bool found = false;
-  for (long i = ci - r; i <= ci + r; ++i)
-    for (long j = cj - r; j <= cj + r; ++j) {
-      long di = i > ci ? i - ci : ci - i, dj = j > cj ? j - cj : cj - j;
-      if ((di > dj ? di : dj) != r || !nav_ok(sc, i, j)) continue;
-      double cx = sc.nav_origin[0] + ((double)i + 0.5) * sc.nav_cell;
-      double cy = sc.nav_origin[1] + ((double)j + 0.5) * sc.nav_cell;
-      double ex = cx - x, ey = cy - y, d2 = ex * ex + ey * ey;
-      if (!found || d2 < bd || (d2 == bd && (i < bi || (i == bi && j < bj)))) { bd = d2; bi = i; bj = j; found = true; }
-    }
-  return found;
-}
 // robot.py:349-368 + navgrid.py:55-105
 __device__ void move_base(const DevScene &sc, double *base, double lin, double ang, double dt) {
   double x = base[0], y = base[1], yaw = base[2];
   double nx = x + cos(yaw) * lin * dt, ny = y + sin(yaw) * lin * dt;
   double nyaw = py_mod(yaw + ang * dt + M_PI, 2.0 * M_PI) - M_PI;
-  long ci = (long)floor((nx - sc.nav_origin[0]) / sc.nav_cell);
-  long cj = (long)floor((ny - sc.nav_origin[1]) / sc.nav_cell);
-  if (!nav_ok(sc, ci, cj)) {
-    long maxr = sc.nav_nx > sc.nav_ny ? sc.nav_nx : sc.nav_ny;
-    for (long r = 0; r <= maxr; ++r) {
-      double bd, bd2;
-      long bi, bj, bi2, bj2;
-      if (!nav_ring(sc, ci, cj, r, nx, ny, bd, bi, bj)) continue;
-      if (nav_ring(sc, ci, cj, r + 1, nx, ny, bd2, bi2, bj2) && bd2 < bd) { bi = bi2; bj = bj2; }
-      nx = sc.nav_origin[0] + ((double)bi + 0.5) * sc.nav_cell;
-      ny = sc.nav_origin[1] + ((double)bj + 0.5) * sc.nav_cell;
-      break;
-    }
-  }
-  base[0] = nx; base[1] = ny; base[2] = nyaw;
+  double p[2];
+  nav_nearest_walkable(sc, nx, ny, p);
+  base[0] = p[0]; base[1] = p[1]; base[2] = nyaw;
 }
 
 __device__ void joint_child_pose(Ctx &c, int ji, double q, Pose &o) {

@@ -280,6 +280,53 @@ class BatchSimulator:
                                            _stream_ptr()), "rs_render_mesh")
         return rgba, depth, ids
 
+    # -------------------------------------------- geodesics (navgrid.py:109-172)
+    def nav_shape(self) -> tuple[int, int]:
+        nx, ny = C.c_int32(), C.c_int32()
+        native.check(self.L.rs_nav_shape(self._batch, C.byref(nx), C.byref(ny)), "rs_nav_shape")
+        return nx.value, ny.value
+
+    def distance_fields(self, goals_xy, layouts=None):
+        """NavGrid.distance_field for G goals: ``[G, nx, ny]`` float64 device
+        tensor (+inf unreachable) and the goal cells ``[G]`` (i*ny + j).
+        ``layouts[g]`` indexes the batch's layouts (default: the first)."""
+        nx, ny = self.nav_shape()
+        n = len(goals_xy)
+        g = self._dev(goals_xy, (n, 2), torch.float64)
+        fields = torch.empty((n, nx, ny), dtype=torch.float64, device=self.device)
+        cells = torch.empty(n, dtype=torch.int32, device=self.device)
+        sc = None if layouts is None else self._dev(torch.as_tensor([self.layouts.index(v) for v in layouts]), (n,),
+                                                    torch.int32)
+        native.check(self.L.rs_nav_fields(self._batch, _dptr(sc), _dptr(g), n, _dptr(fields), _dptr(cells),
+                                          _stream_ptr()), "rs_nav_fields")
+        return fields, cells
+
+    def geodesic_distance(self, fields, field_idx, from_xy=None, layouts=None):
+        """NavGrid.geodesic_distance against ``fields``: from ``from_xy [Q, 2]``
+        (scene ``layouts[q]``), or from every env's robot base when None."""
+        n = len(field_idx)
+        fi = self._dev(field_idx, (n,), torch.int32)
+        fx = None if from_xy is None else self._dev(from_xy, (n, 2), torch.float64)
+        sc = None if layouts is None else self._dev(torch.as_tensor([self.layouts.index(v) for v in layouts]), (n,),
+                                                    torch.int32)
+        out = torch.empty(n, dtype=torch.float64, device=self.device)
+        native.check(self.L.rs_nav_geodesic(self._batch, _dptr(fields), _dptr(fi), _dptr(sc), _dptr(fx), n,
+                                            _dptr(out), _stream_ptr()), "rs_nav_geodesic")
+        return out
+
+    def shortest_path(self, fields, field_idx, from_xy, layouts=None, cap: int = 512):
+        """NavGrid.shortest_path: waypoints ``[Q, cap, 2]`` and counts ``[Q]``."""
+        n = len(field_idx)
+        fi = self._dev(field_idx, (n,), torch.int32)
+        fx = self._dev(from_xy, (n, 2), torch.float64)
+        sc = None if layouts is None else self._dev(torch.as_tensor([self.layouts.index(v) for v in layouts]), (n,),
+                                                    torch.int32)
+        wp = torch.empty((n, cap, 2), dtype=torch.float64, device=self.device)
+        cnt = torch.empty(n, dtype=torch.int32, device=self.device)
+        native.check(self.L.rs_nav_path(self._batch, _dptr(fields), _dptr(fi), _dptr(sc), _dptr(fx), n, cap,
+                                        _dptr(wp), _dptr(cnt), _stream_ptr()), "rs_nav_path")
+        return wp, cnt
+
     # ------------------------------------------------------- end-to-end (host)
     def step_host(self, h_arm: torch.Tensor, h_base: torch.Tensor, cams=("head", "arm"), out=None,
                   h_stats: torch.Tensor | None = None, dt=1.0 / 30.0, substeps=4):

@@ -25,6 +25,9 @@ as-is.  Fixtures:
   (|t_b - t_min| <= 1e-9 -> lowest body id; ``physics.py:1096-1100`` keeps
   the lowest id on exact ties).
 * ``kat.npz``  known-answer values (SPEC.md examples) from the reference.
+* ``nav.npz``  geodesic distance fields (Dijkstra, ``navgrid.py:109-143``),
+  geodesic distances and steepest-descent shortest paths
+  (``navgrid.py:145-172``) on the layouts' walk grids.
 
 The numpy/scipy versions and the OpenBLAS core type are recorded in every
 file (``meta`` key): the oracle's float64 last bits depend on them
@@ -543,9 +546,48 @@ def gen_ik():
     print(f"  ik: {len(qs)} actions ({sum(fails)} failures), {len(sq)} solves ({sum(sok)} ok)")
 
 
+# --------------------------------------------------------------------------
+# geodesics (navgrid.py:109-172)
+# --------------------------------------------------------------------------
+
+def gen_nav():
+    """Distance fields (Dijkstra), geodesic distances and steepest-descent
+    shortest paths of the reference NavGrid, layouts 0-2."""
+    rng = np.random.default_rng(11)
+    goals, fields, layouts = [], [], []
+    q_layout, q_from, q_goal, q_dist, paths, path_len = [], [], [], [], [], []
+    for v in range(3):
+        sim, _ = make_sim(v)
+        ng = sim.scene.navgrid
+        cells = np.argwhere(ng.walkable)
+        # walkable centres, random walkable points, a blocked point, an out-of-grid point
+        gs = [ng.center_of(tuple(cells[rng.integers(len(cells))])) for _ in range(2)]
+        gs.append(ng.origin + (cells[rng.integers(len(cells))] + rng.uniform(0.05, 0.95, 2)) * ng.cell)
+        gs.append(np.array([1.6, 1.1]) if v == 0 else np.array([9.0, 0.5]))
+        for g in gs:
+            goals.append(np.asarray(g, float)); layouts.append(v)
+            fields.append(ng.distance_field(g).copy())
+        for k in range(40):
+            g = gs[k % len(gs)]
+            f = ng.origin + rng.uniform(0, 1, 2) * np.array([ng.nx, ng.ny]) * ng.cell
+            q_layout.append(v); q_from.append(f); q_goal.append(np.asarray(g, float))
+            q_dist.append(ng.geodesic_distance(f, g))
+            pth = ng.shortest_path(f, g)
+            path_len.append(len(pth))
+            pad = np.full((400, 2), np.nan)
+            if pth:
+                pad[:len(pth)] = np.array(pth)[:400]
+            paths.append(pad)
+    np.savez_compressed(os.path.join(OUT, "nav.npz"), meta=meta(), goal=np.array(goals), layout=np.array(layouts),
+                        field=np.array(fields), q_layout=np.array(q_layout), q_from=np.array(q_from),
+                        q_goal=np.array(q_goal), q_dist=np.array(q_dist), path=np.array(paths),
+                        path_len=np.array(path_len))
+    print(f"  nav: {len(fields)} fields, {len(q_dist)} queries, max path {max(path_len)}")
+
+
 if __name__ == "__main__":
     t0 = time.time()
-    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik"]
+    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
     blobs = tags = None
@@ -562,3 +604,5 @@ if __name__ == "__main__":
         gen_kat(); print("kat", time.time() - t0)
     if "ik" in what:
         gen_ik(); print("ik", time.time() - t0)
+    if "nav" in what:
+        gen_nav(); print("nav", time.time() - t0)

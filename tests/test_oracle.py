@@ -152,3 +152,17 @@ def test_ik_matches_reference():
         r, q = orc.solve_ik(tgt, seed)
         assert (r >= 0) == bool(ok)
         np.testing.assert_allclose(q, res, rtol=0, atol=1e-9)
+
+
+def test_geodesics_match_reference():
+    """NavGrid.distance_field / geodesic_distance / shortest_path
+    (navgrid.py:109-172) restated: fields, distances and waypoints identical
+    bit for bit to the reference's Dijkstra and steepest descent."""
+    k = golden("nav.npz")
+    for g, v, f in zip(k["goal"], k["layout"], k["field"]):
+        np.testing.assert_array_equal(oracle_for(int(v)).nav_field(g), f)
+    for v, fr, g, dist, path, n in zip(k["q_layout"], k["q_from"], k["q_goal"], k["q_dist"], k["path"], k["path_len"]):
+        orc = oracle_for(int(v))
+        field = orc.nav_field(g)
+        assert orc.nav_geodesic(field, fr) == dist or (np.isinf(dist) and np.isinf(orc.nav_geodesic(field, fr)))
+        np.testing.assert_array_equal(orc.nav_path(field, fr), path[:n])
