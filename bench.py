@@ -478,6 +478,27 @@ def run_b200(args):
                              "note": "rs_nav_fields (one CTA per goal, bit-exact vs the reference Dijkstra) and "
                                      "rs_nav_geodesic from every robot base"}
         del fields
+        # batched settle (fast resets): the reference recipe's spawn
+        # states (settle.npz, 24 layout/seed cases incl. 6 clearance failures) tiled
+        # over all envs, GJK clearance + steps until every placed body sleeps
+        sg = np.load(os.path.join(ROOT, "tests", "golden", "settle.npz"))
+        sel = [i for i in range(len(sg["tags"])) if int(sg["tags"][i][0]) in (0, 1, 2)]
+        by_layout = {v: [i for i in sel if int(sg["tags"][i][0]) == v] for v in range(3)}
+        lay = layout_of(gids)
+        spawns = [sg["spawn"][by_layout[int(lay[e])][e // 3 % len(by_layout[int(lay[e])])]].tobytes() for e in range(E)]
+        clutter = sim.worlds[0].clutter_body_ids
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        st_, _, _, steps_ = sim.settle(spawns, [clutter] * E)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        st_ = st_.cpu().numpy()
+        line["settle"] = {"envs_per_s": E / (ev0.elapsed_time(ev1) * 1e-3), "envs": E,
+                          "settled": int((st_ == 0).sum()), "clearance_failures": int((st_ == 1).sum()),
+                          "max_steps_taken": int(steps_.max()),
+                          "note": "timed: upload of the spawn snapshots (rs_set_state) + rs_settle (GJK spawn "
+                                  "clearance, control steps until every placed body sleeps)"}
         if world == 1 and not args.no_cpu_baseline:
             sps, cores, wall, steps = cpu_oracle_sps(args.cpu_baseline_steps)
             line["cpu_baseline"] = {"value": sps, "unit": UNIT, "cores": cores, "kind": "port",

@@ -220,6 +220,23 @@ int rs_scene_set_mesh(rs_scene *scene, const rs_mesh_desc *mesh);
  * rs_render; a camera inside a closed mesh sees its exit faces). */
 int rs_render_mesh(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream);
 
+/* ---- batched settle (Simulator.settle physics.py:1113-1176)
+ * for fast resets.  The caller writes each settling env's spawn state with
+ * rs_set_state (placements applied the way settle does: pose set, awake,
+ * zero velocity, sleep counter 0, no rider; physics.py:1124-1137).  For the
+ * envs with active[e] = 1 (device uint8, cleared as envs finish):
+ * _assert_spawn_clearance over the placed bodies (device uint64 bitmask
+ * placed[e], checked in ascending body id) with GJK parts_distance, then
+ * control steps without targets (dt 1/30, 4 substeps) until every placed
+ * body sleeps.  Per env: status 0 settled after steps[e] control steps,
+ * 1 clearance < 1 mm (info[e] = body, other; value[e] = clearance), 2 a
+ * placed body fell below floor_z - 0.5 (info[e][0] = body), 3 still awake
+ * after max_steps (max_time 10 s = 301 steps), 4 physics fault (info[e][0]
+ * = fault word).  Envs with active[e] = 0 are not modified.  Synchronises
+ * `stream` every 8 steps to stop early. */
+int rs_settle(rs_batch *batch, const uint64_t *placed, uint8_t *active, int32_t max_steps, double floor_z,
+              int32_t *status, int32_t *info, double *value, int32_t *steps, void *stream);
+
 /* ---- geodesics on the walk grid (navgrid.py:109-172).
  * Every scene of the batch must share the walk-grid shape (rs_nav_shape).
  * Fields are float64 [nx][ny] (x-major, the reference's NavGrid layout),

@@ -64,6 +64,13 @@ def lib():
         L.orc_nav_geodesic.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double]
         L.orc_nav_path.restype = C.c_int
         L.orc_nav_path.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_int]
+        L.orc_spawn_clearance.restype = C.c_int
+        L.orc_spawn_clearance.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_parts_distance.restype = C.c_double
+        L.orc_parts_distance.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int]
+        L.orc_settle.restype = C.c_int
+        L.orc_settle.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p]
         L.orc_snapshot_size.restype = C.c_int64
         L.orc_snapshot_size.argtypes = [C.c_int, C.c_int]
         _lib = L
@@ -172,6 +179,26 @@ class Oracle:
         out = np.zeros((cap, 2))
         n = lib().orc_nav_path(self.h, f.ctypes.data, float(from_xy[0]), float(from_xy[1]), out.ctypes.data, cap)
         return out[:n]
+
+    def parts_distance(self, snapshot: bytes, a: int, b: int) -> float:
+        """geometry.parts_distance (GJK over part pairs) of bodies a, b."""
+        return lib().orc_parts_distance(self.h, bytes(snapshot), a, b)
+
+    def spawn_clearance(self, snapshot: bytes, placed_mask: int):
+        """physics._assert_spawn_clearance: None, or the first (body, other, clearance) below 1 mm."""
+        b, o, d = C.c_int(), C.c_int(), C.c_double()
+        r = lib().orc_spawn_clearance(self.h, bytes(snapshot), placed_mask, C.byref(b), C.byref(o), C.byref(d))
+        return (b.value, o.value, d.value) if r == 1 else None
+
+    def settle(self, spawn: bytes, placed_mask: int, max_steps: int = 300, floor_z: float = 0.0):
+        """Simulator.settle from a spawn state: (status, snapshot, info, value, steps);
+        status 0 settled, 1 clearance, 2 fell, 3 timeout, 4 fault."""
+        out = np.zeros(self.snap_size, np.uint8)
+        info = np.zeros(2, np.int32)
+        val, steps = C.c_double(), C.c_int()
+        st = lib().orc_settle(self.h, bytes(spawn), placed_mask, max_steps, floor_z, out.ctypes.data,
+                              info.ctypes.data, C.byref(val), C.byref(steps))
+        return st, out.tobytes(), info, val.value, steps.value
 
     def apply_arm_action(self, q, delta):
         """(joint targets, ik_failed) -- robot.apply_arm_action restated."""

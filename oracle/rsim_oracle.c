@@ -1571,6 +1571,239 @@ int orc_step(const orc_world *w, const uint8_t *snap_in, uint8_t *snap_out, cons
   return 0;
 }
 
+/* ---------------------------------------------------------------- settle */
+
+/* geometry.py:262-275 support_local / support_world */
+static void support_world(const orc_world *w, int p, const pose_t *wp, const double *d, double *out) {
+  double dl[3], s[3];
+  mattvec(wp->R, d, dl);
+  int k = w->part_kind[p];
+  if (k == RS_BOX) {
+    const double *h = w->part_param + 3 * p;
+    for (int i = 0; i < 3; ++i) s[i] = dl[i] >= 0 ? h[i] : -h[i];
+  } else if (k == RS_SPHERE) {
+    double r = w->part_param[3 * p], n = sqrt(dot3(dl, dl));
+    if (n == 0.0) { s[0] = r; s[1] = 0.0; s[2] = 0.0; }
+    else for (int i = 0; i < 3; ++i) s[i] = (r / n) * dl[i];
+  } else {
+    int best = w->part_vert_begin[p];
+    double bv = -INFINITY;
+    for (int v = w->part_vert_begin[p]; v < w->part_vert_begin[p + 1]; ++v) {
+      double x = dot3(w->vert + 3 * v, dl);
+      if (x > bv) { bv = x; best = v; }  /* np.argmax: first maximum */
+    }
+    for (int i = 0; i < 3; ++i) s[i] = w->vert[3 * best + i];
+  }
+  matvec(wp->R, s, out);
+  for (int i = 0; i < 3; ++i) out[i] += wp->p[i];
+}
+
+/* geometry.py:431-467 _closest_triangle over Minkowski points W[idx[0..2]];
+ * writes the closest point and the reduced simplex (indices into W) */
+static void closest_triangle(double W[][3], const int *idx, double *pt, int *sub, int *nsub) {
+  const double *w1 = W[idx[0]], *w2 = W[idx[1]], *w3 = W[idx[2]];
+  double ab[3], ac[3], ap[3], bp[3], cp[3];
+  for (int i = 0; i < 3; ++i) { ab[i] = w2[i] - w1[i]; ac[i] = w3[i] - w1[i]; ap[i] = -w1[i]; }
+  double d1 = dot3(ab, ap), d2 = dot3(ac, ap);
+  if (d1 <= 0 && d2 <= 0) { memcpy(pt, w1, 24); sub[0] = idx[0]; *nsub = 1; return; }
+  for (int i = 0; i < 3; ++i) bp[i] = -w2[i];
+  double d3 = dot3(ab, bp), d4 = dot3(ac, bp);
+  if (d3 >= 0 && d4 <= d3) { memcpy(pt, w2, 24); sub[0] = idx[1]; *nsub = 1; return; }
+  double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0 && d1 >= 0 && d3 <= 0) {
+    double t = d1 != d3 ? d1 / (d1 - d3) : 0.0;
+    for (int i = 0; i < 3; ++i) pt[i] = w1[i] + t * ab[i];
+    sub[0] = idx[0]; sub[1] = idx[1]; *nsub = 2; return;
+  }
+  for (int i = 0; i < 3; ++i) cp[i] = -w3[i];
+  double d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+  if (d6 >= 0 && d5 <= d6) { memcpy(pt, w3, 24); sub[0] = idx[2]; *nsub = 1; return; }
+  double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) {
+    double t = d2 != d6 ? d2 / (d2 - d6) : 0.0;
+    for (int i = 0; i < 3; ++i) pt[i] = w1[i] + t * ac[i];
+    sub[0] = idx[0]; sub[1] = idx[2]; *nsub = 2; return;
+  }
+  double va = d3 * d6 - d5 * d4;
+  if (va <= 0 && (d4 - d3) >= 0 && (d5 - d6) >= 0) {
+    double t = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+    for (int i = 0; i < 3; ++i) pt[i] = w2[i] + t * (w3[i] - w2[i]);
+    sub[0] = idx[1]; sub[1] = idx[2]; *nsub = 2; return;
+  }
+  double denom = va + vb + vc, v = vb / denom, ww = vc / denom;
+  for (int i = 0; i < 3; ++i) pt[i] = w1[i] + ab[i] * v + ac[i] * ww;
+  sub[0] = idx[0]; sub[1] = idx[1]; sub[2] = idx[2]; *nsub = 3;
+}
+
+/* geometry.py:383-428 _closest_simplex; simplex = W[0..n-1], reduced in place.
+ * Returns 1 when a tetrahedron contains the origin. */
+static int closest_simplex(double W[4][3], int *n, double *pt) {
+  int sub[4], ns = 0;
+  if (*n == 1) { memcpy(pt, W[0], 24); return 0; }
+  if (*n == 2) {
+    double d[3];
+    for (int i = 0; i < 3; ++i) d[i] = W[1][i] - W[0][i];
+    double dd = dot3(d, d), t = dd == 0.0 ? 0.0 : -dot3(W[0], d) / dd;
+    if (t <= 0.0) { memcpy(pt, W[0], 24); *n = 1; return 0; }
+    if (t >= 1.0) { memcpy(pt, W[1], 24); memcpy(W[0], W[1], 24); *n = 1; return 0; }
+    for (int i = 0; i < 3; ++i) pt[i] = W[0][i] + t * d[i];
+    return 0;
+  }
+  if (*n == 3) {
+    int idx[3] = {0, 1, 2};
+    closest_triangle(W, idx, pt, sub, &ns);
+  } else {
+    static const int faces[4][4] = {{0, 1, 2, 3}, {0, 1, 3, 2}, {0, 2, 3, 1}, {1, 2, 3, 0}};
+    int contained = 1, have = 0;
+    double bd2 = 0.0;
+    for (int f = 0; f < 4; ++f) {
+      const double *a = W[faces[f][0]], *b = W[faces[f][1]], *c = W[faces[f][2]], *o = W[faces[f][3]];
+      double ba[3], ca[3], nrm[3], ma[3], oa[3];
+      for (int i = 0; i < 3; ++i) { ba[i] = b[i] - a[i]; ca[i] = c[i] - a[i]; ma[i] = -a[i]; oa[i] = o[i] - a[i]; }
+      cross(ba, ca, nrm);
+      double side_origin = dot3(nrm, ma), side_opp = dot3(nrm, oa);
+      if (side_origin * side_opp > 0) continue;
+      contained = 0;
+      double p2[3];
+      int s2[4], n2 = 0;
+      closest_triangle(W, faces[f], p2, s2, &n2);
+      double d2 = dot3(p2, p2);
+      if (!have || d2 < bd2) { have = 1; bd2 = d2; memcpy(pt, p2, 24); memcpy(sub, s2, sizeof s2); ns = n2; }
+    }
+    if (contained) { pt[0] = pt[1] = pt[2] = 0.0; return 1; }
+  }
+  double T[4][3];
+  for (int k = 0; k < ns; ++k) memcpy(T[k], W[sub[k]], 24);
+  for (int k = 0; k < ns; ++k) memcpy(W[k], T[k], 24);
+  *n = ns;
+  return 0;
+}
+
+/* geometry.py:486-525 gjk_distance (distance only; witnesses unused by settle) */
+static double gjk_distance(const orc_world *w, int pa, const pose_t *wa, int pb, const pose_t *wb) {
+  const double tol = 1e-10;
+  double d[3], nd[3], sa[3], sb[3], W[4][3], pt[3];
+  for (int i = 0; i < 3; ++i) d[i] = wb->p[i] - wa->p[i];
+  if (dot3(d, d) == 0.0) { d[0] = 1.0; d[1] = 0.0; d[2] = 0.0; }
+  for (int i = 0; i < 3; ++i) nd[i] = -d[i];
+  support_world(w, pa, wa, d, sa);
+  support_world(w, pb, wb, nd, sb);
+  int n = 1;
+  for (int i = 0; i < 3; ++i) { W[0][i] = sa[i] - sb[i]; pt[i] = W[0][i]; }
+  double last_d2 = INFINITY;
+  for (int it = 0; it < 64; ++it) {
+    int contains = closest_simplex(W, &n, pt);
+    double d2 = dot3(pt, pt);
+    if (contains || d2 < tol) return 0.0;
+    if (isfinite(last_d2) && last_d2 - d2 <= tol * fmax(1.0, last_d2)) break;
+    last_d2 = d2;
+    for (int i = 0; i < 3; ++i) { d[i] = -pt[i]; nd[i] = pt[i]; }
+    support_world(w, pa, wa, d, sa);
+    support_world(w, pb, wb, nd, sb);
+    double wv[3];
+    for (int i = 0; i < 3; ++i) wv[i] = sa[i] - sb[i];
+    if (dot3(wv, d) - dot3(pt, d) <= tol * fmax(1.0, sqrt(d2))) break;
+    memcpy(W[n++], wv, 24);
+  }
+  return sqrt(dot3(pt, pt));
+}
+
+/* geometry.py:528-539 parts_distance */
+static double parts_distance(const orc_world *w, const ostate *st, int a, int b) {
+  pose_t pa, pb, wa, wb;
+  body_pose(st, a, &pa);
+  body_pose(st, b, &pb);
+  double best = INFINITY;
+  for (int i = w->body_part_begin[a]; i < w->body_part_begin[a + 1]; ++i) {
+    part_world(w, &pa, i, &wa);
+    for (int j = w->body_part_begin[b]; j < w->body_part_begin[b + 1]; ++j) {
+      part_world(w, &pb, j, &wb);
+      double d = gjk_distance(w, i, &wa, j, &wb);
+      if (d < best) best = d;
+      if (best == 0.0) return 0.0;
+    }
+  }
+  return best;
+}
+
+/* physics.py:1156-1176 _assert_spawn_clearance over the placed bodies
+ * (ascending id).  Returns 1 and the first (body, other, clearance) whose
+ * clearance is below 1 mm, else 0. */
+static int spawn_clearance(const orc_world *w, const ostate *st, uint64_t placed, int *fb, int *fo, double *fd) {
+  const double margin = 1e-3;
+  for (int b = 0; b < w->nb; ++b) {
+    if (!((placed >> b) & 1ull)) continue;
+    double la[3], ha[3];
+    body_aabb(w, st, b, la, ha);
+    for (int o = 0; o < w->nb; ++o) {
+      if (o == b || w->body_robot[o]) continue;
+      if (st->pos[o][2] > 40.0 / 2) continue; /* parked, not yet placed (PARK_Z / 2) */
+      double lb[3], hb[3];
+      body_aabb(w, st, o, lb, hb);
+      int ov = 1;
+      for (int i = 0; i < 3; ++i) ov &= (la[i] - margin <= hb[i]) && (lb[i] - margin <= ha[i]);
+      if (!ov) continue;
+      double d = parts_distance(w, st, b, o);
+      if (d < margin) { *fb = b; *fo = o; *fd = d; return 1; }
+    }
+  }
+  return 0;
+}
+int orc_spawn_clearance(const orc_world *w, const uint8_t *snap, uint64_t placed, int *body, int *other,
+                        double *dist) {
+  static ostate st;
+  int rc = unpack(snap, &st, w->nb, w->nsj + w->narm);
+  if (rc) return -rc;
+  return spawn_clearance(w, &st, placed, body, other, dist);
+}
+double orc_parts_distance(const orc_world *w, const uint8_t *snap, int a, int b) {
+  static ostate st;
+  if (unpack(snap, &st, w->nb, w->nsj + w->narm)) return NAN;
+  return parts_distance(w, &st, a, b);
+}
+
+/* physics.py:1113-1154 settle from a spawn state (placements already
+ * applied): clearance check, then control steps without targets until every
+ * placed body sleeps.  status: 0 settled after *steps, 1 clearance (info =
+ * body, other; *value = clearance), 2 a placed body fell below floor_z - 0.5
+ * (info[0] = body), 3 still awake after max_steps, 4 physics fault. */
+int orc_settle(const orc_world *w, const uint8_t *spawn, uint64_t placed, int max_steps, double floor_z,
+               uint8_t *snap_out, int *info, double *value, int *steps) {
+  size_t sz = (size_t)orc_snapshot_size(w->nb, w->nsj + w->narm);
+  uint8_t *cur = (uint8_t *)malloc(sz), *nxt = (uint8_t *)malloc(sz);
+  memcpy(cur, spawn, sz);
+  static ostate st;
+  int status = 3;
+  *steps = 0;
+  info[0] = info[1] = -1;
+  *value = 0.0;
+  unpack(cur, &st, w->nb, w->nsj + w->narm);
+  if (spawn_clearance(w, &st, placed, &info[0], &info[1], value)) {
+    status = 1;
+  } else {
+    for (int k = 0; k < max_steps; ++k) {
+      uint32_t fault = 0;
+      int rc = orc_step(w, cur, nxt, NULL, NULL, 1.0 / 30.0, 4, NULL, &fault);
+      if (rc) { status = 4; info[0] = (int)fault; break; }
+      memcpy(cur, nxt, sz);
+      *steps = k + 1;
+      unpack(cur, &st, w->nb, w->nsj + w->narm);
+      int fell = -1, awake = 0;
+      for (int b = 0; b < w->nb; ++b) {
+        if (!((placed >> b) & 1ull)) continue;
+        if (fell < 0 && st.pos[b][2] < floor_z - 0.5) fell = b;
+        awake |= !st.asleep[b];
+      }
+      if (fell >= 0) { status = 2; info[0] = fell; break; }
+      if (!awake) { status = 0; break; }
+    }
+  }
+  memcpy(snap_out, cur, sz);
+  free(cur);
+  free(nxt);
+  return status;
+}
+
 /* forward kinematics through the oracle (tests) */
 void orc_link_poses(const orc_world *w, const double *q, const double *base, double *links12, double *ee12) {
   pose_t l[16], e;

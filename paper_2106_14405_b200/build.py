@@ -25,6 +25,7 @@ UNITS = {
     "abi.cu": [],
     "peak.cu": [],
     "nav.cu": ["-fmad=false"],
+    "settle.cu": ["-fmad=false"],
 }
 HEADERS = ["device.cuh", "se3.cuh", "navgrid.cuh"]
 

@@ -22,6 +22,11 @@ cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, f
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_tables(const DevBatch &B, cudaStream_t stream);
+cudaError_t launch_settle_clearance(const DevBatch &B, const uint64_t *placed, uint8_t *active, int32_t *status,
+                                    int32_t *info, double *value, int32_t *steps, cudaStream_t stream);
+cudaError_t launch_settle_check(const DevBatch &B, const uint64_t *placed, uint8_t *active, int32_t *status,
+                                int32_t *info, double *value, int32_t *steps, double floor_limit, int step_no,
+                                int max_steps, int32_t *n_active, cudaStream_t stream);
 cudaError_t launch_nav_fields(const DevBatch &B, int nx, int ny, const int32_t *scene_of_goal, const double *goal_xy,
                               int n_goals, double *fields, int32_t *goal_cell, cudaStream_t stream);
 cudaError_t launch_nav_geodesic(const DevBatch &B, int nx, int ny, const double *fields, const int32_t *field_of_query,
@@ -67,6 +72,10 @@ struct rs_batch {
   int narm = 0;
   bool has_mesh = false;
   int nav_nx = -1, nav_ny = -1;  // shared walk-grid shape (-1: scenes differ)
+  // rs_settle scratch: zero targets, has_targets = 0, active-env counter
+  double *d_settle_zero = nullptr;
+  uint8_t *d_settle_noct = nullptr;
+  int32_t *d_settle_count = nullptr, *h_settle_count = nullptr;
   int n_scenes = 0;
   // ping-pong state buffers: rs_step reads buf[cur] and writes buf[cur ^ 1]
   double *sd_buf[2] = {nullptr, nullptr};
@@ -299,6 +308,10 @@ void rs_batch_destroy(rs_batch *b) {
   if (b->d_targets) cudaFree(b->d_targets);
   if (b->d_ik_failed) cudaFree(b->d_ik_failed);
   if (b->d_ik_scratch) cudaFree(b->d_ik_scratch);
+  if (b->d_settle_zero) cudaFree(b->d_settle_zero);
+  if (b->d_settle_noct) cudaFree(b->d_settle_noct);
+  if (b->d_settle_count) cudaFree(b->d_settle_count);
+  if (b->h_settle_count) cudaFreeHost(b->h_settle_count);
   if (b->side) cudaStreamDestroy(b->side);
   if (b->phys_side) cudaStreamDestroy(b->phys_side);
   if (b->ph_fork) cudaEventDestroy(b->ph_fork);
@@ -536,6 +549,42 @@ int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d
   if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
   return RS_OK;
+}
+
+// ---- batched settle (physics.py:1113-1176)
+int rs_settle(rs_batch *b, const uint64_t *placed, uint8_t *active, int32_t max_steps, double floor_z,
+              int32_t *status, int32_t *info, double *value, int32_t *steps, void *stream) {
+  if (!b || !placed || !active || !status || !info || !value || !steps || max_steps < 0)
+    return fail(RS_ERR_ARG, "bad settle arguments");
+  const int E = b->d.n_env;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!b->d_settle_zero) {
+    CUDA_TRY(cudaMalloc(&b->d_settle_zero, sizeof(double) * (size_t)E * (b->narm > 2 ? b->narm : 2)));
+    CUDA_TRY(cudaMemset(b->d_settle_zero, 0, sizeof(double) * (size_t)E * (b->narm > 2 ? b->narm : 2)));
+    CUDA_TRY(cudaMalloc(&b->d_settle_noct, E));
+    CUDA_TRY(cudaMemset(b->d_settle_noct, 0, E));
+    CUDA_TRY(cudaMalloc(&b->d_settle_count, sizeof(int32_t)));
+    CUDA_TRY(cudaMallocHost(&b->h_settle_count, sizeof(int32_t)));
+  }
+  CUDA_TRY(launch_settle_clearance(b->view(), placed, active, status, info, value, steps, st));
+  const double floor_limit = floor_z - 0.5;
+  int rc = RS_OK;
+  for (int k = 1; k <= max_steps; ++k) {
+    b->d.env_active = active;  // Simulator.step_physics(state, None) on the envs still settling
+    cudaError_t e = launch_step_b(b, b->d_settle_zero, b->d_settle_zero, 2, b->d_settle_noct, 1.0 / 30.0, 4, st);
+    b->d.env_active = nullptr;
+    if (e != cudaSuccess) { rc = fail(RS_ERR_CUDA, cudaGetErrorString(e)); break; }
+    b->cur ^= 1;
+    CUDA_TRY(cudaMemsetAsync(b->d_settle_count, 0, sizeof(int32_t), st));
+    CUDA_TRY(launch_settle_check(b->view(), placed, active, status, info, value, steps, floor_limit, k, max_steps,
+                                 b->d_settle_count, st));
+    if (k % 8 == 0 || k == max_steps) {  // stop once every env is done
+      CUDA_TRY(cudaMemcpyAsync(b->h_settle_count, b->d_settle_count, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (*b->h_settle_count == 0) break;
+    }
+  }
+  return rc;
 }
 
 // ---- geodesics (navgrid.py:109-172)

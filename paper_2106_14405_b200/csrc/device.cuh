@@ -117,6 +117,8 @@ struct DevBatch {
   int trace_cap, trace_sub;
   // render tables (render_tables_kernel): unit camera-frame ray per pixel, tile frustum planes
   const double *ray_dir, *tile_frustum;
+  // optional per-env step mask (rs_settle): envs with env_active[e] == 0 are copied through unchanged
+  const uint8_t *env_active;
   // optional per-env step latency probe (rsim_bench_env_cycles): SM clock cycles of the last step
   long long *env_cycles;
 };

@@ -1610,6 +1610,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   const int env = blockIdx.x * kWarpsPerBlock + warp;
   if (env >= B.n_env) return;
   if (heavy_in && heavy_in[env]) return;
+  if (B.env_active && !B.env_active[env]) {  // not stepping (rs_settle): state copied through
+    copy_through(B, env, lane);
+    if (lane == 0 && heavy_out) heavy_out[env] = 0;
+    return;
+  }
   const long long t_begin = B.env_cycles ? clock64() : 0;
   WarpSmem &S = smem[warp];
   Ctx c;
@@ -1641,6 +1646,11 @@ __global__ void __launch_bounds__(32 * kHeavyWarps) step_kernel_cta(DevBatch B, 
   HeavyShared &H = *reinterpret_cast<HeavyShared *>(dsm + ((sizeof(WarpSmem) + 15) & ~(size_t)15));
   const int env = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!heavy_in[env]) return;
+  if (B.env_active && !B.env_active[env]) {
+    if (threadIdx.x < 32) copy_through(B, env, threadIdx.x);
+    if (threadIdx.x == 0) heavy_out[env] = 0;
+    return;
+  }
   const long long t_begin = B.env_cycles ? clock64() : 0;
   Ctx c;
   make_ctx(c, B, S, env, lane, warp);

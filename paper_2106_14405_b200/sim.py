@@ -280,6 +280,46 @@ class BatchSimulator:
                                            _stream_ptr()), "rs_render_mesh")
         return rgba, depth, ids
 
+    # ------------------------------------------ settle (physics.py:1113-1176)
+    SETTLED, CLEARANCE, FELL, TIMEOUT, FAULT = range(5)
+
+    @staticmethod
+    def settle_steps(max_time: float = 10.0) -> int:
+        """Control steps of ``while t < max_time: step; t += 1/30`` (float accumulation as in the reference)."""
+        t, n = 0.0, 0
+        while t < max_time:
+            t += 1.0 / 30.0
+            n += 1
+        return n
+
+    def settle(self, spawn_snapshots, placed, env_ids=None, max_time: float = 10.0, floor_z: float = 0.0):
+        """Simulator.settle for many envs at once (fast resets): ``spawn_snapshots``
+        are the states settle steps from (``state.spawn_state``), ``placed`` the
+        placed body ids per env.  Returns device tensors status [n] (SETTLED,
+        CLEARANCE, FELL, TIMEOUT, FAULT), info [n, 2], value [n], steps [n];
+        the envs' states are the settled (or last) states."""
+        ids = list(range(self.n_env)) if env_ids is None else [int(e) for e in env_ids]
+        self.set_state(spawn_snapshots, env_ids=ids)
+        masks = np.zeros(self.n_env, np.uint64)
+        active = np.zeros(self.n_env, np.uint8)
+        for e, bodies in zip(ids, placed):
+            m = 0
+            for b in bodies:
+                m |= 1 << int(b)
+            masks[e] = np.uint64(m)
+            active[e] = 1
+        d_mask = torch.from_numpy(masks.view(np.int64)).to(self.device)
+        d_active = torch.from_numpy(active).to(self.device)
+        status = torch.empty(self.n_env, dtype=torch.int32, device=self.device)
+        info = torch.empty((self.n_env, 2), dtype=torch.int32, device=self.device)
+        value = torch.empty(self.n_env, dtype=torch.float64, device=self.device)
+        steps = torch.empty(self.n_env, dtype=torch.int32, device=self.device)
+        native.check(self.L.rs_settle(self._batch, _dptr(d_mask), _dptr(d_active), self.settle_steps(max_time),
+                                      float(floor_z), _dptr(status), _dptr(info), _dptr(value), _dptr(steps),
+                                      _stream_ptr()), "rs_settle")
+        sel = torch.as_tensor(ids, device=self.device)
+        return status[sel], info[sel], value[sel], steps[sel]
+
     # -------------------------------------------- geodesics (navgrid.py:109-172)
     def nav_shape(self) -> tuple[int, int]:
         nx, ny = C.c_int32(), C.c_int32()

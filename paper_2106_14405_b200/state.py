@@ -185,3 +185,35 @@ def _bind_riders(world, st):
                 rel = owner.inverse().compose(st.body_pose(bid))
                 st.rider_offset[bid] = np.concatenate([rel.pos, rel.quat()])
                 break
+
+
+PARK_Z = 40.0  # physics.py:1103: unplaced clutter is parked asleep high above the scene
+
+
+def park_state(world) -> WorldState:
+    """Simulator.park_state (physics.py:1105-1111): clutter parked asleep in the air."""
+    from .geom import Pose
+
+    park = [Pose(pos=np.array([-6.0 + 0.6 * i, 0.0, PARK_Z])) for i in range(len(world.clutter_body_ids))]
+    return make_initial_state(world, park, clutter_asleep=True)
+
+
+def spawn_state(base: WorldState, placements) -> WorldState:
+    """The state Simulator.settle steps from (physics.py:1124-1137): each
+    placed body gets its pose, wakes, and loses velocity, sleep count and rider
+    binding -- unless the placement equals its current pose exactly."""
+    st = base.clone()
+    for bid, pose in placements:
+        old = st.body_pose(bid)
+        q = pose.quat()
+        if np.array_equal(old.pos, pose.pos) and np.array_equal(old.quat(), q):
+            continue
+        st.pos[bid] = pose.pos
+        st.quat[bid] = q
+        st.asleep[bid] = False
+        st.sleep_counter[bid] = 0
+        st.rider_joint[bid] = -1
+        st.lin_vel[bid] = 0.0
+        st.ang_vel[bid] = 0.0
+    return st
+

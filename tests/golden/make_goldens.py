@@ -25,6 +25,10 @@ as-is.  Fixtures:
   (|t_b - t_min| <= 1e-9 -> lowest body id; ``physics.py:1096-1100`` keeps
   the lowest id on exact ties).
 * ``kat.npz``  known-answer values (SPEC.md examples) from the reference.
+* ``settle.npz``  per (layout, seed) of the pool recipe: the spawn state
+  ``Simulator.settle`` builds, every AABB-overlapping ``parts_distance``
+  (GJK, ``geometry.py:486-539``) and the settle outcome (final state + steps
+  or the ``SettleUnstable`` reason), ``physics.py:1113-1176``.
 * ``nav.npz``  geodesic distance fields (Dijkstra, ``navgrid.py:109-143``),
   geodesic distances and steepest-descent shortest paths
   (``navgrid.py:145-172``) on the layouts' walk grids.
@@ -547,6 +551,82 @@ def gen_ik():
 
 
 # --------------------------------------------------------------------------
+# settle (physics.py:1113-1176) and GJK clearances (geometry.py:486-539)
+# --------------------------------------------------------------------------
+
+def spawn_state(sim, base, placements):
+    """The state Simulator.settle builds before its clearance check (physics.py:1124-1137)."""
+    state = base.clone()
+    for bid, pose in placements:
+        old = state.body_pose(bid)
+        if np.array_equal(old.pos, pose.pos) and np.array_equal(old.quat(), pose.quat()):
+            continue
+        state.set_body_pose(bid, pose)
+        state.asleep[bid] = False
+        state.sleep_counter[bid] = 0
+        state.rider_joint[bid] = -1
+        state.lin_vel[bid] = 0.0
+        state.ang_vel[bid] = 0.0
+    return state
+
+
+def gen_settle(seeds=range(8)):
+    """Per (layout, seed) of the pool recipe: the spawn snapshot, every
+    AABB-overlapping (placed, other) parts_distance, and the settle outcome
+    (0 settled + final snapshot + steps, 1 clearance (body, other, d),
+    2 fell, 3 timeout)."""
+    spawns, outcome, info, value, steps, finals, tags = [], [], [], [], [], [], []
+    pd_tag, pd_pair, pd_dist = [], [], []
+    for v in range(3):
+        sim, _ = make_sim(v)
+        for sd in seeds:
+            base = sim.park_state()
+            slots = slots_for(sim)
+            rng = np.random.default_rng(sd)
+            order = rng.permutation(len(slots))
+            placements = []
+            for k, bid in enumerate(sim.clutter_body_ids):
+                owner, local = slots[order[k]]
+                lo, _ = geo.parts_aabb(sim.bodies[bid].parts, geo.Pose())
+                pos = owner.apply(local) + np.array([0.0, 0.0, -lo[2] + 0.01])
+                placements.append((bid, geo.Pose(geo.rot_z(rng.uniform(-math.pi, math.pi)), pos)))
+            sp = spawn_state(sim, base, placements)
+            spawns.append(np.frombuffer(sp.to_bytes(), np.uint8))
+            tags.append((v, sd))
+            for bid, _ in placements:
+                lo_a, hi_a = geo.parts_aabb(sim.bodies[bid].parts, sp.body_pose(bid))
+                for o in range(sim.n_bodies):
+                    if o == bid or o in sim._robot_set or sp.pos[o][2] > sim.PARK_Z / 2:
+                        continue
+                    lo_b, hi_b = sim.body_aabb(sp, o)
+                    if geo.aabb_overlap(lo_a, hi_a, lo_b, hi_b, margin=1e-3):
+                        pd_tag.append(len(spawns) - 1); pd_pair.append((bid, o))
+                        pd_dist.append(geo.parts_distance(sim.bodies[bid].parts, sp.body_pose(bid),
+                                                          sim.bodies[o].parts, sp.body_pose(o)))
+            try:
+                _, st = sim.settle(placements, max_time=10.0, base_state=base)
+                outcome.append(0); info.append((-1, -1)); value.append(0.0)
+                steps.append(st.step_index - base.step_index)
+                finals.append(np.frombuffer(st.to_bytes(), np.uint8))
+            except physics.SettleUnstable as exc:
+                msg = str(exc)
+                kind = 1 if "clearance" in msg else (2 if "fell" in msg else 3)
+                ids = [int(t) for t in msg.replace("(", " ").replace(")", " ").replace(":", " ").replace(",", " ")
+                       .replace("[", " ").replace("]", " ").split() if t.isdigit()]
+                outcome.append(kind); steps.append(-1); finals.append(np.zeros_like(spawns[-1]))
+                if kind == 1:
+                    d_mm = float(msg.split(" has ")[1].split(" mm")[0])
+                    info.append((ids[0], ids[1])); value.append(d_mm * 1e-3)
+                else:
+                    info.append((ids[0] if ids else -1, -1)); value.append(0.0)
+            print(f"  settle layout {v} seed {sd}: outcome {outcome[-1]} steps {steps[-1]} info {info[-1]}")
+    np.savez_compressed(os.path.join(OUT, "settle.npz"), meta=meta(), tags=np.array(tags, np.int32),
+                        spawn=np.stack(spawns), outcome=np.array(outcome), info=np.array(info, np.int32),
+                        value=np.array(value), steps=np.array(steps), final=np.stack(finals),
+                        pd_tag=np.array(pd_tag), pd_pair=np.array(pd_pair, np.int32), pd_dist=np.array(pd_dist))
+
+
+# --------------------------------------------------------------------------
 # geodesics (navgrid.py:109-172)
 # --------------------------------------------------------------------------
 
@@ -587,7 +667,7 @@ def gen_nav():
 
 if __name__ == "__main__":
     t0 = time.time()
-    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav"]
+    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav", "settle"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
     blobs = tags = None
@@ -606,3 +686,5 @@ if __name__ == "__main__":
         gen_ik(); print("ik", time.time() - t0)
     if "nav" in what:
         gen_nav(); print("nav", time.time() - t0)
+    if "settle" in what:
+        gen_settle(); print("settle", time.time() - t0)
