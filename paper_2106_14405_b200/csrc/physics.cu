@@ -76,8 +76,6 @@ struct WarpSmem {
     struct { double lo[kMaxBodies][3], hi[kMaxBodies][3]; } bp;
     struct {
       double planes[2][kMaxFacetsPerPart * 4];
-      double pw[2][kMaxPartsPerBody][12];  // world frames of the pair's parts
-      double pab[2][kMaxPartsPerBody][6];  // their AABBs (lo, hi)
     } np;
     struct { double vel[kMaxBodies][6]; BlockWS ws; } sol;
   } u;
@@ -90,6 +88,7 @@ struct WarpSmem {
   uint16_t cand[kMaxCand];
   uint16_t adm[kMaxAdm];
   int16_t g_a[kMaxGroups], g_b[kMaxGroups], g_first[kMaxGroups], g_n[kMaxGroups];
+  int wake_idx[kMaxBodies];  // admission: index of the candidate pair that wakes each body
   int ncand, nadm, nc, ng, fault;
   unsigned long long awake_dyn;
   int moved_mask, dragged, n_active, max_active;
@@ -502,33 +501,33 @@ __device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
   const DevScene &sc = *c.sc;
   const int a0 = sc.body_part_begin[a], na = sc.body_part_begin[a + 1] - a0;
   const int b0 = sc.body_part_begin[b], nbp = sc.body_part_begin[b + 1] - b0;
-  auto &NP = c.S->u.np;
-  for (int e = c.lane; e < 18 * (na + nbp); e += 32) {  // this substep's part frames + AABBs (body_aabb_cached)
-    const int k = e / 18, q = e % 18, side = k < na ? 0 : 1, kk = side ? k - na : k;
-    const double v = c.pcache[18 * ((side ? b0 : a0) + kk) + q];
-    if (q < 12) NP.pw[side][kk][q] = v; else NP.pab[side][kk][q - 12] = v;
-  }
-  __syncwarp();
-  int base = c.S->nc, n = 0;
-  for (int ii = 0; ii < na; ++ii) {
-    unsigned live = 0u;  // parts of b whose AABB meets part ii of a (lanes per part of b)
-    {
-      bool ok = false;
-      if (c.lane < nbp) {
-        const double *la = NP.pab[0][ii], *ha = NP.pab[0][ii] + 3, *lb = NP.pab[1][c.lane], *hb = NP.pab[1][c.lane] + 3;
-        bool sep = false;
-        for (int k = 0; k < 3; ++k) sep |= (la[k] > hb[k] + margin) || (lb[k] > ha[k] + margin);
-        ok = !sep;
-      }
-      live = __ballot_sync(0xffffffffu, ok);
+  // this substep's part frames + AABBs (body_aabb_cached): [R(9), p(3), lo(3), hi(3)] per part
+  const double *PA = c.pcache + 18 * a0, *PB = c.pcache + 18 * b0;
+  // cull every part pair at once (e = ii * nbp + jj < 64; the reference's margin test),
+  // then visit the survivors in (ii, jj) order
+  unsigned long long live = 0ull;
+  for (int e0 = 0; e0 < na * nbp; e0 += 32) {
+    const int e = e0 + c.lane;
+    bool ok = false;
+    if (e < na * nbp) {
+      const int ii = e / nbp, jj = e - ii * nbp;
+      const double *la = PA + 18 * ii + 12, *ha = la + 3, *lb = PB + 18 * jj + 12, *hb = lb + 3;
+      bool sep = false;
+      for (int k = 0; k < 3; ++k) sep |= (la[k] > hb[k] + margin) || (lb[k] > ha[k] + margin);
+      ok = !sep;
     }
-    while (live) {
-      const int jj = __ffs(live) - 1;
-      live &= live - 1;
+    live |= (unsigned long long)__ballot_sync(0xffffffffu, ok) << e0;
+  }
+  int base = c.S->nc, n = 0;
+  while (live) {
+    const int e = __ffsll((long long)live) - 1;
+    live &= live - 1;
+    {
+      const int ii = e / nbp, jj = e - ii * nbp;
       const int i = a0 + ii, j = b0 + jj;
       Pose wa, wb;
-      pose_load12(NP.pw[0][ii], wa);
-      pose_load12(NP.pw[1][jj], wb);
+      pose_load12(PA + 18 * ii, wa);
+      pose_load12(PB + 18 * jj, wb);
       int ka = sc.part_kind[i], kb = sc.part_kind[j];
       if (ka == RS_SPHERE && kb == RS_SPHERE) {
         int r = 0;
@@ -1044,58 +1043,115 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     for (int i = 0; i < 3; ++i) { S.u.bp.lo[b][i] = lo[i]; S.u.bp.hi[b][i] = hi[i]; }
   }
   __syncwarp();
-  // ---- overlap candidates in sorted (a, b) order (lanes per pair, ballot compaction)
+  // ---- overlap candidates in sorted (a, b) order: lane l owns bodies l and l + 32
+  //      (AABB, kind, group in registers); per a one or two ballots compact the
+  //      overlapping b > a in ascending order
   int ncand = 0;
   bool overflow = false;
-  for (int a = 0; a < nb - 1; ++a) {
-    const int ka = sc.body_kind[a], ga = sc.body_group[a];
-    for (int b0 = a + 1; b0 < nb; b0 += 32) {
-      int b = b0 + lane;
-      bool ov = false;
-      if (b < nb) {
-        const int kb = sc.body_kind[b];
-        ov = !(ka == RS_STATIC && kb == RS_STATIC) && !(ga != RS_NO_GROUP && ga == sc.body_group[b]) &&
-             S.u.bp.lo[a][0] <= S.u.bp.hi[b][0] && S.u.bp.lo[b][0] <= S.u.bp.hi[a][0] && S.u.bp.lo[b][1] <= S.u.bp.hi[a][1] &&
-             S.u.bp.lo[a][1] <= S.u.bp.hi[b][1] && S.u.bp.lo[b][2] <= S.u.bp.hi[a][2] && S.u.bp.lo[a][2] <= S.u.bp.hi[b][2];
+  {
+    double l0[3], h0[3], l1[3], h1[3];
+    int k0 = 0, g0 = 0, k1 = 0, g1 = 0;
+    const int b0 = lane, b1 = lane + 32;
+    if (b0 < nb) {
+      for (int i = 0; i < 3; ++i) { l0[i] = S.u.bp.lo[b0][i]; h0[i] = S.u.bp.hi[b0][i]; }
+      k0 = sc.body_kind[b0]; g0 = sc.body_group[b0];
+    }
+    if (b1 < nb) {
+      for (int i = 0; i < 3; ++i) { l1[i] = S.u.bp.lo[b1][i]; h1[i] = S.u.bp.hi[b1][i]; }
+      k1 = sc.body_kind[b1]; g1 = sc.body_group[b1];
+    }
+    for (int a = 0; a < nb - 1; ++a) {
+      const int ka = sc.body_kind[a], ga = sc.body_group[a];
+      const double la0 = S.u.bp.lo[a][0], la1 = S.u.bp.lo[a][1], la2 = S.u.bp.lo[a][2];
+      const double ha0 = S.u.bp.hi[a][0], ha1 = S.u.bp.hi[a][1], ha2 = S.u.bp.hi[a][2];
+      for (int half = 0; half < 2; ++half) {
+        const int b = half ? b1 : b0;
+        if (half && nb <= 32) break;
+        const double *lb = half ? l1 : l0, *hb = half ? h1 : h0;
+        const int kb = half ? k1 : k0, gb = half ? g1 : g0;
+        const bool ov = b > a && b < nb && !(ka == RS_STATIC && kb == RS_STATIC) &&
+                        !(ga != RS_NO_GROUP && ga == gb) && la0 <= hb[0] && lb[0] <= ha0 && lb[1] <= ha1 &&
+                        la1 <= hb[1] && lb[2] <= ha2 && la2 <= hb[2];
+        const unsigned m = __ballot_sync(0xffffffffu, ov);
+        if (ov) {
+          const int idx = ncand + __popc(m & ((1u << lane) - 1));
+          if (idx < kMaxCand) S.cand[idx] = (uint16_t)((a << 8) | b);
+        }
+        ncand += __popc(m);
       }
-      unsigned m = __ballot_sync(0xffffffffu, ov);
-      if (ov) {
-        int idx = ncand + __popc(m & ((1u << lane) - 1));
-        if (idx < kMaxCand) S.cand[idx] = (uint16_t)((a << 8) | b);
-      }
-      ncand += __popc(m);
     }
   }
   if (ncand > kMaxCand) overflow = true;
   __syncwarp();
-  // ---- admission walk (lane 0, physics.py:528-571)
-  if (lane == 0 && !overflow) {
-    int nadm = 0;
+  // ---- admission walk (physics.py:528-571), lanes per candidate.  The walk is
+  // sequential in the reference only through wakes: a sleeping dynamic body x
+  // paired with a robot/held kinematic body is woken when that pair is
+  // reached, and every later pair sees x awake.  So x's state at candidate k
+  // is "asleep" iff it slept at the start and k <= wake_idx[x], the index of
+  // the first such waker pair -- computed first (atomicMin), then every
+  // candidate is decided independently and compacted in order.
+  if (!overflow) {
     const int held = HELD(c);
-    for (int k = 0; k < ncand; ++k) {
-      int a = S.cand[k] >> 8, b = S.cand[k] & 0xff;
-      int ka = sc.body_kind[a], kb = sc.body_kind[b];
-      bool dyn_a = ka == RS_DYNAMIC, dyn_b = kb == RS_DYNAMIC, kin_a = ka == RS_KINEMATIC, kin_b = kb == RS_KINEMATIC;
-      bool adm;
-      if (!dyn_a && !dyn_b) {
-        bool robot = sc.body_robot[a] || sc.body_robot[b] || a == held || b == held;
-        adm = robot || sc.body_joint[a] >= 0 || sc.body_joint[b] >= 0;
-      } else {
-        bool sa = dyn_a && ASLEEP(c, a), sb = dyn_b && ASLEEP(c, b);
-        if (sa && sb) { S.ctr[1]++; continue; }
-        if ((sa && kb == RS_STATIC) || (sb && ka == RS_STATIC)) { S.ctr[1]++; continue; }
-        if (sa && kin_b && sc.body_joint[b] >= 0 && RIDER(c, a) == sc.body_joint[b]) continue;
-        if (sb && kin_a && sc.body_joint[a] >= 0 && RIDER(c, b) == sc.body_joint[a]) continue;
-        bool rkb = kin_b && (sc.body_robot[b] || b == held), rka = kin_a && (sc.body_robot[a] || a == held);
-        if (sa && rkb) wake(c, a);
-        if (sb && rka) wake(c, b);
-        adm = true;
-      }
-      if (!adm) continue;
-      if (nadm < kMaxAdm) S.adm[nadm] = S.cand[k];
-      ++nadm;
+    for (int b = lane; b < nb; b += 32) S.wake_idx[b] = 1 << 30;
+    __syncwarp();
+    for (int k = lane; k < ncand; k += 32) {
+      const int a = S.cand[k] >> 8, b = S.cand[k] & 0xff;
+      const int ka = sc.body_kind[a], kb = sc.body_kind[b];
+      // x asleep-dynamic at the start, the other kinematic robot/held, not x's rider joint
+      if (ka == RS_DYNAMIC && ASLEEP(c, a) && kb == RS_KINEMATIC && (sc.body_robot[b] || b == held) &&
+          !(sc.body_joint[b] >= 0 && RIDER(c, a) == sc.body_joint[b]))
+        atomicMin(&S.wake_idx[a], k);
+      if (kb == RS_DYNAMIC && ASLEEP(c, b) && ka == RS_KINEMATIC && (sc.body_robot[a] || a == held) &&
+          !(sc.body_joint[a] >= 0 && RIDER(c, b) == sc.body_joint[a]))
+        atomicMin(&S.wake_idx[b], k);
     }
-    S.nadm = nadm;
+    __syncwarp();
+    int nadm = 0, nskip = 0;
+    for (int k0 = 0; k0 < ncand; k0 += 32) {
+      const int k = k0 + lane;
+      bool adm = false, skip = false;
+      if (k < ncand) {
+        const int a = S.cand[k] >> 8, b = S.cand[k] & 0xff;
+        const int ka = sc.body_kind[a], kb = sc.body_kind[b];
+        const bool dyn_a = ka == RS_DYNAMIC, dyn_b = kb == RS_DYNAMIC, kin_a = ka == RS_KINEMATIC,
+                   kin_b = kb == RS_KINEMATIC;
+        if (!dyn_a && !dyn_b) {
+          const bool robot = sc.body_robot[a] || sc.body_robot[b] || a == held || b == held;
+          adm = robot || sc.body_joint[a] >= 0 || sc.body_joint[b] >= 0;
+        } else {
+          const bool sa = dyn_a && ASLEEP(c, a) && k <= S.wake_idx[a];
+          const bool sb = dyn_b && ASLEEP(c, b) && k <= S.wake_idx[b];
+          if ((sa && sb) || (sa && kb == RS_STATIC) || (sb && ka == RS_STATIC)) {
+            skip = true;  // skipped_sleeping_pairs
+          } else if ((sa && kin_b && sc.body_joint[b] >= 0 && RIDER(c, a) == sc.body_joint[b]) ||
+                     (sb && kin_a && sc.body_joint[a] >= 0 && RIDER(c, b) == sc.body_joint[a])) {
+            adm = false;  // a sleeping rider ignores its container
+          } else {
+            adm = true;
+          }
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, adm);
+      if (adm) {
+        const int idx = nadm + __popc(m & ((1u << lane) - 1));
+        if (idx < kMaxAdm) S.adm[idx] = S.cand[k];
+      }
+      nadm += __popc(m);
+      nskip += __popc(__ballot_sync(0xffffffffu, skip));
+    }
+    __syncwarp();
+    int nwake = 0;  // wake() on each woken body (dynamic and asleep at the start by construction)
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int b = b0 + lane;
+      const bool w = b < nb && S.wake_idx[b] < (1 << 30);
+      if (w) { ASLEEP(c, b) = 0; SLEEPC(c, b) = 0; RIDER(c, b) = -1; }
+      nwake += __popc(__ballot_sync(0xffffffffu, w));
+    }
+    if (lane == 0) {
+      S.nadm = nadm;
+      S.ctr[1] += nskip;
+      S.ctr[2] += nwake;
+    }
   }
   __syncwarp();
   if (overflow || S.nadm > kMaxAdm) return false;
