@@ -67,7 +67,7 @@ for k in range(args.steps):
 sim.L.rsim_bench_env_cycles(sim._batch, None)
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 if dump["pre"]:
-  np.savez(os.path.join(ROOT, "gpurun_out", "heavy_envs.npz"), pre=np.stack(dump["pre"]), action=np.stack(dump["action"]),
-         env=np.array(dump["env"]), step=np.array(dump["step"]), cycles=np.array(dump["cycles"]),
-         layout=layout_of(np.array(dump["env"])))
+    np.savez(os.path.join(ROOT, "gpurun_out", "heavy_envs.npz"), pre=np.stack(dump["pre"]),
+             action=np.stack(dump["action"]), env=np.array(dump["env"]), step=np.array(dump["step"]),
+             cycles=np.array(dump["cycles"]), layout=layout_of(np.array(dump["env"])))
 sim.close()
