@@ -545,9 +545,25 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
   return RS_OK;
 }
 
+int rsim_bench_render_work_detail(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counters, void *stream) {
+  if (!b || !d_counters) return fail(RS_ERR_ARG, "null argument");
+  CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counters));
+  return RS_OK;
+}
+
+__global__ void work_total_kernel(const unsigned long long *w, unsigned long long *out) {
+  *out += w[0] + w[1] + w[2] + w[6];
+}
+
 int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
   if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");
-  CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
+  unsigned long long *w = nullptr;
+  CUDA_TRY(cudaMalloc(&w, 8 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(w, 0, 8 * sizeof(unsigned long long), (cudaStream_t)stream));
+  CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, w));
+  work_total_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(w, d_counter);
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  cudaFree(w);
   return RS_OK;
 }
 
@@ -641,7 +657,13 @@ int rsim_bench_render_exact(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float
 
 int rsim_bench_render_mesh_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
   if (!b || !d_counter || !b->has_mesh) return fail(RS_ERR_ARG, "null argument or no mesh");
-  CUDA_TRY(launch_render_mesh(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counter));
+  unsigned long long *w = nullptr;
+  CUDA_TRY(cudaMalloc(&w, 8 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(w, 0, 8 * sizeof(unsigned long long), (cudaStream_t)stream));
+  CUDA_TRY(launch_render_mesh(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, w));
+  work_total_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(w, d_counter);
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  cudaFree(w);
   return RS_OK;
 }
 

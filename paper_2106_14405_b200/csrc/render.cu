@@ -51,6 +51,15 @@ struct PartW {
   int f0, nf, kind, body;
 };
 
+// executed-work counters of the counting variant (rsim_bench_render_work*):
+// 0 FP32 box plane tests, 1 FP64 plane tests in the walk (uncertain boxes,
+// hulls, spheres = 1), 2 FP64 plane tests resolving candidates, 3 pixels that
+// fell back to the all-FP64 walk, 4 uncertain boxes, 5 hull tests in the walk,
+// 6 FP64 plane tests of the all-FP64 walk, 7 pixels
+struct Work {
+  unsigned long long v[8];
+};
+
 // render variants
 constexpr int kProxyMixed = 0;  // FP32 box tests select candidates, FP64 resolves them (default)
 constexpr int kMeshExact = 1;   // triangle soup, FP64
@@ -267,7 +276,7 @@ template <bool kMesh>
 __device__ __forceinline__ double trace_exact(const DevScene &sc, const RenderSmem &S, const double *plane,
                                               const uint8_t *list, int nl, const uint32_t *mask, const double *o,
                                               const double *d, double eps, int &id, int &wpart, int &wface,
-                                              unsigned long long &tests, bool count) {
+                                              Work &w, bool count) {
   double tmin = INFINITY, t2 = INFINITY;
   id = -1; wpart = -1; wface = -1;
 #pragma unroll 1
@@ -277,7 +286,7 @@ __device__ __forceinline__ double trace_exact(const DevScene &sc, const RenderSm
     if (P.lb > tmin + eps) break;  // sorted: nothing later can be nearer or tie
     int fc;
     const double t = kMesh ? mesh_hit(sc, S, plane, p, o, d, tmin + eps, fc) : part_hit(S, plane, p, o, d, fc, tmin + eps);
-    if (count) tests += kMesh ? 1 : (P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf));
+    if (count) w.v[6] += kMesh ? 1 : (P.kind == RS_SPHERE ? 1 : (P.kind == RS_BOX ? 6 : P.nf));
     if (!(t < INFINITY)) continue;
     const int b = P.body;
     if (b == id) {
@@ -339,7 +348,7 @@ __device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float
 // false if a third candidate was live (the caller falls back to trace_exact).
 __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *plane, const uint8_t *list, int nl,
                                             const double *o, const double *d, double eps, double &tmin, int &id,
-                                            int &wpart, int &wface, unsigned long long &tests, bool count) {
+                                            int &wpart, int &wface, Work &w, bool count) {
   const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
   const float eps32 = __double2float_ru(eps);
   float tup = INFINITY, bound = INFINITY;  // upper bound of the nearest hit range; + tie_eps
@@ -356,14 +365,14 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
     if (kind == RS_BOX) {
       float t, e;
       st = box32(S.box32[p], dx, dy, dz, t, e);
-      if (count) tests += 6;
+      if (count) { w.v[0] += 6; w.v[4] += st == 2; }
       if (st == 0) continue;
       if (st == 1) { tl = __fsub_rd(t, e); tu = __fadd_ru(t, e); }
     }
     if (st == 2) {
       int fc;
       const double t = part_hit(S, plane, p, o, d, fc);
-      if (count) tests += kind == RS_BOX ? 6 : (kind == RS_SPHERE ? 1 : S.part[p].nf);
+      if (count) { w.v[1] += kind == RS_BOX ? 6 : (kind == RS_SPHERE ? 1 : S.part[p].nf); w.v[5] += kind == RS_HULL; }
       if (!(t < INFINITY)) continue;
       tl = __double2float_rd(t);
       tu = __double2float_ru(t);
@@ -379,7 +388,7 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
   double t1 = INFINITY, t2 = INFINITY;
   if (p1 >= 0 && l1 <= bound) t1 = part_hit(S, plane, p1, o, d, f1);
   if (p2 >= 0 && l2 <= bound) t2 = part_hit(S, plane, p2, o, d, f2);
-  if (count) tests += 12;
+  if (count) w.v[2] += (p1 >= 0 && l1 <= bound ? 6 : 0) + (p2 >= 0 && l2 <= bound ? 6 : 0);
   tmin = fmin(t1, t2);
   id = -1; wpart = -1; wface = -1;
   if (!(tmin < INFINITY)) return true;
@@ -392,7 +401,7 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
   return true;
 }
 
-template <int kMode>
+template <int kMode, bool kCount>
 __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBlocksMesh : kMinBlocksProxy)
     render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out, uint32_t *rgba, float *depth, int32_t *ids,
                   unsigned long long *work) {
@@ -460,7 +469,18 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       for (int k = 0; k < 9; ++k) S.u.R[p][k] = wp.R[k];
     }
     double v[3] = {wp.p[0] - o[0], wp.p[1] - o[1], wp.p[2] - o[2]};
-    double dist = sqrt(dot3(v, v)) - P.r * (1.0 + 1e-9) - 1e-9;
+    double dist;
+    if (!kMesh && P.kind == RS_BOX) {  // distance from the camera to the box (tighter than its sphere)
+      double l[3], q2 = 0.0;
+      mattvec(wp.R, v, l);
+      for (int k = 0; k < 3; ++k) {
+        const double e = fabs(l[k]) - sc.part_param[3 * p + k];
+        q2 += e > 0.0 ? e * e : 0.0;
+      }
+      dist = sqrt(q2) * (1.0 - 1e-9) - 1e-9;
+    } else {
+      dist = sqrt(dot3(v, v)) - P.r * (1.0 + 1e-9) - 1e-9;
+    }
     P.lb = dist > 0.0 ? dist : 0.0;
     S.trace[p] = make_float2(__double2float_rd(P.lb), __int_as_float((P.kind << 8) | b));
   }
@@ -503,21 +523,39 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   //    front-to-back order of parts (rank by (lb, index)).
   if (warp < kMaskWords) {
     const int p = warp * 32 + lane;
-    double c[3] = {0.0, 0.0, 0.0}, r = 0.0;
+    double c[3] = {0.0, 0.0, 0.0}, r = 0.0, ax[3][3] = {}, h[3] = {0.0, 0.0, 0.0};
     const bool live = p < np;
+    bool box = false;
     if (live) {
       const PartW &P = S.part[p];
       double v[3] = {P.c[0] - o[0], P.c[1] - o[1], P.c[2] - o[2]};
       mattvec(S.cam.R, v, c);  // camera frame: x right, y down, z view
       r = P.r * (1.0 + 1e-9) + 1e-9;
+      box = !kMesh && P.kind == RS_BOX;
+      if (box)  // box axes in the camera frame (world axis k = column k of the part rotation)
+        for (int k = 0; k < 3; ++k) {
+          const double u[3] = {S.u.R[p][k], S.u.R[p][3 + k], S.u.R[p][6 + k]};
+          mattvec(S.cam.R, u, ax[k]);
+          h[k] = sc.part_param[3 * p + k] * (1.0 + 1e-9) + 1e-9;
+        }
     }
-    const bool front = live && c[2] > -r;
+    // support radius of the part along the (unnormalised) plane normal n = (nx, ny, nz), |n| = nn
+    auto radius = [&](double nx, double ny, double nz, double nn) {
+      if (!box) return r * nn;
+      double s = 0.0;
+      for (int k = 0; k < 3; ++k) s += fabs(nx * ax[k][0] + ny * ax[k][1] + nz * ax[k][2]) * h[k];
+      return s * (1.0 + 1e-9) + 1e-9 * nn;
+    };
+    const bool front = live && c[2] > -radius(0.0, 0.0, 1.0, 1.0);
     for (int tile = 0; tile < ntiles; ++tile) {
       bool in = false;
       if (front) {
         const double *T = B.tile_frustum + 8 * tile;  // u0, u1, v0, v1, |(1,u0)|, |(1,u1)|, |(1,v0)|, |(1,v1)|
-        in = c[0] - T[0] * c[2] >= -r * T[4] && -c[0] + T[1] * c[2] >= -r * T[5] &&
-             c[1] - T[2] * c[2] >= -r * T[6] && -c[1] + T[3] * c[2] >= -r * T[7];
+        // inward side planes: x - u0 z >= 0, -x + u1 z >= 0, y - v0 z >= 0, -y + v1 z >= 0
+        in = c[0] - T[0] * c[2] >= -radius(1.0, 0.0, -T[0], T[4]) &&
+             -c[0] + T[1] * c[2] >= -radius(-1.0, 0.0, T[1], T[5]) &&
+             c[1] - T[2] * c[2] >= -radius(0.0, 1.0, -T[2], T[6]) &&
+             -c[1] + T[3] * c[2] >= -radius(0.0, -1.0, T[3], T[7]);
       }
       const unsigned m = __ballot_sync(0xffffffffu, in);
       if (lane == 0) S.mask[tile][warp] = m;
@@ -552,8 +590,10 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   // -- trace
   const double eps = B.rcfg.tie_eps, zfar = B.rcfg.zfar, znear = B.rcfg.znear;
   const size_t img = (size_t)(env * n_cam_out + slot) * H * W;
-  unsigned long long tests = 0;
-  const bool count = work != nullptr;
+  Work wk;
+  constexpr bool count = kCount;
+  if (count)
+    for (int i = 0; i < 8; ++i) wk.v[i] = 0;
 #pragma unroll 1
   for (int tile = warp; tile < ntiles; tile += nwarps) {
     const uint8_t *list = S.u.list[tile];
@@ -568,8 +608,11 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       double tmin;
       int id, wpart, wface;
       if (kMode != kProxyMixed ||
-          !trace_mixed(S, plane, list, nl, o, d, eps, tmin, id, wpart, wface, tests, count))
-        tmin = trace_exact<kMesh>(sc, S, plane, list, nl, S.mask[tile], o, d, eps, id, wpart, wface, tests, count);
+          !trace_mixed(S, plane, list, nl, o, d, eps, tmin, id, wpart, wface, wk, count)) {
+        if (count && kMode == kProxyMixed) wk.v[3] += 1;
+        tmin = trace_exact<kMesh>(sc, S, plane, list, nl, S.mask[tile], o, d, eps, id, wpart, wface, wk, count);
+      }
+      if (count) wk.v[7] += 1;
 
       const size_t px = img + (size_t)v * W + u;
       if (!(tmin <= zfar)) {
@@ -612,7 +655,8 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       }
     }
   }
-  if (work) atomicAdd(work, tests);
+  if (count)
+    for (int i = 0; i < 8; ++i) atomicAdd(work + i, wk.v[i]);
 }
 
 // Per-batch constant tables: unit camera-frame ray per pixel centre
@@ -650,7 +694,7 @@ static size_t render_smem(const DevBatch &B, int mode) {
   return kPlaneOff + sizeof(double) * planes;
 }
 
-template <int kMode>
+template <int kMode, bool kCount>
 static cudaError_t launch_render_t(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                    cudaStream_t stream, unsigned long long *work) {
   int n_cam_out = __builtin_popcount(cam_mask);
@@ -658,29 +702,38 @@ static cudaError_t launch_render_t(const DevBatch &B, uint32_t cam_mask, uint8_t
   static bool configured = false;
   if (!configured) {  // the largest any batch can ask for: 1024 facets
     const size_t cap = kPlaneOff + sizeof(double) * (kMode == kMeshExact ? 9 * kMaxParts : 4 * 1024);
-    cudaError_t e = cudaFuncSetAttribute(render_kernel<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+    cudaError_t e = cudaFuncSetAttribute(render_kernel<kMode, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)cap);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   dim3 grid(B.n_env * n_cam_out);
-  render_kernel<kMode><<<grid, kRenderThreads, render_smem(B, kMode), stream>>>(
+  render_kernel<kMode, kCount><<<grid, kRenderThreads, render_smem(B, kMode), stream>>>(
       B, cam_mask, n_cam_out, reinterpret_cast<uint32_t *>(rgba), depth, ids, work);
   return cudaGetLastError();
 }
 
+// work: NULL, or 8 device uint64 counters (struct Work) -- the counting variant
+template <int kMode>
+static cudaError_t launch_render_any(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
+                                     cudaStream_t stream, unsigned long long *work) {
+  return work ? launch_render_t<kMode, true>(B, cam_mask, rgba, depth, ids, stream, work)
+              : launch_render_t<kMode, false>(B, cam_mask, rgba, depth, ids, stream, nullptr);
+}
+
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                           cudaStream_t stream, unsigned long long *work) {
-  return launch_render_t<kProxyMixed>(B, cam_mask, rgba, depth, ids, stream, work);
+  return launch_render_any<kProxyMixed>(B, cam_mask, rgba, depth, ids, stream, work);
 }
 
 cudaError_t launch_render_exact(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                 cudaStream_t stream, unsigned long long *work) {
-  return launch_render_t<kProxyExact>(B, cam_mask, rgba, depth, ids, stream, work);
+  return launch_render_any<kProxyExact>(B, cam_mask, rgba, depth, ids, stream, work);
 }
 
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work) {
-  return launch_render_t<kMeshExact>(B, cam_mask, rgba, depth, ids, stream, work);
+  return launch_render_any<kMeshExact>(B, cam_mask, rgba, depth, ids, stream, work);
 }
 
 }  // namespace rsim
