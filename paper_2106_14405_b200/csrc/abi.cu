@@ -648,6 +648,12 @@ int rsim_bench_env_cycles(rs_batch *b, long long *d_cycles) {
   return RS_OK;
 }
 
+int rsim_bench_phase_cycles(rs_batch *b, long long *d_cycles) {
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  b->d.phase_cycles = d_cycles;
+  return RS_OK;
+}
+
 int rsim_bench_render_exact(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                             void *stream) {
   if (!b) return fail(RS_ERR_ARG, "null batch");

@@ -121,6 +121,8 @@ struct DevBatch {
   const uint8_t *env_active;
   // optional per-env step latency probe (rsim_bench_env_cycles): SM clock cycles of the last step
   long long *env_cycles;
+  // optional per-env phase clock accumulators [E][8] (rsim_bench_phase_cycles)
+  long long *phase_cycles;
 };
 
 }  // namespace rsim

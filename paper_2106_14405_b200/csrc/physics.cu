@@ -63,7 +63,10 @@ struct BlockWS {
       ck[kMaxBlockRows];
   double cs[kMaxBlockRows], sn[kMaxBlockRows];  // rotations (m/2) / row-norm scratch (m)
   int pp[kMaxBlockRows / 2], qq[kMaxBlockRows / 2];
-  double A[kSmemEig * kSmemEig], V[kSmemEig * kSmemEig];
+  union {
+    struct { double A[kSmemEig * kSmemEig], V[kSmemEig * kSmemEig]; };
+    double F[2 * kSmemEig * kSmemEig];  // block_impulse_friction staging (after the LCP)
+  };
   int active[kMaxBlockRows];
   int na, worst, converged, slot;
 };
@@ -556,6 +559,17 @@ __device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
   return n;
 }
 
+// phase clocks (rsim_bench_phase_cycles): 0 front, 1 sweeps, 2 eigensolves,
+// 3 block LCP iterations, 4 block impulse + friction, 5 scalar rows, 6 back
+__device__ __forceinline__ long long phase_now(const Ctx &c) { return c.B->phase_cycles ? clock64() : 0; }
+struct PhaseClock {
+  long long t0;
+  __device__ __forceinline__ explicit PhaseClock(const Ctx &c) { t0 = phase_now(c); }
+  __device__ __forceinline__ void add(const Ctx &c, int k) {
+    if (c.B->phase_cycles && c.lane == 0) c.B->phase_cycles[8 * (size_t)c.env + k] += phase_now(c) - t0;
+  }
+};
+
 // ------------------------------------------------------------------ solver
 
 __device__ __forceinline__ void row_rel_vel(Ctx &c, const double *r, double *o) {
@@ -658,7 +672,10 @@ __device__ void row_solve(Ctx &c, double *r) {
 __device__ __forceinline__ void jacobi_pair(int n, int r, int k, int &p, int &q) {
   int a, b;
   if (k == 0) { a = n - 1; b = r; }
-  else { a = (r + k) % (n - 1); b = (r - k + n - 1) % (n - 1); }
+  else {  // (r + k) mod (n - 1), (r - k) mod (n - 1) with 0 <= r < n - 1, 0 < k < n / 2
+    a = r + k; if (a >= n - 1) a -= n - 1;
+    b = r - k + n - 1; if (b >= n - 1) b -= n - 1;
+  }
   p = a < b ? a : b;
   q = a < b ? b : a;
 }
@@ -668,10 +685,16 @@ __device__ __forceinline__ void jacobi_pair(int n, int r, int k, int &p, int &q)
 // parameters from the matrix at the start of the round (one pair per lane),
 // then a column pass and a row pass (one element pair per lane).  Identical
 // per-element arithmetic to oracle/rsim_oracle.c sym_eig.
+constexpr int kEigCached = 4;  // items per lane with cached indices (half * m <= 128, i.e. m <= 16)
 __device__ void sym_eig_warp(int m, double *A, double *V, double *ev, double *cs, double *sn, int *pp, int *qq,
                              int lane) {
   const int n = m + (m & 1), half = n / 2;
   for (int e = lane; e < m * m; e += 32) V[e] = (e / m == e % m);
+  // this lane's (rotation, row) items it = lane + 32 t of the column / row
+  // passes, fixed for the whole decomposition (no integer division per round)
+  int ik[kEigCached], ii[kEigCached];
+#pragma unroll
+  for (int t = 0; t < kEigCached; ++t) { ik[t] = (lane + 32 * t) / m; ii[t] = (lane + 32 * t) % m; }
   __syncwarp();
   for (int sweep = 0; sweep < 64 && m > 1; ++sweep) {
     // Frobenius norms: row partial sums (lane per row), rows added in order
@@ -709,9 +732,9 @@ __device__ void sym_eig_warp(int m, double *A, double *V, double *ev, double *cs
         pp[lane] = p; qq[lane] = q; cs[lane] = c; sn[lane] = sv;
       }
       __syncwarp();
-      for (int it = lane; it < half * m; it += 32) {  // column pass
-        const int k = it / m, i = it % m, p = pp[k], q = qq[k];
-        if (q >= m || sn[k] == 0.0) continue;
+      auto col = [&](int k, int i) {  // column pass element: rows i of columns p, q (A and V)
+        const int p = pp[k], q = qq[k];
+        if (q >= m || sn[k] == 0.0) return;
         const double c = cs[k], sv = sn[k];
         double aip = A[i * m + p], aiq = A[i * m + q];
         A[i * m + p] = c * aip - sv * aiq;
@@ -719,16 +742,24 @@ __device__ void sym_eig_warp(int m, double *A, double *V, double *ev, double *cs
         double vip = V[i * m + p], viq = V[i * m + q];
         V[i * m + p] = c * vip - sv * viq;
         V[i * m + q] = sv * vip + c * viq;
-      }
-      __syncwarp();
-      for (int it = lane; it < half * m; it += 32) {  // row pass
-        const int k = it / m, j = it % m, p = pp[k], q = qq[k];
-        if (q >= m || sn[k] == 0.0) continue;
+      };
+      auto row = [&](int k, int j) {  // row pass element: column j of rows p, q
+        const int p = pp[k], q = qq[k];
+        if (q >= m || sn[k] == 0.0) return;
         const double c = cs[k], sv = sn[k];
         double apj = A[p * m + j], aqj = A[q * m + j];
         A[p * m + j] = c * apj - sv * aqj;
         A[q * m + j] = sv * apj + c * aqj;
-      }
+      };
+#pragma unroll
+      for (int t = 0; t < kEigCached; ++t)
+        if (lane + 32 * t < half * m) col(ik[t], ii[t]);
+      for (int it = lane + 32 * kEigCached; it < half * m; it += 32) col(it / m, it % m);
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < kEigCached; ++t)
+        if (lane + 32 * t < half * m) row(ik[t], ii[t]);
+      for (int it = lane + 32 * kEigCached; it < half * m; it += 32) row(it / m, it % m);
       __syncwarp();
     }
   }
@@ -736,10 +767,98 @@ __device__ void sym_eig_warp(int m, double *A, double *V, double *ev, double *cs
   __syncwarp();
 }
 
+// physics.py:800-816 after a converged block LCP: apply the normal impulse
+// deltas in row order, then one Gauss-Seidel friction pass in row order
+// (row_apply / row_friction / row_rel_vel), for a block whose rows touch no
+// articulation joint.  The block's rows are staged into shared memory by the
+// warp; lane 0 then runs the order-dependent sequence with both bodies'
+// velocities and inverse inertias in registers.  Same operations in the same
+// order as the generic path (this unit is built with -fmad=false): results
+// are bit-identical.
+constexpr int kFastRows = 12;
+constexpr int kFastD = 23;  // n, t1, t2, ra, rb, k, mu, fric, lam_old, lt1, lt2, ima, imb
+static_assert(kFastRows * kFastD <= 2 * kSmemEig * kSmemEig, "staging area");
+__constant__ int kFastSrc[kFastD] = {RN, RN + 1, RN + 2, RT1, RT1 + 1, RT1 + 2, RT2, RT2 + 1, RT2 + 2,
+                                     RRA, RRA + 1, RRA + 2, RRB, RRB + 1, RRB + 2, RK, RMU, RFRIC, RLAM,
+                                     RLT1, RLT2, RIMA, RIMB};
+__device__ void block_impulse_friction(Ctx &c, int g, int first, int m, BlockWS &ws) {
+  double *F = ws.F;  // [m][kFastD]
+  const int lane = c.lane;
+  for (int e = lane; e < m * kFastD; e += 32) {
+    const int i = e / kFastD, q = e - i * kFastD;
+    const double *r = c.rows + kRowD * (first + i);
+    F[e] = r[kFastSrc[q]];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const double *r0 = c.rows + kRowD * first;
+    const int a = (int)r0[RA], b = (int)r0[RB];
+    const double *pg = c.pairs + kPairD * g;
+    double va[6], vb[6], Ia[9], Ib[9];
+    for (int k = 0; k < 6; ++k) { va[k] = c.S->u.sol.vel[a][k]; vb[k] = c.S->u.sol.vel[b][k]; }
+    for (int k = 0; k < 9; ++k) { Ia[k] = pg[PIA + k]; Ib[k] = pg[PIB + k]; }
+    auto apply = [&](const double *f, double ix, double iy, double iz) {  // row_apply
+      if (f[21] > 0.0) {
+        const double mm = f[21], *ra = f + 9;
+        va[0] += ix * mm; va[1] += iy * mm; va[2] += iz * mm;
+        double tx = ra[1] * iz - ra[2] * iy, ty = ra[2] * ix - ra[0] * iz, tz = ra[0] * iy - ra[1] * ix;
+        va[3] += Ia[0] * tx + Ia[1] * ty + Ia[2] * tz;
+        va[4] += Ia[3] * tx + Ia[4] * ty + Ia[5] * tz;
+        va[5] += Ia[6] * tx + Ia[7] * ty + Ia[8] * tz;
+      }
+      if (f[22] > 0.0) {
+        const double mm = f[22], *rb = f + 12;
+        vb[0] -= ix * mm; vb[1] -= iy * mm; vb[2] -= iz * mm;
+        double tx = rb[1] * iz - rb[2] * iy, ty = rb[2] * ix - rb[0] * iz, tz = rb[0] * iy - rb[1] * ix;
+        vb[3] -= Ib[0] * tx + Ib[1] * ty + Ib[2] * tz;
+        vb[4] -= Ib[3] * tx + Ib[4] * ty + Ib[5] * tz;
+        vb[5] -= Ib[6] * tx + Ib[7] * ty + Ib[8] * tz;
+      }
+    };
+    for (int i = 0; i < m; ++i) {  // normal impulse deltas
+      double *f = F + kFastD * i;
+      const double l = ws.lam[i] > 0.0 ? ws.lam[i] : 0.0;
+      const double d = l - f[18];
+      f[18] = l;
+      c.rows[kRowD * (first + i) + RLAM] = l;
+      if (d != 0.0) apply(f, f[0] * d, f[1] * d, f[2] * d);
+    }
+    for (int i = 0; i < m; ++i) {  // row_friction
+      double *f = F + kFastD * i;
+      if (f[15] <= 0.0 || f[17] == 0.0) continue;
+      const double max_t = f[16] * f[18], *ra = f + 9, *rb = f + 12;
+      for (int w = 0; w < 2; ++w) {
+        const double *t = f + (w ? 6 : 3);
+        double &acc = f[w ? 20 : 19];
+        const double ax = va[0] + va[4] * ra[2] - va[5] * ra[1];
+        const double ay = va[1] + va[5] * ra[0] - va[3] * ra[2];
+        const double az = va[2] + va[3] * ra[1] - va[4] * ra[0];
+        const double bx = vb[0] + vb[4] * rb[2] - vb[5] * rb[1];
+        const double by = vb[1] + vb[5] * rb[0] - vb[3] * rb[2];
+        const double bz = vb[2] + vb[3] * rb[1] - vb[4] * rb[0];
+        const double v0 = ax - bx, v1 = ay - by, v2 = az - bz;
+        const double vt = v0 * t[0] + v1 * t[1] + v2 * t[2];
+        double lt = -vt / f[15], nt = acc + lt;
+        if (nt > max_t) nt = max_t;
+        else if (nt < -max_t) nt = -max_t;
+        lt = nt - acc;
+        acc = nt;
+        if (lt != 0.0) apply(f, t[0] * lt, t[1] * lt, t[2] * lt);
+      }
+      double *r = c.rows + kRowD * (first + i);
+      r[RLT1] = f[19];
+      r[RLT2] = f[20];
+    }
+    for (int k = 0; k < 6; ++k) { c.S->u.sol.vel[a][k] = va[k]; c.S->u.sol.vel[b][k] = vb[k]; }
+  }
+  __syncwarp();
+}
+
 // physics.py:760-816; warp-collective.  Kc/evc: this block's eigen cache.
 __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, BlockWS &ws, double *W, double *Vc,
                             double *evc) {
   const int lane = c.lane;
+  PhaseClock pl(c);
   double *P = c.pairs + kPairD * g;
   if (lane < m) {
     double *r = c.rows + kRowD * (first + lane);
@@ -776,7 +895,9 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
         double *Vt = na <= kSmemEig ? ws.V : Vc + slot * m * m;
         for (int e = lane; e < na * na; e += 32) A[e] = K[ws.active[e / na] * m + ws.active[e % na]];
         __syncwarp();
+        PhaseClock pe(c);
         sym_eig_warp(na, A, Vt, evc + slot * m, ws.cs, ws.sn, ws.pp, ws.qq, lane);
+        pe.add(c, 2);
         if (na <= kSmemEig)
           for (int e = lane; e < na * na; e += 32) Vc[slot * m * m + e] = Vt[e];
         if (lane == 0) { P[PMASK + slot] = (double)mask; P[PREPL] = (double)(slot ^ 1); }
@@ -855,7 +976,22 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     __syncwarp();
     if (ws.converged) break;
   }
-  if (lane == 0) {
+  pl.add(c, 3);
+  PhaseClock pf(c);
+  // register-resident impulse + friction pass for blocks without joint
+  // coupling that fit the staging area (A/V of the workspace, free now)
+  bool fast = ws.converged && m <= kFastRows;
+  if (fast) {
+    bool nojoint = true;
+    if (lane < m) {
+      const double *r = c.rows + kRowD * (first + lane);
+      nojoint = r[RJA] < 0.0 && r[RJB] < 0.0;
+    }
+    fast = __all_sync(0xffffffffu, nojoint);
+  }
+  if (fast) {
+    block_impulse_friction(c, g, first, m, ws);
+  } else if (lane == 0) {
     if (!ws.converged) {
       for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
     } else {
@@ -870,6 +1006,7 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     }
   }
   __syncwarp();
+  pf.add(c, 4);
 }
 
 __device__ __forceinline__ bool solver_dynamic(Ctx &c, int b) {
@@ -1346,9 +1483,11 @@ __device__ void substep_sweeps(Ctx &c) {
           const int first = S.g_first[g], m = S.g_n[g];
           const double *P = c.pairs + kPairD * g;
           if (P[PHASK] == 0.0) {
+            PhaseClock pr(c);
             if (lane == 0)
               for (int i = 0; i < m; ++i) row_solve(c, c.rows + kRowD * (first + i));
             __syncwarp();
+            pr.add(c, 5);
           } else {
             const int koff = (int)P[PKOFF];
             solve_block(c, g, first, m, c.K + koff, S.u.sol.ws, c.W, c.Vc + 2 * koff, c.evc + 2 * first);
@@ -1471,9 +1610,15 @@ __device__ void substep_back(Ctx &c, double dt) {
 }
 
 __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double dt, int sub) {
+  PhaseClock p0(c);
   if (!substep_front(c, arm, basecmd, dt, sub)) return false;
+  p0.add(c, 0);
+  PhaseClock p1(c);
   substep_sweeps(c);
+  p1.add(c, 1);
+  PhaseClock p2(c);
   substep_back(c, dt);
+  p2.add(c, 6);
   return true;
 }
 

@@ -31,7 +31,11 @@ if args.env >= 0:
 print(f"env {d['env'][i]} step {d['step'][i]} layout {d['layout'][i]} recorded {abs(d['cycles'][i]) / 1.965e3:.0f} us")
 sim = BatchSimulator(layouts=(int(d["layout"][i]),), n_env=args.n, device="cuda")
 act = torch.tensor(np.tile(d["action"][i], (args.n, 1)), device="cuda")
+import ctypes as C  # noqa: E402
+
+ph = torch.zeros((args.n, 8), dtype=torch.int64, device="cuda")
 for rep in range(args.reps):
+    sim.L.rsim_bench_phase_cycles(sim._batch, C.c_void_p(ph.data_ptr()) if rep == 0 else None)
     sim.set_state([d["pre"][i].tobytes()] * args.n)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -40,5 +44,8 @@ for rep in range(args.reps):
     e1.record()
     torch.cuda.synchronize()
     print(f"rep {rep}: {e0.elapsed_time(e1):.3f} ms for {args.n} copies")
+names = ["front", "sweeps", "eigen", "lcp(incl eigen)", "impulse+friction", "scalar rows", "back"]
+v = ph.double().mean(0).cpu().numpy() / 1.965e3
+print("phase us (warp kernel, rep 0): " + ", ".join(f"{n} {x:.0f}" for n, x in zip(names, v)))
 sim.raise_faults()
 sim.close()
