@@ -362,7 +362,7 @@ def run_b200(args):
     acc = float(h_stats[:, 0].sum())
 
     # ---- each half alone (same launches, no overlap partner): the interleaved
-    # timings above share the SMs, so the dominant kernel is picked from these
+    # timings above share the SMs; the roofline uses the render kernel alone
     iso = {"render": [], "phys": []}
     for k in range(args.steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -392,7 +392,7 @@ def run_b200(args):
     e2e_value = total_envs * args.steps / (ms_e2e * 1e-3)
 
     if rank == 0:
-        # roofline: dominant kernel against the measured FMA pipe peak
+        # roofline of the render kernel against the measured FMA pipe peak
         import ctypes as C
 
         peak64, peak32 = C.c_double(0), C.c_double(0)
@@ -401,19 +401,20 @@ def run_b200(args):
         L.rsim_bench_fma_peak(1, C.byref(peak64))
         L.rsim_bench_fma_peak(0, C.byref(peak32))
         render_flop = N_CAMS * H * W * (14 * 566 + 22 * 4)  # SURVEY.md §8d W_r (brute-force proxy raycast)
-        L.rsim_bench_render_work.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p]
-        ctr = torch.zeros(1, dtype=torch.int64, device=dev)
-        L.rsim_bench_render_work(sim._batch, 3, C.c_void_p(ctr.data_ptr()), C.c_void_p(stream.cuda_stream))
-        torch.cuda.synchronize(dev)
-        executed_tests = float(ctr.item()) / E  # ray-plane (+ sphere) tests per env-step actually executed
         phys_flop = 0.09e6  # SURVEY.md §8d idle W_p per env-step
-        if ms_rend_iso >= ms_phys_iso:
-            dom, ms_dom, flop, grid = "render_kernel", ms_rend_iso, render_flop, E * N_CAMS
-        else:
-            dom, ms_dom, flop, grid = "step_kernel", ms_phys_iso, phys_flop, (E + 1) // 2
+        wd = torch.zeros(8, dtype=torch.int64, device=dev)
+        L.rsim_bench_render_work_detail.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p]
+        L.rsim_bench_render_work_detail(sim._batch, 3, C.c_void_p(wd.data_ptr()), C.c_void_p(stream.cuda_stream))
+        torch.cuda.synchronize(dev)
+        wd = wd.cpu().numpy().astype(float)
+        fp32_tests, fp64_tests = wd[0] / E, (wd[1] + wd[2] + wd[6]) / E  # ray-plane tests per env-step
+        # The render kernel dominates the GPU's work (SM-time); the physics step is
+        # latency-bound (its duration is the slowest env's dependency chain on one
+        # warp, see "physics_latency"), so the roofline is the render kernel's.
+        dom, ms_dom, flop, grid = "render_kernel", ms_rend_iso, render_flop, E * N_CAMS
         achieved = flop * E / (ms_dom * 1e-3) / 1e12
-        ex_flop = 14.0 * executed_tests if dom == "render_kernel" else None
-        ex_ach = ex_flop * E / (ms_dom * 1e-3) / 1e12 if ex_flop else None
+        ex_flop = 14.0 * (fp32_tests + fp64_tests)
+        ex_ach = ex_flop * E / (ms_dom * 1e-3) / 1e12
         traffic, prof = None, None
         try:  # dram read+write per launch of this kernel from the committed ncu --set full capture
             pj = json.load(open(os.path.join(ROOT, PROFILE_JSON)))
@@ -422,6 +423,14 @@ def run_b200(args):
                 traffic, prof = kk["dram_bytes_per_launch"], PROFILE_JSON
         except (OSError, ValueError, KeyError):
             pass
+        # per-env step latency of one more control step (rsim_bench_env_cycles probe)
+        cyc = torch.zeros(E, dtype=torch.int64, device=dev)
+        L.rsim_bench_env_cycles.argtypes = [C.c_void_p, C.c_void_p]
+        L.rsim_bench_env_cycles(sim._batch, C.c_void_p(cyc.data_ptr()))
+        sim.env_step(act_d[args.warmup + args.steps - 1])
+        torch.cuda.synchronize(dev)
+        L.rsim_bench_env_cycles(sim._batch, None)
+        us = np.abs(cyc.cpu().numpy()) / (clk.summary().get("sm_mhz") or 1965.0)
         obs_bytes = E * N_CAMS * H * W * (4 + 4 + 4)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -436,20 +445,27 @@ def run_b200(args):
                        "l2": "inputs > L2: 805 MB of RGBD/id writes per step at 2048 envs evict the state slabs"},
             "kernels_ms_per_step": {"interleaved": {"ik+step+grasp": ms_phys, "render_kernel": ms_rend},
                                     "alone": {"ik+step+grasp": ms_phys_iso, "render_kernel": ms_rend_iso}},
-            "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": peak64.value,
-                         "unit": "TFLOP/s", "frac": achieved / peak64.value if peak64.value else None,
+            "roofline": {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak32.value,
+                         "unit": "TFLOP/s", "frac": achieved / peak32.value if peak32.value else None,
                          "traffic": traffic, "traffic_source": prof,
                          "algorithmic_bytes_per_launch": obs_bytes if dom == "render_kernel" else None,
-                         "peak_source": "measured FP64 FMA microbenchmark (rsim_bench_fma_peak); "
+                         "peak_source": "measured FP32 FMA microbenchmark (rsim_bench_fma_peak); "
                                         "MEASURED_PEAKS.json has no FP64/FP32 entry",
-                         "fp32_peak_tflops": peak32.value,
+                         "fp64_peak_tflops": peak64.value,
                          "algorithmic_flop_per_unit": flop,
                          "algorithmic_note": "SURVEY.md §8d W_r = brute-force proxy raycast (every ray vs every "
-                                             "plane); the kernel culls, so frac can exceed 1 -- executed_frac is "
-                                             "the FP64-pipe utilisation of the work actually done",
+                                             "plane, 14 flop per ray-plane); the kernel culls, so frac can exceed 1 "
+                                             "-- executed_frac is the FMA-pipe utilisation of the ray-plane work "
+                                             "actually done (bounded-error FP32 tests + FP64 resolution)",
+                         "executed_plane_tests_per_unit": {"fp32": fp32_tests, "fp64": fp64_tests},
                          "executed_flop_per_unit": ex_flop, "executed_achieved": ex_ach,
-                         "executed_frac": ex_ach / peak64.value if ex_ach and peak64.value else None,
+                         "executed_frac": ex_ach / peak32.value if peak32.value else None,
                          "hbm_gbs_obs_writes": obs_bytes / (ms_rend_iso * 1e-3) / 1e9},
+            "physics_latency": {"note": "step kernel = one warp per env, latency-bound (serial Gauss-Seidel "
+                                        "order inside an env); per-env SM time of one control step",
+                                "p50_us": float(np.percentile(us, 50)), "p99_us": float(np.percentile(us, 99)),
+                                "max_us": float(us.max()), "envs_on_cta_kernel": int((cyc < 0).sum().item()),
+                                "algorithmic_flop_per_unit": phys_flop},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(E * 6 * 8),
                     "d2h_bytes_per_step": int(E * 4 * 8)},
             "gpu_launches": 6 * args.steps,  # ik_first, ik_fallback, step, step_cta, grasp, render per env step
