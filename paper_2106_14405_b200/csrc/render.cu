@@ -466,11 +466,12 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       for (int k = 0; k < 9; ++k) plane[9 * p + k] = wp.R[k];
     } else {
       P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : sc.part_bound[p];
-      for (int k = 0; k < 9; ++k) S.u.R[p][k] = wp.R[k];
     }
+    for (int k = 0; k < 9; ++k) S.u.R[p][k] = wp.R[k];
     double v[3] = {wp.p[0] - o[0], wp.p[1] - o[1], wp.p[2] - o[2]};
     double dist;
-    if (!kMesh && P.kind == RS_BOX) {  // distance from the camera to the box (tighter than its sphere)
+    if (P.kind == RS_BOX) {  // distance from the camera to the box (tighter than its sphere; a box
+                             // part's triangle soup lies on the box surface, mesh.py part_triangles)
       double l[3], q2 = 0.0;
       mattvec(wp.R, v, l);
       for (int k = 0; k < 3; ++k) {
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       double v[3] = {P.c[0] - o[0], P.c[1] - o[1], P.c[2] - o[2]};
       mattvec(S.cam.R, v, c);  // camera frame: x right, y down, z view
       r = P.r * (1.0 + 1e-9) + 1e-9;
-      box = !kMesh && P.kind == RS_BOX;
+      box = P.kind == RS_BOX;
       if (box)  // box axes in the camera frame (world axis k = column k of the part rotation)
         for (int k = 0; k < 3; ++k) {
           const double u[3] = {S.u.R[p][k], S.u.R[p][3 + k], S.u.R[p][6 + k]};
