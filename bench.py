@@ -290,22 +290,27 @@ def run_b200(args):
     stream = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)
 
+    hp = torch.cuda.Stream(dev, priority=-1)  # physics ahead of queued render CTAs
+
     def step(k, ev=None):
         # one env step, paper pipeline (SPEC StepConfig defaults
-        # observation_delay=1, interleave=true): render(s_t) on a side stream
-        # concurrently with physics s_t -> s_{t+1}, then join.
+        # observation_delay=1, interleave=true): physics s_t -> s_{t+1} on a
+        # high-priority stream, render(s_t) concurrently on a side stream, join.
+        hp.wait_stream(stream)
         side.wait_stream(stream)
-        with torch.cuda.stream(side):
+        with torch.cuda.stream(side):  # enqueued first: it reads s_t before env_step flips the state buffers
             if ev is not None:
                 ev[2].record(side)
             sim.render(("head", "arm"), out=obs)
             if ev is not None:
                 ev[3].record(side)
-        if ev is not None:
-            ev[0].record(stream)
-        sim.env_step(act_d[k])  # IK -> physics -> grasp rule
-        if ev is not None:
-            ev[1].record(stream)
+        with torch.cuda.stream(hp):
+            if ev is not None:
+                ev[0].record(hp)
+            sim.env_step(act_d[k])  # IK -> physics -> grasp rule
+            if ev is not None:
+                ev[1].record(hp)
+        stream.wait_stream(hp)
         stream.wait_stream(side)
 
     for k in range(args.warmup):

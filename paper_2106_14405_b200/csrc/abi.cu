@@ -97,6 +97,9 @@ struct rs_batch {
   uint8_t *heavy[2] = {nullptr, nullptr};
   cudaStream_t phys_side = nullptr;
   cudaEvent_t ph_fork = nullptr, ph_join = nullptr;
+  // host-buffer steps: physics on a high-priority stream next to the render
+  cudaStream_t phys_hp = nullptr;
+  cudaEvent_t hp_join = nullptr;
 };
 
 // exported functions take C linkage from their declarations in rsim.h
@@ -314,6 +317,8 @@ void rs_batch_destroy(rs_batch *b) {
   if (b->h_settle_count) cudaFreeHost(b->h_settle_count);
   if (b->side) cudaStreamDestroy(b->side);
   if (b->phys_side) cudaStreamDestroy(b->phys_side);
+  if (b->phys_hp) cudaStreamDestroy(b->phys_hp);
+  if (b->hp_join) cudaEventDestroy(b->hp_join);
   if (b->ph_fork) cudaEventDestroy(b->ph_fork);
   if (b->ph_join) cudaEventDestroy(b->ph_join);
   if (b->ev_fork) cudaEventDestroy(b->ev_fork);
@@ -448,13 +453,30 @@ int rs_get_state(rs_batch *b, uint8_t *snaps, int64_t stride, const int32_t *env
 static cudaError_t launch_step_b(rs_batch *b, const double *arm, const double *base_cmd, int base_stride,
                                  const uint8_t *has_targets, double dt, int substeps, cudaStream_t st) {
   if (!b->phys_side) {
-    cudaError_t e = cudaStreamCreateWithFlags(&b->phys_side, cudaStreamNonBlocking);
+    // highest priority: contact-heavy envs (the step's latency tail) get SMs
+    // ahead of queued render CTAs of an interleaved observation render
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaError_t e = cudaStreamCreateWithPriority(&b->phys_side, cudaStreamNonBlocking, hi);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_join, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
   return launch_step(b->view(), arm, base_cmd, base_stride, has_targets, dt, substeps, st, b->heavy[b->cur],
                      b->heavy[b->cur ^ 1], b->phys_side, b->ph_fork, b->ph_join);
+}
+
+// physics of a host-buffer step runs on a highest-priority stream so that the
+// contact-heavy envs (the step's latency tail) get SMs ahead of queued render
+// CTAs; `st` joins it at the end
+static int ensure_phys_hp(rs_batch *b) {
+  if (!b->phys_hp) {
+    int lo = 0, hi = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(cudaStreamCreateWithPriority(&b->phys_hp, cudaStreamNonBlocking, hi));
+    CUDA_TRY(cudaEventCreateWithFlags(&b->hp_join, cudaEventDisableTiming));
+  }
+  return RS_OK;
 }
 
 int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_t *has_targets, double dt,
@@ -524,22 +546,28 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
     CUDA_TRY(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
   }
+  if (int rc0 = ensure_phys_hp(b)) return rc0;
+  cudaStream_t hp = b->phys_hp;
   // render o_t = render(s_t) on the side stream, concurrently with the physics
-  // s_t -> s_{t+1} on `stream` (ping-pong state buffers)
+  // s_t -> s_{t+1} on the high-priority stream (ping-pong state buffers;
+  // PAPER.md:453-457); the render is enqueued before the step flips the buffers
+  CUDA_TRY(cudaEventRecord(b->ev_fork, st));
   if (cam_mask) {
-    CUDA_TRY(cudaEventRecord(b->ev_fork, st));
     CUDA_TRY(cudaStreamWaitEvent(b->side, b->ev_fork, 0));
     int rc = rs_render(b, cam_mask, rgba, depth, ids, b->side);
     if (rc) return rc;
     CUDA_TRY(cudaEventRecord(b->ev_join, b->side));
   }
+  CUDA_TRY(cudaStreamWaitEvent(hp, b->ev_fork, 0));
   double *d_arm = b->d_act, *d_base = b->d_act + (size_t)E * na;
-  CUDA_TRY(cudaMemcpyAsync(d_arm, h_arm, sizeof(double) * (size_t)E * na, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(d_base, h_base, sizeof(double) * (size_t)E * 2, cudaMemcpyHostToDevice, st));
-  int rc = rs_step(b, d_arm, d_base, nullptr, dt, substeps, stream);
+  CUDA_TRY(cudaMemcpyAsync(d_arm, h_arm, sizeof(double) * (size_t)E * na, cudaMemcpyHostToDevice, hp));
+  CUDA_TRY(cudaMemcpyAsync(d_base, h_base, sizeof(double) * (size_t)E * 2, cudaMemcpyHostToDevice, hp));
+  int rc = rs_step(b, d_arm, d_base, nullptr, dt, substeps, hp);
   if (rc) return rc;
-  CUDA_TRY(launch_stats(b->view(), b->d_stats, st));
-  CUDA_TRY(cudaMemcpyAsync(h_out_stats, b->d_stats, sizeof(double) * (size_t)E * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(launch_stats(b->view(), b->d_stats, hp));
+  CUDA_TRY(cudaMemcpyAsync(h_out_stats, b->d_stats, sizeof(double) * (size_t)E * 4, cudaMemcpyDeviceToHost, hp));
+  CUDA_TRY(cudaEventRecord(b->hp_join, hp));
+  CUDA_TRY(cudaStreamWaitEvent(st, b->hp_join, 0));
   if (cam_mask) CUDA_TRY(cudaStreamWaitEvent(st, b->ev_join, 0));
   CUDA_TRY(cudaStreamSynchronize(st));
   return RS_OK;
@@ -709,20 +737,24 @@ int rs_env_step_host(rs_batch *b, const double *h_action, double dt, int32_t sub
   if (!b || !h_action || !h_out_stats) return fail(RS_ERR_ARG, "null argument");
   int rc = ensure_env_buffers(b);
   if (rc) return rc;
+  if ((rc = ensure_phys_hp(b))) return rc;
   const int E = b->d.n_env;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (cam_mask) {  // o_t = render(s_t) on the side stream, concurrently with the step
-    CUDA_TRY(cudaEventRecord(b->ev_fork, st));
+  cudaStream_t st = (cudaStream_t)stream, hp = b->phys_hp;
+  CUDA_TRY(cudaEventRecord(b->ev_fork, st));
+  if (cam_mask) {  // o_t = render(s_t) on the side stream (enqueued before the step flips the buffers)
     CUDA_TRY(cudaStreamWaitEvent(b->side, b->ev_fork, 0));
     rc = rs_render(b, cam_mask, rgba, depth, ids, b->side);
     if (rc) return rc;
     CUDA_TRY(cudaEventRecord(b->ev_join, b->side));
   }
-  CUDA_TRY(cudaMemcpyAsync(b->d_env_act, h_action, sizeof(double) * (size_t)E * 6, cudaMemcpyHostToDevice, st));
-  rc = rs_env_step(b, b->d_env_act, dt, substeps, stream);
+  CUDA_TRY(cudaStreamWaitEvent(hp, b->ev_fork, 0));
+  CUDA_TRY(cudaMemcpyAsync(b->d_env_act, h_action, sizeof(double) * (size_t)E * 6, cudaMemcpyHostToDevice, hp));
+  rc = rs_env_step(b, b->d_env_act, dt, substeps, hp);
   if (rc) return rc;
-  CUDA_TRY(launch_stats(b->view(), b->d_stats, st));
-  CUDA_TRY(cudaMemcpyAsync(h_out_stats, b->d_stats, sizeof(double) * (size_t)E * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(launch_stats(b->view(), b->d_stats, hp));
+  CUDA_TRY(cudaMemcpyAsync(h_out_stats, b->d_stats, sizeof(double) * (size_t)E * 4, cudaMemcpyDeviceToHost, hp));
+  CUDA_TRY(cudaEventRecord(b->hp_join, hp));
+  CUDA_TRY(cudaStreamWaitEvent(st, b->hp_join, 0));
   if (cam_mask) CUDA_TRY(cudaStreamWaitEvent(st, b->ev_join, 0));
   CUDA_TRY(cudaStreamSynchronize(st));
   return RS_OK;

@@ -46,6 +46,9 @@ class BatchEnv:
         self._k = 0
         self.t = 0
         self._render_stream = torch.cuda.Stream(device=self.device)
+        # physics at high priority: the contact-heavy envs (the step's latency
+        # tail) get SMs ahead of queued render CTAs
+        self._phys_stream = torch.cuda.Stream(device=self.device, priority=-1)
         self._phys_done = torch.cuda.Event()
         self._render_done = torch.cuda.Event()
         self._stats = torch.empty((n_env, 4), dtype=torch.float64, device=self.device)
@@ -74,7 +77,10 @@ class BatchEnv:
                 with torch.cuda.stream(self._render_stream):
                     self.sim.render(self.cams, out=obs)
                 self._render_done.record(self._render_stream)
-                self.sim.step_physics(arm_targets, base_cmd)
+                self._phys_stream.wait_stream(main)
+                with torch.cuda.stream(self._phys_stream):
+                    self.sim.step_physics(arm_targets, base_cmd)
+                main.wait_stream(self._phys_stream)
                 # the next step overwrites the buffer this render reads: join here
                 main.wait_event(self._render_done)
                 for t in obs:
