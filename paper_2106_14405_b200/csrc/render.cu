@@ -127,13 +127,17 @@ __device__ __forceinline__ double ray_convex(const double *pl, int nf, const dou
 // +k when s < 0 (else -k) and the exiting plane the other one; both ratios
 // have denominator |s|, so the arg-max / arg-min over the 3 axes compares
 // cross products, and te = -b_e / |s_e| is divided only for hits that matter.
+__device__ __forceinline__ double plane_dot(const double *d, const double *n) {
+  return d[0] * n[0] + d[1] * n[1] + d[2] * n[2];
+}
+
 __device__ __forceinline__ double ray_box(const double *pl, const double *d, double tcut, int &face) {
   bool bad = false, has = false;
   double aE = 0, bE = 0, aX = 0, bX = 0;
   int fE = -1;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const double sv = d[0] * pl[4 * k] + d[1] * pl[4 * k + 1] + d[2] * pl[4 * k + 2];
+    const double sv = plane_dot(d, pl + 4 * k);
     const double bp = pl[4 * k + 3], bm = pl[4 * (k + 3) + 3];
     const bool par = !(sv < -kParallelEps) && !(sv > kParallelEps);
     bad |= par && (bp < 0 || bm < 0);
@@ -320,7 +324,10 @@ constexpr float kEs = 2e-6f;
 constexpr float kRel = 16.0f * 5.9604645e-8f;
 constexpr float kAmin = 1e-3f;
 
-__device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float dz, float &t, float &e) {
+// ax (certain hits with t > 0 only): entering axis k + 4 * (s_k >= 0), + 8
+// when te_k exceeds the other two entering ratios by more than their error
+// bounds -- then the FP64 test picks the same entering plane (ray_box_axis).
+__device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float dz, float &t, float &e, int &ax) {
   const float4 A = bx[0], Bv = bx[1], C = bx[2], M = bx[3];
   const float s0 = fmaf(dx, A.x, fmaf(dy, A.y, dz * A.z));
   const float s1 = fmaf(dx, Bv.x, fmaf(dy, Bv.y, dz * Bv.z));
@@ -329,16 +336,33 @@ __device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float
   const float amin = fminf(a0, fminf(a1, a2));
   if (amin < kAmin) return 2;
   const float r0 = __fdividef(1.0f, a0), r1 = __fdividef(1.0f, a1), r2 = __fdividef(1.0f, a2);
-  const float te = fmaxf(-(s0 < 0.f ? A.w : M.x) * r0, fmaxf(-(s1 < 0.f ? Bv.w : M.y) * r1, -(s2 < 0.f ? C.w : M.z) * r2));
+  const float te0 = -(s0 < 0.f ? A.w : M.x) * r0, te1 = -(s1 < 0.f ? Bv.w : M.y) * r1,
+              te2 = -(s2 < 0.f ? C.w : M.z) * r2;
+  const float te = fmaxf(te0, fmaxf(te1, te2));
   const float tx = fminf((s0 < 0.f ? M.x : A.w) * r0, fminf((s1 < 0.f ? M.y : Bv.w) * r1, (s2 < 0.f ? M.z : C.w) * r2));
-  const float rmax = fmaxf(r0, fmaxf(r1, r2));
-  e = (fabsf(te) + fabsf(tx)) * fmaf(kEs, rmax, kRel);
+  const float rmax = fmaxf(r0, fmaxf(r1, r2)), cr = fmaf(kEs, rmax, kRel);
+  e = (fabsf(te) + fabsf(tx)) * cr;
   if (tx < -e || te - tx > e) return 0;
   if (tx <= e || tx - te <= e) return 2;
-  if (te < -e) { t = 0.0f; e = 0.0f; return 1; }
+  if (te < -e) { t = 0.0f; e = 0.0f; ax = 0; return 1; }
   if (te <= e) return 2;
   t = te;
+  const int k = te0 == te ? 0 : (te1 == te ? 1 : 2);
+  const float second = fmaxf(fminf(te0, te1), fminf(fmaxf(te0, te1), te2));  // middle of the three
+  const float sk = k == 0 ? s0 : (k == 1 ? s1 : s2);
+  ax = k + (sk < 0.f ? 0 : 4) + (te - second > 2.0f * e + 2.0f * cr * fabsf(second) ? 8 : 0);
   return 1;
+}
+
+// ray_box when the entering axis is known to be unique (box32 ax & 8) and the
+// hit certain with t > 0: the same plane, the same -b_e / |s_e| as ray_box
+__device__ __forceinline__ double ray_box_axis(const double *pl, const double *d, int ax, int &face) {
+  const int k = ax & 3;
+  const double sv = plane_dot(d, pl + 4 * k);
+  const double bp = pl[4 * k + 3], bm = pl[4 * (k + 3) + 3];
+  const double be = sv < 0 ? bp : bm;
+  face = sv < 0 ? k : k + 3;
+  return -be / fabs(sv);
 }
 
 // Walk one pixel's tile list with FP32 box tests (spheres and hulls, and
@@ -352,8 +376,8 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
   const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
   const float eps32 = __double2float_ru(eps);
   float tup = INFINITY, bound = INFINITY;  // upper bound of the nearest hit range; + tie_eps
-  int p1 = -1, p2 = -1;
-  float l1 = INFINITY, l2 = INFINITY;  // candidates' lower bounds
+  int p1 = -1, p2 = -1, x1 = 0, x2 = 0;  // candidates, their box32 axis info (0: full FP64 test)
+  float l1 = INFINITY, l2 = INFINITY;    // candidates' lower bounds
 #pragma unroll 1
   for (int j = 0; j < nl; ++j) {
     const int p = list[j];
@@ -361,16 +385,17 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
     if (tr.x > bound) break;  // sorted by lb: nothing later can be nearer or tie
     const int kind = __float_as_int(tr.y) >> 8;
     float tl, tu;
-    int st = 2;
+    int st = 2, ax = 0;
     if (kind == RS_BOX) {
       float t, e;
-      st = box32(S.box32[p], dx, dy, dz, t, e);
+      st = box32(S.box32[p], dx, dy, dz, t, e, ax);
       if (count) { w.v[0] += 6; w.v[4] += st == 2; }
       if (st == 0) continue;
       if (st == 1) { tl = __fsub_rd(t, e); tu = __fadd_ru(t, e); }
     }
     if (st == 2) {
       int fc;
+      ax = 0;
       const double t = part_hit(S, plane, p, o, d, fc);
       if (count) { w.v[1] += kind == RS_BOX ? 6 : (kind == RS_SPHERE ? 1 : S.part[p].nf); w.v[5] += kind == RS_HULL; }
       if (!(t < INFINITY)) continue;
@@ -379,15 +404,24 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
     }
     if (tu < tup) { tup = tu; bound = __fadd_ru(tup, eps32); }
     if (tl > bound) continue;
-    if (l1 > bound) { p1 = p; l1 = tl; }       // slot 1 free or stale
-    else if (l2 > bound) { p2 = p; l2 = tl; }  // slot 2 free or stale
+    if (l1 > bound) { p1 = p; l1 = tl; x1 = ax; }       // slot 1 free or stale
+    else if (l2 > bound) { p2 = p; l2 = tl; x2 = ax; }  // slot 2 free or stale
     else return false;
   }
   // exact resolution: t* = min over candidates; id = lowest body within tie_eps
   int f1 = -1, f2 = -1;
   double t1 = INFINITY, t2 = INFINITY;
-  if (p1 >= 0 && l1 <= bound) t1 = part_hit(S, plane, p1, o, d, f1);
-  if (p2 >= 0 && l2 <= bound) t2 = part_hit(S, plane, p2, o, d, f2);
+  auto resolve = [&](int p, int ax, int &f) {
+    if (ax & 8) {
+      const int f0 = S.part[p].f0;
+      const double t = ray_box_axis(plane + 4 * f0, d, ax, f);
+      f += f0;
+      return t;
+    }
+    return part_hit(S, plane, p, o, d, f);
+  };
+  if (p1 >= 0 && l1 <= bound) t1 = resolve(p1, x1, f1);
+  if (p2 >= 0 && l2 <= bound) t2 = resolve(p2, x2, f2);
   if (count) w.v[2] += (p1 >= 0 && l1 <= bound ? 6 : 0) + (p2 >= 0 && l2 <= bound ? 6 : 0);
   tmin = fmin(t1, t2);
   id = -1; wpart = -1; wface = -1;
