@@ -1201,11 +1201,9 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       const int ka = sc.body_kind[a], ga = sc.body_group[a];
       const double la0 = S.u.bp.lo[a][0], la1 = S.u.bp.lo[a][1], la2 = S.u.bp.lo[a][2];
       const double ha0 = S.u.bp.hi[a][0], ha1 = S.u.bp.hi[a][1], ha2 = S.u.bp.hi[a][2];
-      for (int half = 0; half < 2; ++half) {
-        const int b = half ? b1 : b0;
-        if (half && nb <= 32) break;
-        const double *lb = half ? l1 : l0, *hb = half ? h1 : h0;
-        const int kb = half ? k1 : k0, gb = half ? g1 : g0;
+      // (the two halves are separate inlined calls: selecting between the
+      // register arrays with a runtime index would put them in local memory)
+      auto test = [&](int b, const double (&lb)[3], const double (&hb)[3], int kb, int gb) {
         const bool ov = b > a && b < nb && !(ka == RS_STATIC && kb == RS_STATIC) &&
                         !(ga != RS_NO_GROUP && ga == gb) && la0 <= hb[0] && lb[0] <= ha0 && lb[1] <= ha1 &&
                         la1 <= hb[1] && lb[2] <= ha2 && la2 <= hb[2];
@@ -1215,7 +1213,9 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
           if (idx < kMaxCand) S.cand[idx] = (uint16_t)((a << 8) | b);
         }
         ncand += __popc(m);
-      }
+      };
+      test(b0, l0, h0, k0, g0);
+      if (nb > 32) test(b1, l1, h1, k1, g1);
     }
   }
   if (ncand > kMaxCand) overflow = true;
