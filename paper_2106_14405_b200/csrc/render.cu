@@ -196,19 +196,26 @@ __device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem 
   double v[3] = {o[0] - P.c[0], o[1] - P.c[1], o[2] - P.c[2]}, ol[3], dl[3];
   mattvec(R, v, ol);
   mattvec(R, d, dl);
-  const double inv[3] = {1.0 / dl[0], 1.0 / dl[1], 1.0 / dl[2]};
+  // BVH nodes are tested in FP32 against boxes widened by `slack` (>> the
+  // FP32 rounding of (lo - o) / d for |o| <= ~1e3 m): a superset of the nodes
+  // the exact test would visit; the triangles themselves are tested in FP64,
+  // so the nearest hit is unchanged
+  const float olf[3] = {(float)ol[0], (float)ol[1], (float)ol[2]};
+  const float invf[3] = {1.0f / (float)dl[0], 1.0f / (float)dl[1], 1.0f / (float)dl[2]};
+  const float slack = 1e-4f * (1.0f + fmaxf(fabsf(olf[0]), fmaxf(fabsf(olf[1]), fabsf(olf[2]))));
   double best = tcut;
+  float bestf = tcut < INFINITY ? fmaf(__double2float_ru(tcut), 1e-5f, __double2float_ru(tcut)) + slack : INFINITY;
   face = -1;
   int stack[40], sp = 0;
   int node = sc.part_node_begin[p];
   for (;;) {
     const float *lo = sc.node_lo + 3 * node, *hi = sc.node_hi + 3 * node;
-    double tn = 0.0, tf = best;
+    float tn = 0.0f, tf = bestf;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      double t0 = ((double)lo[a] - ol[a]) * inv[a], t1 = ((double)hi[a] - ol[a]) * inv[a];
-      if (t0 > t1) { double x = t0; t0 = t1; t1 = x; }
-      tn = t0 > tn ? t0 : tn;
+      float t0 = (lo[a] - slack - olf[a]) * invf[a], t1 = (hi[a] + slack - olf[a]) * invf[a];
+      if (t0 > t1) { float x = t0; t0 = t1; t1 = x; }
+      tn = t0 > tn ? t0 : tn;  // NaN (0 * inf) leaves the bound unchanged: conservative
       tf = t1 < tf ? t1 : tf;
     }
     bool visit = tn <= tf;
@@ -232,6 +239,7 @@ __device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem 
         const double tt = sgn * dot3(e2, qv);
         if (tt < 0.0 || tt >= best * adet) continue;
         best = tt / adet;
+        bestf = fmaf(__double2float_ru(best), 1e-5f, __double2float_ru(best)) + slack;
         face = t;
       }
       visit = false;
