@@ -39,7 +39,8 @@ constexpr int kWarpsPerBlock = 2;
 constexpr int kMaxCand = 512;
 constexpr int kMaxAdm = 256;
 constexpr int kMaxContacts = 128;
-constexpr int kMaxPartsPerBody = 8;
+constexpr int kMaxPartsPerBody = 8;  // rs_scene_create rejects more
+static_assert(kMaxPartsPerBody * kMaxPartsPerBody <= 64, "pair_contacts culls all part pairs in one 64-bit mask");
 constexpr int kMaxGroups = 96;
 constexpr int kMaxBlockRows = 32;
 constexpr int kRowD = 44;  // doubles per solver row in global scratch

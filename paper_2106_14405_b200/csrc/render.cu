@@ -463,7 +463,11 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   const double *sd = B.sd + (size_t)env * L.dbl_size;
   const int tid = threadIdx.x, np = sc.np;
 
-  // -- camera pose (robot.py:43-47 mounts; tools_make_robot_json.py:12-19 axes)
+  // -- camera pose (robot.py:43-47 mounts; tools_make_robot_json.py:12-19 axes);
+  //    the arm chain's joint rotations are computed by one thread each first
+  const bool arm_cam = sc.cam_parent[cam] != 0;
+  if (arm_cam && tid < sc.narm) axis_angle_mat(sc.arm_axis + 3 * tid, sd[L.joints + sc.nsj + tid], S.u.R[tid]);
+  if (arm_cam) __syncthreads();
   if (tid == 0) {
     Pose parent, mount;
     if (sc.cam_parent[cam] == 0) {
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       for (int i = 0; i < sc.narm; ++i) {
         off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
         compose(t, off, t);
-        axis_angle_mat(sc.arm_axis + 3 * i, sd[L.joints + sc.nsj + i], rot.R);
+        for (int k = 0; k < 9; ++k) rot.R[k] = S.u.R[i][k];
         compose(t, rot, t);
       }
       Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}};
@@ -590,18 +594,27 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       return s * (1.0 + 1e-9) + 1e-9 * nn;
     };
     const bool front = live && c[2] > -radius(0.0, 0.0, 1.0, 1.0);
-    for (int tile = 0; tile < ntiles; ++tile) {
-      bool in = false;
-      if (front) {
-        const double *T = B.tile_frustum + 8 * tile;  // u0, u1, v0, v1, |(1,u0)|, |(1,u1)|, |(1,v0)|, |(1,v1)|
-        // inward side planes: x - u0 z >= 0, -x + u1 z >= 0, y - v0 z >= 0, -y + v1 z >= 0
-        in = c[0] - T[0] * c[2] >= -radius(1.0, 0.0, -T[0], T[4]) &&
-             -c[0] + T[1] * c[2] >= -radius(-1.0, 0.0, T[1], T[5]) &&
-             c[1] - T[2] * c[2] >= -radius(0.0, 1.0, -T[2], T[6]) &&
-             -c[1] + T[3] * c[2] >= -radius(0.0, -1.0, T[3], T[7]);
+    // B.tile_frustum[tile] = u0, u1, v0, v1, |(1,u0)|, |(1,u1)|, |(1,v0)|, |(1,v1)|; the inward side
+    // planes x - u0 z >= 0, -x + u1 z >= 0 depend on the tile column only, y - v0 z >= 0,
+    // -y + v1 z >= 0 on the row only: test columns and rows once each (ty_n, tx_n <= 8)
+    unsigned rows = 0u;
+    if (front)
+      for (int ty = 0; ty < ty_n; ++ty) {
+        const double *T = B.tile_frustum + 8 * (ty * tx_n);
+        rows |= (unsigned)(c[1] - T[2] * c[2] >= -radius(0.0, 1.0, -T[2], T[6]) &&
+                           -c[1] + T[3] * c[2] >= -radius(0.0, -1.0, T[3], T[7])) << ty;
       }
-      const unsigned m = __ballot_sync(0xffffffffu, in);
-      if (lane == 0) S.mask[tile][warp] = m;
+    for (int tx = 0; tx < tx_n; ++tx) {
+      bool col = false;
+      if (front) {
+        const double *T = B.tile_frustum + 8 * tx;
+        col = c[0] - T[0] * c[2] >= -radius(1.0, 0.0, -T[0], T[4]) &&
+              -c[0] + T[1] * c[2] >= -radius(-1.0, 0.0, T[1], T[5]);
+      }
+      for (int ty = 0; ty < ty_n; ++ty) {
+        const unsigned m = __ballot_sync(0xffffffffu, col && ((rows >> ty) & 1u));
+        if (lane == 0) S.mask[ty * tx_n + tx][warp] = m;
+      }
     }
   } else {
     for (int p = tid - 32 * kMaskWords; p < np; p += blockDim.x - 32 * kMaskWords) {
