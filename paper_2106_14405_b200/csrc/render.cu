@@ -67,7 +67,7 @@ constexpr int kProxyExact = 2;  // every test in FP64 (the parity reference for 
 
 struct RenderSmem {
   PartW part[kMaxParts];
-  float4 box32[kMaxParts][4];  // FP32 box data: (u_k, b0 of +k) k = 0..2, (b0 of -0, -1, -2, 0)
+  float4 box32[kMaxParts][4];  // FP32 box data: (u_k, b0 of +k) k = 0..2, (-b0 of -0, -1, -2, 0)
   float2 trace[kMaxParts];     // (lb rounded down, kind << 8 | body as int bits)
   uint32_t mask[kMaxTiles][kMaskWords];
   union {
@@ -336,19 +336,21 @@ constexpr float kAmin = 1e-3f;
 // when te_k exceeds the other two entering ratios by more than their error
 // bounds -- then the FP64 test picks the same entering plane (ray_box_axis).
 __device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float dz, float &t, float &e, int &ax) {
+  // bx: (u_k, b0 of +k) for k = 0..2, then (-b0 of -0, -1, -2).  With the
+  // signed reciprocal r_k = 1/s_k the slab k is crossed at b+_k r_k and
+  // -b-_k r_k: entering = the smaller, exiting = the larger (no sign selects)
   const float4 A = bx[0], Bv = bx[1], C = bx[2], M = bx[3];
   const float s0 = fmaf(dx, A.x, fmaf(dy, A.y, dz * A.z));
   const float s1 = fmaf(dx, Bv.x, fmaf(dy, Bv.y, dz * Bv.z));
   const float s2 = fmaf(dx, C.x, fmaf(dy, C.y, dz * C.z));
-  const float a0 = fabsf(s0), a1 = fabsf(s1), a2 = fabsf(s2);
-  const float amin = fminf(a0, fminf(a1, a2));
+  const float amin = fminf(fabsf(s0), fminf(fabsf(s1), fabsf(s2)));
   if (amin < kAmin) return 2;
-  const float r0 = __fdividef(1.0f, a0), r1 = __fdividef(1.0f, a1), r2 = __fdividef(1.0f, a2);
-  const float te0 = -(s0 < 0.f ? A.w : M.x) * r0, te1 = -(s1 < 0.f ? Bv.w : M.y) * r1,
-              te2 = -(s2 < 0.f ? C.w : M.z) * r2;
+  const float r0 = __fdividef(1.0f, s0), r1 = __fdividef(1.0f, s1), r2 = __fdividef(1.0f, s2);
+  const float p0 = A.w * r0, q0 = M.x * r0, p1 = Bv.w * r1, q1 = M.y * r1, p2 = C.w * r2, q2 = M.z * r2;
+  const float te0 = fminf(p0, q0), te1 = fminf(p1, q1), te2 = fminf(p2, q2);
   const float te = fmaxf(te0, fmaxf(te1, te2));
-  const float tx = fminf((s0 < 0.f ? M.x : A.w) * r0, fminf((s1 < 0.f ? M.y : Bv.w) * r1, (s2 < 0.f ? M.z : C.w) * r2));
-  const float rmax = fmaxf(r0, fmaxf(r1, r2)), cr = fmaf(kEs, rmax, kRel);
+  const float tx = fminf(fmaxf(p0, q0), fminf(fmaxf(p1, q1), fmaxf(p2, q2)));
+  const float cr = fmaf(kEs, __fdividef(1.0f, amin), kRel);
   e = (fabsf(te) + fabsf(tx)) * cr;
   if (tx < -e || te - tx > e) return 0;
   if (tx <= e || tx - te <= e) return 2;
@@ -556,7 +558,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
         const double *Q = plane + 4 * P.f0;
         for (int k = 0; k < 3; ++k)
           S.box32[p][k] = make_float4((float)Q[4 * k], (float)Q[4 * k + 1], (float)Q[4 * k + 2], (float)Q[4 * k + 3]);
-        S.box32[p][3] = make_float4((float)Q[15], (float)Q[19], (float)Q[23], 0.0f);
+        S.box32[p][3] = make_float4(-(float)Q[15], -(float)Q[19], -(float)Q[23], 0.0f);
       }
   }
   const int W = B.rcfg.width, H = B.rcfg.height;
