@@ -93,6 +93,8 @@ struct WarpSmem {
   uint16_t adm[kMaxAdm];
   int16_t g_a[kMaxGroups], g_b[kMaxGroups], g_first[kMaxGroups], g_n[kMaxGroups];
   int wake_idx[kMaxBodies];  // admission: index of the candidate pair that wakes each body
+  unsigned long long cbits[kMaxBodies];  // overlapping pairs (a, b > a) of the last substep, row a
+  int cbits_valid;
   int ncand, nadm, nc, ng, fault;
   unsigned long long awake_dyn;
   int moved_mask, dragged, n_active, max_active;
@@ -112,6 +114,7 @@ struct Ctx {
   double *W;      // [kMaxBlockRows^2] eigensolver workspace
   double *bcache; // [kMaxBodies][14]: pose key (pos bits, quat bits, valid) + body AABB
   double *pcache; // [kMaxPartsCache][18]: world frame (R, p) + AABB of every part, valid for the key pose
+  double *ccache; // [kMaxBodies + 1]: candidate pair bit matrix of the last substep + valid flag (bit patterns)
   int env, lane;
   const StateLayout *L;
 };
@@ -303,7 +306,7 @@ __device__ void body_aabb(Ctx &c, int b, double *lo, double *hi) {
 // quaternion bits changed (static and sleeping bodies: once), and stay in
 // c.pcache for the narrowphase of the same substep.  The cached values are
 // the ones the computation would produce (same inputs, same code).
-__device__ void body_aabb_cached(Ctx &c, int b, double *lo, double *hi) {
+__device__ bool body_aabb_cached(Ctx &c, int b, double *lo, double *hi) {
   const DevScene &sc = *c.sc;
   const double *pos = POS(c, b), *q = QUAT(c, b);
   double *K = c.bcache + 14 * b;
@@ -313,7 +316,7 @@ __device__ void body_aabb_cached(Ctx &c, int b, double *lo, double *hi) {
   for (int i = 0; i < 4 && hit; ++i) hit = kb[3 + i] == __double_as_longlong(q[i]);
   if (hit) {
     for (int i = 0; i < 3; ++i) { lo[i] = K[8 + i]; hi[i] = K[11 + i]; }
-    return;
+    return false;
   }
   Pose bp, wp;
   body_pose(c, b, bp);
@@ -330,6 +333,7 @@ __device__ void body_aabb_cached(Ctx &c, int b, double *lo, double *hi) {
   for (int i = 0; i < 3; ++i) { K[i] = pos[i]; K[8 + i] = lo[i]; K[11 + i] = hi[i]; }
   for (int i = 0; i < 4; ++i) K[3 + i] = q[i];
   K[7] = 1.0;
+  return true;
 }
 
 // world planes of part p into S->planes[slot] (lanes per facet)
@@ -1172,52 +1176,71 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   __syncwarp();
 
   // ---- broadphase: AABBs (lanes per body) through the pose-keyed cache: only
-  // bodies that moved are recomputed (body_aabb_cached)
-  for (int b = lane; b < nb; b += 32) {
-    double lo[3], hi[3];
-    body_aabb_cached(c, b, lo, hi);
-    if (sc.body_kind[b] == RS_KINEMATIC)
-      for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
-    for (int i = 0; i < 3; ++i) { S.u.bp.lo[b][i] = lo[i]; S.u.bp.hi[b][i] = hi[i]; }
+  // bodies that moved are recomputed (body_aabb_cached); `changed` = those
+  unsigned long long changed = 0ull;
+  for (int b0 = 0; b0 < nb; b0 += 32) {
+    const int b = b0 + lane;
+    bool miss = false;
+    if (b < nb) {
+      double lo[3], hi[3];
+      miss = body_aabb_cached(c, b, lo, hi);
+      if (sc.body_kind[b] == RS_KINEMATIC)
+        for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
+      for (int i = 0; i < 3; ++i) { S.u.bp.lo[b][i] = lo[i]; S.u.bp.hi[b][i] = hi[i]; }
+    }
+    changed |= (unsigned long long)__ballot_sync(0xffffffffu, miss) << b0;
   }
+  if (!S.cbits_valid) changed = nb == 64 ? ~0ull : ((1ull << nb) - 1ull);
   __syncwarp();
-  // ---- overlap candidates in sorted (a, b) order: lane l owns bodies l and l + 32
-  //      (AABB, kind, group in registers); per a one or two ballots compact the
-  //      overlapping b > a in ascending order
+  // ---- overlap candidates (inclusive AABB overlap, not static-static, not
+  //      the same no-collide group) kept as a bit matrix across substeps: a
+  //      pair of unchanged bodies keeps its bit; the rows / columns of the
+  //      changed bodies are re-tested (lanes per partner), then the matrix is
+  //      emitted in sorted (a, b) order -- the reference's SAP order
   int ncand = 0;
   bool overflow = false;
   {
-    double l0[3], h0[3], l1[3], h1[3];
-    int k0 = 0, g0 = 0, k1 = 0, g1 = 0;
-    const int b0 = lane, b1 = lane + 32;
-    if (b0 < nb) {
-      for (int i = 0; i < 3; ++i) { l0[i] = S.u.bp.lo[b0][i]; h0[i] = S.u.bp.hi[b0][i]; }
-      k0 = sc.body_kind[b0]; g0 = sc.body_group[b0];
+    for (int a = lane; a < nb; a += 32) S.cbits[a] = ((changed >> a) & 1ull) ? 0ull : (S.cbits[a] & ~changed);
+    __syncwarp();
+    auto overlap = [&](int a, int b) {  // a < b
+      const int ka = sc.body_kind[a], kb = sc.body_kind[b], ga = sc.body_group[a];
+      return !(ka == RS_STATIC && kb == RS_STATIC) && !(ga != RS_NO_GROUP && ga == sc.body_group[b]) &&
+             S.u.bp.lo[a][0] <= S.u.bp.hi[b][0] && S.u.bp.lo[b][0] <= S.u.bp.hi[a][0] &&
+             S.u.bp.lo[b][1] <= S.u.bp.hi[a][1] && S.u.bp.lo[a][1] <= S.u.bp.hi[b][1] &&
+             S.u.bp.lo[b][2] <= S.u.bp.hi[a][2] && S.u.bp.lo[a][2] <= S.u.bp.hi[b][2];
+    };
+    for (unsigned long long rest = changed; rest; rest &= rest - 1) {
+      const int cb = __ffsll((long long)rest) - 1;
+      unsigned long long row = 0ull;
+      for (int y0 = 0; y0 < nb; y0 += 32) {
+        const int y = y0 + lane;
+        // pairs (cb, y > cb); pairs (y < cb, cb) once: only from an unchanged y
+        bool ov = false;
+        if (y < nb && y != cb && (y > cb || !((changed >> y) & 1ull)))
+          ov = y > cb ? overlap(cb, y) : overlap(y, cb);
+        if (ov && y < cb) S.cbits[y] |= 1ull << cb;  // lane y owns row y
+        row |= (unsigned long long)__ballot_sync(0xffffffffu, ov && y > cb) << y0;
+      }
+      __syncwarp();
+      if (lane == 0) S.cbits[cb] |= row;
+      __syncwarp();
     }
-    if (b1 < nb) {
-      for (int i = 0; i < 3; ++i) { l1[i] = S.u.bp.lo[b1][i]; h1[i] = S.u.bp.hi[b1][i]; }
-      k1 = sc.body_kind[b1]; g1 = sc.body_group[b1];
+    // emit rows in order (lanes per row, prefix sums of the row counts)
+    for (int a0 = 0; a0 < nb; a0 += 32) {
+      const int a = a0 + lane;
+      const unsigned long long row = a < nb ? S.cbits[a] : 0ull;
+      const int cnt = __popcll(row);
+      int incl = cnt;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      int idx = ncand + incl - cnt;
+      for (unsigned long long r = row; r; r &= r - 1, ++idx)
+        if (idx < kMaxCand) S.cand[idx] = (uint16_t)((a << 8) | (__ffsll((long long)r) - 1));
+      ncand += __shfl_sync(0xffffffffu, incl, 31);
     }
-    for (int a = 0; a < nb - 1; ++a) {
-      const int ka = sc.body_kind[a], ga = sc.body_group[a];
-      const double la0 = S.u.bp.lo[a][0], la1 = S.u.bp.lo[a][1], la2 = S.u.bp.lo[a][2];
-      const double ha0 = S.u.bp.hi[a][0], ha1 = S.u.bp.hi[a][1], ha2 = S.u.bp.hi[a][2];
-      // (the two halves are separate inlined calls: selecting between the
-      // register arrays with a runtime index would put them in local memory)
-      auto test = [&](int b, const double (&lb)[3], const double (&hb)[3], int kb, int gb) {
-        const bool ov = b > a && b < nb && !(ka == RS_STATIC && kb == RS_STATIC) &&
-                        !(ga != RS_NO_GROUP && ga == gb) && la0 <= hb[0] && lb[0] <= ha0 && lb[1] <= ha1 &&
-                        la1 <= hb[1] && lb[2] <= ha2 && la2 <= hb[2];
-        const unsigned m = __ballot_sync(0xffffffffu, ov);
-        if (ov) {
-          const int idx = ncand + __popc(m & ((1u << lane) - 1));
-          if (idx < kMaxCand) S.cand[idx] = (uint16_t)((a << 8) | b);
-        }
-        ncand += __popc(m);
-      };
-      test(b0, l0, h0, k0, g0);
-      if (nb > 32) test(b1, l1, h1, k1, g1);
-    }
+    if (lane == 0) S.cbits_valid = 1;
   }
   if (ncand > kMaxCand) overflow = true;
   __syncwarp();
@@ -1730,7 +1753,8 @@ __device__ void make_ctx(Ctx &c, const DevBatch &B, WarpSmem &S, int env, int la
   c.evc = c.Vc + 2 * kKCap;
   c.bcache = c.evc + 2 * kMaxContacts;
   c.pcache = c.bcache + 14 * kMaxBodies;
-  c.W = c.pcache + 18 * kMaxPartsCache + (size_t)warp * kMaxBlockRows * kMaxBlockRows;
+  c.ccache = c.pcache + 18 * kMaxPartsCache;
+  c.W = c.ccache + kMaxBodies + 1 + (size_t)warp * kMaxBlockRows * kMaxBlockRows;
 }
 
 // stage scene header + state slab, _check_finite (physics.py:596-606), per-step
@@ -1772,6 +1796,16 @@ __device__ bool env_begin(Ctx &c, const DevBatch &B, int env) {
     return false;
   }
   if (lane < kMaxArm) S.budget[lane] = B.cfg.motor_impulse_cap;
+  {  // candidate bit matrix of the last completed step (invalid until env_end stores it again)
+    const unsigned long long *cg = reinterpret_cast<const unsigned long long *>(c.ccache);
+    const bool valid = cg[kMaxBodies] == 1ull;
+    for (int b = lane; b < kMaxBodies; b += 32) S.cbits[b] = valid ? cg[b] : 0ull;
+    __syncwarp();
+    if (lane == 0) {
+      S.cbits_valid = valid;
+      reinterpret_cast<unsigned long long *>(c.ccache)[kMaxBodies] = 0ull;
+    }
+  }
   __syncwarp();
   return true;
 }
@@ -1792,6 +1826,12 @@ __device__ void env_end(Ctx &c, const DevBatch &B, int env, double dt, bool ok, 
     B.step_index[env] += 1;
     B.fault[env] = 0;
     for (int i = 0; i < 3; ++i) B.counters[3 * env + i] += S.ctr[i];
+  }
+  {
+    unsigned long long *cg = reinterpret_cast<unsigned long long *>(c.ccache);
+    for (int b = lane; b < kMaxBodies; b += 32) cg[b] = S.cbits[b];
+    __syncwarp();
+    if (lane == 0) cg[kMaxBodies] = S.cbits_valid ? 1ull : 0ull;
   }
   __syncwarp();
   double *wsd = B.sd_out + (size_t)env * L.dbl_size;
@@ -1891,7 +1931,7 @@ __global__ void __launch_bounds__(32 * kHeavyWarps) step_kernel_cta(DevBatch B, 
 
 __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
   return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + 14 * kMaxBodies +
-         18 * kMaxPartsCache +
+         18 * kMaxPartsCache + kMaxBodies + 1 +
          (size_t)kHeavyWarps * kMaxBlockRows * kMaxBlockRows;
 }
 int step_row_cap() { return kMaxContacts; }
