@@ -36,10 +36,12 @@ int rsim_bench_render_exact(struct rs_batch *batch, unsigned int cam_mask, unsig
  * write-back (negated for envs run by the contact-heavy CTA kernel); NULL
  * turns the probe off. */
 int rsim_bench_env_cycles(struct rs_batch *batch, long long *d_cycles);
-/* Per-env phase clock accumulators (device int64 [n_env][8], added to by
+/* Per-env phase clock accumulators (device int64 [n_env][16], added to by
  * every warp-per-env step; NULL = off): 0 substep front (kinematics, broad-
  * and narrowphase, rows), 1 Gauss-Seidel sweeps, 2 eigensolves, 3 block LCP
- * iterations, 4 block impulse + friction, 5 scalar rows, 6 integrate/joints. */
+ * iterations, 4 block impulse + friction, 5 scalar rows, 6 integrate/joints;
+ * the front split into 7 kinematics, 8 AABBs + overlap, 9 admission,
+ * 10 narrowphase, 11 rows + blocks. */
 int rsim_bench_phase_cycles(struct rs_batch *batch, long long *d_cycles);
 /* same for rs_render_mesh: counts candidate-part BVH traversals */
 int rsim_bench_render_mesh_work(struct rs_batch *batch, unsigned int cam_mask, unsigned long long *d_counter,

@@ -311,9 +311,11 @@ __device__ bool body_aabb_cached(Ctx &c, int b, double *lo, double *hi) {
   const double *pos = POS(c, b), *q = QUAT(c, b);
   double *K = c.bcache + 14 * b;
   const long long *kb = reinterpret_cast<const long long *>(K);
-  bool hit = K[7] == 1.0;
-  for (int i = 0; i < 3 && hit; ++i) hit = kb[i] == __double_as_longlong(pos[i]);
-  for (int i = 0; i < 4 && hit; ++i) hit = kb[3 + i] == __double_as_longlong(q[i]);
+  bool hit = K[7] == 1.0;  // all key words loaded at once (independent loads)
+#pragma unroll
+  for (int i = 0; i < 3; ++i) hit &= kb[i] == __double_as_longlong(pos[i]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) hit &= kb[3 + i] == __double_as_longlong(q[i]);
   if (hit) {
     for (int i = 0; i < 3; ++i) { lo[i] = K[8 + i]; hi[i] = K[11 + i]; }
     return false;
@@ -565,13 +567,16 @@ __device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
 }
 
 // phase clocks (rsim_bench_phase_cycles): 0 front, 1 sweeps, 2 eigensolves,
-// 3 block LCP iterations, 4 block impulse + friction, 5 scalar rows, 6 back
+// 3 block LCP iterations, 4 block impulse + friction, 5 scalar rows, 6 back;
+// front split: 7 kinematics, 8 AABBs + overlap, 9 admission, 10 narrowphase,
+// 11 rows + blocks
+constexpr int kPhases = 16;
 __device__ __forceinline__ long long phase_now(const Ctx &c) { return c.B->phase_cycles ? clock64() : 0; }
 struct PhaseClock {
   long long t0;
   __device__ __forceinline__ explicit PhaseClock(const Ctx &c) { t0 = phase_now(c); }
   __device__ __forceinline__ void add(const Ctx &c, int k) {
-    if (c.B->phase_cycles && c.lane == 0) c.B->phase_cycles[8 * (size_t)c.env + k] += phase_now(c) - t0;
+    if (c.B->phase_cycles && c.lane == 0) c.B->phase_cycles[kPhases * (size_t)c.env + k] += phase_now(c) - t0;
   }
 };
 
@@ -1063,6 +1068,7 @@ __device__ void emit_event(Ctx &c, const double *r, double lam, double force) {
 // physics.py:657-701; returns false on capacity overflow
 // physics.py:657-699 up to the solver set-up (rows, blocks); false on capacity overflow
 __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, double dt, int sub) {
+  PhaseClock pk(c);
   const DevScene &sc = *c.sc;
   const rs_physics_config &cfg = *c.cfg;
   WarpSmem &S = *c.S;
@@ -1175,6 +1181,8 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   }
   __syncwarp();
 
+  pk.add(c, 7);
+  PhaseClock pb(c);
   // ---- broadphase: AABBs (lanes per body) through the pose-keyed cache: only
   // bodies that moved are recomputed (body_aabb_cached); `changed` = those
   unsigned long long changed = 0ull;
@@ -1244,6 +1252,8 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   }
   if (ncand > kMaxCand) overflow = true;
   __syncwarp();
+  pb.add(c, 8);
+  PhaseClock pa(c);
   // ---- admission walk (physics.py:528-571), lanes per candidate.  The walk is
   // sequential in the reference only through wakes: a sleeping dynamic body x
   // paired with a robot/held kinematic body is woken when that pair is
@@ -1317,6 +1327,8 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   __syncwarp();
   if (overflow || S.nadm > kMaxAdm) return false;
 
+  pa.add(c, 9);
+  PhaseClock pn(c);
   // ---- narrowphase (physics.py:703-719)
   if (lane == 0) {
     S.nc = 0;
@@ -1353,6 +1365,8 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   }
   const int nc = S.nc, ng = S.ng;
 
+  pn.add(c, 10);
+  PhaseClock pr(c);
   // ---- solver (physics.py:846-960)
   for (int b = lane; b < nb; b += 32) {
     const double *lv = LV(c, b), *av = AV(c, b);
@@ -1385,12 +1399,13 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     P[PE] = fmax(sc.restitution[a], sc.restitution[b]);
   }
   __syncwarp();
-  // rows (lanes per contact)
-  for (int g = 0; g < ng; ++g) {
-    const int first = S.g_first[g], m = S.g_n[g];
-    const double *P = c.pairs + kPairD * g;
-    for (int i = lane; i < m; i += 32) {
-      const int ci = first + i;
+  // rows (lanes per contact, over all groups at once; the groups partition
+  // the contacts in order: g_first ascending)
+  for (int ci = lane; ci < nc; ci += 32) {
+    {
+      int g = 0;
+      while (g + 1 < ng && S.g_first[g + 1] <= ci) ++g;
+      const double *P = c.pairs + kPairD * g;
       double *r = c.rows + kRowD * ci;
       const double *n = r + RN, *pt = r + RPT;
       r[RA] = S.g_a[g]; r[RB] = S.g_b[g]; r[RGRP] = g;
@@ -1486,6 +1501,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     __syncwarp();
   }
   __syncwarp();
+  pr.add(c, 11);
   return true;
 }
 

@@ -21,6 +21,7 @@ ap.add_argument("--rank", type=int, default=0, help="0 = slowest recorded step")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--env", type=int, default=-1, help="pick this recorded env (with --step) instead of --rank")
 ap.add_argument("--step", type=int, default=-1)
+ap.add_argument("--phase-rep", type=int, default=0, help="rep whose phases are clocked (1+: warm caches)")
 ap.add_argument("--file", default=os.path.join(ROOT, "gpurun_out", "heavy_envs.npz"))
 args = ap.parse_args()
 
@@ -33,9 +34,9 @@ sim = BatchSimulator(layouts=(int(d["layout"][i]),), n_env=args.n, device="cuda"
 act = torch.tensor(np.tile(d["action"][i], (args.n, 1)), device="cuda")
 import ctypes as C  # noqa: E402
 
-ph = torch.zeros((args.n, 8), dtype=torch.int64, device="cuda")
+ph = torch.zeros((args.n, 16), dtype=torch.int64, device="cuda")
 for rep in range(args.reps):
-    sim.L.rsim_bench_phase_cycles(sim._batch, C.c_void_p(ph.data_ptr()) if rep == 0 else None)
+    sim.L.rsim_bench_phase_cycles(sim._batch, C.c_void_p(ph.data_ptr()) if rep == args.phase_rep else None)
     sim.set_state([d["pre"][i].tobytes()] * args.n)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -44,8 +45,9 @@ for rep in range(args.reps):
     e1.record()
     torch.cuda.synchronize()
     print(f"rep {rep}: {e0.elapsed_time(e1):.3f} ms for {args.n} copies")
-names = ["front", "sweeps", "eigen", "lcp(incl eigen)", "impulse+friction", "scalar rows", "back"]
+names = ["front", "sweeps", "eigen", "lcp(incl eigen)", "impulse+friction", "scalar rows", "back",
+         "f:kinematics", "f:aabb+overlap", "f:admission", "f:narrowphase", "f:rows"]
 v = ph.double().mean(0).cpu().numpy() / 1.965e3
-print("phase us (warp kernel, rep 0): " + ", ".join(f"{n} {x:.0f}" for n, x in zip(names, v)))
+print(f"phase us (warp kernel, rep {args.phase_rep}): " + ", ".join(f"{n} {x:.0f}" for n, x in zip(names, v)))
 sim.raise_faults()
 sim.close()
