@@ -569,7 +569,7 @@ __device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
 // phase clocks (rsim_bench_phase_cycles): 0 front, 1 sweeps, 2 eigensolves,
 // 3 block LCP iterations, 4 block impulse + friction, 5 scalar rows, 6 back;
 // front split: 7 kinematics, 8 AABBs + overlap, 9 admission, 10 narrowphase,
-// 11 rows + blocks
+// 11 rows + blocks; 8 split: 12 AABB cache, 13 pair re-tests, 14 candidate emission
 constexpr int kPhases = 16;
 __device__ __forceinline__ long long phase_now(const Ctx &c) { return c.B->phase_cycles ? clock64() : 0; }
 struct PhaseClock {
@@ -1185,6 +1185,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   PhaseClock pb(c);
   // ---- broadphase: AABBs (lanes per body) through the pose-keyed cache: only
   // bodies that moved are recomputed (body_aabb_cached); `changed` = those
+  PhaseClock pb1(c);
   unsigned long long changed = 0ull;
   for (int b0 = 0; b0 < nb; b0 += 32) {
     const int b = b0 + lane;
@@ -1200,6 +1201,8 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   }
   if (!S.cbits_valid) changed = nb == 64 ? ~0ull : ((1ull << nb) - 1ull);
   __syncwarp();
+  pb1.add(c, 12);
+  PhaseClock pb2(c);
   // ---- overlap candidates (inclusive AABB overlap, not static-static, not
   //      the same no-collide group) kept as a bit matrix across substeps: a
   //      pair of unchanged bodies keeps its bit; the rows / columns of the
@@ -1210,29 +1213,44 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   {
     for (int a = lane; a < nb; a += 32) S.cbits[a] = ((changed >> a) & 1ull) ? 0ull : (S.cbits[a] & ~changed);
     __syncwarp();
-    auto overlap = [&](int a, int b) {  // a < b
-      const int ka = sc.body_kind[a], kb = sc.body_kind[b], ga = sc.body_group[a];
-      return !(ka == RS_STATIC && kb == RS_STATIC) && !(ga != RS_NO_GROUP && ga == sc.body_group[b]) &&
-             S.u.bp.lo[a][0] <= S.u.bp.hi[b][0] && S.u.bp.lo[b][0] <= S.u.bp.hi[a][0] &&
-             S.u.bp.lo[b][1] <= S.u.bp.hi[a][1] && S.u.bp.lo[a][1] <= S.u.bp.hi[b][1] &&
-             S.u.bp.lo[b][2] <= S.u.bp.hi[a][2] && S.u.bp.lo[a][2] <= S.u.bp.hi[b][2];
-    };
+    // lane l keeps partners y = l and l + 32 (AABB, kind, group) in registers;
+    // the changed body's data is a shared-memory broadcast.  The predicate is
+    // symmetric in (a, b), so the partner order does not matter.
+    double yl0[3], yh0[3], yl1[3], yh1[3];
+    int yk0 = 0, yg0 = 0, yk1 = 0, yg1 = 0;
+    if (changed) {
+      if (lane < nb) {
+        for (int i = 0; i < 3; ++i) { yl0[i] = S.u.bp.lo[lane][i]; yh0[i] = S.u.bp.hi[lane][i]; }
+        yk0 = sc.body_kind[lane]; yg0 = sc.body_group[lane];
+      }
+      if (lane + 32 < nb) {
+        for (int i = 0; i < 3; ++i) { yl1[i] = S.u.bp.lo[lane + 32][i]; yh1[i] = S.u.bp.hi[lane + 32][i]; }
+        yk1 = sc.body_kind[lane + 32]; yg1 = sc.body_group[lane + 32];
+      }
+    }
     for (unsigned long long rest = changed; rest; rest &= rest - 1) {
       const int cb = __ffsll((long long)rest) - 1;
-      unsigned long long row = 0ull;
-      for (int y0 = 0; y0 < nb; y0 += 32) {
-        const int y = y0 + lane;
+      const int kc = sc.body_kind[cb], gc = sc.body_group[cb];
+      const double cl0 = S.u.bp.lo[cb][0], cl1 = S.u.bp.lo[cb][1], cl2 = S.u.bp.lo[cb][2];
+      const double ch0 = S.u.bp.hi[cb][0], ch1 = S.u.bp.hi[cb][1], ch2 = S.u.bp.hi[cb][2];
+      auto test = [&](int y, const double (&l)[3], const double (&h)[3], int ky, int gy) {
         // pairs (cb, y > cb); pairs (y < cb, cb) once: only from an unchanged y
-        bool ov = false;
-        if (y < nb && y != cb && (y > cb || !((changed >> y) & 1ull)))
-          ov = y > cb ? overlap(cb, y) : overlap(y, cb);
-        if (ov && y < cb) S.cbits[y] |= 1ull << cb;  // lane y owns row y
-        row |= (unsigned long long)__ballot_sync(0xffffffffu, ov && y > cb) << y0;
-      }
+        if (y >= nb || y == cb || (y < cb && ((changed >> y) & 1ull))) return false;
+        return !(kc == RS_STATIC && ky == RS_STATIC) && !(gc != RS_NO_GROUP && gc == gy) && cl0 <= h[0] &&
+               l[0] <= ch0 && l[1] <= ch1 && cl1 <= h[1] && l[2] <= ch2 && cl2 <= h[2];
+      };
+      const bool ov0 = test(lane, yl0, yh0, yk0, yg0);
+      const bool ov1 = nb > 32 && test(lane + 32, yl1, yh1, yk1, yg1);
+      if (ov0 && lane < cb) S.cbits[lane] |= 1ull << cb;  // lane y owns row y
+      if (ov1 && lane + 32 < cb) S.cbits[lane + 32] |= 1ull << cb;
+      const unsigned long long row = (unsigned long long)__ballot_sync(0xffffffffu, ov0 && lane > cb) |
+                                     ((unsigned long long)__ballot_sync(0xffffffffu, ov1 && lane + 32 > cb) << 32);
       __syncwarp();
       if (lane == 0) S.cbits[cb] |= row;
       __syncwarp();
     }
+    pb2.add(c, 13);
+    PhaseClock pb3(c);
     // emit rows in order (lanes per row, prefix sums of the row counts)
     for (int a0 = 0; a0 < nb; a0 += 32) {
       const int a = a0 + lane;
@@ -1249,6 +1267,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       ncand += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) S.cbits_valid = 1;
+    pb3.add(c, 14);
   }
   if (ncand > kMaxCand) overflow = true;
   __syncwarp();

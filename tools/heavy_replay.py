@@ -46,7 +46,8 @@ for rep in range(args.reps):
     torch.cuda.synchronize()
     print(f"rep {rep}: {e0.elapsed_time(e1):.3f} ms for {args.n} copies")
 names = ["front", "sweeps", "eigen", "lcp(incl eigen)", "impulse+friction", "scalar rows", "back",
-         "f:kinematics", "f:aabb+overlap", "f:admission", "f:narrowphase", "f:rows"]
+         "f:kinematics", "f:aabb+overlap", "f:admission", "f:narrowphase", "f:rows", "b:aabb", "b:retest",
+         "b:emit"]
 v = ph.double().mean(0).cpu().numpy() / 1.965e3
 print(f"phase us (warp kernel, rep {args.phase_rep}): " + ", ".join(f"{n} {x:.0f}" for n, x in zip(names, v)))
 sim.raise_faults()
