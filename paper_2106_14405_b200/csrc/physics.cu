@@ -502,6 +502,66 @@ __device__ int sphere_sphere(Ctx &c, int pa, const Pose &wa, int pb, const Pose 
   return 1;
 }
 
+// geometry.py:667-698 convex_contacts for one part pair: i's vertices against
+// j's planes, then j's against i's planes (normals negated).  Both plane sets
+// are built in one pass (lanes per facet) and, when both vertex sets fit the
+// warp together, both vertex passes run in one round (lanes 0..nvi-1: i's
+// vertices, then j's) -- one ballot keeps the reference's contact order.
+__device__ int convex_pair_contacts(Ctx &c, int i, const Pose &wa, int j, const Pose &wb, double margin, int base) {
+  const DevScene &sc = *c.sc;
+  const int fi0 = sc.part_facet_begin[i], nfi = sc.part_facet_begin[i + 1] - fi0;
+  const int fj0 = sc.part_facet_begin[j], nfj = sc.part_facet_begin[j + 1] - fj0;
+  for (int e = c.lane; e < nfj + nfi; e += 32) {  // slot 0: j's planes, slot 1: i's planes (planes_world)
+    const bool bj = e < nfj;
+    const int f = bj ? e : e - nfj;
+    const Pose &wp = bj ? wb : wa;
+    const double *F = sc.facet + 4 * ((bj ? fj0 : fi0) + f);
+    double *o = c.S->u.np.planes[bj ? 0 : 1] + 4 * f;
+    double nrm[3];
+    matvec(wp.R, F, nrm);
+    o[0] = nrm[0]; o[1] = nrm[1]; o[2] = nrm[2];
+    o[3] = F[3] + dot3(nrm, wp.p);
+  }
+  __syncwarp();
+  const int vi0 = sc.part_vert_begin[i], nvi = sc.part_vert_begin[i + 1] - vi0;
+  const int vj0 = sc.part_vert_begin[j], nvj = sc.part_vert_begin[j + 1] - vj0;
+  int n = 0;
+  if (nvi + nvj <= 32) {
+    const int v = c.lane;
+    bool inside = false, neg_n = false;
+    double x[3], best = 0.0;
+    const double *pl = nullptr;
+    int face = 0;
+    if (v < nvi + nvj) {  // vertices_vs_planes for either side
+      const bool si = v < nvi;
+      neg_n = !si;
+      pl = c.S->u.np.planes[si ? 0 : 1];
+      const int nf = si ? nfj : nfi;
+      apply(si ? wa : wb, sc.vert + 3 * (si ? vi0 + v : vj0 + v - nvi), x);
+      int neg = 0;
+      for (int f = 0; f < nf; ++f) {
+        const double *P = pl + 4 * f;
+        double s = P[3] - (x[0] * P[0] + x[1] * P[1] + x[2] * P[2]);
+        if (f == 0 || s < best) { best = s; face = f; }
+        neg += (s < 0.0);
+      }
+      inside = neg == 0 || (neg == 1 && best >= -margin);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, inside);
+    if (inside) {
+      double nn[3];
+      for (int k = 0; k < 3; ++k) nn[k] = neg_n ? -pl[4 * face + k] : pl[4 * face + k];
+      add_contact(c, base + __popc(m & ((1u << c.lane) - 1)), x, nn, best);
+    }
+    n = __popc(m);
+  } else {
+    n += vertices_vs_planes(c, i, wa, j, 0, false, margin, base + n);
+    n += vertices_vs_planes(c, j, wb, i, 1, true, margin, base + n);
+  }
+  __syncwarp();
+  return n;
+}
+
 // geometry.py:701-716: contacts of body pair (a, b), appended at S->nc. warp-collective.
 // The world frame and AABB of every part of a and b are computed once per
 // pair (lanes per part) into shared memory; the part-pair loop then culls
@@ -554,12 +614,7 @@ __device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
         n += __shfl_sync(0xffffffffu, r, 0);
         __syncwarp();
       } else {
-        planes_world(c, j, wb, 0);
-        planes_world(c, i, wa, 1);
-        __syncwarp();
-        n += vertices_vs_planes(c, i, wa, j, 0, false, margin, base + n);
-        n += vertices_vs_planes(c, j, wb, i, 1, true, margin, base + n);
-        __syncwarp();
+        n += convex_pair_contacts(c, i, wa, j, wb, margin, base + n);
       }
     }
   }
