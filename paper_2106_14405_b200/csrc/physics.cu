@@ -1496,16 +1496,18 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       r[RJA] = ja; r[RJB] = jb; r[RJIA] = jia; r[RJIB] = jib;
       if (ja >= 0) { double jn = dot3(r + RJACA, n); kk += jn * jn * jia; }
       if (jb >= 0) { double jn = dot3(r + RJACB, n); kk += jn * jn * jib; }
-      // tangents physics.py:1329-1336
-      double ref[3] = {0.0, 0.0, 0.0};
-      if (fabs(n[0]) < 0.9) ref[0] = 1.0; else ref[1] = 1.0;
-      double *t1 = r + RT1, *t2 = r + RT2;
-      cross3(n, ref, t1);
-      double l = sqrt(dot3(t1, t1));
-      for (int k = 0; k < 3; ++k) t1[k] /= l;
-      cross3(n, t1, t2);
-      l = sqrt(dot3(t2, t2));
-      for (int k = 0; k < 3; ++k) t2[k] /= l;
+      // tangents physics.py:1329-1336 (read only by friction, which skips k <= 0 rows)
+      if (kk > 0.0) {
+        double ref[3] = {0.0, 0.0, 0.0};
+        if (fabs(n[0]) < 0.9) ref[0] = 1.0; else ref[1] = 1.0;
+        double *t1 = r + RT1, *t2 = r + RT2;
+        cross3(n, ref, t1);
+        double l = sqrt(dot3(t1, t1));
+        for (int k = 0; k < 3; ++k) t1[k] /= l;
+        cross3(n, t1, t2);
+        l = sqrt(dot3(t2, t2));
+        for (int k = 0; k < 3; ++k) t2[k] /= l;
+      }
       r[RK] = kk; r[RMU] = P[PMU]; r[RIMA] = P[PIMA]; r[RIMB] = P[PIMB];
       r[RLAM] = r[RLT1] = r[RLT2] = 0.0;
       double vn = row_vn(c, r);
