@@ -1487,9 +1487,10 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
         r[RRA + k] = pt[k] - P[PCA + k];
         r[RRB + k] = pt[k] - P[PCB + k];
       }
+      // (a side with zero inverse mass has a zero inverse inertia: its term is +0)
       double kk = P[PIMA] + P[PIMB], t[3], u[3], v[3];
-      cross3(r + RRA, n, t); matvec(P + PIA, t, u); cross3(u, r + RRA, v); kk += dot3(n, v);
-      cross3(r + RRB, n, t); matvec(P + PIB, t, u); cross3(u, r + RRB, v); kk += dot3(n, v);
+      if (P[PIMA] > 0.0) { cross3(r + RRA, n, t); matvec(P + PIA, t, u); cross3(u, r + RRA, v); kk += dot3(n, v); }
+      if (P[PIMB] > 0.0) { cross3(r + RRB, n, t); matvec(P + PIB, t, u); cross3(u, r + RRB, v); kk += dot3(n, v); }
       double jia = 0.0, jib = 0.0;
       int ja = joint_jacobian(c, S.g_a[g], pt, r + RJACA, jia);
       int jb = joint_jacobian(c, S.g_b[g], pt, r + RJACB, jib);
