@@ -55,8 +55,9 @@ typedef struct {
 } orc_world;
 
 static void *dup(const void *src, size_t n) {
+  if (n > ((size_t)1 << 32)) return NULL; /* a negative count converted to size_t: reject */
   void *p = malloc(n ? n : 1);
-  if (n) memcpy(p, src, n);
+  if (n && p) memcpy(p, src, n);
   return p;
 }
 
