@@ -19,7 +19,12 @@ sequential execution produce bit-identical states and observations
 
 Rewards/tasks are outside this hot path: ``reward`` is
 0 and ``done`` marks the horizon or a physics fault; ``info`` carries the
-per-env accumulated contact force, fault word and event count.
+per-env fault word and event count.  With ``set_nav_goals`` the geodesic
+navigation terms the skill rewards are built from (Navigate
+"20 Delta_agent^goal") are computed on the device every step:
+``info["geodesic"]`` = NavGrid.geodesic_distance(robot base, goal)
+(navgrid.py:145-148) of s_{t+1} and ``info["geodesic_delta"]`` = its
+decrease since s_t.
 """
 
 from __future__ import annotations
@@ -52,16 +57,29 @@ class BatchEnv:
         self._phys_done = torch.cuda.Event()
         self._render_done = torch.cuda.Event()
         self._stats = torch.empty((n_env, 4), dtype=torch.float64, device=self.device)
+        self._nav_fields = None
+        self._geo = None
 
     def close(self):
         self.sim.close()
 
     # -------------------------------------------------------------------- API
+    def set_nav_goals(self, goals_xy):
+        """Per-env navigation goals [n_env, 2] (m): one geodesic distance field
+        per env on its layout's walk grid (rs_nav_fields, NavGrid.distance_field)."""
+        lay = [self.sim.layouts[i] for i in self.sim.env_scene]
+        self._nav_fields, _ = self.sim.distance_fields(goals_xy, layouts=lay)
+        self._nav_idx = torch.arange(self.n_env, dtype=torch.int32, device=self.device)
+        self._geo = self.sim.geodesic_distance(self._nav_fields, self._nav_idx)
+        return self._geo.clone()
+
     def reset(self, snapshots, env_ids=None):
         """Load episode start states (reference snapshot bytes) and return o_0."""
         torch.cuda.current_stream(self.device).wait_stream(self._render_stream)
         self.sim.set_state(snapshots, env_ids)
         self.t = 0
+        if self._nav_fields is not None:
+            self._geo = self.sim.geodesic_distance(self._nav_fields, self._nav_idx)
         obs = self._obs[self._k]
         self.sim.render(self.cams, out=obs)
         return {"rgba": obs[0], "depth": obs[1], "ids": obs[2], "rendered_from_step": 0}
@@ -102,6 +120,11 @@ class BatchEnv:
             done = torch.ones_like(done)
         reward = torch.zeros(self.n_env, dtype=torch.float32, device=self.device)
         info = {"fault": fault, "event_count": self.sim.event_counts(), "step_index": self.t}
+        if self._nav_fields is not None:  # geodesic terms of s_{t+1} from every robot base
+            geo = self.sim.geodesic_distance(self._nav_fields, self._nav_idx)
+            info["geodesic"] = geo
+            info["geodesic_delta"] = self._geo - geo
+            self._geo = geo
         return {"rgba": obs[0], "depth": obs[1], "ids": obs[2], "rendered_from_step": rendered}, reward, done, info
 
     def states(self) -> list[bytes]:

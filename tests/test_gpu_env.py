@@ -66,3 +66,36 @@ def test_delay_semantics():
     assert s1 == s0
     for k in range(5):
         assert torch.equal(f1[k + 2], f0[k + 1])
+
+
+def test_geodesic_navigation_terms_vs_oracle():
+    """BatchEnv.set_nav_goals: per-step geodesic distance from every robot
+    base (rs_nav_geodesic over rs_nav_fields) equals the oracle's Dijkstra
+    field at the base's nearest walkable cell, and geodesic_delta is its
+    decrease."""
+    from oracle.oracle import Oracle
+    from paper_2106_14405_b200.compiler import compile_world
+    from paper_2106_14405_b200.env import BatchEnv
+    from paper_2106_14405_b200.scene import build_world, flat_clutter
+    from paper_2106_14405_b200.state import WorldState
+
+    n, steps = 12, 3
+    snaps, layouts = _episode(n)
+    env = BatchEnv(n, layouts=(0, 1, 2), env_layout=layouts)
+    env.reset(snaps)
+    goals = np.random.default_rng(2).uniform([-4.0, -2.5], [4.0, 2.5], (n, 2))
+    g0 = env.set_nav_goals(goals).cpu().numpy()
+    orcs = {v: Oracle(compile_world(build_world(v, flat_clutter()))) for v in range(3)}
+    fields = [orcs[layouts[e]].nav_field(goals[e]) for e in range(n)]
+    arm, base = _actions(n, steps)
+    prev = g0
+    for k in range(steps):
+        _, _, _, info = env.step(arm[k], base[k])
+        torch.cuda.synchronize()
+        geo = info["geodesic"].cpu().numpy()
+        for e, blob in enumerate(env.sim.get_state()):
+            st = WorldState.from_bytes(blob)
+            assert geo[e] == orcs[layouts[e]].nav_geodesic(fields[e], st.base[:2])
+        np.testing.assert_array_equal(info["geodesic_delta"].cpu().numpy(), prev - geo)
+        prev = geo
+    env.close()
