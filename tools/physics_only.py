@@ -64,6 +64,18 @@ def run(name, states, actions, sim, dev):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / STEPS
+    phases = None
+    if os.environ.get("PHASES"):  # per-env phase clocks of one more step (rsim_bench_phase_cycles)
+        ph = torch.zeros((E, 16), dtype=torch.int64, device=dev)
+        sim.L.rsim_bench_phase_cycles(sim._batch, C.c_void_p(ph.data_ptr()))
+        sim.env_step(act[WARM + STEPS - 1])
+        torch.cuda.synchronize()
+        sim.L.rsim_bench_phase_cycles(sim._batch, None)
+        names = ["front", "sweeps", "eigen", "lcp", "impulse_friction", "scalar_rows", "back", "kin", "bp", "adm",
+                 "narrow", "rows", "bp_aabb", "bp_retest", "bp_emit"]
+        v = ph.double().cpu().numpy() / 1965.0
+        phases = {n: {"mean_us": float(v[:, i].mean()), "p99_us": float(np.percentile(v[:, i], 99))}
+                  for i, n in enumerate(names)}
     cyc = torch.zeros(E, dtype=torch.int64, device=dev)
     sim.L.rsim_bench_env_cycles(sim._batch, C.c_void_p(cyc.data_ptr()))
     sim.env_step(act[WARM + STEPS])
@@ -78,7 +90,8 @@ def run(name, states, actions, sim, dev):
                       "latency_us": {"p50": float(np.percentile(us, 50)), "p99": float(np.percentile(us, 99)),
                                      "max": float(us.max())},
                       "envs_with_awake_clutter": awake, "articulated_joints_per_env": 4, "dynamic_objects": 20,
-                      "dtype": "f64", "data": "synthetic (settled pool, reference recipe)"}), flush=True)
+                      "dtype": "f64", "data": "synthetic (settled pool, reference recipe)",
+                      **({"phases_warp_kernel": phases} if phases else {})}), flush=True)
 
 
 def main():
