@@ -287,21 +287,8 @@ __device__ void prim_aabb(Ctx &c, int p, const Pose &wp, double *lo, double *hi)
   }
 }
 
-// union of the part AABBs of body b (geometry.py:289-296)
-__device__ void body_aabb(Ctx &c, int b, double *lo, double *hi) {
-  const DevScene &sc = *c.sc;
-  Pose bp, wp;
-  body_pose(c, b, bp);
-  for (int i = 0; i < 3; ++i) { lo[i] = INFINITY; hi[i] = -INFINITY; }
-  for (int p = sc.body_part_begin[b]; p < sc.body_part_begin[b + 1]; ++p) {
-    double l[3], h[3];
-    part_world(c, bp, p, wp);
-    prim_aabb(c, p, wp, l, h);
-    for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], l[i]); hi[i] = fmax(hi[i], h[i]); }
-  }
-}
-
-// body_aabb with a pose-keyed cache in the env's global scratch: the part
+// geometry.py:289-296 parts_aabb (the body AABB = union of its part AABBs)
+// with a pose-keyed cache in the env's global scratch: the part
 // world frames and AABBs of body b are recomputed only when its position or
 // quaternion bits changed (static and sleeping bodies: once), and stay in
 // c.pcache for the narrowphase of the same substep.  The cached values are
