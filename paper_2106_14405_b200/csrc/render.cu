@@ -55,9 +55,12 @@ struct PartW {
 // 0 FP32 box plane tests, 1 FP64 plane tests in the walk (uncertain boxes,
 // hulls, spheres = 1), 2 FP64 plane tests resolving candidates, 3 pixels that
 // fell back to the all-FP64 walk, 4 uncertain boxes, 5 hull tests in the walk,
-// 6 FP64 plane tests of the all-FP64 walk, 7 pixels
+// 6 FP64 plane tests of the all-FP64 walk, 7 pixels, 8 FP32 box tests that
+// missed, 9 FP32 box hits that did not become candidates, 10 list entries
+// visited (incl. the one that ends the walk)
+constexpr int kWorkCounters = 12;
 struct Work {
-  unsigned long long v[8];
+  unsigned long long v[kWorkCounters];
 };
 
 // render variants
@@ -392,6 +395,7 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
   for (int j = 0; j < nl; ++j) {
     const int p = list[j];
     const float2 tr = S.trace[p];
+    if (count) w.v[10] += 1;
     if (tr.x > bound) break;  // sorted by lb: nothing later can be nearer or tie
     const int kind = __float_as_int(tr.y) >> 8;
     float tl, tu;
@@ -399,7 +403,7 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
     if (kind == RS_BOX) {
       float t, e;
       st = box32(S.box32[p], dx, dy, dz, t, e, ax);
-      if (count) { w.v[0] += 6; w.v[4] += st == 2; }
+      if (count) { w.v[0] += 6; w.v[4] += st == 2; w.v[8] += st == 0; }
       if (st == 0) continue;
       if (st == 1) { tl = __fsub_rd(t, e); tu = __fadd_ru(t, e); }
     }
@@ -413,7 +417,10 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
       tu = __double2float_ru(t);
     }
     if (tu < tup) { tup = tu; bound = __fadd_ru(tup, eps32); }
-    if (tl > bound) continue;
+    if (tl > bound) {
+      if (count) w.v[9] += 1;
+      continue;
+    }
     if (l1 > bound) { p1 = p; l1 = tl; x1 = ax; }       // slot 1 free or stale
     else if (l2 > bound) { p2 = p; l2 = tl; x2 = ax; }  // slot 2 free or stale
     else return false;
@@ -651,7 +658,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   Work wk;
   constexpr bool count = kCount;
   if (count)
-    for (int i = 0; i < 8; ++i) wk.v[i] = 0;
+    for (int i = 0; i < kWorkCounters; ++i) wk.v[i] = 0;
 #pragma unroll 1
   for (int tile = warp; tile < ntiles; tile += nwarps) {
     const uint8_t *list = S.u.list[tile];
@@ -714,7 +721,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     }
   }
   if (count)
-    for (int i = 0; i < 8; ++i) atomicAdd(work + i, wk.v[i]);
+    for (int i = 0; i < kWorkCounters; ++i) atomicAdd(work + i, wk.v[i]);
 }
 
 // Per-batch constant tables: unit camera-frame ray per pixel centre

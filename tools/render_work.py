@@ -16,13 +16,14 @@ E = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 gids = shard_env_ids(0, 1, E)
 sim = BatchSimulator(layouts=(0, 1, 2), n_env=E, env_layout=layout_of(gids).tolist())
 sim.set_state(bench.idle_states(gids, bench.settled_pool()))
-w = torch.zeros(8, dtype=torch.int64, device="cuda")
+w = torch.zeros(12, dtype=torch.int64, device="cuda")
 sim.L.rsim_bench_render_work_detail(sim._batch, 3, C.c_void_p(w.data_ptr()), None)
 torch.cuda.synchronize()
 v = w.cpu().numpy().astype(float)
 px = v[7]
 names = ["fp32 box plane tests", "fp64 plane tests in walk", "fp64 resolve plane tests", "fallback pixels",
-         "uncertain boxes", "hull tests in walk", "fp64 plane tests (all-FP64 walk)", "pixels"]
+         "uncertain boxes", "hull tests in walk", "fp64 plane tests (all-FP64 walk)", "pixels", "fp32 box misses",
+         "hits not candidates", "list entries visited", "reserved"]
 for n, x in zip(names, v):
     print(f"{n:36s} {x:14.0f}  per pixel {x / px:8.4f}")
 sim.close()
