@@ -95,52 +95,102 @@ def action_table(n_env, n_steps, seed):
 # ------------------------------------------------------------------- clocks
 
 class ClockSampler:
+    """SM clocks, max clocks, clock-event (throttle) reasons and power sampled
+    DURING the timed region: NVML in a background thread every 2 ms (plus one
+    sample at entry and one at exit, so even a 50 ms region has samples);
+    nvidia-smi as the fallback when NVML is unavailable."""
     QUERY = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw"
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+             0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x100: "display_clock_setting"}
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.rows = []
+        self.nvml = None
+        self.source = "none"
+
+    def _nvml_sample(self):
+        import pynvml as N
+
+        h = self.handle
+        try:
+            reasons = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except (AttributeError, N.NVMLError):
+            reasons = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                          float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)), int(reasons),
+                          N.nvmlDeviceGetPowerUsage(h) / 1000.0))
 
     def __enter__(self):
+        import threading
+
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.handle = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = N
+            self.source = "nvml"
+            self._stop = threading.Event()
+            self._nvml_sample()
+
+            def loop():
+                while not self._stop.wait(0.002):
+                    try:
+                        self._nvml_sample()
+                    except Exception:  # noqa: BLE001 - sampling must never break the bench
+                        break
+
+            self._thread = threading.Thread(target=loop, daemon=True)
+            self._thread.start()
+            return self
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi"
         except OSError:
             self.proc = None
         return self
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self._stop.set()
+            self._thread.join(timeout=1.0)
+            try:
+                self._nvml_sample()
+            except Exception:  # noqa: BLE001
+                pass
+            return False
         if self.proc:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                out, _ = self.proc.communicate(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                self.out = ""
+                out = ""
+            for line in (out or "").strip().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                try:
+                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16), float(parts[3])))
+                except (ValueError, IndexError):
+                    continue
         return False
 
     def summary(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        for line in (self.out or "").strip().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            try:
-                rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16), float(parts[3])))
-            except (ValueError, IndexError):
-                continue
+        rows = self.rows
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
-                 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-                 0x100: "display_clock_setting"}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "source": self.source}
         mask = 0
         for r in rows:
             mask |= r[2]
         return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": [n for b, n in names.items() if mask & b], "samples": len(rows),
-                "power_w_max": max(r[3] for r in rows)}
+                "reasons": [n for b, n in self.NAMES.items() if mask & b], "samples": len(rows),
+                "power_w_max": max(r[3] for r in rows), "source": self.source}
 
 
 # --------------------------------------------------------------- CPU oracle
