@@ -342,7 +342,7 @@ def run_b200(args):
 
     hp = torch.cuda.Stream(dev, priority=-1)  # physics ahead of queued render CTAs
 
-    def step(k, ev=None):
+    def step(k, ev=None, cams=("head", "arm"), out=None):
         # one env step, paper pipeline (SPEC StepConfig defaults
         # observation_delay=1, interleave=true): physics s_t -> s_{t+1} on a
         # high-priority stream, render(s_t) concurrently on a side stream, join.
@@ -351,7 +351,7 @@ def run_b200(args):
         with torch.cuda.stream(side):  # enqueued first: it reads s_t before env_step flips the state buffers
             if ev is not None:
                 ev[2].record(side)
-            sim.render(("head", "arm"), out=obs)
+            sim.render(cams, out=obs if out is None else out)
             if ev is not None:
                 ev[3].record(side)
         with torch.cuda.stream(hp):
@@ -386,6 +386,22 @@ def run_b200(args):
     ms_phys = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     ms_rend = float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))
     sim.raise_faults()
+
+    # ---- the same trajectory with one camera (head): BASELINE.md asks for the
+    # headline with 2 cameras and also with 1
+    obs1 = sim.alloc_obs(("head",))
+    sim.set_state(init_states)
+    for k in range(args.warmup):
+        step(k, cams=("head",), out=obs1)
+    torch.cuda.synchronize(dev)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for k in range(args.steps):
+        step(args.warmup + k, cams=("head",), out=obs1)
+    c1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_one_cam = c0.elapsed_time(c1)
+    del obs1
 
     # ---- end-to-end through the C-ABI with host buffers (e2e): replay the
     # same trajectory (same initial states, same actions) as the timed region
@@ -438,10 +454,10 @@ def run_b200(args):
     # ---- across ranks: max time, summed stats (the only collectives)
     stats, tms = reduce_window({"acc": acc, "envs": float(E)},
                                {"total": ms_total, "e2e": ms_e2e, "phys": ms_phys, "rend": ms_rend,
-                                "phys_iso": ms_phys_iso, "rend_iso": ms_rend_iso},
+                                "phys_iso": ms_phys_iso, "rend_iso": ms_rend_iso, "one_cam": ms_one_cam},
                                device=dev if backend == "nccl" else "cpu")
     ms_total, ms_e2e, ms_phys, ms_rend = tms["total"], tms["e2e"], tms["phys"], tms["rend"]
-    ms_phys_iso, ms_rend_iso = tms["phys_iso"], tms["rend_iso"]
+    ms_phys_iso, ms_rend_iso, ms_one_cam = tms["phys_iso"], tms["rend_iso"], tms["one_cam"]
     total_envs = E * world
     value = total_envs * args.steps / (ms_total * 1e-3)
     e2e_value = total_envs * args.steps / (ms_e2e * 1e-3)
@@ -523,6 +539,9 @@ def run_b200(args):
                                 "algorithmic_flop_per_unit": phys_flop},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(E * 6 * 8),
                     "d2h_bytes_per_step": int(E * 4 * 8)},
+            "one_camera": {"value": total_envs * args.steps / (ms_one_cam * 1e-3), "unit": UNIT,
+                           "ms_per_step": ms_one_cam / args.steps,
+                           "note": "same trajectory, head camera only (PAPER.md:97 '1 RGBD observation')"},
             "gpu_launches": 6 * args.steps,  # ik_first, ik_fallback, step, step_cta, grasp, render per env step
             "clocks": clk.summary(),
             "episode_stats_allreduce": {"accumulated_contact_force_sum": stats["acc"], "envs": int(stats["envs"])},
