@@ -220,6 +220,14 @@ int rs_scene_set_mesh(rs_scene *scene, const rs_mesh_desc *mesh);
  * rs_render; a camera inside a closed mesh sees its exit faces). */
 int rs_render_mesh(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream);
 
+/* Simulator.sphere_cast (physics.py:1088-1101) for n_queries rays: query q
+ * in env env_of_query[q] (NULL: env q), unit direction dirs[q], hits farther
+ * than max_dist[q] ignored.  out_body[q] = nearest body (lowest id on ties),
+ * -1 for no hit, -2 when the direction is not unit length (the reference's
+ * PhysicsFault); out_t[q] its range.  Device pointers, stream-ordered. */
+int rs_sphere_cast(rs_batch *batch, const int32_t *env_of_query, const double *origins, const double *dirs,
+                   const double *max_dist, int32_t n_queries, int32_t *out_body, double *out_t, void *stream);
+
 /* ---- batched settle (Simulator.settle physics.py:1113-1176)
  * for fast resets.  The caller writes each settling env's spawn state with
  * rs_set_state (placements applied the way settle does: pose set, awake,

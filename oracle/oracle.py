@@ -71,6 +71,8 @@ def lib():
         L.orc_settle.restype = C.c_int
         L.orc_settle.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p]
+        L.orc_sphere_cast.restype = C.c_int
+        L.orc_sphere_cast.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p]
         L.orc_snapshot_size.restype = C.c_int64
         L.orc_snapshot_size.argtypes = [C.c_int, C.c_int]
         _lib = L
@@ -179,6 +181,16 @@ class Oracle:
         out = np.zeros((cap, 2))
         n = lib().orc_nav_path(self.h, f.ctypes.data, float(from_xy[0]), float(from_xy[1]), out.ctypes.data, cap)
         return out[:n]
+
+    def sphere_cast(self, snapshot: bytes, origin, direction, max_dist: float):
+        """Simulator.sphere_cast: (body, t), None on no hit; ValueError for a non-unit direction."""
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        d = np.ascontiguousarray(direction, dtype=np.float64)
+        t = C.c_double()
+        b = lib().orc_sphere_cast(self.h, bytes(snapshot), o.ctypes.data, d.ctypes.data, max_dist, C.byref(t))
+        if b == -2:
+            raise ValueError("sphere_cast direction must be unit length")
+        return None if b < 0 else (b, t.value)
 
     def parts_distance(self, snapshot: bytes, a: int, b: int) -> float:
         """geometry.parts_distance (GJK over part pairs) of bodies a, b."""

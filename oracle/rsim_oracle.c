@@ -1859,6 +1859,41 @@ void orc_camera_pose(const orc_world *w, const uint8_t *snap, int cam, double *p
   memcpy(pose12_out + 9, cp.p, 24);
 }
 
+/* physics.py:1088-1101 Simulator.sphere_cast: nearest proxy hit along a unit
+ * ray, bodies in id order, t_b = min over parts of the reference ray
+ * primitive, kept if t_b <= max_dist and finite, strict < (lowest id wins
+ * ties).  Returns the body id (-1: none; -2: direction not unit length,
+ * PhysicsFault) and *t_out. */
+int orc_sphere_cast(const orc_world *w, const uint8_t *snap, const double *o, const double *d, double max_dist,
+                    double *t_out) {
+  static ostate st;
+  if (unpack(snap, &st, w->nb, w->nsj + w->narm)) return -3;
+  if (fabs(sqrt(dot3(d, d)) - 1.0) > 1e-6) return -2;
+  int best = -1;
+  double bt = INFINITY;
+  double nw[3 * 64], dw[64];
+  for (int b = 0; b < w->nb; ++b) {
+    pose_t bp, wp;
+    body_pose(&st, b, &bp);
+    double tb = INFINITY;
+    for (int p = w->body_part_begin[b]; p < w->body_part_begin[b + 1]; ++p) {
+      part_world(w, &bp, p, &wp);
+      double t;
+      if (w->part_kind[p] == RS_SPHERE) {
+        t = ray_sphere(wp.p, w->part_param[3 * p], o, d);
+      } else {
+        int f0 = w->part_facet_begin[p], nf = w->part_facet_begin[p + 1] - f0, fe;
+        planes_world(w, p, &wp, nw, dw);
+        t = ray_convex(nw, dw, nf, o, d, &fe);
+      }
+      if (t < tb) tb = t;
+    }
+    if (tb <= max_dist && isfinite(tb) && (best < 0 || tb < bt)) { best = b; bt = tb; }
+  }
+  *t_out = bt;
+  return best;
+}
+
 /* Render restatement (pinned in DESIGN.md §5):
  * ray through pixel centre (u+.5, v+.5), camera frame (right, down, view),
  * normalised then rotated to world; per body t_b = min over parts of the

@@ -26,6 +26,7 @@ UNITS = {
     "peak.cu": [],
     "nav.cu": ["-fmad=false"],
     "settle.cu": ["-fmad=false"],
+    "query.cu": ["-fmad=false"],
 }
 HEADERS = ["device.cuh", "se3.cuh", "navgrid.cuh"]
 

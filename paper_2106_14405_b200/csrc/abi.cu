@@ -22,6 +22,9 @@ cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, f
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_tables(const DevBatch &B, cudaStream_t stream);
+cudaError_t launch_sphere_cast(const DevBatch &B, const int32_t *env_of_query, const double *origins,
+                               const double *dirs, const double *max_dist, int nq, int32_t *out_body, double *out_t,
+                               cudaStream_t stream);
 cudaError_t launch_settle_clearance(const DevBatch &B, const uint64_t *placed, uint8_t *active, int32_t *status,
                                     int32_t *info, double *value, int32_t *steps, cudaStream_t stream);
 cudaError_t launch_settle_check(const DevBatch &B, const uint64_t *placed, uint8_t *active, int32_t *status,
@@ -592,6 +595,17 @@ int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d
   work_total_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(w, d_counter);
   CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   cudaFree(w);
+  return RS_OK;
+}
+
+// ---- point queries (physics.py:1088-1101)
+int rs_sphere_cast(rs_batch *b, const int32_t *env_of_query, const double *origins, const double *dirs,
+                   const double *max_dist, int32_t n_queries, int32_t *out_body, double *out_t, void *stream) {
+  if (!b || !origins || !dirs || !max_dist || !out_body || !out_t || n_queries < 0)
+    return fail(RS_ERR_ARG, "bad sphere_cast arguments");
+  if (!env_of_query && n_queries > b->d.n_env) return fail(RS_ERR_ARG, "env_of_query = NULL needs n_queries <= n_env");
+  CUDA_TRY(launch_sphere_cast(b->view(), env_of_query, origins, dirs, max_dist, n_queries, out_body, out_t,
+                              (cudaStream_t)stream));
   return RS_OK;
 }
 

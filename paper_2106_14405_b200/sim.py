@@ -280,6 +280,21 @@ class BatchSimulator:
                                            _stream_ptr()), "rs_render_mesh")
         return rgba, depth, ids
 
+    # ---------------------------------------- point query (physics.py:1088-1101)
+    def sphere_cast(self, origins, dirs, max_dist, env_ids=None):
+        """Simulator.sphere_cast for Q rays: (body [Q] int32: -1 no hit, -2
+        non-unit direction; t [Q] float64) on the envs ``env_ids`` (default 0..Q-1)."""
+        n = len(origins)
+        o = self._dev(origins, (n, 3), torch.float64)
+        d = self._dev(dirs, (n, 3), torch.float64)
+        md = self._dev(np.broadcast_to(np.asarray(max_dist, dtype=np.float64), (n,)).copy(), (n,), torch.float64)
+        ev = None if env_ids is None else self._dev(env_ids, (n,), torch.int32)
+        body = torch.empty(n, dtype=torch.int32, device=self.device)
+        t = torch.empty(n, dtype=torch.float64, device=self.device)
+        native.check(self.L.rs_sphere_cast(self._batch, _dptr(ev), _dptr(o), _dptr(d), _dptr(md), n, _dptr(body),
+                                           _dptr(t), _stream_ptr()), "rs_sphere_cast")
+        return body, t
+
     # ------------------------------------------ settle (physics.py:1113-1176)
     SETTLED, CLEARANCE, FELL, TIMEOUT, FAULT = range(5)
 

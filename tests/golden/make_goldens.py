@@ -29,6 +29,8 @@ as-is.  Fixtures:
   ``Simulator.settle`` builds, every AABB-overlapping ``parts_distance``
   (GJK, ``geometry.py:486-539``) and the settle outcome (final state + steps
   or the ``SettleUnstable`` reason), ``physics.py:1113-1176``.
+* ``cast.npz``  ``Simulator.sphere_cast`` point queries (physics.py:1088-1101)
+  from random origins / unit directions on settled states.
 * ``nav.npz``  geodesic distance fields (Dijkstra, ``navgrid.py:109-143``),
   geodesic distances and steepest-descent shortest paths
   (``navgrid.py:145-172``) on the layouts' walk grids.
@@ -627,6 +629,34 @@ def gen_settle(seeds=range(8)):
 
 
 # --------------------------------------------------------------------------
+# point queries (physics.py:1088-1101 sphere_cast)
+# --------------------------------------------------------------------------
+
+def gen_cast():
+    """Simulator.sphere_cast from random origins / unit directions on settled
+    states of the three layouts (nearest proxy hit, lowest id on ties)."""
+    rng = np.random.default_rng(17)
+    pool = np.load(os.path.join(OUT, "settled_pool.npz"))
+    out = {k: [] for k in ("state", "layout", "origin", "dir", "max_dist", "body", "t")}
+    for v in range(3):
+        sim, _ = make_sim(v)
+        blobs = [b for b, (lv, _s) in zip(pool["snapshots"], pool["tags"]) if lv == v][:2]
+        for blob in blobs:
+            st = physics.WorldState.from_bytes(blob.tobytes())
+            for k in range(60):
+                o = rng.uniform([-4.5, -2.5, 0.1], [4.5, 2.5, 2.2])
+                d = rng.normal(size=3)
+                d /= np.linalg.norm(d)
+                md = [2.0, 10.0, np.inf][k % 3]
+                hit = sim.sphere_cast(st, o, d, md)
+                out["state"].append(np.frombuffer(blob.tobytes(), np.uint8)); out["layout"].append(v)
+                out["origin"].append(o); out["dir"].append(d); out["max_dist"].append(md)
+                out["body"].append(-1 if hit is None else hit[0]); out["t"].append(np.inf if hit is None else hit[1])
+    np.savez_compressed(os.path.join(OUT, "cast.npz"), meta=meta(), **{k: np.array(v) for k, v in out.items()})
+    print(f"  cast: {len(out['t'])} rays, {int(np.sum(np.array(out['body']) >= 0))} hits")
+
+
+# --------------------------------------------------------------------------
 # geodesics (navgrid.py:109-172)
 # --------------------------------------------------------------------------
 
@@ -667,7 +697,7 @@ def gen_nav():
 
 if __name__ == "__main__":
     t0 = time.time()
-    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav", "settle"]
+    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav", "settle", "cast"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
     blobs = tags = None
@@ -688,3 +718,5 @@ if __name__ == "__main__":
         gen_nav(); print("nav", time.time() - t0)
     if "settle" in what:
         gen_settle(); print("settle", time.time() - t0)
+    if "cast" in what:
+        gen_cast(); print("cast", time.time() - t0)

@@ -80,3 +80,20 @@ def test_random_goals_vs_oracle_and_robot_base_queries():
         base = WorldState.from_bytes(states[e]).base
         assert d[e] == orcs[lay[e]].nav_geodesic(f[e], base[:2])
     s.close()
+
+
+def test_sphere_cast_matches_reference():
+    """rs_sphere_cast vs Simulator.sphere_cast (cast.npz): same body (lowest id
+    on ties), same range; a non-unit direction reports -2 (PhysicsFault)."""
+    k = golden("cast.npz")
+    n = len(k["t"])
+    s = BatchSimulator(layouts=(0, 1, 2), n_env=n, env_layout=k["layout"].tolist())
+    s.set_state([b.tobytes() for b in k["state"]])
+    body, t = s.sphere_cast(k["origin"], k["dir"], k["max_dist"])
+    body, t = body.cpu().numpy(), t.cpu().numpy()
+    np.testing.assert_array_equal(body, k["body"])
+    hit = body >= 0
+    np.testing.assert_array_equal(t[hit], k["t"][hit])
+    bad, _ = s.sphere_cast(k["origin"][:2], k["dir"][:2] * 1.01, [10.0, 10.0])
+    assert (bad.cpu().numpy() == -2).all()
+    s.close()

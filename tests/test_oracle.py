@@ -211,3 +211,15 @@ def test_host_spawn_state_matches_reference():
         np.testing.assert_array_equal(me.rider_joint, ref.rider_joint)
         np.testing.assert_allclose(me.pos, ref.pos, rtol=0, atol=0)
         np.testing.assert_allclose(me.quat, ref.quat, rtol=0, atol=1e-15)
+
+
+def test_sphere_cast_matches_reference():
+    """Simulator.sphere_cast (physics.py:1088-1101) restated: bodies and
+    ranges identical to the reference on 360 random rays."""
+    k = golden("cast.npz")
+    for i in range(len(k["t"])):
+        r = oracle_for(int(k["layout"][i])).sphere_cast(k["state"][i].tobytes(), k["origin"][i], k["dir"][i],
+                                                        k["max_dist"][i])
+        assert (-1 if r is None else r[0]) == k["body"][i]
+        if r is not None:
+            assert r[1] == k["t"][i]
