@@ -86,3 +86,44 @@ def test_hundred_steps_free_running(kind):
     print(f"{kind}: max |GPU - oracle| after {STEPS} steps = {worst:.3e}; robot contact force tally {force}")
     assert worst <= POS_TOL
     sim.close()
+
+
+def test_config1_64_envs_pairs_and_render():
+    """configs[1]: 64 envs (three layouts) stepping physics + RGBD together;
+    every substep's admitted collision-pair list bit-exact vs the oracle, and
+    the head/arm id images bit-exact for a sample of envs."""
+    pool = golden("settled_pool.npz")
+    rng = np.random.default_rng(64)
+    n = 64
+    blobs = [(b.tobytes(), int(v)) for b, (v, _s) in zip(pool["snapshots"], pool["tags"])]
+    states, layouts = [], []
+    for e in range(n):
+        b, v = blobs[e % len(blobs)]
+        st = WorldState.from_bytes(b)
+        st.base = np.array([rng.uniform(1.8, 2.8), rng.uniform(-0.6, 0.2), rng.uniform(-3, 3)])
+        states.append(st.to_bytes())
+        layouts.append(v)
+    sim = BatchSimulator(layouts=(0, 1, 2), n_env=n, env_layout=layouts)
+    sim.set_trace(cap=256)
+    sim.set_state(states)
+    orcs = {v: Oracle(compile_world(build_world(v, flat_clutter()))) for v in range(3)}
+    cur = list(states)
+    for step in range(3):
+        q = np.stack([WorldState.from_bytes(s).joints[-7:] for s in cur])
+        arm = q + rng.uniform(-0.05, 0.05, q.shape)
+        base = np.stack([rng.uniform(-0.5, 1.0, n), rng.uniform(-1, 1, n)], axis=1)
+        rgba, depth, ids = sim.render(("head", "arm"))
+        sim.step_physics(torch.tensor(arm), torch.tensor(base), check=True)
+        torch.cuda.synchronize()
+        got = sim.get_state()
+        ids = ids.cpu().numpy()
+        for e in range(n):
+            r = orcs[layouts[e]].step(cur[e], arm[e], base[e])
+            tr = np.array(sim.trace(e)).reshape(-1, 4)
+            np.testing.assert_array_equal(tr[:, :3], r.pairs, err_msg=f"step {step} env {e}")
+            if e % 16 == step:
+                for cam in (0, 1):
+                    _, _, o_ids, _ = orcs[layouts[e]].render(cur[e], cam)
+                    np.testing.assert_array_equal(ids[e, cam], o_ids, err_msg=f"step {step} env {e} cam {cam}")
+            cur[e] = got[e]
+    sim.close()
