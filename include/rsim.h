@@ -21,6 +21,11 @@
  *   rs_grasp          <- grasp_rule + apply_grasp              robot.py:323-346, physics.py:1039-1079
  *   rs_arm_action     <- apply_arm_action / solve_ik           robot.py:185-313
  *   rs_render_mesh    <- render over AssetDef.visual_mesh      scene.py:63-76
+ *   rs_sphere_cast    <- Simulator.sphere_cast                 physics.py:1088-1101
+ *   rs_settle         <- Simulator.settle (+ spawn clearance)  physics.py:1113-1176
+ *   rs_nav_fields     <- NavGrid.distance_field                navgrid.py:109-143
+ *   rs_nav_geodesic   <- NavGrid.geodesic_distance             navgrid.py:145-148
+ *   rs_nav_path       <- NavGrid.shortest_path                 navgrid.py:150-172
  *
  * Conventions:
  *   - every call is stream-ordered on the cudaStream_t passed as `stream`
