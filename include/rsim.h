@@ -21,6 +21,7 @@
  *   rs_grasp          <- grasp_rule + apply_grasp              robot.py:323-346, physics.py:1039-1079
  *   rs_arm_action     <- apply_arm_action / solve_ik           robot.py:185-313
  *   rs_render_mesh    <- render over AssetDef.visual_mesh      scene.py:63-76
+ *   rs_proprio        <- Observation proprioception fields
  *   rs_sphere_cast    <- Simulator.sphere_cast                 physics.py:1088-1101
  *   rs_settle         <- Simulator.settle (+ spawn clearance)  physics.py:1113-1176
  *   rs_nav_fields     <- NavGrid.distance_field                navgrid.py:109-143
@@ -224,6 +225,17 @@ int rs_scene_set_mesh(rs_scene *scene, const rs_mesh_desc *mesh);
 /* RGBD render against the triangle soups (same outputs and conventions as
  * rs_render; a camera inside a closed mesh sees its exit faces). */
 int rs_render_mesh(rs_batch *batch, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream);
+
+/* Observation proprioception of the current state (PAPER
+ * §5.1): out [n_env][16 + 3 n_goals] = arm joints (7), end-effector position
+ * in the robot frame (3), base egomotion since base_prev [n_env][3] (x, y,
+ * yaw; NULL = zero) in the previous robot frame (dx, dy, 0, 0, 0, dyaw), and
+ * the goal vectors goals [n_env][n_goals][3] (world) in the robot frame;
+ * base_out [n_env][3] (optional) receives the current base for the next call.
+ * Reads the state a render enqueued at the same point would read (s_t of an
+ * interleaved step when enqueued before the step). */
+int rs_proprio(rs_batch *batch, const double *base_prev, const double *goals, int32_t n_goals, double *out,
+               double *base_out, void *stream);
 
 /* Simulator.sphere_cast (physics.py:1088-1101) for n_queries rays: query q
  * in env env_of_query[q] (NULL: env q), unit direction dirs[q], hits farther

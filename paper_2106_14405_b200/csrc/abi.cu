@@ -22,6 +22,8 @@ cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, f
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_tables(const DevBatch &B, cudaStream_t stream);
+cudaError_t launch_proprio(const DevBatch &B, const double *base_prev, const double *goals, int n_goals, double *out,
+                           double *base_out, cudaStream_t stream);
 cudaError_t launch_sphere_cast(const DevBatch &B, const int32_t *env_of_query, const double *origins,
                                const double *dirs, const double *max_dist, int nq, int32_t *out_body, double *out_t,
                                cudaStream_t stream);
@@ -595,6 +597,14 @@ int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d
   work_total_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(w, d_counter);
   CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   cudaFree(w);
+  return RS_OK;
+}
+
+// ---- observation proprioception
+int rs_proprio(rs_batch *b, const double *base_prev, const double *goals, int32_t n_goals, double *out,
+               double *base_out, void *stream) {
+  if (!b || !out || n_goals < 0 || (n_goals > 0 && !goals)) return fail(RS_ERR_ARG, "bad proprioception arguments");
+  CUDA_TRY(launch_proprio(b->view(), base_prev, goals, n_goals, out, base_out, (cudaStream_t)stream));
   return RS_OK;
 }
 

@@ -2191,6 +2191,53 @@ __device__ void ik_link_poses(const DevScene &sc, const double *q, Pose *links, 
   compose(t, g, ee);
 }
 
+// SPEC.md:247-249 Observation proprioception (PAPER §5.1: "arm joint angles
+// (7-dim), end-effector position (3-dim), and base-egomotion (6-dim)") and
+// goal vectors, from the batch's current state; thread per env.  out[e]:
+// [0,7) arm joints, [7,10) EE position in the robot frame (FK from the base,
+// robot.py:161-169), [10,16) base egomotion since base_prev[e] in the previous
+// robot frame (dx, dy, dz = 0, droll = 0, dpitch = 0, dyaw wrapped to
+// [-pi, pi)), [16, 16 + 3 K) goal vectors (world goals in the robot frame).
+__global__ void proprio_kernel(DevBatch B, const double *base_prev, const double *goals, int n_goals, double *out,
+                               double *base_out) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env >= B.n_env) return;
+  const DevScene &sc = B.scenes[B.env_scene[env]];
+  const StateLayout &L = B.L;
+  const double *sd = B.sd + (size_t)env * L.dbl_size;
+  const int stride = 16 + 3 * n_goals;
+  double *o = out + (size_t)env * stride;
+  const double *q = sd + L.joints + sc.nsj, *base = sd + L.base;
+  for (int i = 0; i < 7; ++i) o[i] = i < sc.narm ? q[i] : 0.0;
+  Pose ee;
+  ik_link_poses(sc, q, nullptr, ee);
+  for (int i = 0; i < 3; ++i) o[7 + i] = ee.p[i];
+  for (int i = 0; i < 6; ++i) o[10 + i] = 0.0;
+  if (base_prev) {
+    const double *bp = base_prev + 3 * env, c = cos(bp[2]), s = sin(bp[2]);
+    const double dx = base[0] - bp[0], dy = base[1] - bp[1];
+    o[10] = c * dx + s * dy;
+    o[11] = -s * dx + c * dy;
+    o[15] = py_mod(base[2] - bp[2] + M_PI, 2.0 * M_PI) - M_PI;
+  }
+  const double c = cos(base[2]), s = sin(base[2]);
+  for (int k = 0; k < n_goals; ++k) {
+    const double *g = goals + ((size_t)env * n_goals + k) * 3;
+    const double gx = g[0] - base[0], gy = g[1] - base[1];
+    o[16 + 3 * k] = c * gx + s * gy;
+    o[17 + 3 * k] = -s * gx + c * gy;
+    o[18 + 3 * k] = g[2];
+  }
+  if (base_out)
+    for (int i = 0; i < 3; ++i) base_out[3 * env + i] = base[i];
+}
+
+cudaError_t launch_proprio(const DevBatch &B, const double *base_prev, const double *goals, int n_goals, double *out,
+                           double *base_out, cudaStream_t stream) {
+  proprio_kernel<<<(B.n_env + 127) / 128, 128, 0, stream>>>(B, base_prev, goals, n_goals, out, base_out);
+  return cudaGetLastError();
+}
+
 __device__ void ik_solve3(const double *A_in, double *B, int nrhs) {
   double A[9];
   int piv[3];

@@ -59,11 +59,32 @@ class BatchEnv:
         self._stats = torch.empty((n_env, 4), dtype=torch.float64, device=self.device)
         self._nav_fields = None
         self._geo = None
+        self._goal_pos = None  # [E, K, 3] world goal positions (goal_vectors)
+        self._obs_base = None  # base (x, y, yaw) of the state the last observation was taken from
 
     def close(self):
         self.sim.close()
 
     # -------------------------------------------------------------------- API
+    def set_goal_positions(self, goals):
+        """World goal positions [n_env, K, 3] reported as ``goal_vectors`` in the
+        robot frame."""
+        self._goal_pos = torch.as_tensor(np.asarray(goals) if not isinstance(goals, torch.Tensor) else goals,
+                                         dtype=torch.float64).to(self.device).contiguous()
+
+    def _proprio(self, obs: dict):
+        """Proprioception of the state being rendered (same stream, same point in
+        the order): joints, EE in the robot frame, egomotion since the previous
+        observation, goal vectors (rs_proprio)."""
+        p, base = self.sim.proprioception(base_prev=self._obs_base, goals=self._goal_pos)
+        self._obs_base = base
+        obs["joint_positions"] = p[:, 0:7]
+        obs["ee_position"] = p[:, 7:10]
+        obs["base_egomotion"] = p[:, 10:16]
+        if self._goal_pos is not None:
+            obs["goal_vectors"] = p[:, 16:].reshape(self.n_env, -1, 3)
+        return obs
+
     def set_nav_goals(self, goals_xy):
         """Per-env navigation goals [n_env, 2] (m): one geodesic distance field
         per env on its layout's walk grid (rs_nav_fields, NavGrid.distance_field)."""
@@ -81,8 +102,9 @@ class BatchEnv:
         if self._nav_fields is not None:
             self._geo = self.sim.geodesic_distance(self._nav_fields, self._nav_idx)
         obs = self._obs[self._k]
+        self._obs_base = None
         self.sim.render(self.cams, out=obs)
-        return {"rgba": obs[0], "depth": obs[1], "ids": obs[2], "rendered_from_step": 0}
+        return self._proprio({"rgba": obs[0], "depth": obs[1], "ids": obs[2], "rendered_from_step": 0})
 
     def step(self, arm_targets: torch.Tensor, base_cmd: torch.Tensor, gripper: torch.Tensor | None = None):
         main = torch.cuda.current_stream(self.device)
@@ -94,6 +116,7 @@ class BatchEnv:
                 self._render_stream.wait_stream(main)
                 with torch.cuda.stream(self._render_stream):
                     self.sim.render(self.cams, out=obs)
+                    extra = self._proprio({})
                 self._render_done.record(self._render_stream)
                 self._phys_stream.wait_stream(main)
                 with torch.cuda.stream(self._phys_stream):
@@ -103,13 +126,17 @@ class BatchEnv:
                 main.wait_event(self._render_done)
                 for t in obs:
                     t.record_stream(self._render_stream)
+                for t in extra.values():  # made on the render stream, consumed on the caller's
+                    t.record_stream(main)
             else:
                 self.sim.render(self.cams, out=obs)
+                extra = self._proprio({})
                 self.sim.step_physics(arm_targets, base_cmd)
             rendered = self.t
         else:
             self.sim.step_physics(arm_targets, base_cmd)
             self.sim.render(self.cams, out=obs)
+            extra = self._proprio({})
             rendered = self.t + 1
         if gripper is not None:
             self.sim.grasp(gripper)
@@ -125,7 +152,7 @@ class BatchEnv:
             info["geodesic"] = geo
             info["geodesic_delta"] = self._geo - geo
             self._geo = geo
-        return {"rgba": obs[0], "depth": obs[1], "ids": obs[2], "rendered_from_step": rendered}, reward, done, info
+        return {"rgba": obs[0], "depth": obs[1], "ids": obs[2], "rendered_from_step": rendered, **extra}, reward, done, info
 
     def states(self) -> list[bytes]:
         torch.cuda.current_stream(self.device).wait_stream(self._render_stream)

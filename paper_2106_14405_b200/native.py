@@ -18,7 +18,7 @@ EXPORTS = ("rs_abi_version", "rs_last_error", "rs_snapshot_size", "rs_scene_crea
            "rs_batch_create", "rs_batch_destroy", "rs_batch_buffers", "rs_set_state", "rs_get_state", "rs_step",
            "rs_render", "rs_grasp", "rs_step_host", "rs_set_trace", "rs_scene_set_mesh", "rs_render_mesh", "rs_arm_action", "rs_env_step", "rs_env_step_host",
            "rs_nav_shape", "rs_nav_fields", "rs_nav_geodesic", "rs_nav_path", "rs_settle",
-           "rs_sphere_cast")
+           "rs_sphere_cast", "rs_proprio")
 
 
 class NativeLibraryError(RuntimeError):
@@ -71,6 +71,7 @@ def lib():
     L.rs_env_step_host.argtypes = [vp, vp, dbl, i32, u32, vp, vp, vp, vp, vp]
     L.rs_settle.argtypes = [vp, vp, vp, i32, dbl, vp, vp, vp, vp, vp]
     L.rs_sphere_cast.argtypes = [vp, vp, vp, vp, vp, i32, vp, vp, vp]
+    L.rs_proprio.argtypes = [vp, vp, vp, i32, vp, vp, vp]
     L.rs_nav_shape.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
     L.rs_nav_fields.argtypes = [vp, vp, vp, i32, vp, vp, vp]
     L.rs_nav_geodesic.argtypes = [vp, vp, vp, vp, vp, i32, vp, vp]

@@ -280,6 +280,23 @@ class BatchSimulator:
                                            _stream_ptr()), "rs_render_mesh")
         return rgba, depth, ids
 
+    # ------------------------------------ proprioception
+    def proprioception(self, base_prev=None, goals=None, out=None, base_out=None):
+        """Observation fields of the current state: ``[E, 16 + 3K]`` = arm joints
+        (7), EE position in the robot frame (3), base egomotion since
+        ``base_prev`` [E, 3] (6), goal vectors of ``goals`` [E, K, 3] in the
+        robot frame (3K); and the current base [E, 3]."""
+        k = 0 if goals is None else int(goals.shape[1])
+        g = None if goals is None else self._dev(goals, (self.n_env, k, 3), torch.float64)
+        bp = None if base_prev is None else self._dev(base_prev, (self.n_env, 3), torch.float64)
+        out = out if out is not None else torch.empty((self.n_env, 16 + 3 * k), dtype=torch.float64,
+                                                      device=self.device)
+        base_out = base_out if base_out is not None else torch.empty((self.n_env, 3), dtype=torch.float64,
+                                                                     device=self.device)
+        native.check(self.L.rs_proprio(self._batch, _dptr(bp), _dptr(g), k, _dptr(out), _dptr(base_out),
+                                       _stream_ptr()), "rs_proprio")
+        return out, base_out
+
     # ---------------------------------------- point query (physics.py:1088-1101)
     def sphere_cast(self, origins, dirs, max_dist, env_ids=None):
         """Simulator.sphere_cast for Q rays: (body [Q] int32: -1 no hit, -2

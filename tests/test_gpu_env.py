@@ -99,3 +99,53 @@ def test_geodesic_navigation_terms_vs_oracle():
         np.testing.assert_array_equal(info["geodesic_delta"].cpu().numpy(), prev - geo)
         prev = geo
     env.close()
+
+
+def test_proprioception_fields_match_host_restatement():
+    """Observation fields: joint positions, EE position in
+    the robot frame (robot.py:161-169 FK), base egomotion since the previous
+    observation and goal vectors -- of the state each observation is rendered
+    from (o_t from s_t with the 1-step delay)."""
+    import math
+
+    from paper_2106_14405_b200.env import BatchEnv
+    from paper_2106_14405_b200.scene import build_world, flat_clutter
+    from paper_2106_14405_b200.state import WorldState, link_poses
+
+    n, steps = 9, 4
+    snaps, layouts = _episode(n)
+    env = BatchEnv(n, layouts=(0, 1, 2), env_layout=layouts)
+    goals = np.random.default_rng(5).uniform([-3, -2, 0.3], [3, 2, 1.2], (n, 2, 3))
+    env.set_goal_positions(goals)
+    robot = build_world(0, flat_clutter()).robot
+    arm, base = _actions(n, steps)
+
+    def expect(obs, st_now, st_prev):
+        for e in range(n):
+            a, p = WorldState.from_bytes(st_now[e]), None if st_prev is None else WorldState.from_bytes(st_prev[e])
+            q = a.joints[-7:]
+            np.testing.assert_array_equal(obs["joint_positions"][e].cpu().numpy(), q)
+            _, ee = link_poses(robot, q)  # FK from the robot base (base frame)
+            np.testing.assert_allclose(obs["ee_position"][e].cpu().numpy(), ee.pos, rtol=0, atol=1e-12)
+            ego = np.zeros(6)
+            if p is not None:
+                c, s = math.cos(p.base[2]), math.sin(p.base[2])
+                dx, dy = a.base[0] - p.base[0], a.base[1] - p.base[1]
+                ego[0], ego[1] = c * dx + s * dy, -s * dx + c * dy
+                ego[5] = (a.base[2] - p.base[2] + math.pi) % (2 * math.pi) - math.pi
+            np.testing.assert_allclose(obs["base_egomotion"][e].cpu().numpy(), ego, rtol=0, atol=1e-12)
+            c, s = math.cos(a.base[2]), math.sin(a.base[2])
+            gv = np.stack([[c * (g[0] - a.base[0]) + s * (g[1] - a.base[1]),
+                            -s * (g[0] - a.base[0]) + c * (g[1] - a.base[1]), g[2]] for g in goals[e]])
+            np.testing.assert_allclose(obs["goal_vectors"][e].cpu().numpy(), gv, rtol=0, atol=1e-12)
+
+    obs = env.reset(snaps)
+    torch.cuda.synchronize()
+    prev, cur = None, env.sim.get_state()
+    expect(obs, cur, prev)
+    for k in range(steps):
+        obs, _, _, _ = env.step(arm[k], base[k])  # o_t from s_t (= cur)
+        torch.cuda.synchronize()
+        expect(obs, cur, prev)
+        prev, cur = cur, env.sim.get_state()
+    env.close()
