@@ -953,9 +953,13 @@ static void sym_eig(int m, double *A, double *V, double *ev) {
         double apq = A[p * m + q];
         if (apq == 0.0) continue;
         double app = A[p * m + p], aqq = A[q * m + q];
-        double theta = (aqq - app) / (2.0 * apq);
-        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        cs[k] = 1.0 / sqrt(t * t + 1.0);
+        /* t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = a / b, and
+           c = 1 / sqrt(t^2 + 1), multiplied through by |b| */
+        double a = aqq - app, b = 2.0 * apq;
+        double num = a > 0.0 ? b : (a < 0.0 ? -b : fabs(b));
+        double den = fabs(a) + sqrt(a * a + b * b);
+        double t = num / den;
+        cs[k] = den / sqrt(den * den + b * b);
         sn[k] = t * cs[k];
       }
       /* column pass (A and V) */

@@ -775,9 +775,14 @@ __device__ void sym_eig_warp(int m, double *A, double *V, double *ev, double *cs
           const double apq = A[p * m + q];
           if (apq != 0.0) {
             const double app = A[p * m + p], aqq = A[q * m + q];
-            const double theta = (aqq - app) / (2.0 * apq);
-            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
+            // t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = a / b, and
+            // c = 1 / sqrt(t^2 + 1), multiplied through by |b| (fewer dependent
+            // divisions / square roots; oracle sym_eig does the same)
+            const double a = aqq - app, b = 2.0 * apq;
+            const double num = a > 0.0 ? b : (a < 0.0 ? -b : fabs(b));
+            const double den = fabs(a) + sqrt(a * a + b * b);
+            const double t = num / den;
+            c = den / sqrt(den * den + b * b);
             sv = t * c;
           }
         }

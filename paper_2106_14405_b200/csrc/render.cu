@@ -335,6 +335,12 @@ constexpr float kEs = 2e-6f;
 constexpr float kRel = 16.0f * 5.9604645e-8f;
 constexpr float kAmin = 1e-3f;
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // ax (certain hits with t > 0 only): entering axis k + 4 * (s_k >= 0), + 8
 // when te_k exceeds the other two entering ratios by more than their error
 // bounds -- then the FP64 test picks the same entering plane (ray_box_axis).
@@ -346,14 +352,15 @@ __device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float
   const float s0 = fmaf(dx, A.x, fmaf(dy, A.y, dz * A.z));
   const float s1 = fmaf(dx, Bv.x, fmaf(dy, Bv.y, dz * Bv.z));
   const float s2 = fmaf(dx, C.x, fmaf(dy, C.y, dz * C.z));
-  const float amin = fminf(fabsf(s0), fminf(fabsf(s1), fabsf(s2)));
-  if (amin < kAmin) return 2;
-  const float r0 = __fdividef(1.0f, s0), r1 = __fdividef(1.0f, s1), r2 = __fdividef(1.0f, s2);
+  // r_k = 1/s_k to 1 ulp (MUFU.RCP; a zero or subnormal s_k gives inf); 1/amin = max |r_k|
+  const float r0 = rcp_approx(s0), r1 = rcp_approx(s1), r2 = rcp_approx(s2);
+  const float ramax = fmaxf(fabsf(r0), fmaxf(fabsf(r1), fabsf(r2)));
+  if (!(ramax <= 1.0f / kAmin)) return 2;
   const float p0 = A.w * r0, q0 = M.x * r0, p1 = Bv.w * r1, q1 = M.y * r1, p2 = C.w * r2, q2 = M.z * r2;
   const float te0 = fminf(p0, q0), te1 = fminf(p1, q1), te2 = fminf(p2, q2);
   const float te = fmaxf(te0, fmaxf(te1, te2));
   const float tx = fminf(fmaxf(p0, q0), fminf(fmaxf(p1, q1), fmaxf(p2, q2)));
-  const float cr = fmaf(kEs, __fdividef(1.0f, amin), kRel);
+  const float cr = fmaf(kEs, ramax, kRel);
   e = (fabsf(te) + fabsf(tx)) * cr;
   if (tx < -e || te - tx > e) return 0;
   if (tx <= e || tx - te <= e) return 2;
