@@ -441,6 +441,9 @@ def run_b200(args):
         sim.render(("head", "arm"), out=obs)
         b.record(stream)
         iso["render"].append((a, b))
+    sim.set_state(init_states)  # physics alone on the timed region's trajectory
+    for k in range(args.warmup):
+        sim.env_step(act_d[k])
     for k in range(args.steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)

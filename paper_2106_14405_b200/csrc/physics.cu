@@ -80,6 +80,8 @@ struct WarpSmem {
     struct { double lo[kMaxBodies][3], hi[kMaxBodies][3]; } bp;
     struct {
       double planes[2][kMaxFacetsPerPart * 4];
+      int off[kMaxAdm];  // first part-pair index of each admitted pair
+      int npc[kMaxAdm];  // contacts of each admitted pair
     } np;
     struct { double vel[kMaxBodies][6]; BlockWS ws; } sol;
   } u;
@@ -549,63 +551,33 @@ __device__ int convex_pair_contacts(Ctx &c, int i, const Pose &wa, int j, const 
   return n;
 }
 
-// geometry.py:701-716: contacts of body pair (a, b), appended at S->nc. warp-collective.
-// The world frame and AABB of every part of a and b are computed once per
-// pair (lanes per part) into shared memory; the part-pair loop then culls
-// from there (the reference's margin test) and generates contacts in the
-// reference's part order.
-__device__ int pair_contacts(Ctx &c, int a, int b, double margin) {
+// geometry.py:701-716 for one part pair (i, j) that passed the margin-AABB
+// cull: its contacts, appended at `base`, from the substep's part frames in
+// c.pcache ([R(9), p(3), lo(3), hi(3)] per part).  warp-collective.
+__device__ int part_pair_contacts(Ctx &c, int i, int j, double margin, int base) {
   const DevScene &sc = *c.sc;
-  const int a0 = sc.body_part_begin[a], na = sc.body_part_begin[a + 1] - a0;
-  const int b0 = sc.body_part_begin[b], nbp = sc.body_part_begin[b + 1] - b0;
-  // this substep's part frames + AABBs (body_aabb_cached): [R(9), p(3), lo(3), hi(3)] per part
-  const double *PA = c.pcache + 18 * a0, *PB = c.pcache + 18 * b0;
-  // cull every part pair at once (e = ii * nbp + jj < 64; the reference's margin test),
-  // then visit the survivors in (ii, jj) order
-  unsigned long long live = 0ull;
-  for (int e0 = 0; e0 < na * nbp; e0 += 32) {
-    const int e = e0 + c.lane;
-    bool ok = false;
-    if (e < na * nbp) {
-      const int ii = e / nbp, jj = e - ii * nbp;
-      const double *la = PA + 18 * ii + 12, *ha = la + 3, *lb = PB + 18 * jj + 12, *hb = lb + 3;
-      bool sep = false;
-      for (int k = 0; k < 3; ++k) sep |= (la[k] > hb[k] + margin) || (lb[k] > ha[k] + margin);
-      ok = !sep;
-    }
-    live |= (unsigned long long)__ballot_sync(0xffffffffu, ok) << e0;
+  Pose wa, wb;
+  pose_load12(c.pcache + 18 * i, wa);
+  pose_load12(c.pcache + 18 * j, wb);
+  const int ka = sc.part_kind[i], kb = sc.part_kind[j];
+  if (ka == RS_SPHERE && kb == RS_SPHERE) {
+    int r = 0;
+    if (c.lane == 0) r = sphere_sphere(c, i, wa, j, wb, margin, base);
+    return __shfl_sync(0xffffffffu, r, 0);
   }
-  int base = c.S->nc, n = 0;
-  while (live) {
-    const int e = __ffsll((long long)live) - 1;
-    live &= live - 1;
-    {
-      const int ii = e / nbp, jj = e - ii * nbp;
-      const int i = a0 + ii, j = b0 + jj;
-      Pose wa, wb;
-      pose_load12(PA + 18 * ii, wa);
-      pose_load12(PB + 18 * jj, wb);
-      int ka = sc.part_kind[i], kb = sc.part_kind[j];
-      if (ka == RS_SPHERE && kb == RS_SPHERE) {
-        int r = 0;
-        if (c.lane == 0) r = sphere_sphere(c, i, wa, j, wb, margin, base + n);
-        n += __shfl_sync(0xffffffffu, r, 0);
-      } else if (ka == RS_SPHERE || kb == RS_SPHERE) {
-        bool flip = kb == RS_SPHERE;
-        int ps = flip ? j : i, pc = flip ? i : j;
-        const Pose &ws = flip ? wb : wa, &wc = flip ? wa : wb;
-        planes_world(c, pc, wc, 0);
-        __syncwarp();
-        int r = 0;
-        if (c.lane == 0) r = sphere_convex(c, ps, ws, pc, wc, 0, flip, margin, base + n);
-        n += __shfl_sync(0xffffffffu, r, 0);
-        __syncwarp();
-      } else {
-        n += convex_pair_contacts(c, i, wa, j, wb, margin, base + n);
-      }
-    }
+  if (ka == RS_SPHERE || kb == RS_SPHERE) {
+    const bool flip = kb == RS_SPHERE;
+    const int ps = flip ? j : i, pc = flip ? i : j;
+    const Pose &ws = flip ? wb : wa, &wc = flip ? wa : wb;
+    planes_world(c, pc, wc, 0);
+    __syncwarp();
+    int r = 0;
+    if (c.lane == 0) r = sphere_convex(c, ps, ws, pc, wc, 0, flip, margin, base);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    __syncwarp();
+    return r;
   }
-  return n;
+  return convex_pair_contacts(c, i, wa, j, wb, margin, base);
 }
 
 // phase clocks (rsim_bench_phase_cycles): 0 front, 1 sweeps, 2 eigensolves,
@@ -1395,40 +1367,111 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
 
   pa.add(c, 9);
   PhaseClock pn(c);
-  // ---- narrowphase (physics.py:703-719)
-  if (lane == 0) {
-    S.nc = 0;
-    S.ng = 0;
-    if (c.B->trace_pairs && sub < c.B->trace_sub) c.B->trace_count[(size_t)c.env * c.B->trace_sub + sub] = 0;
+  // ---- narrowphase (physics.py:703-719).  The part pairs of all admitted
+  // pairs form one index space (pair k owns [off_k, off_k + na_k nb_k),
+  // ii-major like the reference's part loops, geometry.py:701-716); the
+  // margin-AABB cull runs over it 32 part pairs at a time and the survivors
+  // are visited in index order -- the reference's pair order, then part
+  // order -- each appending its contacts.  Then, lanes per pair in order:
+  // the pair trace, the contact groups and the wakes of pairs with contacts
+  // (wake() of a body is idempotent, so their order does not matter).
+  const int nadm = S.nadm;
+  int *const off = S.u.np.off, *const npc = S.u.np.npc;
+  const double margin = cfg.contact_margin;
+  int tot = 0;
+  for (int k0 = 0; k0 < nadm; k0 += 32) {
+    const int k = k0 + lane;
+    int cnt = 0;
+    if (k < nadm) {
+      const int a = S.adm[k] >> 8, b = S.adm[k] & 0xff;
+      cnt = (sc.body_part_begin[a + 1] - sc.body_part_begin[a]) * (sc.body_part_begin[b + 1] - sc.body_part_begin[b]);
+      npc[k] = 0;
+    }
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (k < nadm) off[k] = tot + incl - cnt;
+    tot += __shfl_sync(0xffffffffu, incl, 31);
   }
   __syncwarp();
-  const int nadm = S.nadm;
-  for (int k = 0; k < nadm; ++k) {
-    int a = S.adm[k] >> 8, b = S.adm[k] & 0xff;
-    int n = pair_contacts(c, a, b, cfg.contact_margin);
-    if (lane == 0) {
-      S.ctr[0]++;
-      if (c.B->trace_pairs && sub < c.B->trace_sub) {
-        int32_t *cnt = c.B->trace_count + (size_t)c.env * c.B->trace_sub + sub;
-        int t = (*cnt)++;
-        if (t < c.B->trace_cap) {
-          int32_t *o = c.B->trace_pairs + (((size_t)c.env * c.B->trace_sub + sub) * c.B->trace_cap + t) * 3;
-          o[0] = a; o[1] = b; o[2] = n;
-        }
+  int nct = 0;
+  for (int e0 = 0; e0 < tot; e0 += 32) {
+    const int e = e0 + lane;
+    bool live = false;
+    int k = 0, pi = 0, pj = 0;
+    if (e < tot) {
+      int lo = 0, hi = nadm - 1;  // the pair owning e: last k with off[k] <= e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= e) lo = mid; else hi = mid - 1;
       }
-      if (n > 0) {
-        if (sc.body_kind[a] == RS_DYNAMIC && ASLEEP(c, a)) wake(c, a);
-        if (sc.body_kind[b] == RS_DYNAMIC && ASLEEP(c, b)) wake(c, b);
-        if (S.ng < kMaxGroups) {
-          S.g_a[S.ng] = a; S.g_b[S.ng] = b; S.g_first[S.ng] = S.nc; S.g_n[S.ng] = n;
-        }
-        S.ng++;
-        S.nc += n;
-      }
+      k = lo;
+      const int a = S.adm[k] >> 8, b = S.adm[k] & 0xff;
+      const int b0 = sc.body_part_begin[b], nbp = sc.body_part_begin[b + 1] - b0;
+      const int r = e - off[k], ii = r / nbp;
+      pi = sc.body_part_begin[a] + ii;
+      pj = b0 + (r - ii * nbp);
+      const double *la = c.pcache + 18 * pi + 12, *ha = la + 3, *lb = c.pcache + 18 * pj + 12, *hb = lb + 3;
+      bool sep = false;
+      for (int x = 0; x < 3; ++x) sep |= (la[x] > hb[x] + margin) || (lb[x] > ha[x] + margin);
+      live = !sep;
     }
-    __syncwarp();
-    if (S.nc > kMaxContacts || S.ng > kMaxGroups) return false;
+    for (unsigned m = __ballot_sync(0xffffffffu, live); m; m &= m - 1) {
+      const int src = __ffs(m) - 1;
+      const int kk = __shfl_sync(0xffffffffu, k, src);
+      const int n = part_pair_contacts(c, __shfl_sync(0xffffffffu, pi, src), __shfl_sync(0xffffffffu, pj, src),
+                                       margin, nct);
+      nct += n;
+      if (lane == 0) npc[kk] += n;
+      __syncwarp();
+    }
   }
+  __syncwarp();
+  const bool tr = c.B->trace_pairs && sub < c.B->trace_sub;
+  int ngp = 0, cfirst = 0;
+  unsigned long long wmask = 0ull;
+  for (int k0 = 0; k0 < nadm; k0 += 32) {
+    const int k = k0 + lane;
+    const int a = k < nadm ? S.adm[k] >> 8 : 0, b = k < nadm ? S.adm[k] & 0xff : 0;
+    const int n = k < nadm ? npc[k] : 0;
+    if (tr && k < nadm && k < c.B->trace_cap) {
+      int32_t *o = c.B->trace_pairs + (((size_t)c.env * c.B->trace_sub + sub) * c.B->trace_cap + k) * 3;
+      o[0] = a; o[1] = b; o[2] = n;
+    }
+    const unsigned hm = __ballot_sync(0xffffffffu, n > 0);
+    int incl = n;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (n > 0) {
+      const int g = ngp + __popc(hm & ((1u << lane) - 1));
+      if (g < kMaxGroups) { S.g_a[g] = a; S.g_b[g] = b; S.g_first[g] = cfirst + incl - n; S.g_n[g] = n; }
+      wmask |= (1ull << a) | (1ull << b);
+    }
+    ngp += __popc(hm);
+    cfirst += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  wmask = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(wmask >> 32)) << 32) |
+          __reduce_or_sync(0xffffffffu, (unsigned)(wmask & 0xffffffffu));
+  int nwoken = 0;
+  for (int b0 = 0; b0 < nb; b0 += 32) {
+    const int b = b0 + lane;
+    const bool w = b < nb && ((wmask >> b) & 1ull) && sc.body_kind[b] == RS_DYNAMIC && ASLEEP(c, b);
+    if (w) { ASLEEP(c, b) = 0; SLEEPC(c, b) = 0; RIDER(c, b) = -1; }  // wake()
+    nwoken += __popc(__ballot_sync(0xffffffffu, w));
+  }
+  if (lane == 0) {
+    S.ctr[0] += nadm;
+    S.ctr[2] += nwoken;
+    S.nc = nct;
+    S.ng = ngp;
+    if (tr) c.B->trace_count[(size_t)c.env * c.B->trace_sub + sub] = nadm;
+  }
+  __syncwarp();
+  if (nct > kMaxContacts || ngp > kMaxGroups) return false;
   const int nc = S.nc, ng = S.ng;
 
   pn.add(c, 10);

@@ -341,9 +341,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-// ax (certain hits with t > 0 only): entering axis k + 4 * (s_k >= 0), + 8
-// when te_k exceeds the other two entering ratios by more than their error
-// bounds -- then the FP64 test picks the same entering plane (ray_box_axis).
+// ax (certain hits with t > 0 only): entering axis k, + 8 when te_k exceeds
+// the other two entering ratios by more than their error bounds -- then the
+// FP64 test picks the same entering axis (ray_box_axis; its side from the
+// FP64 sign of s_k, which |s_k| >= kAmin makes the FP32 one).
 __device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float dz, float &t, float &e, int &ax) {
   // bx: (u_k, b0 of +k) for k = 0..2, then (-b0 of -0, -1, -2).  With the
   // signed reciprocal r_k = 1/s_k the slab k is crossed at b+_k r_k and
@@ -369,8 +370,7 @@ __device__ __forceinline__ int box32(const float4 *bx, float dx, float dy, float
   t = te;
   const int k = te0 == te ? 0 : (te1 == te ? 1 : 2);
   const float second = fmaxf(fminf(te0, te1), fminf(fmaxf(te0, te1), te2));  // middle of the three
-  const float sk = k == 0 ? s0 : (k == 1 ? s1 : s2);
-  ax = k + (sk < 0.f ? 0 : 4) + (te - second > 2.0f * e + 2.0f * cr * fabsf(second) ? 8 : 0);
+  ax = k + (te - second > 2.0f * e + 2.0f * cr * fabsf(second) ? 8 : 0);
   return 1;
 }
 
