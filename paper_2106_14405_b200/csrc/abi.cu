@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -271,7 +272,7 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   if (!rc) rc = balloc(b, &p, 2 * (size_t)n_env), b->heavy[0] = (uint8_t *)p, b->heavy[1] = (uint8_t *)p + n_env;
 #undef BA
   if (!rc) rc = balloc(b, &p, sizeof(DevScene) * n_scenes), b->d_scenes = (DevScene *)p;
-  if (!rc) rc = balloc(b, &p, sizeof(int32_t) * n_env), b->d_env_scene = (int32_t *)p;
+  if (!rc) rc = balloc(b, &p, sizeof(int32_t) * 2 * (size_t)n_env), b->d_env_scene = (int32_t *)p;
   if (rc) {
     rs_batch_destroy(b);
     return rc;
@@ -289,13 +290,16 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
   std::vector<int32_t> es(n_env, 0);
   if (env_scene) memcpy(es.data(), env_scene, sizeof(int32_t) * n_env);
   cudaError_t e1 = cudaMemcpy(b->d_scenes, hs.data(), sizeof(DevScene) * n_scenes, cudaMemcpyHostToDevice);
-  cudaError_t e2 = cudaMemcpy(b->d_env_scene, es.data(), sizeof(int32_t) * n_env, cudaMemcpyHostToDevice);
+  for (int e = 0; e < n_env; ++e) es.push_back(e);  // env_order: envs stably sorted by scene
+  std::stable_sort(es.begin() + n_env, es.end(), [&](int32_t x, int32_t y) { return es[x] < es[y]; });
+  cudaError_t e2 = cudaMemcpy(b->d_env_scene, es.data(), sizeof(int32_t) * 2 * n_env, cudaMemcpyHostToDevice);
   if (e1 != cudaSuccess || e2 != cudaSuccess) {
     rs_batch_destroy(b);
     return fail(RS_ERR_CUDA, "batch table upload failed");
   }
   d.scenes = b->d_scenes;
   d.env_scene = b->d_env_scene;
+  d.env_order = b->d_env_scene + n_env;
   if (launch_render_tables(d, 0) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
     rs_batch_destroy(b);
     return fail(RS_ERR_CUDA, "render table setup failed");

@@ -102,6 +102,8 @@ struct DevBatch {
   int64_t *step_index; // [E]
   const DevScene *scenes;  // device array
   const int32_t *env_scene;
+  const int32_t *env_order;  // envs sorted by scene (stable): the warp-per-env step kernel's order, so
+                             // co-resident warps share their scene tables in L1
   rs_physics_config cfg;
   rs_render_config rcfg;
   uint32_t *fault;

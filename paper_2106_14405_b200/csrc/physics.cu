@@ -290,41 +290,50 @@ __device__ void prim_aabb(Ctx &c, int p, const Pose &wp, double *lo, double *hi)
 }
 
 // geometry.py:289-296 parts_aabb (the body AABB = union of its part AABBs)
-// with a pose-keyed cache in the env's global scratch: the part
-// world frames and AABBs of body b are recomputed only when its position or
-// quaternion bits changed (static and sleeping bodies: once), and stay in
-// c.pcache for the narrowphase of the same substep.  The cached values are
-// the ones the computation would produce (same inputs, same code).
-__device__ bool body_aabb_cached(Ctx &c, int b, double *lo, double *hi) {
-  const DevScene &sc = *c.sc;
+// with a pose-keyed cache in the env's global scratch: the part world frames
+// and AABBs of body b are recomputed only when its position or quaternion
+// bits changed (static and sleeping bodies: once), and stay in c.pcache for
+// the narrowphase of the same substep.  The cached values are the ones the
+// computation would produce (same inputs, same code).
+//   bcache[b] = key (pos bits 3, quat bits 4, valid 1) + AABB (lo 3, hi 3)
+//   pcache[p] = world frame (R 9, p 3) + AABB (lo 3, hi 3)
+__device__ bool body_key_hit(Ctx &c, int b) {
   const double *pos = POS(c, b), *q = QUAT(c, b);
-  double *K = c.bcache + 14 * b;
+  const double *K = c.bcache + 14 * b;
   const long long *kb = reinterpret_cast<const long long *>(K);
   bool hit = K[7] == 1.0;  // all key words loaded at once (independent loads)
 #pragma unroll
   for (int i = 0; i < 3; ++i) hit &= kb[i] == __double_as_longlong(pos[i]);
 #pragma unroll
   for (int i = 0; i < 4; ++i) hit &= kb[3 + i] == __double_as_longlong(q[i]);
-  if (hit) {
-    for (int i = 0; i < 3; ++i) { lo[i] = K[8 + i]; hi[i] = K[11 + i]; }
-    return false;
-  }
+  return hit;
+}
+
+// part p's world frame and AABB from its body's current pose -> pcache
+__device__ void part_frame_aabb(Ctx &c, int p) {
   Pose bp, wp;
-  body_pose(c, b, bp);
+  body_pose(c, c.sc->part_body[p], bp);
+  part_world(c, bp, p, wp);
+  double l[3], h[3];
+  prim_aabb(c, p, wp, l, h);
+  double *P = c.pcache + 18 * p;
+  for (int k = 0; k < 9; ++k) P[k] = wp.R[k];
+  for (int i = 0; i < 3; ++i) { P[9 + i] = wp.p[i]; P[12 + i] = l[i]; P[15 + i] = h[i]; }
+}
+
+// body b's AABB = union of its parts' (pcache, in part order) -> bcache with the key
+__device__ void body_aabb_store(Ctx &c, int b, double *lo, double *hi) {
+  const DevScene &sc = *c.sc;
   for (int i = 0; i < 3; ++i) { lo[i] = INFINITY; hi[i] = -INFINITY; }
   for (int p = sc.body_part_begin[b]; p < sc.body_part_begin[b + 1]; ++p) {
-    double l[3], h[3];
-    part_world(c, bp, p, wp);
-    prim_aabb(c, p, wp, l, h);
-    double *P = c.pcache + 18 * p;
-    for (int k = 0; k < 9; ++k) P[k] = wp.R[k];
-    for (int i = 0; i < 3; ++i) { P[9 + i] = wp.p[i]; P[12 + i] = l[i]; P[15 + i] = h[i]; }
-    for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], l[i]); hi[i] = fmax(hi[i], h[i]); }
+    const double *P = c.pcache + 18 * p;
+    for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], P[12 + i]); hi[i] = fmax(hi[i], P[15 + i]); }
   }
+  const double *pos = POS(c, b), *q = QUAT(c, b);
+  double *K = c.bcache + 14 * b;
   for (int i = 0; i < 3; ++i) { K[i] = pos[i]; K[8 + i] = lo[i]; K[11 + i] = hi[i]; }
   for (int i = 0; i < 4; ++i) K[3 + i] = q[i];
   K[7] = 1.0;
-  return true;
 }
 
 // world planes of part p into S->planes[slot] (lanes per facet)
@@ -1205,18 +1214,38 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   // ---- broadphase: AABBs (lanes per body) through the pose-keyed cache: only
   // bodies that moved are recomputed (body_aabb_cached); `changed` = those
   PhaseClock pb1(c);
+  // key check lanes per body (hits: the cached AABB); the parts of the moved
+  // bodies recomputed lanes per part; their body AABBs (unions) lanes per body
+  auto bp_store = [&](int b, const double *lo, const double *hi) {
+    const bool kin = sc.body_kind[b] == RS_KINEMATIC;
+    for (int i = 0; i < 3; ++i) {
+      S.u.bp.lo[b][i] = kin ? lo[i] - cfg.wake_margin : lo[i];
+      S.u.bp.hi[b][i] = kin ? hi[i] + cfg.wake_margin : hi[i];
+    }
+  };
   unsigned long long changed = 0ull;
   for (int b0 = 0; b0 < nb; b0 += 32) {
     const int b = b0 + lane;
     bool miss = false;
     if (b < nb) {
-      double lo[3], hi[3];
-      miss = body_aabb_cached(c, b, lo, hi);
-      if (sc.body_kind[b] == RS_KINEMATIC)
-        for (int i = 0; i < 3; ++i) { lo[i] -= cfg.wake_margin; hi[i] += cfg.wake_margin; }
-      for (int i = 0; i < 3; ++i) { S.u.bp.lo[b][i] = lo[i]; S.u.bp.hi[b][i] = hi[i]; }
+      miss = !body_key_hit(c, b);
+      if (!miss) bp_store(b, c.bcache + 14 * b + 8, c.bcache + 14 * b + 11);
     }
     changed |= (unsigned long long)__ballot_sync(0xffffffffu, miss) << b0;
+  }
+  if (changed) {
+    const int np = sc.np;
+    for (int p0 = 0; p0 < np; p0 += 32) {
+      const int p = p0 + lane;
+      if (p < np && ((changed >> sc.part_body[p]) & 1ull)) part_frame_aabb(c, p);
+    }
+    __syncwarp();
+    for (int b = lane; b < nb; b += 32)
+      if ((changed >> b) & 1ull) {
+        double lo[3], hi[3];
+        body_aabb_store(c, b, lo, hi);
+        bp_store(b, lo, hi);
+      }
   }
   if (!S.cbits_valid) changed = nb == 64 ? ~0ull : ((1ull << nb) - 1ull);
   __syncwarp();
@@ -1977,8 +2006,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   extern __shared__ __align__(16) unsigned char dsm[];
   WarpSmem *smem = reinterpret_cast<WarpSmem *>(dsm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int env = blockIdx.x * kWarpsPerBlock + warp;
-  if (env >= B.n_env) return;
+  const int slot = blockIdx.x * kWarpsPerBlock + warp;
+  if (slot >= B.n_env) return;
+  const int env = B.env_order ? B.env_order[slot] : slot;
   if (heavy_in && heavy_in[env]) return;
   if (B.env_active && !B.env_active[env]) {  // not stepping (rs_settle): state copied through
     copy_through(B, env, lane);
