@@ -90,6 +90,7 @@ struct WarpSmem {
   double links[kMaxArm][12];
   double ee[12];
   double raa[kMaxArm][9];
+  double aoff[kMaxArm + 1][3];  // FK: link offsets, then the gripper offset (staged by lanes)
   double budget[kMaxArm];
   uint16_t cand[kMaxCand];
   uint16_t adm[kMaxAdm];
@@ -175,6 +176,10 @@ __device__ int set_kinematic(Ctx &c, int b, const Pose &p, double dt, bool zero_
 // lane 0 chains them; results in S->links / S->ee.
 __device__ void forward_kinematics(Ctx &c) {
   const DevScene &sc = *c.sc;
+  if (c.lane <= sc.narm) {  // the chain's constants staged in parallel (no global loads inside it)
+    const double *src = c.lane < sc.narm ? sc.arm_offset + 3 * c.lane : sc.gripper;
+    for (int k = 0; k < 3; ++k) c.S->aoff[c.lane][k] = src[k];
+  }
   if (c.lane < sc.narm) axis_angle_mat(sc.arm_axis + 3 * c.lane, JOINTS(c)[sc.nsj + c.lane], c.S->raa[c.lane]);
   __syncwarp();
   if (c.lane == 0) {
@@ -183,14 +188,15 @@ __device__ void forward_kinematics(Ctx &c) {
     rot_z(0.0, off.R);
     rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
     for (int i = 0; i < sc.narm; ++i) {
-      off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
+      off.p[0] = c.S->aoff[i][0]; off.p[1] = c.S->aoff[i][1]; off.p[2] = c.S->aoff[i][2];
       compose(t, off, t);
       for (int k = 0; k < 9; ++k) rot.R[k] = c.S->raa[i][k];
       compose(t, rot, t);
       for (int k = 0; k < 9; ++k) c.S->links[i][k] = t.R[k];
       for (int k = 0; k < 3; ++k) c.S->links[i][9 + k] = t.p[k];
     }
-    Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}}, e;
+    const double *gp = c.S->aoff[sc.narm];
+    Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {gp[0], gp[1], gp[2]}}, e;
     compose(t, g, e);
     for (int k = 0; k < 9; ++k) c.S->ee[k] = e.R[k];
     for (int k = 0; k < 3; ++k) c.S->ee[9 + k] = e.p[k];
@@ -1278,7 +1284,8 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     }
     for (unsigned long long rest = changed; rest; rest &= rest - 1) {
       const int cb = __ffsll((long long)rest) - 1;
-      const int kc = sc.body_kind[cb], gc = sc.body_group[cb];
+      const int kc = __shfl_sync(0xffffffffu, cb < 32 ? yk0 : yk1, cb & 31);  // lane cb % 32 holds body cb's
+      const int gc = __shfl_sync(0xffffffffu, cb < 32 ? yg0 : yg1, cb & 31);
       const double cl0 = S.u.bp.lo[cb][0], cl1 = S.u.bp.lo[cb][1], cl2 = S.u.bp.lo[cb][2];
       const double ch0 = S.u.bp.hi[cb][0], ch1 = S.u.bp.hi[cb][1], ch2 = S.u.bp.hi[cb][2];
       auto test = [&](int y, const double (&l)[3], const double (&h)[3], int ky, int gy) {
