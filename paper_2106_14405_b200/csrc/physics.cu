@@ -315,16 +315,45 @@ __device__ bool body_key_hit(Ctx &c, int b) {
   return hit;
 }
 
-// part p's world frame and AABB from its body's current pose -> pcache
-__device__ void part_frame_aabb(Ctx &c, int p) {
+// part p's world frame and AABB from its body's current pose -> pcache.  A
+// hull's AABB (a vertex loop) is left to hull_aabb_warp: returns true then.
+__device__ bool part_frame_aabb(Ctx &c, int p) {
   Pose bp, wp;
   body_pose(c, c.sc->part_body[p], bp);
   part_world(c, bp, p, wp);
-  double l[3], h[3];
-  prim_aabb(c, p, wp, l, h);
   double *P = c.pcache + 18 * p;
   for (int k = 0; k < 9; ++k) P[k] = wp.R[k];
-  for (int i = 0; i < 3; ++i) { P[9 + i] = wp.p[i]; P[12 + i] = l[i]; P[15 + i] = h[i]; }
+  for (int i = 0; i < 3; ++i) P[9 + i] = wp.p[i];
+  if (c.sc->part_kind[p] == RS_HULL) return true;
+  double l[3], h[3];
+  prim_aabb(c, p, wp, l, h);
+  for (int i = 0; i < 3; ++i) { P[12 + i] = l[i]; P[15 + i] = h[i]; }
+  return false;
+}
+
+// prim_aabb of hull part q (frame already in pcache), lanes per vertex; the
+// min / max reductions are exact, so any order gives the vertex loop's bounds.
+// warp-collective.
+__device__ void hull_aabb_warp(Ctx &c, int q) {
+  const DevScene &sc = *c.sc;
+  __syncwarp();
+  double *P = c.pcache + 18 * q;
+  Pose wp;
+  pose_load12(P, wp);
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int v = sc.part_vert_begin[q] + c.lane; v < sc.part_vert_begin[q + 1]; v += 32) {
+    double x[3];
+    apply(wp, sc.vert + 3 * v, x);
+    for (int i = 0; i < 3; ++i) { lo[i] = fmin(lo[i], x[i]); hi[i] = fmax(hi[i], x[i]); }
+  }
+  for (int o = 16; o; o >>= 1)
+    for (int i = 0; i < 3; ++i) {
+      lo[i] = fmin(lo[i], __shfl_xor_sync(0xffffffffu, lo[i], o));
+      hi[i] = fmax(hi[i], __shfl_xor_sync(0xffffffffu, hi[i], o));
+    }
+  if (c.lane == 0)
+    for (int i = 0; i < 3; ++i) { P[12 + i] = lo[i]; P[15 + i] = hi[i]; }
+  __syncwarp();
 }
 
 // body b's AABB = union of its parts' (pcache, in part order) -> bcache with the key
@@ -1243,7 +1272,8 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     const int np = sc.np;
     for (int p0 = 0; p0 < np; p0 += 32) {
       const int p = p0 + lane;
-      if (p < np && ((changed >> sc.part_body[p]) & 1ull)) part_frame_aabb(c, p);
+      const bool hull = p < np && ((changed >> sc.part_body[p]) & 1ull) && part_frame_aabb(c, p);
+      for (unsigned m = __ballot_sync(0xffffffffu, hull); m; m &= m - 1) hull_aabb_warp(c, p0 + __ffs(m) - 1);
     }
     __syncwarp();
     for (int b = lane; b < nb; b += 32)
