@@ -258,11 +258,16 @@ __device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem 
   return face >= 0 ? best : INFINITY;
 }
 
-// exact lowest-id rule for near-tie pixels: bodies in id order, parts in order
+// exact lowest-id rule for near-tie pixels: bodies in id order, parts in order.
+// Out of line (rare) and by value: no caller variable needs a stack address.
+struct TieHit {
+  int id, wpart, wface;
+};
 template <bool kMesh>
-__device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S, const double *plane,
-                                         const uint32_t *mask, const double *o, const double *d, double tmin,
-                                         double eps, int &id, int &wpart, int &wface) {
+__device__ __noinline__ TieHit resolve_tie(const DevScene &sc, const RenderSmem &S, const double *plane,
+                                           const uint32_t *mask, const double *o, double dx, double dy, double dz,
+                                           double tmin, double eps, TieHit h) {
+  const double d[3] = {dx, dy, dz};
   int cur_b = -1, cur_p = -1, cur_f = -1;
   double cur_t = INFINITY;
   for (int w = 0; w < kMaskWords; ++w) {
@@ -272,7 +277,7 @@ __device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S
       m &= m - 1;
       int b = S.part[p].body;
       if (b != cur_b) {
-        if (cur_b >= 0 && cur_t <= tmin + eps) { id = cur_b; wpart = cur_p; wface = cur_f; return; }
+        if (cur_b >= 0 && cur_t <= tmin + eps) return {cur_b, cur_p, cur_f};
         cur_b = b;
         cur_t = INFINITY;
       }
@@ -281,7 +286,8 @@ __device__ __noinline__ void resolve_tie(const DevScene &sc, const RenderSmem &S
       if (t < cur_t) { cur_t = t; cur_p = p; cur_f = f; }
     }
   }
-  if (cur_b >= 0 && cur_t <= tmin + eps) { id = cur_b; wpart = cur_p; wface = cur_f; }
+  if (cur_b >= 0 && cur_t <= tmin + eps) return {cur_b, cur_p, cur_f};
+  return h;
 }
 
 // All-FP64 walk of one pixel's tile list (front to back, exact early-out,
@@ -313,7 +319,10 @@ __device__ __forceinline__ double trace_exact(const DevScene &sc, const RenderSm
       t2 = t;
     }
   }
-  if (tmin < INFINITY && t2 - tmin <= eps) resolve_tie<kMesh>(sc, S, plane, mask, o, d, tmin, eps, id, wpart, wface);
+  if (tmin < INFINITY && t2 - tmin <= eps) {
+    const TieHit h = resolve_tie<kMesh>(sc, S, plane, mask, o, d[0], d[1], d[2], tmin, eps, {id, wpart, wface});
+    id = h.id; wpart = h.wpart; wface = h.wface;
+  }
   return tmin;
 }
 
