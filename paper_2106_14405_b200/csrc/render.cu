@@ -79,6 +79,7 @@ struct RenderSmem {
   } u;
   int nlist[kMaxTiles];
   uint8_t order[kMaxParts];
+  float color[kMaxBodies][3];  // body albedo (shading reads it per pixel)
   Pose cam;
 };
 // world planes (n.xyz, b0 per facet; mesh variant: part rotations) follow the struct
@@ -516,6 +517,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   }
   __syncthreads();
   const double *o = S.cam.p;
+  for (int i = tid; i < 3 * sc.nb; i += blockDim.x) S.color[i / 3][i % 3] = sc.color[i];
 
   // -- world part frames and bounds (lanes per part), then world planes
   //    (geometry.py:554-557), b0 = d - n.o (lanes per facet)
@@ -726,7 +728,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
           cosv = -(d[0] * Q[0] + d[1] * Q[1] + d[2] * Q[2]);
         }
         float shade = __fadd_rn(0.3f, __fmul_rn(0.7f, (float)(cosv > 0.0 ? cosv : 0.0)));
-        const float *col = sc.color + 3 * id;
+        const float *col = S.color[id];
         uint32_t px4 = 0xff000000u;
         for (int i = 0; i < 3; ++i) {
           float cv = __fadd_rn(__fmul_rn(__fmul_rn(255.0f, col[i]), shade), 0.5f);
