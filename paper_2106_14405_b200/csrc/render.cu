@@ -744,16 +744,16 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
 
 // Per-batch constant tables: unit camera-frame ray per pixel centre
 // (u + 1/2, v + 1/2; f = (W/2)/tan(fov/2); normalise) and the inward side
-// planes of every 16x16 tile frustum.
-__global__ void render_tables_kernel(int W, int H, double fov, double *ray_dir, double *tile_frustum) {
+// planes of every 16x16 tile frustum.  Evaluated exactly as the oracle does
+// (oracle/rsim_oracle.c render: f from the host's tan, no contraction,
+// dc / l by division), so every ray is the oracle's bit for bit.
+__global__ void render_tables_kernel(int W, int H, double f, double *ray_dir, double *tile_frustum) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const double f = (W / 2.0) / tan(fov / 2.0);
   if (i < W * H) {
     const int u = i % W, v = i / W;
-    double dc[3] = {(u + 0.5 - W / 2.0) / f, (v + 0.5 - H / 2.0) / f, 1.0};
-    double l = sqrt(dot3(dc, dc));
-    const double rl = 1.0 / l;
-    ray_dir[3 * i] = dc[0] * rl; ray_dir[3 * i + 1] = dc[1] * rl; ray_dir[3 * i + 2] = dc[2] * rl;
+    const double x = (u + 0.5 - W / 2.0) / f, y = (v + 0.5 - H / 2.0) / f;
+    const double l = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), 1.0));
+    ray_dir[3 * i] = x / l; ray_dir[3 * i + 1] = y / l; ray_dir[3 * i + 2] = 1.0 / l;
   }
   const int tx_n = W / kTile;
   if (i < tx_n * (H / kTile)) {
@@ -766,7 +766,8 @@ __global__ void render_tables_kernel(int W, int H, double fov, double *ray_dir, 
 
 cudaError_t launch_render_tables(const DevBatch &B, cudaStream_t stream) {
   const int n = B.rcfg.width * B.rcfg.height;
-  render_tables_kernel<<<(n + 255) / 256, 256, 0, stream>>>(B.rcfg.width, B.rcfg.height, B.rcfg.fov,
+  const double f = (B.rcfg.width / 2.0) / tan(B.rcfg.fov / 2.0);  // host libm, as the oracle
+  render_tables_kernel<<<(n + 255) / 256, 256, 0, stream>>>(B.rcfg.width, B.rcfg.height, f,
                                                             const_cast<double *>(B.ray_dir),
                                                             const_cast<double *>(B.tile_frustum));
   return cudaGetLastError();
