@@ -39,8 +39,8 @@ constexpr int kWarpsPerBlock = 2;
 constexpr int kMaxCand = 512;
 constexpr int kMaxAdm = 256;
 constexpr int kMaxContacts = 128;
-constexpr int kMaxPartsPerBody = 8;  // rs_scene_create rejects more
-static_assert(kMaxPartsPerBody * kMaxPartsPerBody <= 64, "pair_contacts culls all part pairs in one 64-bit mask");
+constexpr int kMaxPartsPerBody = 8;  // rs_scene_create rejects more (the narrowphase index space
+                                     // of the part pairs stays < kMaxAdm * 64)
 constexpr int kMaxGroups = 96;
 constexpr int kMaxBlockRows = 32;
 constexpr int kRowD = 44;  // doubles per solver row in global scratch
@@ -1246,8 +1246,9 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
 
   pk.add(c, 7);
   PhaseClock pb(c);
-  // ---- broadphase: AABBs (lanes per body) through the pose-keyed cache: only
-  // bodies that moved are recomputed (body_aabb_cached); `changed` = those
+  // ---- broadphase: AABBs through the pose-keyed cache (body_key_hit,
+  // part_frame_aabb, body_aabb_store): only bodies that moved are recomputed;
+  // `changed` = those
   PhaseClock pb1(c);
   // key check lanes per body (hits: the cached AABB); the parts of the moved
   // bodies recomputed lanes per part; their body AABBs (unions) lanes per body
