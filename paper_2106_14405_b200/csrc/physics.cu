@@ -39,8 +39,6 @@ constexpr int kWarpsPerBlock = 2;
 constexpr int kMaxCand = 512;
 constexpr int kMaxAdm = 256;
 constexpr int kMaxContacts = 128;
-constexpr int kMaxPartsPerBody = 8;  // rs_scene_create rejects more (the narrowphase index space
-                                     // of the part pairs stays < kMaxAdm * 64)
 constexpr int kMaxGroups = 96;
 constexpr int kMaxBlockRows = 32;
 constexpr int kRowD = 44;  // doubles per solver row in global scratch
