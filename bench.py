@@ -92,6 +92,33 @@ def action_table(n_env, n_steps, seed):
     return a
 
 
+def interact_states(global_ids, pool):
+    """Interact scenario: settled clutter, robot spawned at
+    (1.6, 0.2, yaw pi/2) facing the light table (per-env jitter)."""
+    from paper_2106_14405_b200.state import WorldState
+
+    out = []
+    for gid in global_ids:
+        blobs = pool[gid % 3]
+        st = WorldState.from_bytes(blobs[(gid // 3) % len(blobs)])
+        rng = np.random.default_rng(3000 + gid)
+        st.base = np.array([1.6 + rng.uniform(-0.05, 0.05), 0.2 + rng.uniform(-0.05, 0.05), math.pi / 2])
+        out.append(st.to_bytes())
+    return out
+
+
+def interact_actions(n_env, n_steps):
+    """[n_steps, n_env, 6] scripted EE pushes into the clutter: dEE (0.015, 0,
+    -0.012) for 20 steps, then +-0.015 y sweeps; base still, gripper 0."""
+    a = np.zeros((n_steps, n_env, 6))
+    for k in range(n_steps):
+        if k < 20:
+            a[k, :, :3] = (0.015, 0.0, -0.012)
+        else:
+            a[k, :, :3] = (0.0, 0.015 if (k // 10) % 2 == 0 else -0.015, 0.0)
+    return a
+
+
 # ------------------------------------------------------------------- clocks
 
 class ClockSampler:
@@ -342,7 +369,7 @@ def run_b200(args):
 
     hp = torch.cuda.Stream(dev, priority=-1)  # physics ahead of queued render CTAs
 
-    def step(k, ev=None, cams=("head", "arm"), out=None):
+    def step(k, ev=None, cams=("head", "arm"), out=None, acts=act_d):
         # one env step, paper pipeline (SPEC StepConfig defaults
         # observation_delay=1, interleave=true): physics s_t -> s_{t+1} on a
         # high-priority stream, render(s_t) concurrently on a side stream, join.
@@ -357,7 +384,7 @@ def run_b200(args):
         with torch.cuda.stream(hp):
             if ev is not None:
                 ev[0].record(hp)
-            sim.env_step(act_d[k])  # IK -> physics -> grasp rule
+            sim.env_step(acts[k])  # IK -> physics -> grasp rule
             if ev is not None:
                 ev[1].record(hp)
         stream.wait_stream(hp)
@@ -402,6 +429,22 @@ def run_b200(args):
     torch.cuda.synchronize(dev)
     ms_one_cam = c0.elapsed_time(c1)
     del obs1
+
+    # ---- Interact (second column): robots facing the light
+    # table pushing into the clutter, same interleaved step
+    act_i = torch.tensor(interact_actions(E, n_tab), device=dev)
+    sim.set_state(interact_states(gids, settled_pool()))
+    for k in range(args.warmup):
+        step(k, acts=act_i)
+    torch.cuda.synchronize(dev)
+    c0.record(stream)
+    for k in range(args.steps):
+        step(args.warmup + k, acts=act_i)
+    c1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_interact = c0.elapsed_time(c1)
+    sim.raise_faults()
+    del act_i
 
     # ---- end-to-end through the C-ABI with host buffers (e2e): replay the
     # same trajectory (same initial states, same actions) as the timed region
@@ -457,10 +500,12 @@ def run_b200(args):
     # ---- across ranks: max time, summed stats (the only collectives)
     stats, tms = reduce_window({"acc": acc, "envs": float(E)},
                                {"total": ms_total, "e2e": ms_e2e, "phys": ms_phys, "rend": ms_rend,
-                                "phys_iso": ms_phys_iso, "rend_iso": ms_rend_iso, "one_cam": ms_one_cam},
+                                "phys_iso": ms_phys_iso, "rend_iso": ms_rend_iso, "one_cam": ms_one_cam,
+                                "interact": ms_interact},
                                device=dev if backend == "nccl" else "cpu")
     ms_total, ms_e2e, ms_phys, ms_rend = tms["total"], tms["e2e"], tms["phys"], tms["rend"]
     ms_phys_iso, ms_rend_iso, ms_one_cam = tms["phys_iso"], tms["rend_iso"], tms["one_cam"]
+    ms_interact = tms["interact"]
     total_envs = E * world
     value = total_envs * args.steps / (ms_total * 1e-3)
     e2e_value = total_envs * args.steps / (ms_e2e * 1e-3)
@@ -545,6 +590,11 @@ def run_b200(args):
             "one_camera": {"value": total_envs * args.steps / (ms_one_cam * 1e-3), "unit": UNIT,
                            "ms_per_step": ms_one_cam / args.steps,
                            "note": "same trajectory, head camera only (PAPER.md:97 '1 RGBD observation')"},
+            "interact": {"value": total_envs * args.steps / (ms_interact * 1e-3), "unit": UNIT,
+                         "ms_per_step": ms_interact / args.steps,
+                         "note": "Interact scenario (PAPER.md:530 second column; SURVEY.md §8d): robots at "
+                                 "(1.6, 0.2) facing the light table, scripted EE pushes into the clutter; "
+                                 "same interleaved physics + 2-camera render step"},
             "gpu_launches": 6 * args.steps,  # ik_first, ik_fallback, step, step_cta, grasp, render per env step
             "clocks": clk.summary(),
             "episode_stats_allreduce": {"accumulated_contact_force_sum": stats["acc"], "envs": int(stats["envs"])},

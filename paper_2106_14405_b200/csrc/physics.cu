@@ -42,7 +42,8 @@ constexpr int kMaxContacts = 128;
 constexpr int kMaxGroups = 96;
 constexpr int kMaxBlockRows = 32;
 constexpr int kRowD = 44;  // doubles per solver row in global scratch
-constexpr int kPairD = 34; // doubles per contact group (pair) in global scratch
+constexpr int kEigSlots = 16;  // cached eigendecompositions per block (LRU over active sets)
+constexpr int kPairD = 31 + 2 * kEigSlots;  // doubles per contact group (pair) in global scratch
 constexpr int kKCap = kMaxContacts * kMaxBlockRows;  // Sigma m^2 <= 32 * 128
 constexpr int kMaxPartsCache = 128;
 
@@ -53,7 +54,9 @@ enum {
   RA = 35, RB = 36, RPT = 37, RDEPTH = 40, RGRP = 41
 };
 // ---- pair (group) field offsets --------------------------------------------
-enum { PIA = 0, PIB = 9, PCA = 18, PCB = 21, PIMA = 24, PIMB = 25, PMU = 26, PE = 27, PKOFF = 28, PHASK = 29, PMASK = 30, PREPL = 32 };  // PMASK, PMASK+1: cached active sets
+// PMASK + s: active set cached in slot s (-1: empty); PSTAMP + s: its last use (PCLK ticks)
+enum { PIA = 0, PIB = 9, PCA = 18, PCB = 21, PIMA = 24, PIMB = 25, PMU = 26, PE = 27, PKOFF = 28, PHASK = 29,
+       PCLK = 30, PMASK = 31, PSTAMP = 31 + kEigSlots };
 
 // block workspace in shared memory (per warp), m <= kMaxBlockRows
 constexpr int kSmemEig = 12;  // eigensolver matrices live in shared memory up to this size
@@ -101,6 +104,9 @@ struct WarpSmem {
   int moved_mask, dragged, n_active, max_active;
   int64_t ctr[3];
 };
+
+// 5 two-warp CTAs per SM (228 KB of shared memory, 1 KB reserved per CTA)
+static_assert(5 * (2 * sizeof(WarpSmem) + 1024) <= 228 * 1024, "step_kernel occupancy");
 
 struct Ctx {
   const DevScene *sc;
@@ -958,10 +964,21 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     for (int i = 0; i < na; ++i) mask |= 1u << ws.active[i];
     if (na) {
       if (lane < na) ws.rhs[lane] = -ws.q[ws.active[lane]];
-      // two cached decompositions per block, keyed by the active set
-      int slot = (double)mask == P[PMASK] ? 0 : ((double)mask == P[PMASK + 1] ? 1 : -1);
+      // kEigSlots cached decompositions per block, keyed by the active set
+      // (a decomposition is a pure function of K_AA: caching changes no bit);
+      // lanes per slot look up, a miss replaces the least recently used slot
+      const double key = (double)mask;
+      const unsigned hm = __ballot_sync(0xffffffffu, lane < kEigSlots && P[PMASK + lane] == key);
+      int slot = hm ? __ffs(hm) - 1 : -1;
       if (slot < 0) {
-        slot = (int)P[PREPL];
+        double st = lane < kEigSlots ? P[PSTAMP + lane] : INFINITY;
+        int sl = lane;
+        for (int o = kEigSlots / 2; o; o >>= 1) {
+          const double os = __shfl_xor_sync(0xffffffffu, st, o);
+          const int ol = __shfl_xor_sync(0xffffffffu, sl, o);
+          if (os < st || (os == st && ol < sl)) { st = os; sl = ol; }
+        }
+        slot = __shfl_sync(0xffffffffu, sl, 0);
         double *A = na <= kSmemEig ? ws.A : W;
         double *Vt = na <= kSmemEig ? ws.V : Vc + slot * m * m;
         for (int e = lane; e < na * na; e += 32) A[e] = K[ws.active[e / na] * m + ws.active[e % na]];
@@ -971,7 +988,12 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
         pe.add(c, 2);
         if (na <= kSmemEig)
           for (int e = lane; e < na * na; e += 32) Vc[slot * m * m + e] = Vt[e];
-        if (lane == 0) { P[PMASK + slot] = (double)mask; P[PREPL] = (double)(slot ^ 1); }
+        if (lane == 0) P[PMASK + slot] = key;
+      }
+      if (lane == 0) {
+        const double t = P[PCLK] + 1.0;
+        P[PCLK] = t;
+        P[PSTAMP + slot] = t;
       }
       __syncwarp();
       const double *Vs = Vc + slot * m * m, *es = evc + slot * m;
@@ -1643,7 +1665,8 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       bool hask = m > 1 && c.rows[kRowD * first + RK] > 0.0;
       if (hask && m > kMaxBlockRows) return false;
       if (hask && koff + m * m > kKCap) return false;
-      if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; P[PMASK] = P[PMASK + 1] = -1.0; P[PREPL] = 0.0; }
+      if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; P[PCLK] = 0.0; }
+      if (lane < kEigSlots) { P[PMASK + lane] = -1.0; P[PSTAMP + lane] = 0.0; }
       if (hask) {
         double *K = c.K + koff;
         const double *r0 = c.rows + kRowD * first;
@@ -1707,7 +1730,7 @@ __device__ void substep_sweeps(Ctx &c) {
             pr.add(c, 5);
           } else {
             const int koff = (int)P[PKOFF];
-            solve_block(c, g, first, m, c.K + koff, S.u.sol.ws, c.W, c.Vc + 2 * koff, c.evc + 2 * first);
+            solve_block(c, g, first, m, c.K + koff, S.u.sol.ws, c.W, c.Vc + kEigSlots * koff, c.evc + kEigSlots * first);
           }
         }
     }
@@ -1909,7 +1932,7 @@ __device__ void sweeps_cta(Ctx &c, HeavyShared &H, int warp, BlockWS &ws, double
           __syncwarp();
         } else {
           const int koff = (int)P[PKOFF];
-          solve_block(c, g, first, m, c.K + koff, ws, W, c.Vc + 2 * koff, c.evc + 2 * first);
+          solve_block(c, g, first, m, c.K + koff, ws, W, c.Vc + kEigSlots * koff, c.evc + kEigSlots * first);
         }
       }
       __syncthreads();
@@ -1943,8 +1966,8 @@ __device__ void make_ctx(Ctx &c, const DevBatch &B, WarpSmem &S, int env, int la
   c.pairs = c.rows + (size_t)B.row_cap * kRowD;
   c.K = c.pairs + kMaxGroups * kPairD;
   c.Vc = c.K + kKCap;
-  c.evc = c.Vc + 2 * kKCap;
-  c.bcache = c.evc + 2 * kMaxContacts;
+  c.evc = c.Vc + kEigSlots * kKCap;
+  c.bcache = c.evc + kEigSlots * kMaxContacts;
   c.pcache = c.bcache + 14 * kMaxBodies;
   c.ccache = c.pcache + 18 * kMaxPartsCache;
   c.W = c.ccache + kMaxBodies + 1 + (size_t)warp * kMaxBlockRows * kMaxBlockRows;
@@ -2124,7 +2147,8 @@ __global__ void __launch_bounds__(32 * kHeavyWarps) step_kernel_cta(DevBatch B, 
 }
 
 __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
-  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + 3 * kKCap + 2 * kMaxContacts + 14 * kMaxBodies +
+  return (size_t)row_cap * kRowD + kMaxGroups * kPairD + (1 + kEigSlots) * kKCap + kEigSlots * kMaxContacts +
+         14 * kMaxBodies +
          18 * kMaxPartsCache + kMaxBodies + 1 +
          (size_t)kHeavyWarps * kMaxBlockRows * kMaxBlockRows;
 }

@@ -11,7 +11,6 @@ Prints one JSON line per scenario: env-steps/s (IK + 4 substeps + grasp),
 ms per step, per-env latency p50/p99/max, envs with awake clutter."""
 import ctypes as C
 import json
-import math
 import os
 import sys
 
@@ -28,27 +27,6 @@ from paper_2106_14405_b200.state import WorldState  # noqa: E402
 E = int(os.environ.get("ENVS", "4096"))
 STEPS = int(os.environ.get("STEPS", "30"))
 WARM = 3
-
-
-def interact_states(gids, pool):
-    out = []
-    for gid in gids:
-        blobs = pool[gid % 3]
-        st = WorldState.from_bytes(blobs[(gid // 3) % len(blobs)])
-        rng = np.random.default_rng(3000 + gid)
-        st.base = np.array([1.6 + rng.uniform(-0.05, 0.05), 0.2 + rng.uniform(-0.05, 0.05), math.pi / 2])
-        out.append(st.to_bytes())
-    return out
-
-
-def interact_actions(n_env, n_steps):
-    a = np.zeros((n_steps, n_env, 6))
-    for k in range(n_steps):
-        if k < 20:
-            a[k, :, :3] = (0.015, 0.0, -0.012)
-        else:
-            a[k, :, :3] = (0.0, 0.015 if (k // 10) % 2 == 0 else -0.015, 0.0)
-    return a
 
 
 def run(name, states, actions, sim, dev):
@@ -100,7 +78,7 @@ def main():
     sim = BatchSimulator(layouts=(0, 1, 2), n_env=E, env_layout=layout_of(gids).tolist(), device=dev)
     pool = bench.settled_pool()
     run("idle", bench.idle_states(gids, pool), bench.action_table(E, WARM + STEPS + 1, seed=7), sim, dev)
-    run("interact", interact_states(gids, pool), interact_actions(E, WARM + STEPS + 1), sim, dev)
+    run("interact", bench.interact_states(gids, pool), bench.interact_actions(E, WARM + STEPS + 1), sim, dev)
     sim.close()
 
 

@@ -68,6 +68,19 @@ for i in np.argsort(-np.abs(d["cycles"])):
         miss_na.append(na_)
         slots[slots[2]] = mask_
         slots[2] ^= 1
+    def sim_cache(nslots):  # LRU over (substep, group) blocks, keyed by the active mask
+        lru, miss = {}, 0
+        for s_, g_, mask_ in zip(sub, g, mask):
+            q = lru.setdefault((s_, g_), [])
+            if mask_ in q:
+                q.remove(mask_)
+            else:
+                miss += 1
+                if len(q) >= nslots:
+                    q.pop(0)
+            q.append(mask_)
+        return miss
+    lru_misses = {k: sim_cache(k) for k in (2, 4, 8, 16)}
     blocks = collections.Counter()
     for s_, it_, g_, m_ in zip(sub, it, g, m):
         blocks[(s_, it_, g_)] = m_
@@ -75,4 +88,4 @@ for i in np.argsort(-np.abs(d["cycles"])):
           f"{len(blocks):4d} (m: {dict(collections.Counter(blocks.values()))}) | pinv calls {n:5d} "
           f"(na mean {na.mean() if n else 0:.1f}) sweeps/call {sweeps.mean() if n else 0:.1f} | "
           f"GPU-cache misses {misses} (na mean {np.mean(miss_na) if miss_na else 0:.1f}, sweeps {miss_sweeps}) | "
-          f"AS iters/solve {n / max(1, len(blocks)):.1f} | rows/substep {r.counters}", flush=True)
+          f"AS iters/solve {n / max(1, len(blocks)):.1f} | LRU misses by slots {lru_misses}", flush=True)

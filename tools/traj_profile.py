@@ -4,7 +4,7 @@ the rsim_bench_env_cycles probe, and the slowest envs.  Dumps the slowest
 envs' pre-step snapshots + actions to gpurun_out/heavy_envs.npz for offline
 replay on the oracle.
 
-    python tools/traj_profile.py [--envs 2048] [--steps 40]
+    python tools/traj_profile.py [--envs 2048] [--steps 40] [--interact]
 """
 import argparse
 import ctypes as C
@@ -25,14 +25,19 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--envs", type=int, default=2048)
 ap.add_argument("--steps", type=int, default=40)
 ap.add_argument("--top", type=int, default=6)
+ap.add_argument("--interact", action="store_true", help="the bench's Interact scenario instead of Idle")
 args = ap.parse_args()
 
 E = args.envs
 gids = shard_env_ids(0, 1, E)
 sim = BatchSimulator(layouts=(0, 1, 2), n_env=E, env_layout=layout_of(gids).tolist(), device="cuda")
-init = bench.idle_states(gids, bench.settled_pool())
+if args.interact:
+    init = bench.interact_states(gids, bench.settled_pool())
+    act = bench.interact_actions(E, args.steps)
+else:
+    init = bench.idle_states(gids, bench.settled_pool())
+    act = bench.action_table(E, args.steps, seed=7)
 sim.set_state(init)
-act = bench.action_table(E, args.steps, seed=7)
 act_d = torch.tensor(act, device="cuda")
 cyc = torch.zeros(E, dtype=torch.int64, device="cuda")
 sim.L.rsim_bench_env_cycles(sim._batch, C.c_void_p(cyc.data_ptr()))
