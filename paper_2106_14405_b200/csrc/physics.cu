@@ -70,7 +70,7 @@ struct BlockWS {
     double F[2 * kSmemEig * kSmemEig];  // block_impulse_friction staging (after the LCP)
   };
   int active[kMaxBlockRows];
-  int na, worst, converged, slot;
+  int na, converged, slot;
 };
 
 struct WarpSmem {
@@ -957,13 +957,23 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     ws.converged = 0;
   }
   __syncwarp();
+  // lexicographic (value, row) minimum over the lanes: the oracle's serial
+  // scans ("strictly smaller, or equal with a lower row") in one reduction
+  auto argmin = [&](double v, int r) {
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int orow = __shfl_xor_sync(0xffffffffu, r, o);
+      if (ov < v || (ov == v && orow < r)) { v = ov; r = orow; }
+    }
+    return r;
+  };
   for (int it = 0; it < 4 * m + 4; ++it) {
     const int na = ws.na;
+    const int act = lane < na ? ws.active[lane] : -1;  // this lane's active row (active is sorted)
     if (lane < m) ws.lam[lane] = 0.0;
-    unsigned mask = 0u;  // active set as a bitmask over the block's rows
-    for (int i = 0; i < na; ++i) mask |= 1u << ws.active[i];
+    const unsigned mask = __reduce_or_sync(0xffffffffu, act >= 0 ? 1u << act : 0u);  // the active set
     if (na) {
-      if (lane < na) ws.rhs[lane] = -ws.q[ws.active[lane]];
+      if (lane < na) ws.rhs[lane] = -ws.q[act];
       // kEigSlots cached decompositions per block, keyed by the active set
       // (a decomposition is a pure function of K_AA: caching changes no bit);
       // lanes per slot look up, a miss replaces the least recently used slot
@@ -997,12 +1007,14 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
       }
       __syncwarp();
       const double *Vs = Vc + slot * m * m, *es = evc + slot * m;
-      // x = sum_k (V_k . b / ev_k) V_k over ev_k > rcond * max|ev| (oracle pinv_solve order)
-      double smax = 0.0;
-      for (int i = 0; i < na; ++i) smax = fmax(smax, fabs(es[i]));
+      // x = sum_k (V_k . b / ev_k) V_k over ev_k > rcond * max|ev| (oracle pinv_solve
+      // order; the sums stay sequential, unrolled only to overlap the loads)
+      double smax = lane < na ? fabs(es[lane]) : 0.0;  // max is exact in any order
+      for (int o = 16; o; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
       if (lane < na) {
         const int k = lane;
         double cc = 0.0;
+#pragma unroll 4
         for (int i = 0; i < na; ++i) cc += Vs[i * na + k] * ws.rhs[i];
         ws.ck[k] = cc / es[k];
       }
@@ -1010,64 +1022,52 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
       if (lane < na) {
         const int i = lane;
         double x = 0.0;
+#pragma unroll 4
         for (int k = 0; k < na; ++k) {
           if (fabs(es[k]) <= 1e-8 * smax) continue;
           x += ws.ck[k] * Vs[i * na + k];
         }
-        ws.lam[ws.active[i]] = x;
+        ws.lam[act] = x;
       }
     }
     __syncwarp();
-    if (lane == 0) {
-      int worst = -1;
-      for (int i = 0; i < na; ++i) {
-        int ii = ws.active[i];
-        double l = ws.lam[ii];
-        if (l < -1e-10 && (worst < 0 || l < ws.lam[worst] || (l == ws.lam[worst] && ii < worst))) worst = ii;
-      }
-      ws.worst = worst;
+    // drop the most negative lambda (physics.py:790-800; lowest row on ties)
+    double lv = INFINITY;
+    if (lane < na) {
+      const double l = ws.lam[act];
+      if (l < -1e-10) lv = l;
     }
-    __syncwarp();
-    if (ws.worst >= 0) {
-      if (lane == 0) {
-        int k = 0;
-        for (int i = 0; i < na; ++i)
-          if (ws.active[i] != ws.worst) ws.active[k++] = ws.active[i];
-        ws.na = k;
-      }
+    int worst = argmin(lv, lv < INFINITY ? act : 0x7fffffff);
+    if (worst != 0x7fffffff) {
+      const bool keep = lane < na && act != worst;
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (keep) ws.active[__popc(km & ((1u << lane) - 1))] = act;
+      if (lane == 0) ws.na = na - 1;
       __syncwarp();
       continue;
     }
     // w = K lam + q on the inactive rows (lane i, oracle order)
-    if (lane < m) {
+    double wv = INFINITY;
+    if (lane < m && !((mask >> lane) & 1u)) {
       const int i = lane;
-      if (!((mask >> i) & 1u)) {
-        double wi = 0.0;
-        for (int j = 0; j < m; ++j) wi += K[i * m + j] * ws.lam[j];
-        wi += ws.q[i];
-        ws.wv[i] = wi;
-      }
+      double wi = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < m; ++j) wi += K[i * m + j] * ws.lam[j];
+      wi += ws.q[i];
+      ws.wv[i] = wi;
+      if (wi < -1e-10) wv = wi;
     }
-    __syncwarp();
-    if (lane == 0) {
-      int worst = -1;
-      for (int i = 0; i < m; ++i) {
-        if ((mask >> i) & 1u) continue;
-        double wi = ws.wv[i];
-        if (wi < -1e-10 && (worst < 0 || wi < ws.wv[worst] || (wi == ws.wv[worst] && i < worst))) worst = i;
-      }
-      if (worst >= 0) {
-        int k = na;
-        while (k > 0 && ws.active[k - 1] > worst) { ws.active[k] = ws.active[k - 1]; --k; }
-        ws.active[k] = worst;
-        ws.na = na + 1;
-      } else {
-        ws.converged = 1;
-      }
-      ws.worst = worst;
+    // add the most violated inactive row (lowest row on ties), keeping active sorted
+    worst = argmin(wv, wv < INFINITY ? lane : 0x7fffffff);
+    if (worst == 0x7fffffff) {
+      if (lane == 0) ws.converged = 1;
+      __syncwarp();
+      break;
     }
+    const int below = __popc(__ballot_sync(0xffffffffu, lane < na && act < worst));
+    if (lane < na) ws.active[act > worst ? lane + 1 : lane] = act;
+    if (lane == 0) { ws.active[below] = worst; ws.na = na + 1; }
     __syncwarp();
-    if (ws.converged) break;
   }
   pl.add(c, 3);
   PhaseClock pf(c);
