@@ -943,17 +943,19 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     ws.wv[lane] = row_vn(c, r) - r[RTGT];
   }
   __syncwarp();
+  bool start = false;  // initial active set: rows with lambda > 0 or w < 0, in row order
   if (lane < m) {
     const int i = lane;
     double s = 0.0;
+#pragma unroll 4
     for (int j = 0; j < m; ++j) s += K[i * m + j] * ws.cur[j];
     ws.q[i] = ws.wv[i] - s;
+    start = ws.cur[i] > 0.0 || ws.wv[i] < 0.0;
   }
+  const unsigned am = __ballot_sync(0xffffffffu, start);
+  if (start) ws.active[__popc(am & ((1u << lane) - 1))] = lane;
   if (lane == 0) {
-    int na = 0;
-    for (int i = 0; i < m; ++i)
-      if (ws.cur[i] > 0.0 || ws.wv[i] < 0.0) ws.active[na++] = i;
-    ws.na = na;
+    ws.na = __popc(am);
     ws.converged = 0;
   }
   __syncwarp();
