@@ -969,6 +969,10 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     }
     return r;
   };
+  // the block's decomposition cache directory in registers for the solve
+  // (lane s < kEigSlots: slot s's active-set key and last use), written back after it
+  double skey = lane < kEigSlots ? P[PMASK + lane] : -2.0, sstamp = lane < kEigSlots ? P[PSTAMP + lane] : INFINITY;
+  double clk = P[PCLK];
   for (int it = 0; it < 4 * m + 4; ++it) {
     const int na = ws.na;
     const int act = lane < na ? ws.active[lane] : -1;  // this lane's active row (active is sorted)
@@ -980,10 +984,10 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
       // (a decomposition is a pure function of K_AA: caching changes no bit);
       // lanes per slot look up, a miss replaces the least recently used slot
       const double key = (double)mask;
-      const unsigned hm = __ballot_sync(0xffffffffu, lane < kEigSlots && P[PMASK + lane] == key);
+      const unsigned hm = __ballot_sync(0xffffffffu, lane < kEigSlots && skey == key);
       int slot = hm ? __ffs(hm) - 1 : -1;
       if (slot < 0) {
-        double st = lane < kEigSlots ? P[PSTAMP + lane] : INFINITY;
+        double st = sstamp;
         int sl = lane;
         for (int o = kEigSlots / 2; o; o >>= 1) {
           const double os = __shfl_xor_sync(0xffffffffu, st, o);
@@ -1000,13 +1004,10 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
         pe.add(c, 2);
         if (na <= kSmemEig)
           for (int e = lane; e < na * na; e += 32) Vc[slot * m * m + e] = Vt[e];
-        if (lane == 0) P[PMASK + slot] = key;
+        if (lane == slot) skey = key;
       }
-      if (lane == 0) {
-        const double t = P[PCLK] + 1.0;
-        P[PCLK] = t;
-        P[PSTAMP + slot] = t;
-      }
+      clk += 1.0;
+      if (lane == slot) sstamp = clk;
       __syncwarp();
       const double *Vs = Vc + slot * m * m, *es = evc + slot * m;
       // x = sum_k (V_k . b / ev_k) V_k over ev_k > rcond * max|ev| (oracle pinv_solve
@@ -1071,6 +1072,8 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     if (lane == 0) { ws.active[below] = worst; ws.na = na + 1; }
     __syncwarp();
   }
+  if (lane < kEigSlots) { P[PMASK + lane] = skey; P[PSTAMP + lane] = sstamp; }
+  if (lane == 0) P[PCLK] = clk;
   pl.add(c, 3);
   PhaseClock pf(c);
   // register-resident impulse + friction pass for blocks without joint
