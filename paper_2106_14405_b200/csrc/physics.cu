@@ -1754,22 +1754,30 @@ __device__ void substep_back(Ctx &c, double dt) {
         double *lv = LV(c, b), *av = AV(c, b);
         for (int i = 0; i < 3; ++i) { lv[i] = S.u.sol.vel[b][i]; av[i] = S.u.sol.vel[b][3 + i]; }
       }
-    // events + force tally in row order (lane 0)
-    if (lane == 0) {
-      const int held = HELD(c);
-      double acc = S.sd[c.L->acc];
-      for (int i = 0; i < nc; ++i) {
-        const double *r = c.rows + kRowD * i;
-        double lam = r[RLAM];
+    // events + force tally in row order: each row's impulse lanes-parallel,
+    // then lane 0 visits the rows that register one, in order
+    const int held = HELD(c);
+    double acc = S.sd[c.L->acc];
+    for (int i0 = 0; i0 < nc; i0 += 32) {
+      double lam = 0.0;
+      if (i0 + lane < nc) {
+        const double *r = c.rows + kRowD * (i0 + lane);
+        lam = r[RLAM];
         if (r[RK] <= 0.0) lam = fmax(-r[RVN], 0.0);
-        if (lam <= 0.0) continue;
-        double force = lam / dt;
-        emit_event(c, r, lam, force);
-        int a = (int)r[RA], b = (int)r[RB];
-        if (sc.body_robot[a] || sc.body_robot[b] || a == held || b == held) acc += force;
       }
-      S.sd[c.L->acc] = acc;
+      for (unsigned m = __ballot_sync(0xffffffffu, i0 + lane < nc && !(lam <= 0.0)); m; m &= m - 1) {
+        const int src = __ffs(m) - 1;
+        const double l = __shfl_sync(0xffffffffu, lam, src);
+        if (lane == 0) {
+          const double *r = c.rows + kRowD * (i0 + src);
+          const double force = l / dt;
+          emit_event(c, r, l, force);
+          const int a = (int)r[RA], b = (int)r[RB];
+          if (sc.body_robot[a] || sc.body_robot[b] || a == held || b == held) acc += force;
+        }
+      }
     }
+    if (lane == 0) S.sd[c.L->acc] = acc;
     __syncwarp();
   }
 
