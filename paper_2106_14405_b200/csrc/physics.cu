@@ -103,6 +103,7 @@ struct WarpSmem {
   unsigned long long awake_dyn;
   int moved_mask, dragged, n_active, max_active;
   int64_t ctr[3];
+  unsigned kpos[kMaxContacts / 32];  // rows with k > 0, by ballot of the row build (bit i % 32 of word i / 32)
 };
 
 // 5 two-warp CTAs per SM (228 KB of shared memory, 1 KB reserved per CTA)
@@ -1153,6 +1154,18 @@ __device__ void emit_event(Ctx &c, const double *r, double lam, double force) {
   }
 }
 
+// does group g hold a row with k > 0 (S.kpos of the row build)
+__device__ __forceinline__ bool group_has_k(const WarpSmem &S, int g) {
+  const int first = S.g_first[g], end = first + S.g_n[g];
+  for (int w = first >> 5; w <= (end - 1) >> 5; ++w) {
+    unsigned bits = S.kpos[w];
+    const int lo = w * 32 > first ? 0 : first - w * 32, hi = (w + 1) * 32 < end ? 32 : end - w * 32;
+    bits &= (hi == 32 ? ~0u : (1u << hi) - 1u) & ~((1u << lo) - 1u);
+    if (bits) return true;
+  }
+  return false;
+}
+
 // physics.py:657-701; returns false on capacity overflow
 // physics.py:657-699 up to the solver set-up (rows, blocks); false on capacity overflow
 __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, double dt, int sub) {
@@ -1602,8 +1615,10 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   __syncwarp();
   // rows (lanes per contact, over all groups at once; the groups partition
   // the contacts in order: g_first ascending)
-  for (int ci = lane; ci < nc; ci += 32) {
-    {
+  for (int c0 = 0; c0 < nc; c0 += 32) {
+    const int ci = c0 + lane;
+    bool kpos = false;
+    if (ci < nc) {
       int g = 0;
       while (g + 1 < ng && S.g_first[g + 1] <= ci) ++g;
       const double *P = c.pairs + kPairD * g;
@@ -1637,6 +1652,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
         for (int k = 0; k < 3; ++k) t2[k] /= l;
       }
       r[RK] = kk; r[RMU] = P[PMU]; r[RIMA] = P[PIMA]; r[RIMB] = P[PIMB];
+      kpos = kk > 0.0;
       r[RLAM] = r[RLT1] = r[RLT2] = 0.0;
       double vn = row_vn(c, r);
       r[RVN] = vn;
@@ -1649,15 +1665,13 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
         r[RFRIC] = 1.0;
       }
     }
+    const unsigned kb = __ballot_sync(0xffffffffu, kpos);
+    if (lane == 0) S.kpos[c0 >> 5] = kb;
   }
   __syncwarp();
   {  // groups with a row of k > 0 (the only ones the sweeps change): load metric for scheduling
     int act = 0;
-    for (int g = lane; g < ng; g += 32) {
-      bool a = false;
-      for (int i = S.g_first[g]; i < S.g_first[g] + S.g_n[g]; ++i) a |= c.rows[kRowD * i + RK] > 0.0;
-      act += a;
-    }
+    for (int g = lane; g < ng; g += 32) act += group_has_k(S, g);
     act = __reduce_add_sync(0xffffffffu, act);
     if (lane == 0) S.n_active = act;
   }
@@ -1667,7 +1681,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     for (int g = 0; g < ng; ++g) {
       const int first = S.g_first[g], m = S.g_n[g];
       double *P = c.pairs + kPairD * g;
-      bool hask = m > 1 && c.rows[kRowD * first + RK] > 0.0;
+      bool hask = m > 1 && ((S.kpos[first >> 5] >> (first & 31)) & 1u);  // first row's k > 0
       if (hask && m > kMaxBlockRows) return false;
       if (hask && koff + m * m > kKCap) return false;
       if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; P[PCLK] = 0.0; }
@@ -1719,10 +1733,7 @@ __device__ void substep_sweeps(Ctx &c) {
     // blocks in sorted pair order (physics.py:931-937).
     // Rows with k <= 0 are no-ops in the reference (physics.py:1294): when
     // every row is such, the sweeps change nothing and are skipped.
-    bool any_k = false;
-    for (int i = lane; i < nc; i += 32) any_k |= c.rows[kRowD * i + RK] > 0.0;
-    any_k = __any_sync(0xffffffffu, any_k);
-    if (any_k) {
+    if (S.n_active > 0) {  // some row has k > 0
       for (int it = 0; it < cfg.solver_iterations; ++it)
         for (int g = 0; g < ng; ++g) {
           const int first = S.g_first[g], m = S.g_n[g];
@@ -1902,9 +1913,8 @@ __device__ void build_levels(Ctx &c, HeavyShared &H) {
   int count[kMaxGroups + 1];
   int nlev = 0;
   for (int g = 0; g < ng; ++g) {
-    const int first = S.g_first[g], m = S.g_n[g];
-    bool act = false;
-    for (int i = first; i < first + m; ++i) act |= c.rows[kRowD * i + RK] > 0.0;
+    const int first = S.g_first[g];
+    const bool act = group_has_k(S, g);
     level[g] = -1;
     if (!act) continue;
     const double *r0 = c.rows + kRowD * first;
