@@ -1375,20 +1375,41 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     }
     pb2.add(c, 13);
     PhaseClock pb3(c);
-    // emit rows in order (lanes per row, prefix sums of the row counts)
+    // emit the pairs in (a, b) order: row offsets by a prefix sum over the
+    // rows (lanes per row; kept in S.wake_idx, scratch until the admission
+    // walk), then lanes per output pair: its row by binary search over the
+    // offsets, its partner as the j-th set bit of the row (rank select)
+    int *const roff = S.wake_idx;
     for (int a0 = 0; a0 < nb; a0 += 32) {
       const int a = a0 + lane;
-      const unsigned long long row = a < nb ? S.cbits[a] : 0ull;
-      const int cnt = __popcll(row);
+      const int cnt = a < nb ? __popcll(S.cbits[a]) : 0;
       int incl = cnt;
       for (int off = 1; off < 32; off <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += v;
       }
-      int idx = ncand + incl - cnt;
-      for (unsigned long long r = row; r; r &= r - 1, ++idx)
-        if (idx < kMaxCand) S.cand[idx] = (uint16_t)((a << 8) | (__ffsll((long long)r) - 1));
+      if (a < nb) roff[a] = ncand + incl - cnt;
       ncand += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    const int nemit = ncand < kMaxCand ? ncand : kMaxCand;
+    for (int k = lane; k < nemit; k += 32) {
+      int lo = 0, hi = nb - 1;  // the row owning k: last a with roff[a] <= k
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (roff[mid] <= k) lo = mid; else hi = mid - 1;
+      }
+      const unsigned long long row = S.cbits[lo];
+      int j = k - roff[lo];  // rank of the partner bit within the row
+      unsigned m = (unsigned)row;
+      int pos = 0;
+      const int nlo = __popc(m);
+      if (j >= nlo) { j -= nlo; m = (unsigned)(row >> 32); pos = 32; }
+      for (int w = 16; w; w >>= 1) {
+        const int cw = __popc(m & ((1u << w) - 1u));
+        if (j >= cw) { j -= cw; m >>= w; pos += w; }
+      }
+      S.cand[k] = (uint16_t)((lo << 8) | pos);
     }
     if (lane == 0) S.cbits_valid = 1;
     pb3.add(c, 14);
