@@ -189,7 +189,11 @@ int rs_env_step(rs_batch *batch, const double *action, double dt, int32_t subste
 
 /* rs_env_step with a HOST action buffer, the observation o_t = render(s_t)
  * rendered concurrently on an internal stream (observation delay 1,
- * interleaved), and the per-env results of rs_step_host copied back. */
+ * interleaved), and the per-env results of rs_step_host copied back.
+ * Returns when the step and h_out_stats are complete (h_action may be
+ * reused); the observation tensors complete in `stream` order (`stream` is
+ * left waiting on the render), so a consumer on `stream`, or the next call,
+ * sees o_t. */
 int rs_env_step_host(rs_batch *batch, const double *h_action, double dt, int32_t substeps, uint32_t cam_mask,
                      uint8_t *rgba, float *depth, int32_t *ids, double *h_out_stats, void *stream);
 

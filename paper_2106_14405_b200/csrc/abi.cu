@@ -578,7 +578,10 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
   CUDA_TRY(cudaEventRecord(b->hp_join, hp));
   CUDA_TRY(cudaStreamWaitEvent(st, b->hp_join, 0));
   if (cam_mask) CUDA_TRY(cudaStreamWaitEvent(st, b->ev_join, 0));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  // return once the step and its host results are done; the observation
+  // completes in `stream` order (the next call's step waits for it there, so
+  // the host can enqueue step t+1 while o_t is still rendering)
+  CUDA_TRY(cudaEventSynchronize(b->hp_join));
   return RS_OK;
 }
 
@@ -784,6 +787,9 @@ int rs_env_step_host(rs_batch *b, const double *h_action, double dt, int32_t sub
   CUDA_TRY(cudaEventRecord(b->hp_join, hp));
   CUDA_TRY(cudaStreamWaitEvent(st, b->hp_join, 0));
   if (cam_mask) CUDA_TRY(cudaStreamWaitEvent(st, b->ev_join, 0));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  // return once the step and its host results are done; the observation
+  // completes in `stream` order (the next call's step waits for it there, so
+  // the host can enqueue step t+1 while o_t is still rendering)
+  CUDA_TRY(cudaEventSynchronize(b->hp_join));
   return RS_OK;
 }
