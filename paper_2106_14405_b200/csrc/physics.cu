@@ -1915,18 +1915,20 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
 // non-zero solver inverse mass, or a scene joint's joint_dv); groups of one
 // level touch disjoint state, so solving them concurrently gives bit-identical
 // results to the reference's sequential order (physics.py:931-937).
-constexpr int kHeavyWarps = 4;
+constexpr int kHeavyWarps = 16;  // the widest CTA (scratch is sized for it)
 constexpr int kHeavyGroups = 2;  // envs with >= this many active groups go to the CTA kernel
 
+template <int kW>
 struct HeavyShared {
-  BlockWS ws[kHeavyWarps - 1];  // block-solver workspaces of warps 1..
+  BlockWS ws[kW - 1];  // block-solver workspaces of warps 1..
   int16_t lvl_order[kMaxGroups];
   int16_t lvl_start[kMaxGroups + 1];
   int nlev, ok;
 };
 
 // wavefront levels of the active groups (warp 0, lane 0)
-__device__ void build_levels(Ctx &c, HeavyShared &H) {
+template <class HS>
+__device__ void build_levels(Ctx &c, HS &H) {
   WarpSmem &S = *c.S;
   const int ng = S.ng, nb = c.sc->nb;
   int16_t level[kMaxGroups];
@@ -1962,11 +1964,12 @@ __device__ void build_levels(Ctx &c, HeavyShared &H) {
 }
 
 // all warps of the CTA; ends with a CTA barrier
-__device__ void sweeps_cta(Ctx &c, HeavyShared &H, int warp, BlockWS &ws, double *W) {
+template <int kW>
+__device__ void sweeps_cta(Ctx &c, HeavyShared<kW> &H, int warp, BlockWS &ws, double *W) {
   const int iters = c.cfg->solver_iterations, nlev = H.nlev;
   for (int it = 0; it < iters; ++it)
     for (int l = 0; l < nlev; ++l) {
-      for (int idx = H.lvl_start[l] + warp; idx < H.lvl_start[l + 1]; idx += kHeavyWarps) {
+      for (int idx = H.lvl_start[l] + warp; idx < H.lvl_start[l + 1]; idx += kW) {
         const int g = H.lvl_order[idx];
         const int first = c.S->g_first[g], m = c.S->g_n[g];
         const double *P = c.pairs + kPairD * g;
@@ -2138,15 +2141,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
   if (B.env_cycles && lane == 0) B.env_cycles[env] = clock64() - t_begin;
 }
 
-// CTA of kHeavyWarps warps per env (envs flagged heavy by the previous step)
-__global__ void __launch_bounds__(32 * kHeavyWarps) step_kernel_cta(DevBatch B, const double *arm_targets,
+// CTA of kW warps per env (envs flagged heavy by the previous step)
+template <int kW>
+__global__ void __launch_bounds__(32 * kW) step_kernel_cta(DevBatch B, const double *arm_targets,
                                                                    const double *base_cmd, int base_stride,
                                                                    const uint8_t *has_targets, double dt,
                                                                    int substeps, const uint8_t *heavy_in,
                                                                    uint8_t *heavy_out) {
   extern __shared__ __align__(16) unsigned char dsm[];
   WarpSmem &S = *reinterpret_cast<WarpSmem *>(dsm);
-  HeavyShared &H = *reinterpret_cast<HeavyShared *>(dsm + ((sizeof(WarpSmem) + 15) & ~(size_t)15));
+  HeavyShared<kW> &H = *reinterpret_cast<HeavyShared<kW> *>(dsm + ((sizeof(WarpSmem) + 15) & ~(size_t)15));
   const int env = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!heavy_in[env]) return;
   if (B.env_active && !B.env_active[env]) {
@@ -2204,11 +2208,14 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
                         cudaEvent_t join) {
   static bool configured = false;
   const size_t smem = sizeof(WarpSmem) * kWarpsPerBlock;
-  const size_t smem_cta = ((sizeof(WarpSmem) + 15) & ~(size_t)15) + sizeof(HeavyShared);
+  const size_t ws0 = (sizeof(WarpSmem) + 15) & ~(size_t)15;
+  const size_t smem16 = ws0 + sizeof(HeavyShared<16>), smem8 = ws0 + sizeof(HeavyShared<8>);
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(step_kernel_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cta);
+      e = cudaFuncSetAttribute(step_kernel_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem16);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(step_kernel_cta<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -2216,8 +2223,16 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
     // contact-heavy envs (flagged by the previous step) on a second stream, first
     cudaEventRecord(fork, stream);
     cudaStreamWaitEvent(side, fork, 0);
-    step_kernel_cta<<<B.n_env, 32 * kHeavyWarps, smem_cta, side>>>(B, arm, base_cmd, base_stride, has_targets, dt,
-                                                                     substeps, heavy_in, heavy_out);
+    // 16 warps per heavy env for batches up to 2048 envs; 8 for larger ones,
+    // whose many heavy envs would crowd the SMs with mostly idle warps
+    // (measured: bench 2048 envs +2 % with 16; configs[2] 4096 envs Interact
+    // 568 k with 8 vs 500 k with 16)
+    if (B.n_env <= 2048)
+      step_kernel_cta<16><<<B.n_env, 32 * 16, smem16, side>>>(B, arm, base_cmd, base_stride, has_targets, dt,
+                                                              substeps, heavy_in, heavy_out);
+    else
+      step_kernel_cta<8><<<B.n_env, 32 * 8, smem8, side>>>(B, arm, base_cmd, base_stride, has_targets, dt,
+                                                           substeps, heavy_in, heavy_out);
     cudaEventRecord(join, side);
   }
   dim3 grid((B.n_env + kWarpsPerBlock - 1) / kWarpsPerBlock);
