@@ -778,8 +778,10 @@ int rs_env_step_host(rs_batch *b, const double *h_action, double dt, int32_t sub
     if (rc) return rc;
     CUDA_TRY(cudaEventRecord(b->ev_join, b->side));
   }
-  CUDA_TRY(cudaStreamWaitEvent(hp, b->ev_fork, 0));
+  // the action upload first: the previous call's step (the only reader of
+  // d_env_act) is complete, so it overlaps the previous observation's render
   CUDA_TRY(cudaMemcpyAsync(b->d_env_act, h_action, sizeof(double) * (size_t)E * 6, cudaMemcpyHostToDevice, hp));
+  CUDA_TRY(cudaStreamWaitEvent(hp, b->ev_fork, 0));
   rc = rs_env_step(b, b->d_env_act, dt, substeps, hp);
   if (rc) return rc;
   CUDA_TRY(launch_stats(b->view(), b->d_stats, hp));
