@@ -1916,7 +1916,11 @@ __device__ bool substep(Ctx &c, const double *arm, const double *basecmd, double
 // level touch disjoint state, so solving them concurrently gives bit-identical
 // results to the reference's sequential order (physics.py:931-937).
 constexpr int kHeavyWarps = 16;  // the widest CTA (scratch is sized for it)
-constexpr int kHeavyGroups = 2;  // envs with >= this many active groups go to the CTA kernel
+// batches up to this size run their contact-heavy envs in 16-warp CTAs (8 above)
+constexpr int kWideHeavyMaxEnvs = 2048;
+// envs with >= this many active contact groups go to the CTA kernel in the next
+// step: 3 with the 16-warp CTAs, 2 with the 8-warp ones (measured)
+__host__ __device__ inline int heavy_groups(int n_env) { return n_env <= kWideHeavyMaxEnvs ? 3 : 2; }
 
 template <int kW>
 struct HeavyShared {
@@ -2078,7 +2082,7 @@ __device__ void env_end(Ctx &c, const DevBatch &B, int env, double dt, bool ok, 
   WarpSmem &S = *c.S;
   const StateLayout &L = B.L;
   const int lane = c.lane;
-  if (lane == 0 && heavy_out) heavy_out[env] = S.max_active >= kHeavyGroups ? 1 : 0;
+  if (lane == 0 && heavy_out) heavy_out[env] = S.max_active >= heavy_groups(B.n_env) ? 1 : 0;
   if (!ok) {
     if (lane == 0) B.fault[env] = (uint32_t)RS_FAULT_OVERFLOW << 16;
     copy_through(B, env, lane);
@@ -2227,7 +2231,7 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
     // whose many heavy envs would crowd the SMs with mostly idle warps
     // (measured: bench 2048 envs +2 % with 16; configs[2] 4096 envs Interact
     // 568 k with 8 vs 500 k with 16)
-    if (B.n_env <= 2048)
+    if (B.n_env <= kWideHeavyMaxEnvs)
       step_kernel_cta<16><<<B.n_env, 32 * 16, smem16, side>>>(B, arm, base_cmd, base_stride, has_targets, dt,
                                                               substeps, heavy_in, heavy_out);
     else
