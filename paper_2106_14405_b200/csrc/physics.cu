@@ -1925,46 +1925,59 @@ __host__ __device__ inline int heavy_groups(int n_env) { return n_env <= kWideHe
 template <int kW>
 struct HeavyShared {
   BlockWS ws[kW - 1];  // block-solver workspaces of warps 1..
+  unsigned long long res[kMaxGroups];  // per group: the velocities it writes (bodies, then joints)
+  int16_t level[kMaxGroups];           // wavefront level (-1: no row with k > 0)
   int16_t lvl_order[kMaxGroups];
   int16_t lvl_start[kMaxGroups + 1];
   int nlev, ok;
 };
 
-// wavefront levels of the active groups (warp 0, lane 0)
+// wavefront levels of the active groups (warp 0, warp-collective): group g's
+// level is 1 + the highest level of an earlier active group sharing a written
+// velocity (lanes over the earlier groups, max-reduced), 0 if none
 template <class HS>
 __device__ void build_levels(Ctx &c, HS &H) {
   WarpSmem &S = *c.S;
-  const int ng = S.ng, nb = c.sc->nb;
-  int16_t level[kMaxGroups];
-  unsigned long long res[kMaxGroups];
-  int count[kMaxGroups + 1];
+  const int ng = S.ng, nb = c.sc->nb, lane = c.lane;
+  for (int g = lane; g < ng; g += 32) {
+    const bool act = group_has_k(S, g);
+    unsigned long long rs = 0ull;
+    if (act) {
+      const double *r0 = c.rows + kRowD * S.g_first[g];
+      if (r0[RIMA] > 0.0) rs |= 1ull << (int)r0[RA];
+      if (r0[RIMB] > 0.0) rs |= 1ull << (int)r0[RB];
+      if (r0[RJA] >= 0.0) rs |= 1ull << (nb + (int)r0[RJA]);
+      if (r0[RJB] >= 0.0) rs |= 1ull << (nb + (int)r0[RJB]);
+    }
+    H.res[g] = rs;
+    H.level[g] = act ? 0 : -1;
+  }
+  __syncwarp();
   int nlev = 0;
   for (int g = 0; g < ng; ++g) {
-    const int first = S.g_first[g];
-    const bool act = group_has_k(S, g);
-    level[g] = -1;
-    if (!act) continue;
-    const double *r0 = c.rows + kRowD * first;
-    unsigned long long rs = 0ull;
-    if (r0[RIMA] > 0.0) rs |= 1ull << (int)r0[RA];
-    if (r0[RIMB] > 0.0) rs |= 1ull << (int)r0[RB];
-    if (r0[RJA] >= 0.0) rs |= 1ull << (nb + (int)r0[RJA]);
-    if (r0[RJB] >= 0.0) rs |= 1ull << (nb + (int)r0[RJB]);
-    res[g] = rs;
-    int lv = 0;
-    for (int h = 0; h < g; ++h)
-      if (level[h] >= 0 && (res[h] & rs) && level[h] + 1 > lv) lv = level[h] + 1;
-    level[g] = (int16_t)lv;
+    if (H.level[g] < 0) continue;
+    const unsigned long long rs = H.res[g];
+    int lv = -1;
+    for (int h = lane; h < g; h += 32)
+      if (H.level[h] >= 0 && (H.res[h] & rs) && H.level[h] > lv) lv = H.level[h];
+    lv = __reduce_max_sync(0xffffffffu, lv) + 1;
+    __syncwarp();
+    if (lane == 0) H.level[g] = (int16_t)lv;
+    __syncwarp();
     if (lv + 1 > nlev) nlev = lv + 1;
   }
-  for (int l = 0; l <= nlev; ++l) count[l] = 0;
-  for (int g = 0; g < ng; ++g)
-    if (level[g] >= 0) count[level[g] + 1]++;
-  for (int l = 0; l < nlev; ++l) count[l + 1] += count[l];
-  for (int l = 0; l <= nlev; ++l) H.lvl_start[l] = (int16_t)count[l];
-  for (int g = 0; g < ng; ++g)
-    if (level[g] >= 0) H.lvl_order[count[level[g]]++] = (int16_t)g;
-  H.nlev = nlev;
+  if (lane == 0) {  // groups ordered by level, group order within a level (counting sort)
+    int count[kMaxGroups + 1];
+    for (int l = 0; l <= nlev; ++l) count[l] = 0;
+    for (int g = 0; g < ng; ++g)
+      if (H.level[g] >= 0) count[H.level[g] + 1]++;
+    for (int l = 0; l < nlev; ++l) count[l + 1] += count[l];
+    for (int l = 0; l <= nlev; ++l) H.lvl_start[l] = (int16_t)count[l];
+    for (int g = 0; g < ng; ++g)
+      if (H.level[g] >= 0) H.lvl_order[count[H.level[g]]++] = (int16_t)g;
+    H.nlev = nlev;
+  }
+  __syncwarp();
 }
 
 // all warps of the CTA; ends with a CTA barrier
@@ -2180,12 +2193,12 @@ __global__ void __launch_bounds__(32 * kW) step_kernel_cta(DevBatch B, const dou
   bool ok = true;
   for (int s = 0; s < substeps; ++s) {
     if (warp == 0) {
-      bool f = substep_front(c, arm, bc, dts, s);
+      const bool f = substep_front(c, arm, bc, dts, s);
       if (lane == 0) {
         H.ok = f;
         if (S.n_active > S.max_active) S.max_active = S.n_active;
-        if (f) build_levels(c, H);
       }
+      if (f) build_levels(c, H);
     }
     __syncthreads();
     ok = H.ok;
