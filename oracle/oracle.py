@@ -73,6 +73,8 @@ def lib():
                                  C.c_void_p, C.c_void_p]
         L.orc_sphere_cast.restype = C.c_int
         L.orc_sphere_cast.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p]
+        L.orc_grasp.restype = C.c_int
+        L.orc_grasp.argtypes = [C.c_void_p, C.c_char_p, C.c_double, C.c_void_p, C.c_void_p]
         L.orc_snapshot_size.restype = C.c_int64
         L.orc_snapshot_size.argtypes = [C.c_int, C.c_int]
         _lib = L
@@ -211,6 +213,16 @@ class Oracle:
         st = lib().orc_settle(self.h, bytes(spawn), placed_mask, max_steps, floor_z, out.ctypes.data,
                               info.ctypes.data, C.byref(val), C.byref(steps))
         return st, out.tobytes(), info, val.value, steps.value
+
+    def grasp(self, snapshot: bytes, gripper: float):
+        """grasp_rule + apply_grasp: (snapshot after, (kind, body, joint, wakes));
+        kind 0 none, 1 snap, 2 release."""
+        out = np.zeros(self.snap_size, np.uint8)
+        tr = np.zeros(4, np.int32)
+        r = lib().orc_grasp(self.h, bytes(snapshot), float(gripper), out.ctypes.data, tr.ctypes.data)
+        if r:
+            raise ValueError(f"oracle grasp error {r}")
+        return out.tobytes(), tuple(int(x) for x in tr)
 
     def apply_arm_action(self, q, delta):
         """(joint targets, ik_failed) -- robot.apply_arm_action restated."""

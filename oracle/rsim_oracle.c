@@ -2136,3 +2136,79 @@ int orc_apply_arm_action(const orc_world *w, const double *q, const double *delt
   memcpy(targets, q, 8 * n);
   return 1;
 }
+
+/* ------------------------------------------------------------------ grasp
+ * The env pipeline's grasp phase between control steps: robot.py:323-346
+ * grasp_rule over physics.py:1039-1053 grasp_candidates, then
+ * physics.py:1055-1079 apply_grasp.  holding = state.held >= 0 (an object or
+ * a handle).  out[4] = (kind 0 none / 1 snap / 2 release, body, scene-joint
+ * index of a handle snap or -1, wakes counted by Simulator.wake). */
+int orc_grasp(const orc_world *w, const uint8_t *snap_in, double gripper, uint8_t *snap_out, int32_t *out) {
+  static ostate st;
+  int r = unpack(snap_in, &st, w->nb, w->nsj + w->narm);
+  if (r) return r;
+  out[0] = 0; out[1] = -1; out[2] = -1; out[3] = 0;
+  const int holding = st.held >= 0;
+  if (gripper > 0 && !holding) {
+    pose_t ee;
+    ee_pose(w, &st, &ee);
+    double best_d = 0.0;
+    int best_b = -1, best_j = -1;
+    /* candidates: clutter COMs (id order, the held body skipped), then handles */
+    for (int c = 0; c < w->nclutter; ++c) {
+      int b = w->clutter[c];
+      if (b == st.held) continue;
+      pose_t bp;
+      double com[3], e[3];
+      body_pose(&st, b, &bp);
+      apply(&bp, w->com + 3 * b, com);
+      for (int i = 0; i < 3; ++i) e[i] = ee.p[i] - com[i];
+      double d = sqrt(dot3(e, e));
+      /* near.sort(key=(d, body)); near[0] */
+      if (d <= 0.15 && (best_b < 0 || d < best_d || (d == best_d && b < best_b))) { best_d = d; best_b = b; best_j = -1; }
+    }
+    for (int ji = 0; ji < w->nsj; ++ji) {
+      pose_t child;
+      double h[3], e[3];
+      joint_child_pose(w, &st, ji, st.joints[ji], &child);  /* scene.py:439-440 handle_world */
+      apply(&child, w->joint_handle + 3 * ji, h);
+      for (int i = 0; i < 3; ++i) e[i] = ee.p[i] - h[i];
+      double d = sqrt(dot3(e, e));
+      int b = w->joint_body[ji];
+      if (d <= 0.15 && (best_b < 0 || d < best_d || (d == best_d && b < best_b))) { best_d = d; best_b = b; best_j = ji; }
+    }
+    if (best_b >= 0) {
+      out[0] = 1; out[1] = best_b; out[2] = best_j;
+      if (best_j >= 0) {
+        st.held_joint = best_j;
+        st.held = best_b;
+        st.grab_q = st.joints[best_j];
+        memcpy(st.grab_ee, ee.p, 24);
+      } else {
+        orc_trace tr;
+        memset(&tr, 0, sizeof tr);
+        wake(w, &st, best_b, &tr);
+        out[3] = (int32_t)tr.counters[2];
+        pose_t inv, bp, rel;
+        inverse(&ee, &inv);
+        body_pose(&st, best_b, &bp);
+        compose(&inv, &bp, &rel);
+        st.held = best_b;
+        memcpy(st.held_offset, rel.p, 24);
+        mat_to_quat(rel.R, st.held_offset + 3);
+        memset(st.lv[best_b], 0, 24);
+        memset(st.av[best_b], 0, 24);
+      }
+    }
+  } else if (gripper < 0 && holding) {
+    out[0] = 2;
+    if (st.held >= 0 && st.held_joint < 0) {
+      st.asleep[st.held] = 0;
+      st.sleep_counter[st.held] = 0;
+    }
+    st.held = -1;
+    st.held_joint = -1;
+  }
+  pack(&st, snap_out);
+  return 0;
+}

@@ -695,9 +695,291 @@ def gen_nav():
     print(f"  nav: {len(fields)} fields, {len(q_dist)} queries, max path {max(path_len)}")
 
 
+# --------------------------------------------------------------------------
+# env-step records with grasp transitions (riders, pick & place)
+# --------------------------------------------------------------------------
+
+GRASP_KIND = {"none": 0, "snap": 1, "release": 2}
+
+
+def grasp_step(sim, st, gripper):
+    """The restated env pipeline's grasp phase (robot.py:323-346,
+    physics.py:1039-1084): holding = ``state.held >= 0`` (object or handle).
+    Returns (kind, body, joint index, wakes counted)."""
+    w0 = sim.counters["wakes"]
+    tr = rb.grasp_rule(float(gripper), st.held >= 0, sim.grasp_candidates(st))
+    sim.apply_grasp(st, tr)
+    ji = -1
+    if tr.joint is not None:
+        ji = sim.scene.joints.index(sim.scene.joint_by_id(tr.joint))
+    return GRASP_KIND[tr.kind], -1 if tr.body is None else int(tr.body), ji, sim.counters["wakes"] - w0
+
+
+def record_env(sim, st, items, name):
+    """Step records with an optional grasp after each physics step.
+
+    ``items``: callables ``f(sim, st) -> dict`` returning ``action`` (dEE xyz,
+    gripper, base lin, base ang: IK -> physics -> grasp, the device env step)
+    or ``targets`` (JointTargets or None) + ``gripper`` (None = no grasp); an
+    optional ``mutate(sim, st)`` edits the state before the step (teleports).
+    Per step: ``pre``, targets, ``post`` (after the physics step, the
+    teacher-forcing record of ``record``), ``gripper`` (nan = none),
+    ``grasped`` (after the grasp), ``trans`` (kind, body, joint index, wakes)
+    and ``action`` (nan row when the step was not action-driven)."""
+    rec = Recorder(sim)
+    cols = {k: [] for k in ("pre", "post", "arm", "base", "has_targets", "counters", "gripper", "grasped",
+                            "trans", "action")}
+    pairs, pair_off, contacts, contact_off, events, event_off = [], [0], [], [0], [], [0]
+    m = sim.robot
+    for t, item in enumerate(items):
+        spec = item(sim, st)
+        if "mutate" in spec:
+            spec["mutate"](sim, st)
+        action = np.full(6, np.nan)
+        if "action" in spec:
+            action = np.asarray(spec["action"], float)
+            stats = {}
+            tg = rb.apply_arm_action(m, st.joints[sim.arm_slice()], rb.ArmAction(action[:3], action[3]), stats)
+            tg.base = rb.BaseAction(action[4], action[5])
+            gripper = action[3]
+        else:
+            tg, gripper = spec.get("targets"), spec.get("gripper")
+        rec.reset()
+        c0 = dict(sim.counters)
+        pre = st
+        st, ev = sim.step_physics(st, tg)
+        cols["pre"].append(np.frombuffer(pre.to_bytes(), np.uint8))
+        cols["post"].append(np.frombuffer(st.to_bytes(), np.uint8))
+        cols["has_targets"].append(tg is not None)
+        cols["arm"].append(np.asarray(tg.arm, float) if tg is not None else np.zeros(7))
+        cols["base"].append([tg.base.linear_velocity, tg.base.angular_velocity] if tg is not None else [0.0, 0.0])
+        cols["counters"].append([sim.counters[k] - c0[k] for k in ("narrowphase_tests", "skipped_sleeping_pairs", "wakes")])
+        cols["action"].append(action)
+        st = st.clone()
+        if gripper is None:
+            cols["gripper"].append(np.nan)
+            cols["trans"].append([0, -1, -1, 0])
+        else:
+            cols["gripper"].append(float(gripper))
+            cols["trans"].append(list(grasp_step(sim, st, gripper)))
+        cols["grasped"].append(np.frombuffer(st.to_bytes(), np.uint8))
+        assert len(rec.sub_pairs) == 4
+        for sp, sc in zip(rec.sub_pairs, rec.sub_contacts):
+            pairs.extend(sp); pair_off.append(len(pairs))
+            contacts.extend(sc); contact_off.append(len(contacts))
+        for e in ev:
+            events.append([e.bodies[0], e.bodies[1], e.impulse, e.force, *e.point])
+        event_off.append(len(events))
+    out = {k: np.array(v) for k, v in cols.items()}
+    out.update(
+        meta=meta(),
+        pairs=np.array(pairs, np.int32).reshape(-1, 2), pair_off=np.array(pair_off, np.int64),
+        contacts=np.array(contacts, float).reshape(-1, 9), contact_off=np.array(contact_off, np.int64),
+        events=np.array(events, float).reshape(-1, 7), event_off=np.array(event_off, np.int64),
+        final=np.frombuffer(st.to_bytes(), np.uint8),
+    )
+    np.savez_compressed(os.path.join(OUT, f"traj_{name}.npz"), **out)
+    tr = out["trans"]
+    print(f"  traj_{name}: {len(items)} steps, {len(pairs)} pairs, {len(contacts)} contacts, {len(events)} events, "
+          f"snaps {int((tr[:, 0] == 1).sum())} releases {int((tr[:, 0] == 2).sum())}")
+    return st
+
+
+def reach_joints(sim, base, target_world, seed=None):
+    """Arm joints putting the EE at ``target_world`` from ``base`` (reference IK)."""
+    m = sim.robot
+    local = rb.base_pose3(np.asarray(base, float)).inverse().apply(np.asarray(target_world, float))
+    return rb.solve_ik(m, local, m.resting_joints if seed is None else seed)
+
+
+def ee_toward(sim, st, target_world, step=0.015):
+    """dEE (robot base frame) moving the EE toward a world point, clamped."""
+    ee = sim.ee_pose(st).pos
+    d = rb.base_pose3(st.base).rot.T @ (np.asarray(target_world, float) - ee)
+    n = float(np.linalg.norm(d))
+    return d if n <= step else d * (step / n)
+
+
+def rider_state(sim, pool_state, base, arm, drawers=((2, 0, (-0.18, 0.05)), (2, 2, (0.17, -0.06)),
+                                                       (1, 4, (0.0, 0.0)), (0, 3, (0.1, 0.02)))):
+    """``make_initial_state(..., clutter_asleep=True)`` (physics.py:344-380) with
+    clutter resting inside the kitchen-cabinet drawer trays -> ``_bind_riders``
+    (physics.py:383-405) binds them to their drawer joints.  ``drawers`` =
+    (drawer index, clutter index, tray-local xy); the other clutter keeps its
+    settled pool pose."""
+    poses = [pool_state.body_pose(b) for b in sim.clutter_body_ids]
+    for di, ci, (x, y) in drawers:
+        sj = sim.scene.joint_by_id(f"kitchen_cabinet#1:drawer_{di}")
+        tray = sim.scene.bodies[sj.body_id].initial_pose
+        bid = sim.clutter_body_ids[ci]
+        rot = tray.rot @ geo.rot_z(0.3 + 0.7 * ci)
+        lo, _ = geo.parts_aabb(sim.bodies[bid].parts, geo.Pose(rot, np.zeros(3)))
+        p = tray.apply(np.array([x, y, 0.02])) + np.array([0.0, 0.0, -lo[2] + 1e-3])
+        poses[ci] = geo.Pose(rot, p)
+    st = sim.make_initial_state(poses, base=np.asarray(base, float), arm_joints=arm, clutter_asleep=True)
+    return st
+
+
+def gen_env_records(pool_blobs, pool_tags):
+    first = {v: physics.WorldState.from_bytes(b.tobytes()) for b, (v, s) in reversed(list(zip(pool_blobs, pool_tags)))}
+
+    # ---- riders: drawer clutter bound by make_initial_state, drawer pulled
+    # open through a handle snap, released mid-motion (the drawer coasts,
+    # riders follow), then the arm reaches into the tray and wakes a rider.
+    sim, _ = make_sim(0)
+    sj = sim.scene.joint_by_id("kitchen_cabinet#1:drawer_2")
+    ji = sim.scene.joints.index(sj)
+    handle = sj.handle_world(sim.scene.bodies[sj.parent_body].initial_pose, 0.0)
+    base = np.array([handle[0] + 0.75, handle[1], math.pi])
+    arm = reach_joints(sim, base, handle + np.array([0.02, 0.0, 0.0]))
+    st = rider_state(sim, first[0], base, arm)
+    assert sum(int(r) >= 0 for r in st.rider_joint) == 4, st.rider_joint
+    q0 = arm.copy()
+    items = [lambda sim, st: {"targets": rb.JointTargets(arm=q0.copy()), "gripper": 1.0}]
+    items += [lambda sim, st: {"targets": rb.JointTargets(arm=q0.copy(), base=rb.BaseAction(-0.5, 0.0)),
+                               "gripper": 0.0}] * 22
+    items += [lambda sim, st: {"targets": rb.JointTargets(arm=q0.copy(), base=rb.BaseAction(-0.5, 0.0)),
+                               "gripper": -1.0}]
+    items += [lambda sim, st: {"targets": rb.JointTargets(arm=q0.copy())}] * 3
+    rider = sim.clutter_body_ids[2]
+
+    def reach_rider(sim, st):
+        # approach from above, then descend onto the rider; walk in while far
+        com = st.body_pose(rider).apply(sim.bodies[rider].com_local)
+        ee = sim.ee_pose(st).pos
+        above = com + np.array([0.0, 0.0, 0.15])
+        tgt = above if np.linalg.norm((ee - above)[:2]) > 0.03 and ee[2] > com[2] + 0.1 else com + np.array([0.0, 0.0, 0.03])
+        lin = 0.3 if np.linalg.norm(st.base[:2] - com[:2]) > 0.6 else 0.0
+        return {"action": [*ee_toward(sim, st, tgt), 0.0, lin, 0.0]}
+    items += [reach_rider] * 40
+    items += [lambda sim, st: {"action": [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]}]        # snap whatever is nearest
+    items += [lambda sim, st: {"action": [0.0, 0.0, 0.015, 0.0, 0.0, 0.0]}] * 6  # lift
+    items += [lambda sim, st: {"action": [0.0, 0.0, -0.01, -1.0, 0.0, 0.0]}]     # release (wake) while moving
+    items += [lambda sim, st: {"action": [0.0, 0.0, 0.0, 0.0, 0.0, 0.0]}] * 8
+    st = record_env(sim, st, items, "riders")
+
+    # ---- pick & place: Interact spawn facing the light table, reach the
+    # nearest clutter COM, snap, lift and turn, release (falls, wakes others)
+    sim, _ = make_sim(0)
+    st = first[0].clone()
+    st.base = np.array([1.75, 0.44, math.pi / 2])  # walkable, the table clutter within reach
+    sim._update_robot_link_poses(st, 0.0)
+    ee = sim.ee_pose(st).pos
+    coms = {b: st.body_pose(b).apply(sim.bodies[b].com_local) for b in sim.clutter_body_ids}
+    obj = min(coms, key=lambda b: (float(np.linalg.norm(coms[b] - ee)), b))
+
+    def reach_obj(sim, st):
+        com = st.body_pose(obj).apply(sim.bodies[obj].com_local)
+        return {"action": [*ee_toward(sim, st, com + np.array([0.0, 0.0, 0.04])), 0.0, 0.0, 0.0]}
+    items = [reach_obj] * 40
+    items += [lambda sim, st: {"action": [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]}]
+    items += [lambda sim, st: {"action": [0.0, 0.0, 0.015, 0.5, 0.0, 0.4]}] * 8   # hold (scalar > 0 ignored)
+    items += [lambda sim, st: {"action": [0.01, 0.0, 0.0, 0.0, -0.2, 0.0]}] * 4
+    items += [lambda sim, st: {"action": [0.0, 0.0, -0.01, -1.0, 0.0, 0.0]}]
+    items += [lambda sim, st: {"action": [0.0, 0.0, 0.0, 0.0, 0.0, 0.0]}] * 12
+    record_env(sim, st, items, "pick")
+
+
+def gen_grasp():
+    """``grasp_rule`` + ``apply_grasp`` transitions on single states
+    (robot.py:323-346, physics.py:1039-1084): clutter snaps, the 0.15 m
+    boundary, exact ties (same asset, same pose: lowest id), drawer-handle and
+    fridge-door snaps, sleeping riders (wake clears the binding), releases of
+    objects (wake) and handles (no wake), no-ops while holding / empty."""
+    cases = {k: [] for k in ("layout", "pre", "gripper", "post", "trans")}
+    rng = np.random.default_rng(29)
+    pool = np.load(os.path.join(OUT, "settled_pool.npz"))
+
+    def add(v, sim, st, g):
+        pre = np.frombuffer(st.to_bytes(), np.uint8)
+        s2 = st.clone()
+        tr = grasp_step(sim, s2, g)
+        cases["layout"].append(v); cases["pre"].append(pre); cases["gripper"].append(float(g))
+        cases["post"].append(np.frombuffer(s2.to_bytes(), np.uint8)); cases["trans"].append(list(tr))
+        return s2
+
+    def place_com(sim, st, b, com):
+        p = st.body_pose(b)
+        st.pos[b] = com - p.rot @ sim.bodies[b].com_local
+
+    for v in range(3):
+        sim, _ = make_sim(v)
+        blobs = [b for b, t in zip(pool["snapshots"], pool["tags"]) if t[0] == v][:3]
+        for blob in blobs:
+            st0 = physics.WorldState.from_bytes(blob.tobytes())
+            for k in range(14):
+                st = st0.clone()
+                st.base = np.array([rng.uniform(-2, 2), rng.uniform(-1.5, 1.5), rng.uniform(-3, 3)])
+                st.joints[sim.arm_slice()] = rng.uniform(sim.robot.limits_lo(), sim.robot.limits_hi())
+                sim._update_robot_link_poses(st, 0.0)
+                ee = sim.ee_pose(st).pos
+                b = sim.clutter_body_ids[rng.integers(len(sim.clutter_body_ids))]
+                d = rng.normal(size=3)
+                r = [0.149, 0.151, rng.uniform(0.02, 0.2)][k % 3]
+                place_com(sim, st, b, ee + d / np.linalg.norm(d) * r)
+                if k % 5 == 2:  # an awake, moving body: snap zeroes its velocity, no wake counted
+                    st.asleep[b] = False
+                    st.sleep_counter[b] = 3
+                    st.lin_vel[b] = rng.normal(size=3) * 0.1
+                    st.ang_vel[b] = rng.normal(size=3)
+                if k % 7 == 5:  # a second body of the same asset at the identical pose: tie -> lowest id
+                    twin = b + 9 if b + 9 in sim.clutter_body_ids else b - 9
+                    st.pos[twin], st.quat[twin] = st.pos[b].copy(), st.quat[b].copy()
+                    st.asleep[twin] = True
+                s2 = add(v, sim, st, 1.0)
+                if k % 4 == 0:
+                    add(v, sim, st, 0.0)
+                    add(v, sim, st, -1.0)  # not holding: no-op
+                if s2.held >= 0:
+                    add(v, sim, s2, 1.0)   # holding: no-op
+                    s3 = s2.clone()
+                    s3.asleep[s2.held] = True  # release wakes even a sleeping held body
+                    s3.sleep_counter[s2.held] = 7
+                    add(v, sim, s3, -1.0)
+        # handle snaps: every scene joint, EE placed on / near the handle by the reference IK
+        for sj in sim.scene.joints:
+            ji = sim.scene.joints.index(sj)
+            st = physics.WorldState.from_bytes(blobs[0].tobytes())
+            q = float(rng.uniform(*sj.joint.limits)) * 0.5
+            st.joints[ji] = q
+            sim._update_scene_joint_poses(st, [ji], 0.0)
+            h = sj.handle_world(st.body_pose(sj.parent_body), q)
+            yaw = math.atan2(h[1] - 0.0, h[0] - 0.0)
+            for dist, off in ((0.75, 0.03), (0.8, 0.12), (0.7, 0.2)):
+                base = np.array([h[0] - dist * math.cos(yaw), h[1] - dist * math.sin(yaw), yaw])
+                try:
+                    arm = reach_joints(sim, base, h + np.array([0.0, 0.0, off]))
+                except rb.NoSolution:
+                    continue
+                st.base = base
+                st.joints[sim.arm_slice()] = arm
+                sim._update_robot_link_poses(st, 0.0)
+                s2 = add(v, sim, st, 1.0)
+                if s2.held_joint >= 0:
+                    add(v, sim, s2, -1.0)  # handle release: no wake
+    # sleeping riders snapped (wake clears rider_joint) -- layout 0 drawers
+    sim, _ = make_sim(0)
+    st0 = physics.WorldState.from_bytes([b for b, t in zip(pool["snapshots"], pool["tags"]) if t[0] == 0][0].tobytes())
+    for ci in (0, 2, 4, 3):
+        st = rider_state(sim, st0, np.zeros(3), None)
+        bid = sim.clutter_body_ids[ci]
+        com = st.body_pose(bid).apply(sim.bodies[bid].com_local)
+        base = np.array([com[0] + 0.75, com[1], math.pi])
+        st.base = base
+        st.joints[sim.arm_slice()] = reach_joints(sim, base, com + np.array([0.0, 0.0, 0.06]))
+        sim._update_robot_link_poses(st, 0.0)
+        add(0, sim, st, 1.0)
+    out = {k: np.array(v) for k, v in cases.items()}
+    np.savez_compressed(os.path.join(OUT, "grasp.npz"), meta=meta(), **out)
+    kinds = out["trans"][:, 0]
+    print(f"  grasp: {len(kinds)} cases: none {int((kinds == 0).sum())} snap {int((kinds == 1).sum())} "
+          f"(handles {int((out['trans'][:, 2] >= 0).sum())}) release {int((kinds == 2).sum())} "
+          f"wakes {int(out['trans'][:, 3].sum())}")
+
+
 if __name__ == "__main__":
     t0 = time.time()
-    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav", "settle", "cast"]
+    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav", "settle", "cast", "env", "grasp"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
     blobs = tags = None
@@ -720,3 +1002,8 @@ if __name__ == "__main__":
         gen_settle(); print("settle", time.time() - t0)
     if "cast" in what:
         gen_cast(); print("cast", time.time() - t0)
+    if "env" in what:
+        p = np.load(os.path.join(OUT, "settled_pool.npz"))
+        gen_env_records(list(p["snapshots"]), [tuple(t) for t in p["tags"]]); print("env", time.time() - t0)
+    if "grasp" in what:
+        gen_grasp(); print("grasp", time.time() - t0)

@@ -22,7 +22,7 @@ from paper_2106_14405_b200.scene import build_world, flat_clutter
 from paper_2106_14405_b200.state import WorldState
 
 LAYOUT = {"idle": 0, "fixed": 1, "interact": 0, "awake": 2, "drop": 0, "drop_floor": 0, "settle": 1,
-          "tilt": 0, "drawer": 0, "fridge": 0, "held": 0}
+          "tilt": 0, "drawer": 0, "fridge": 0, "held": 0, "riders": 0, "pick": 0}
 EV_NOISE = 1e-12
 POS_TOL, VEL_TOL = 1e-12, 1e-10
 
