@@ -67,7 +67,17 @@ enum {
   RS_FAULT_NONFINITE_QUAT = 2,
   RS_FAULT_NONFINITE_VEL = 3,
   RS_FAULT_NONFINITE_JOINT = 4,
-  RS_FAULT_OVERFLOW = 5 /* contact/pair capacity exceeded: result invalid */
+  RS_FAULT_OVERFLOW = 5 /* a per-substep capacity exceeded: the env keeps its input state;
+                          low 16 bits = which one (RS_OVF_*) */
+};
+/* capacities of one substep of one env (fault word low bits with RS_FAULT_OVERFLOW) */
+enum {
+  RS_OVF_CANDIDATES = 1,   /* overlapping AABB pairs > 1024 */
+  RS_OVF_ADMITTED = 2,     /* admitted pairs > 256 */
+  RS_OVF_CONTACTS = 3,     /* contact rows > 512 */
+  RS_OVF_GROUPS = 4,       /* touching pairs > 96 */
+  RS_OVF_BLOCK_ROWS = 5,   /* contacts of one pair in a block solve > 32 */
+  RS_OVF_BLOCK_MATRIX = 6  /* sum of m^2 over the block matrices > 8192 */
 };
 
 #define RS_NO_GROUP ((int32_t)0x80000000)

@@ -19,6 +19,9 @@ U8P = C.POINTER(C.c_uint8)
 RS_OK, RS_ERR_ARG, RS_ERR_CUDA, RS_ERR_SNAPSHOT, RS_ERR_CAPACITY = 0, 1, 2, 3, 4
 FAULT_KINDS = {1: "non-finite pos", 2: "non-finite quat", 3: "non-finite vel", 4: "non-finite joint position",
                5: "capacity overflow"}
+# low 16 bits of a capacity-overflow fault word (include/rsim.h RS_OVF_*)
+OVERFLOW_KINDS = {1: "AABB-overlap candidates > 1024", 2: "admitted pairs > 256", 3: "contact rows > 512",
+                  4: "touching pairs > 96", 5: "contacts of one pair > 32", 6: "block matrices > 8192 entries"}
 
 
 class rs_scene_desc(C.Structure):

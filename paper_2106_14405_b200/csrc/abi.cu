@@ -17,7 +17,7 @@ namespace rsim {
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
                         const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream,
                         const uint8_t *heavy_in, uint8_t *heavy_out, cudaStream_t side, cudaEvent_t fork,
-                        cudaEvent_t join);
+                        cudaEvent_t join, int force_width);
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                           cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
@@ -101,6 +101,7 @@ struct rs_batch {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // contact-heavy scheduling: per-env flags (ping-pong like the state) and a physics side stream
   uint8_t *heavy[2] = {nullptr, nullptr};
+  int force_heavy = 0;  // rsim_bench_force_heavy: 0, or the CTA width every env is stepped with
   cudaStream_t phys_side = nullptr;
   cudaEvent_t ph_fork = nullptr, ph_join = nullptr;
   // host-buffer steps: physics on a high-priority stream next to the render
@@ -130,8 +131,9 @@ static int upload(rs_scene *s, const T *src, size_t n, const T **dst) {
 int rs_scene_create(const rs_scene_desc *D, rs_scene **out) {
   if (!D || !out) return fail(RS_ERR_ARG, "null argument");
   const int nb = D->n_bodies, np = D->n_parts, nf = D->n_facets, nj = D->n_scene_joints + D->n_arm;
-  if (nb > kMaxBodies || nj > kMaxJoints || D->n_arm > kMaxArm || np > 128 || nf > 1024 || D->n_scene_joints > 30)
-    return fail(RS_ERR_CAPACITY, "scene exceeds compiled capacities (bodies<=48, joints<=16, parts<=128, facets<=1024)");
+  if (nb > kMaxBodies || nj > kMaxJoints || D->n_arm > kMaxArm || np > 128 || nf > kMaxFacets ||
+      D->n_scene_joints > 30)
+    return fail(RS_ERR_CAPACITY, "scene exceeds compiled capacities (bodies<=64, joints<=16, parts<=128, facets<=2048)");
   for (int p = 0; p < np; ++p)
     if (D->part_facet_begin[p + 1] - D->part_facet_begin[p] > kMaxFacetsPerPart)
       return fail(RS_ERR_CAPACITY, "part with more than 48 facets");
@@ -471,8 +473,12 @@ static cudaError_t launch_step_b(rs_batch *b, const double *arm, const double *b
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_join, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
+  if (b->force_heavy) {  // debug: every env through the CTA kernel of that width
+    cudaError_t e = cudaMemsetAsync(b->heavy[b->cur], 1, (size_t)b->d.n_env, st);
+    if (e != cudaSuccess) return e;
+  }
   return launch_step(b->view(), arm, base_cmd, base_stride, has_targets, dt, substeps, st, b->heavy[b->cur],
-                     b->heavy[b->cur ^ 1], b->phys_side, b->ph_fork, b->ph_join);
+                     b->heavy[b->cur ^ 1], b->phys_side, b->ph_fork, b->ph_join, b->force_heavy);
 }
 
 // physics of a host-buffer step runs on a highest-priority stream so that the
@@ -698,6 +704,13 @@ int rs_nav_path(rs_batch *b, const double *fields, const int32_t *field_of_query
   if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
   CUDA_TRY(launch_nav_path(b->view(), b->nav_nx, b->nav_ny, fields, field_of_query, scene_of_query, from_xy,
                            n_queries, cap, waypoints, count, (cudaStream_t)stream));
+  return RS_OK;
+}
+
+int rsim_bench_force_heavy(rs_batch *b, int width) {
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  if (width != 0 && width != 8 && width != 16) return fail(RS_ERR_ARG, "width must be 0, 8 or 16");
+  b->force_heavy = width;
   return RS_OK;
 }
 

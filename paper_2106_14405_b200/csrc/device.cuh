@@ -16,10 +16,11 @@
 
 namespace rsim {
 
-constexpr int kMaxBodies = 48;   // 42 in the benchmark world
+constexpr int kMaxBodies = 64;   // 42 in the benchmark world (64-bit body masks)
 constexpr int kMaxJoints = 16;   // 4 scene + 7 arm
 constexpr int kMaxArm = 8;
 constexpr int kMaxFacetsPerPart = 48;
+constexpr int kMaxFacets = 2048;  // per scene (render stages every world plane in shared memory)
 
 struct DevScene {
   int nb, np, nf, nv, nt, nsj, narm, robot_base, nclutter;
@@ -57,8 +58,9 @@ struct DevScene {
 // offsets (in doubles / int32s) inside one env's slabs
 struct StateLayout {
   int nb, nj;
-  // doubles
-  int pos, quat, lv, av, rider_off, joints, jvel, base, held_off, grab_ee, grab_q, acc, time, dbl_size;
+  // doubles; [0, stage) is what the step kernel stages in shared memory (the
+  // rider offsets after it are constant during a step and stay in HBM)
+  int pos, quat, lv, av, joints, jvel, base, held_off, grab_ee, grab_q, acc, time, stage, rider_off, dbl_size;
   // int32
   int asleep, sleep_ctr, rider_joint, held, held_joint, int_size;
 
@@ -70,7 +72,6 @@ struct StateLayout {
     L.quat = o; o += 4 * nb;
     L.lv = o; o += 3 * nb;
     L.av = o; o += 3 * nb;
-    L.rider_off = o; o += 7 * nb;
     L.joints = o; o += nj;
     L.jvel = o; o += nj;
     L.base = o; o += 3;
@@ -79,6 +80,8 @@ struct StateLayout {
     L.grab_q = o; o += 1;
     L.acc = o; o += 1;
     L.time = o; o += 1;
+    L.stage = o;
+    L.rider_off = o; o += 7 * nb;
     L.dbl_size = (o + 3) & ~3;  // 32-byte multiple
     int i = 0;
     L.asleep = i; i += nb;

@@ -26,6 +26,7 @@
 // arithmetic rounds exactly like the C oracle (tests/test_gpu_physics.py).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 
@@ -36,16 +37,17 @@
 namespace rsim {
 
 constexpr int kWarpsPerBlock = 2;
-constexpr int kMaxCand = 512;
+constexpr int kMaxCand = 1024;
 constexpr int kMaxAdm = 256;
-constexpr int kMaxContacts = 128;
+constexpr int kMaxContacts = 512;  // rows per substep (HBM scratch); 2.8x the 26-object pile's 185
 constexpr int kMaxGroups = 96;
 constexpr int kMaxBlockRows = 32;
 constexpr int kRowD = 44;  // doubles per solver row in global scratch
 constexpr int kEigSlots = 16;  // cached eigendecompositions per block (LRU over active sets)
 constexpr int kPairD = 31 + 2 * kEigSlots;  // doubles per contact group (pair) in global scratch
-constexpr int kKCap = kMaxContacts * kMaxBlockRows;  // Sigma m^2 <= 32 * 128
+constexpr int kKCap = 8192;  // Sigma m^2 of the block matrices of one substep (<= 32 * 256)
 constexpr int kMaxPartsCache = 128;
+constexpr int kStageD = 13 * kMaxBodies + 2 * kMaxJoints + 16;  // most doubles of a staged slab (StateLayout::stage)
 
 // ---- row field offsets (doubles) ------------------------------------------
 enum {
@@ -74,8 +76,7 @@ struct BlockWS {
 };
 
 struct WarpSmem {
-  double sd[1024];
-  int32_t si[160];
+  int32_t si[3 * kMaxBodies + 4];  // asleep, sleep counters, rider joints, held, held joint
   // phase-scoped scratch: broadphase AABBs | narrowphase planes | solver velocities
   union {
     struct { double lo[kMaxBodies][3], hi[kMaxBodies][3]; } bp;
@@ -104,10 +105,19 @@ struct WarpSmem {
   int moved_mask, dragged, n_active, max_active;
   int64_t ctr[3];
   unsigned kpos[kMaxContacts / 32];  // rows with k > 0, by ballot of the row build (bit i % 32 of word i / 32)
+  double sd[2];  // the staged state slab [0, StateLayout::stage): sized at launch (warp_smem_bytes)
 };
 
+// shared memory of one env's warp: the fixed part + its staged slab (16-byte multiple)
+__host__ __device__ constexpr size_t warp_smem_bytes(int stage) {
+  return (sizeof(WarpSmem) - sizeof(double) * 2 + sizeof(double) * (size_t)stage + 15) & ~(size_t)15;
+}
+
 // 5 two-warp CTAs per SM (228 KB of shared memory, 1 KB reserved per CTA)
-static_assert(5 * (2 * sizeof(WarpSmem) + 1024) <= 228 * 1024, "step_kernel occupancy");
+static_assert(13 * kMaxBodies + 2 * kMaxJoints + 16 <= kStageD, "state slab prefix must fit the staging buffer");
+// 5 two-warp CTAs per SM even for a 64-body scene (228 KB of shared memory, 1 KB reserved per CTA)
+static_assert(5 * (2 * warp_smem_bytes(13 * kMaxBodies + 2 * kMaxJoints + 16) + 1024) <= 228 * 1024,
+              "step_kernel occupancy");
 
 struct Ctx {
   const DevScene *sc;
@@ -258,7 +268,8 @@ __device__ void update_scene_joint_poses(Ctx &c, int mask, double dt) {
       if (rj < 0 || !(moved & (1 << rj)) || !ASLEEP(c, b)) continue;
       Pose part, rel, np_;
       body_pose(c, sc.joint_body[rj], part);
-      const double *ro = c.S->sd + c.L->rider_off + 7 * b;
+      // rider offsets are constant during a step: read from the input slab in HBM
+      const double *ro = c.B->sd + (size_t)c.env * c.L->dbl_size + c.L->rider_off + 7 * b;
       quat_to_mat(ro + 3, rel.R);
       rel.p[0] = ro[0]; rel.p[1] = ro[1]; rel.p[2] = ro[2];
       compose(part, rel, np_);
@@ -1414,7 +1425,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     if (lane == 0) S.cbits_valid = 1;
     pb3.add(c, 14);
   }
-  if (ncand > kMaxCand) overflow = true;
+  if (ncand > kMaxCand) { overflow = true; if (lane == 0) S.fault = RS_OVF_CANDIDATES; }
   __syncwarp();
   pb.add(c, 8);
   PhaseClock pa(c);
@@ -1489,7 +1500,10 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     }
   }
   __syncwarp();
-  if (overflow || S.nadm > kMaxAdm) return false;
+  if (overflow || S.nadm > kMaxAdm) {
+    if (lane == 0 && !overflow) S.fault = RS_OVF_ADMITTED;
+    return false;
+  }
 
   pa.add(c, 9);
   PhaseClock pn(c);
@@ -1597,7 +1611,10 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     if (tr) c.B->trace_count[(size_t)c.env * c.B->trace_sub + sub] = nadm;
   }
   __syncwarp();
-  if (nct > kMaxContacts || ngp > kMaxGroups) return false;
+  if (nct > kMaxContacts || ngp > kMaxGroups) {
+    if (lane == 0) S.fault = nct > kMaxContacts ? RS_OVF_CONTACTS : RS_OVF_GROUPS;
+    return false;
+  }
   const int nc = S.nc, ng = S.ng;
 
   pn.add(c, 10);
@@ -1703,8 +1720,10 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       const int first = S.g_first[g], m = S.g_n[g];
       double *P = c.pairs + kPairD * g;
       bool hask = m > 1 && ((S.kpos[first >> 5] >> (first & 31)) & 1u);  // first row's k > 0
-      if (hask && m > kMaxBlockRows) return false;
-      if (hask && koff + m * m > kKCap) return false;
+      if (hask && (m > kMaxBlockRows || koff + m * m > kKCap)) {
+        if (lane == 0) S.fault = m > kMaxBlockRows ? RS_OVF_BLOCK_ROWS : RS_OVF_BLOCK_MATRIX;
+        return false;
+      }
       if (lane == 0) { P[PHASK] = hask ? 1.0 : 0.0; P[PKOFF] = koff; P[PCLK] = 0.0; }
       if (lane < kEigSlots) { P[PMASK + lane] = -1.0; P[PSTAMP + lane] = 0.0; }
       if (hask) {
@@ -1813,9 +1832,19 @@ __device__ void substep_back(Ctx &c, double dt) {
     __syncwarp();
   }
 
-  // ---- integrate (physics.py:962-1011): lanes per body
+  // ---- integrate (physics.py:962-1011): lanes per body.  The corrections
+  // read every body's sleep flag as it was before this loop (the reference
+  // computes all of them first): a snapshot of the flags, because a lane may
+  // put its body to sleep while another lane (or its own second round, body
+  // b + 32) is still summing the corrections of a contact with it.
   {
     const int held = HELD(c);
+    unsigned long long asleep0 = 0ull;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const unsigned m = __ballot_sync(0xffffffffu, b0 + lane < nb && ASLEEP(c, b0 + lane));
+      asleep0 |= (unsigned long long)m << b0;
+    }
+    __syncwarp();
     for (int b = lane; b < nb; b += 32) {
       if (!((S.awake_dyn >> b) & 1ull)) continue;
       double corr[3] = {0.0, 0.0, 0.0};
@@ -1823,8 +1852,8 @@ __device__ void substep_back(Ctx &c, double dt) {
       for (int g = 0; g < ng; ++g) {
         int a = S.g_a[g], bb = S.g_b[g];
         if (a != b && bb != b) continue;
-        double ima = (!ASLEEP(c, a) && a != held) ? sc.inv_mass[a] : 0.0;
-        double imb = (!ASLEEP(c, bb) && bb != held) ? sc.inv_mass[bb] : 0.0;
+        double ima = (!((asleep0 >> a) & 1ull) && a != held) ? sc.inv_mass[a] : 0.0;
+        double imb = (!((asleep0 >> bb) & 1ull) && bb != held) ? sc.inv_mass[bb] : 0.0;
         double tot = ima + imb;
         if (tot <= 0.0) continue;
         for (int i = S.g_first[g]; i < S.g_first[g] + S.g_n[g]; ++i) {
@@ -1925,7 +1954,8 @@ __host__ __device__ inline int heavy_groups(int n_env) { return n_env <= kWideHe
 template <int kW>
 struct HeavyShared {
   BlockWS ws[kW - 1];  // block-solver workspaces of warps 1..
-  unsigned long long res[kMaxGroups];  // per group: the velocities it writes (bodies, then joints)
+  unsigned long long res[kMaxGroups];  // per group: the body velocities it writes
+  unsigned resj[kMaxGroups];           // ... and the scene joints' joint_dv
   int16_t level[kMaxGroups];           // wavefront level (-1: no row with k > 0)
   int16_t lvl_order[kMaxGroups];
   int16_t lvl_start[kMaxGroups + 1];
@@ -1938,18 +1968,20 @@ struct HeavyShared {
 template <class HS>
 __device__ void build_levels(Ctx &c, HS &H) {
   WarpSmem &S = *c.S;
-  const int ng = S.ng, nb = c.sc->nb, lane = c.lane;
+  const int ng = S.ng, lane = c.lane;
   for (int g = lane; g < ng; g += 32) {
     const bool act = group_has_k(S, g);
     unsigned long long rs = 0ull;
+    unsigned rj = 0u;
     if (act) {
       const double *r0 = c.rows + kRowD * S.g_first[g];
       if (r0[RIMA] > 0.0) rs |= 1ull << (int)r0[RA];
       if (r0[RIMB] > 0.0) rs |= 1ull << (int)r0[RB];
-      if (r0[RJA] >= 0.0) rs |= 1ull << (nb + (int)r0[RJA]);
-      if (r0[RJB] >= 0.0) rs |= 1ull << (nb + (int)r0[RJB]);
+      if (r0[RJA] >= 0.0) rj |= 1u << (int)r0[RJA];
+      if (r0[RJB] >= 0.0) rj |= 1u << (int)r0[RJB];
     }
     H.res[g] = rs;
+    H.resj[g] = rj;
     H.level[g] = act ? 0 : -1;
   }
   __syncwarp();
@@ -1957,9 +1989,10 @@ __device__ void build_levels(Ctx &c, HS &H) {
   for (int g = 0; g < ng; ++g) {
     if (H.level[g] < 0) continue;
     const unsigned long long rs = H.res[g];
+    const unsigned rj = H.resj[g];
     int lv = -1;
     for (int h = lane; h < g; h += 32)
-      if (H.level[h] >= 0 && (H.res[h] & rs) && H.level[h] > lv) lv = H.level[h];
+      if (H.level[h] >= 0 && ((H.res[h] & rs) || (H.resj[h] & rj)) && H.level[h] > lv) lv = H.level[h];
     lv = __reduce_max_sync(0xffffffffu, lv) + 1;
     __syncwarp();
     if (lane == 0) H.level[g] = (int16_t)lv;
@@ -2050,7 +2083,7 @@ __device__ bool env_begin(Ctx &c, const DevBatch &B, int env) {
   }
   const double *gsd = B.sd + (size_t)env * L.dbl_size;
   const int32_t *gsi = B.si + (size_t)env * L.int_size;
-  for (int i = lane; i < L.dbl_size; i += 32) S.sd[i] = gsd[i];
+  for (int i = lane; i < L.stage; i += 32) S.sd[i] = gsd[i];
   for (int i = lane; i < L.int_size; i += 32) S.si[i] = gsi[i];
   if (lane < 3) S.ctr[lane] = 0;
   if (lane == 0) { B.event_count[env] = 0; S.fault = 0; S.max_active = 0; }
@@ -2097,7 +2130,7 @@ __device__ void env_end(Ctx &c, const DevBatch &B, int env, double dt, bool ok, 
   const int lane = c.lane;
   if (lane == 0 && heavy_out) heavy_out[env] = S.max_active >= heavy_groups(B.n_env) ? 1 : 0;
   if (!ok) {
-    if (lane == 0) B.fault[env] = (uint32_t)RS_FAULT_OVERFLOW << 16;
+    if (lane == 0) B.fault[env] = ((uint32_t)RS_FAULT_OVERFLOW << 16) | (uint32_t)S.fault;
     copy_through(B, env, lane);
     return;
   }
@@ -2116,7 +2149,9 @@ __device__ void env_end(Ctx &c, const DevBatch &B, int env, double dt, bool ok, 
   __syncwarp();
   double *wsd = B.sd_out + (size_t)env * L.dbl_size;
   int32_t *wsi = B.si_out + (size_t)env * L.int_size;
-  for (int i = lane; i < L.dbl_size; i += 32) wsd[i] = S.sd[i];
+  for (int i = lane; i < L.stage; i += 32) wsd[i] = S.sd[i];
+  const double *rsd = B.sd + (size_t)env * L.dbl_size;  // rider offsets: unchanged by the step
+  for (int i = L.stage + lane; i < L.dbl_size; i += 32) wsd[i] = rsd[i];
   for (int i = lane; i < L.int_size; i += 32) wsi[i] = S.si[i];
 }
 
@@ -2127,7 +2162,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
                                                                    int substeps, const uint8_t *heavy_in,
                                                                    uint8_t *heavy_out) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  WarpSmem *smem = reinterpret_cast<WarpSmem *>(dsm);
+  const size_t stride = warp_smem_bytes(B.L.stage);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * kWarpsPerBlock + warp;
   if (slot >= B.n_env) return;
@@ -2139,7 +2174,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B
     return;
   }
   const long long t_begin = B.env_cycles ? clock64() : 0;
-  WarpSmem &S = smem[warp];
+  WarpSmem &S = *reinterpret_cast<WarpSmem *>(dsm + stride * warp);
   Ctx c;
   make_ctx(c, B, S, env, lane, 0);
   if (!env_begin(c, B, env)) return;
@@ -2167,7 +2202,7 @@ __global__ void __launch_bounds__(32 * kW) step_kernel_cta(DevBatch B, const dou
                                                                    uint8_t *heavy_out) {
   extern __shared__ __align__(16) unsigned char dsm[];
   WarpSmem &S = *reinterpret_cast<WarpSmem *>(dsm);
-  HeavyShared<kW> &H = *reinterpret_cast<HeavyShared<kW> *>(dsm + ((sizeof(WarpSmem) + 15) & ~(size_t)15));
+  HeavyShared<kW> &H = *reinterpret_cast<HeavyShared<kW> *>(dsm + warp_smem_bytes(B.L.stage));
   const int env = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!heavy_in[env]) return;
   if (B.env_active && !B.env_active[env]) {
@@ -2222,19 +2257,26 @@ int step_row_cap() { return kMaxContacts; }
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
                         const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream,
                         const uint8_t *heavy_in, uint8_t *heavy_out, cudaStream_t side, cudaEvent_t fork,
-                        cudaEvent_t join) {
-  static bool configured = false;
-  const size_t smem = sizeof(WarpSmem) * kWarpsPerBlock;
-  const size_t ws0 = (sizeof(WarpSmem) + 15) & ~(size_t)15;
+                        cudaEvent_t join, int force_width) {
+  // kernel attributes are per device context: configure each device once
+  static std::atomic<unsigned long long> configured{0ull};
+  const size_t ws0 = warp_smem_bytes(B.L.stage), wsmax = warp_smem_bytes(kStageD);
+  const size_t smem = ws0 * kWarpsPerBlock;
   const size_t smem16 = ws0 + sizeof(HeavyShared<16>), smem8 = ws0 + sizeof(HeavyShared<8>);
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (!(configured.load() >> dev & 1ull)) {
+    // sized for the largest staged slab any batch can have
+    e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsmax * kWarpsPerBlock));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(step_kernel_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem16);
+      e = cudaFuncSetAttribute(step_kernel_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(wsmax + sizeof(HeavyShared<16>)));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(step_kernel_cta<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8);
+      e = cudaFuncSetAttribute(step_kernel_cta<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(wsmax + sizeof(HeavyShared<8>)));
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(1ull << dev);
   }
   if (heavy_in && side) {
     // contact-heavy envs (flagged by the previous step) on a second stream, first
@@ -2244,7 +2286,7 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
     // whose many heavy envs would crowd the SMs with mostly idle warps
     // (measured: bench 2048 envs +2 % with 16; configs[2] 4096 envs Interact
     // 568 k with 8 vs 500 k with 16)
-    if (B.n_env <= kWideHeavyMaxEnvs)
+    if (force_width ? force_width == 16 : B.n_env <= kWideHeavyMaxEnvs)
       step_kernel_cta<16><<<B.n_env, 32 * 16, smem16, side>>>(B, arm, base_cmd, base_stride, has_targets, dt,
                                                               substeps, heavy_in, heavy_out);
     else

@@ -25,6 +25,8 @@
 // the two winning planes are divided.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cmath>
 #include <cstdint>
 
@@ -774,7 +776,7 @@ cudaError_t launch_render_tables(const DevBatch &B, cudaStream_t stream) {
 }
 
 static size_t render_smem(const DevBatch &B, int mode) {
-  const size_t planes = mode == kMeshExact ? 9 * (size_t)kMaxParts : 4 * (size_t)(B.max_nf > 0 ? B.max_nf : 1024);
+  const size_t planes = mode == kMeshExact ? 9 * (size_t)kMaxParts : 4 * (size_t)(B.max_nf > 0 ? B.max_nf : kMaxFacets);
   return kPlaneOff + sizeof(double) * planes;
 }
 
@@ -783,13 +785,16 @@ static cudaError_t launch_render_t(const DevBatch &B, uint32_t cam_mask, uint8_t
                                    cudaStream_t stream, unsigned long long *work) {
   int n_cam_out = __builtin_popcount(cam_mask);
   if (n_cam_out == 0) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {  // the largest any batch can ask for: 1024 facets
-    const size_t cap = kPlaneOff + sizeof(double) * (kMode == kMeshExact ? 9 * kMaxParts : 4 * 1024);
-    cudaError_t e = cudaFuncSetAttribute(render_kernel<kMode, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)cap);
+  // the attribute is per device context: configure each device once
+  static std::atomic<unsigned long long> configured{0ull};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (!(configured.load() >> dev & 1ull)) {  // the largest any batch can ask for: kMaxFacets facets
+    const size_t cap = kPlaneOff + sizeof(double) * (kMode == kMeshExact ? 9 * kMaxParts : 4 * kMaxFacets);
+    e = cudaFuncSetAttribute(render_kernel<kMode, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(1ull << dev);
   }
   dim3 grid(B.n_env * n_cam_out);
   render_kernel<kMode, kCount><<<grid, kRenderThreads, render_smem(B, kMode), stream>>>(

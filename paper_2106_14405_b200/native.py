@@ -64,6 +64,7 @@ def lib():
     L.rs_render_mesh.argtypes = [vp, u32, vp, vp, vp, vp]
     L.rsim_bench_render_exact.argtypes = [vp, u32, vp, vp, vp, vp]
     L.rsim_bench_env_cycles.argtypes = [vp, vp]
+    L.rsim_bench_force_heavy.argtypes = [vp, C.c_int]
     L.rsim_bench_phase_cycles.argtypes = [vp, vp]
     L.rsim_bench_render_work_detail.argtypes = [vp, u32, vp, vp]
     L.rs_arm_action.argtypes = [vp, vp, vp, vp, vp]

@@ -170,6 +170,8 @@ class BatchSimulator:
             kind, idx = int(f[e]) >> 16, int(f[e]) & 0xFFFF
             name = abi.FAULT_KINDS.get(kind, f"fault {kind}")
             what = self.worlds[self.layouts.index(self.layouts[self.env_scene[e]])].bodies
+            if kind == 5:
+                raise PhysicsFault(f"env {e}: {name} ({abi.OVERFLOW_KINDS.get(idx, idx)}); state unchanged")
             label = what[idx].name if kind in (1, 2, 3) and idx < len(what) else str(idx)
             raise PhysicsFault(f"env {e}: {name} for {'body' if kind in (1, 2, 3) else 'index'} {idx} ({label})")
 
@@ -191,6 +193,11 @@ class BatchSimulator:
                        torch.zeros((self.n_env, max_substeps), dtype=torch.int32, device=self.device))
         native.check(self.L.rs_set_trace(self._batch, _dptr(self._trace[0]), _dptr(self._trace[1]), cap, max_substeps),
                      "rs_set_trace")
+
+    def force_cta(self, width: int):
+        """Debug scheduling (parity tests): 8 / 16 = every env of the following
+        steps runs in the contact-heavy CTA kernel of that width; 0 = normal."""
+        native.check(self.L.rsim_bench_force_heavy(self._batch, int(width)), "rsim_bench_force_heavy")
 
     def trace(self, env: int):
         """[(substep, a, b, n_contacts)] recorded by the last step for `env`."""

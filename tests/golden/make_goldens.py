@@ -74,10 +74,10 @@ def meta():
     })
 
 
-def make_sim(variant, config=None):
+def make_sim(variant, config=None, n_clutter=20):
     cache = builtin.default_cache()
     sh = scene.load_scene(builtin.make_layout(variant), cache)
-    names = [FLAT[i % len(FLAT)] for i in range(20)]
+    names = [FLAT[i % len(FLAT)] for i in range(n_clutter)]
     sim = physics.Simulator(sh, rb.default_model(),
                             [(cache.get_asset(n), f"{n}#{i}") for i, n in enumerate(names)],
                             config or physics.PhysicsConfig())
@@ -977,9 +977,61 @@ def gen_grasp():
           f"wakes {int(out['trans'][:, 3].sum())}")
 
 
+# --------------------------------------------------------------------------
+# capacity: a 26-object awake pile (contacts / pairs / groups well above the
+# 20-object scenes) and a 40-object world (62 bodies)
+# --------------------------------------------------------------------------
+
+def pile_state(sim, seed=4, table="light_table"):
+    """Every clutter body awake in a 3 x 3 x k lattice above a table, random
+    yaw (free fall onto each other: the pile forms within ~0.5 s)."""
+    st = sim.park_state()
+    rec = sim.scene.receptacles[table]
+    owner = sim.scene.bodies[rec.owner_body].initial_pose
+    top = rec.boxes[0].center[2] - rec.boxes[0].half_extents[2]
+    rng = np.random.default_rng(seed)
+    for k, bid in enumerate(sim.clutter_body_ids):
+        layer, cell = divmod(k, 9)
+        gx, gy = (cell % 3 - 1) * 0.24, (cell // 3 - 1) * 0.2
+        rot = geo.rot_z(rng.uniform(-math.pi, math.pi))
+        lo, _ = geo.parts_aabb(sim.bodies[bid].parts, geo.Pose(rot, np.zeros(3)))
+        pos = owner.apply(np.array([gx, gy, top])) + np.array([0.0, 0.0, -lo[2] + 0.04 + 0.16 * layer])
+        st.set_body_pose(bid, geo.Pose(rot, pos))
+        st.asleep[bid] = False
+        st.sleep_counter[bid] = 0
+        st.rider_joint[bid] = -1
+    return st
+
+
+def gen_capacity():
+    sim, _ = make_sim(0, n_clutter=26)
+    st = pile_state(sim)
+    st.base = np.array([2.3, -0.2, 0.0])
+    sim._update_robot_link_poses(st, 0.0)
+    record(sim, st, [None] * 36, "pile26")
+    sim, _ = make_sim(2, n_clutter=40)
+    pool = np.load(os.path.join(OUT, "settled_pool.npz"))
+    ref = physics.WorldState.from_bytes([b for b, t in zip(pool["snapshots"], pool["tags"]) if t[0] == 2][0].tobytes())
+    st = sim.park_state()
+    for k in range(20):  # the settled 20-object state, the other 20 in a falling pile on the light table
+        b = sim.clutter_body_ids[k]
+        st.set_body_pose(b, ref.body_pose(22 + k))
+        st.asleep[b] = True
+    pile = pile_state(sim, seed=6)
+    for b in sim.clutter_body_ids[20:]:
+        k = b - sim.clutter_body_ids[20]
+        p = pile.body_pose(sim.clutter_body_ids[k])
+        st.set_body_pose(b, p)
+        st.asleep[b] = False
+    st.base = np.array([2.3, -0.2, 0.0])
+    sim._update_robot_link_poses(st, 0.0)
+    record(sim, st, idle_targets(sim, st, 24, seed=8), "world62")
+
+
 if __name__ == "__main__":
     t0 = time.time()
-    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav", "settle", "cast", "env", "grasp"]
+    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav", "settle", "cast", "env", "grasp",
+                            "capacity"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
     blobs = tags = None
@@ -1007,3 +1059,5 @@ if __name__ == "__main__":
         gen_env_records(list(p["snapshots"]), [tuple(t) for t in p["tags"]]); print("env", time.time() - t0)
     if "grasp" in what:
         gen_grasp(); print("grasp", time.time() - t0)
+    if "capacity" in what:
+        gen_capacity(); print("capacity", time.time() - t0)

@@ -15,15 +15,17 @@ from paper_2106_14405_b200.sim import BatchSimulator, PhysicsFault  # noqa: E402
 from paper_2106_14405_b200.state import WorldState  # noqa: E402
 
 LAYOUT = {"idle": 0, "fixed": 1, "interact": 0, "awake": 2, "drop": 0, "drop_floor": 0, "settle": 1,
-          "tilt": 0, "drawer": 0, "fridge": 0, "held": 0, "riders": 0, "pick": 0}
+          "tilt": 0, "drawer": 0, "fridge": 0, "held": 0, "riders": 0, "pick": 0,
+          "pile26": 0, "world62": 2}
+CLUTTER = {"pile26": 26, "world62": 40}  # clutter bodies (default 20)
 EV_NOISE = 1e-12
 _orc = {}
 
 
-def oracle(layout, **cfg):
-    key = (layout, tuple(sorted(cfg.items())))
+def oracle(layout, n_clutter=20, **cfg):
+    key = (layout, n_clutter, tuple(sorted(cfg.items())))
     if key not in _orc:
-        _orc[key] = Oracle(compile_world(build_world(layout, flat_clutter())), **cfg)
+        _orc[key] = Oracle(compile_world(build_world(layout, flat_clutter(n_clutter))), **cfg)
     return _orc[key]
 
 
@@ -53,19 +55,22 @@ def test_teacher_forced_vs_oracle_and_reference(name):
     g = golden(f"traj_{name}.npz")
     cfg = {"sleeping_enabled": 0} if name == "awake" else {}
     n = len(g["pre"])
-    sim = BatchSimulator(layouts=(LAYOUT[name],), n_env=n, config=cfg, event_cap=512)
+    nclut = CLUTTER.get(name, 20)
+    sim = BatchSimulator(layouts=(LAYOUT[name],), n_env=n, config=cfg, event_cap=1024, clutter=flat_clutter(nclut))
     sim.set_trace(cap=256)
     sim.set_state([g["pre"][s].tobytes() for s in range(n)])
     arm = torch.tensor(g["arm"], dtype=torch.float64)
     base = torch.tensor(g["base"], dtype=torch.float64)
     ht = torch.tensor(g["has_targets"].astype(np.uint8))
-    orc = oracle(LAYOUT[name], **cfg)
+    orc = oracle(LAYOUT[name], nclut, **cfg)
     # pass 0: warp-per-env kernel (no heavy flags yet); pass 1: the same inputs
     # again -- envs the first pass flagged contact-heavy now take the CTA
-    # (wavefront Gauss-Seidel) kernel; both must match bit for bit.
-    for pass_ in range(2):
+    # (wavefront Gauss-Seidel) kernel; passes 2 / 3: every env forced through
+    # the 16- and the 8-warp CTA kernel.  All must match bit for bit.
+    for pass_ in range(4):
         if pass_:
             sim.set_state([g["pre"][s].tobytes() for s in range(n)])
+        sim.force_cta({2: 16, 3: 8}.get(pass_, 0))
         sim.step_physics(arm, base, ht, check=True)
         torch.cuda.synchronize()
         _check_pass(sim, g, orc, name, n)

@@ -22,17 +22,19 @@ from paper_2106_14405_b200.scene import build_world, flat_clutter
 from paper_2106_14405_b200.state import WorldState
 
 LAYOUT = {"idle": 0, "fixed": 1, "interact": 0, "awake": 2, "drop": 0, "drop_floor": 0, "settle": 1,
-          "tilt": 0, "drawer": 0, "fridge": 0, "held": 0, "riders": 0, "pick": 0}
+          "tilt": 0, "drawer": 0, "fridge": 0, "held": 0, "riders": 0, "pick": 0,
+          "pile26": 0, "world62": 2}
+CLUTTER = {"pile26": 26, "world62": 40}  # clutter bodies (default 20)
 EV_NOISE = 1e-12
 POS_TOL, VEL_TOL = 1e-12, 1e-10
 
 _oracles = {}
 
 
-def oracle_for(layout, **cfg):
-    key = (layout, tuple(sorted(cfg.items())))
+def oracle_for(layout, n_clutter=20, **cfg):
+    key = (layout, n_clutter, tuple(sorted(cfg.items())))
     if key not in _oracles:
-        _oracles[key] = Oracle(compile_world(build_world(layout, flat_clutter())), **cfg)
+        _oracles[key] = Oracle(compile_world(build_world(layout, flat_clutter(n_clutter))), **cfg)
     return _oracles[key]
 
 
@@ -48,7 +50,7 @@ def events_clean(ev):
 def test_teacher_forced_steps(name):
     g = golden(f"traj_{name}.npz")
     cfg = {"sleeping_enabled": 0} if name == "awake" else {}
-    orc = oracle_for(LAYOUT[name], **cfg)
+    orc = oracle_for(LAYOUT[name], CLUTTER.get(name, 20), **cfg)
     for s in range(len(g["pre"])):
         arm = g["arm"][s] if g["has_targets"][s] else None
         r = orc.step(g["pre"][s].tobytes(), arm, g["base"][s])
