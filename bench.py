@@ -48,7 +48,6 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--envs", type=int, default=2048, help="envs per GPU")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-baseline-steps", type=int, default=24, help="env-steps per core in the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -236,18 +235,19 @@ def _cpu_init():
 
 
 def _cpu_worker(args):
-    """Oracle env-steps (IK + physics + 2 camera renders) in one worker process."""
+    """Oracle env-steps in one worker process: IK + physics, then 0, 1 (head)
+    or 2 (head + arm) camera renders."""
     from paper_2106_14405_b200.state import WorldState
 
-    layout, snap, act, n = args
+    layout, snap, act, n, cams = args
     orc = _ORC[layout]
     t0 = time.perf_counter()
     for k in range(n):
         q = WorldState.from_bytes(snap).joints[4:]
         tg, _ = orc.apply_arm_action(q, act[k, :3])
         snap = orc.step(snap, tg, act[k, 4:]).snapshot
-        orc.render(snap, 0)
-        orc.render(snap, 1)
+        for c in range(cams):
+            orc.render(snap, c)
     return n, time.perf_counter() - t0, snap
 
 
@@ -264,9 +264,9 @@ class CpuOracle:
         self.states = idle_states(range(self.cores), settled_pool())
         self.pool = mp.get_context("spawn").Pool(self.cores, initializer=_cpu_init)
 
-    def run(self, steps_per_core, seed):
+    def run(self, steps_per_core, seed, cams=2):
         act = action_table(self.cores, steps_per_core, seed)
-        jobs = [(g % 3, self.states[g], act[:, g], steps_per_core) for g in range(self.cores)]
+        jobs = [(g % 3, self.states[g], act[:, g], steps_per_core, cams) for g in range(self.cores)]
         t0 = time.perf_counter()
         res = self.pool.map(_cpu_worker, jobs)
         wall = time.perf_counter() - t0
@@ -278,14 +278,32 @@ class CpuOracle:
         self.pool.join()
 
 
-def cpu_oracle_sps(n_steps_per_core, cores=None, seed=0):
+# BASELINE.md §2 / SURVEY.md §8d protocol: physics-only, 1-camera and 2-camera
+# rows; per row a 30-step warm-up per core, then 10 runs reported as mean +-
+# 95 % CI (Student t, 9 dof).  Run lengths (env-steps per core per run) keep
+# the whole sample near 10-20 s of host time.
+CPU_ROWS = (("physics_only", 0, 40), ("one_camera", 1, 6), ("two_camera", 2, 4))
+CPU_RUNS, CPU_WARMUP = 10, 30
+T975_9DOF = 2.262
+
+
+def cpu_oracle_protocol(cores=None, seed=0, runs=CPU_RUNS, warmup=CPU_WARMUP, rows=CPU_ROWS):
     c = CpuOracle(cores)
+    out = {}
     try:
-        c.run(1, seed + 1000)  # warm
-        steps, wall = c.run(n_steps_per_core, seed)
+        for name, cams, per_run in rows:
+            c.run(warmup, seed + 1000, cams)
+            sps = []
+            for r in range(runs):
+                steps, wall = c.run(per_run, seed + r, cams)
+                sps.append(steps / wall)
+            sps = np.asarray(sps)
+            half = T975_9DOF * sps.std(ddof=1) / math.sqrt(len(sps)) if len(sps) > 1 else 0.0
+            out[name] = {"mean": float(sps.mean()), "ci95": float(half), "runs": len(sps),
+                         "env_steps_per_core_per_run": per_run, "cameras": cams}
     finally:
         c.close()
-    return steps / wall, c.cores, wall, steps
+    return out, c.cores
 
 
 def cpu_model():
@@ -643,10 +661,15 @@ def run_b200(args):
                           "note": "timed: upload of the spawn snapshots (rs_set_state) + rs_settle (GJK spawn "
                                   "clearance, control steps until every placed body sleeps)"}
         if world == 1 and not args.no_cpu_baseline:
-            sps, cores, wall, steps = cpu_oracle_sps(args.cpu_baseline_steps)
-            line["cpu_baseline"] = {"value": sps, "unit": UNIT, "cores": cores, "kind": "port",
-                                    "sample": f"{steps} env-steps (IK + physics + 2 renders) of the C oracle, "
-                                              f"{args.cpu_baseline_steps} per core, {wall:.1f} s wall, {cpu_model()}"}
+            h0 = time.perf_counter()
+            rows, cores = cpu_oracle_protocol()
+            line["cpu_baseline"] = {
+                "value": rows["two_camera"]["mean"], "unit": UNIT, "cores": cores, "kind": "port",
+                "ci95": rows["two_camera"]["ci95"], "rows": rows, "cpu_model": cpu_model(),
+                "sample": f"C oracle restatement, one env per host core ({cores} cores, {cpu_model()}), "
+                          f"idle env-steps (IK + physics + 0/1/2 camera renders); per row {CPU_WARMUP} warm-up "
+                          f"steps per core then {CPU_RUNS} runs, mean +- 95% CI; value = the 2-camera row; "
+                          f"{time.perf_counter() - h0:.1f} s wall in total"}
         print(json.dumps(line), flush=True)
     sim.close()
     if world > 1:

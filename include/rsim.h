@@ -31,6 +31,9 @@
  * Conventions:
  *   - every call is stream-ordered on the cudaStream_t passed as `stream`
  *     (NULL = legacy default stream); a batch is owned by one host thread;
+ *   - a batch is bound to the CUDA device current at rs_batch_create: every
+ *     rs_* call on it runs on that device (and restores the caller's current
+ *     device), so `stream` must belong to that device;
  *   - device pointers are caller-allocated and never freed by the library;
  *   - return value 0 = success; non-zero = error code, message in
  *     rs_last_error() (thread-local).  Per-env physics faults (non-finite
@@ -218,7 +221,14 @@ int rs_grasp(rs_batch *batch, const double *gripper, void *stream);
  * an internal side stream WHILE copying arm_targets/base_cmd (host) to the
  * device and running rs_step s_t -> s_{t+1} on `stream`; then copies per-env
  * step results back to host: out_stats [n_env][4] = accumulated_contact_force,
- * fault word, event count, sleeping-body count.  Synchronises `stream`. */
+ * fault word, event count, sleeping-body count.  Returns when the step and
+ * h_out_stats are complete (the host buffers may be reused); it does NOT
+ * synchronise `stream`: the observation tensors complete in `stream` order
+ * (`stream` is left waiting on the render).  A host reader of rgba/depth/ids
+ * must synchronise `stream` first; a reader on another stream must wait on an
+ * event recorded on `stream`.  Every later rs_* call on the batch must be
+ * issued on `stream` (or after it), since the next step overwrites the state
+ * buffer the render reads. */
 int rs_step_host(rs_batch *batch, const double *h_arm_targets, const double *h_base_cmd, double dt,
                  int32_t substeps, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                  double *h_out_stats, void *stream);

@@ -107,6 +107,19 @@ struct rs_batch {
   // host-buffer steps: physics on a high-priority stream next to the render
   cudaStream_t phys_hp = nullptr;
   cudaEvent_t hp_join = nullptr;
+  int device = 0;  // the CUDA device current at rs_batch_create; every entry point runs on it
+};
+
+// Entry points run on the batch's device whatever the caller's current
+// device is (kernel attributes, streams and buffers are per device), and
+// restore the caller's device on return.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(const rs_batch *b) {
+    if (b && cudaGetDevice(&prev) == cudaSuccess && prev != b->device) cudaSetDevice(b->device);
+    else prev = -1;
+  }
+  ~DeviceScope() { if (prev >= 0) cudaSetDevice(prev); }
 };
 
 // exported functions take C linkage from their declarations in rsim.h
@@ -245,6 +258,7 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
     return fail(RS_ERR_ARG, "render width/height must be multiples of 16 and <= 128");
   if (cfg->solver_iterations < 0 || cfg->sleep_substeps < 0) return fail(RS_ERR_ARG, "bad physics config");
   rs_batch *b = new rs_batch();
+  if (cudaGetDevice(&b->device) != cudaSuccess) b->device = 0;
   DevBatch &d = b->d;
   memset(&d, 0, sizeof d);
   d.n_env = n_env; d.nb = s0.nb; d.nj = s0.nsj + s0.narm;
@@ -314,6 +328,7 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
 
 void rs_batch_destroy(rs_batch *b) {
   if (!b) return;
+  DeviceScope device_scope(b);
   for (void *p : b->allocs) cudaFree(p);
   if (b->h_pin) cudaFreeHost(b->h_pin);
   if (b->d_act) cudaFree(b->d_act);
@@ -338,6 +353,7 @@ void rs_batch_destroy(rs_batch *b) {
 }
 
 int rs_batch_buffers(rs_batch *b, rs_buffers *o) {
+  DeviceScope device_scope(b);
   if (!b || !o) return fail(RS_ERR_ARG, "null argument");
   o->n_env = b->d.n_env; o->n_bodies = b->d.nb; o->n_joints = b->d.nj; o->event_cap = b->d.event_cap;
   o->fault = b->d.fault; o->event_count = b->d.event_count; o->events = b->d.events; o->counters = b->d.counters;
@@ -391,6 +407,7 @@ static void pack_snapshot(const StateLayout &L, const double *sd, const int32_t 
 }
 
 int rs_set_state(rs_batch *b, const uint8_t *snaps, int64_t stride, const int32_t *env_ids, int32_t n, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !snaps || n < 0) return fail(RS_ERR_ARG, "null argument");
   const DevBatch d = b->view();
   const StateLayout &L = d.L;
@@ -437,6 +454,7 @@ int rs_set_state(rs_batch *b, const uint8_t *snaps, int64_t stride, const int32_
 }
 
 int rs_get_state(rs_batch *b, uint8_t *snaps, int64_t stride, const int32_t *env_ids, int32_t n, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !snaps || n < 0) return fail(RS_ERR_ARG, "null argument");
   const DevBatch d = b->view();
   const StateLayout &L = d.L;
@@ -496,6 +514,7 @@ static int ensure_phys_hp(rs_batch *b) {
 
 int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_t *has_targets, double dt,
             int32_t substeps, void *stream) {
+  DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
   if (!arm || !base_cmd) return fail(RS_ERR_ARG, "arm_targets and base_cmd are required device pointers");
@@ -505,6 +524,7 @@ int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_
 }
 
 int rs_render(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream) {
+  DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (cam_mask >> 2) return fail(RS_ERR_ARG, "camera mask selects a camera the robot does not have");
   CUDA_TRY(launch_render(b->view(), cam_mask, rgba, depth, ids, (cudaStream_t)stream));
@@ -512,6 +532,7 @@ int rs_render(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32
 }
 
 int rs_render_mesh(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream) {
+  DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (cam_mask >> 2) return fail(RS_ERR_ARG, "camera mask selects a camera the robot does not have");
   DevBatch v = b->view();
@@ -526,6 +547,7 @@ static int ensure_ik_scratch(rs_batch *b) {
 }
 
 int rs_arm_action(rs_batch *b, const double *delta_ee, double *arm_targets, int32_t *ik_failed, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !delta_ee || !arm_targets) return fail(RS_ERR_ARG, "null argument");
   int rc = ensure_ik_scratch(b);
   if (rc) return rc;
@@ -534,12 +556,14 @@ int rs_arm_action(rs_batch *b, const double *delta_ee, double *arm_targets, int3
 }
 
 int rs_grasp(rs_batch *b, const double *gripper, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !gripper) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_grasp(b->view(), gripper, 1, (cudaStream_t)stream));
   return RS_OK;
 }
 
 int rs_set_trace(rs_batch *b, int32_t *pairs, int32_t *count, int32_t cap, int32_t max_substeps) {
+  DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if ((pairs == nullptr) != (count == nullptr)) return fail(RS_ERR_ARG, "pairs and count must both be set or NULL");
   b->d.trace_pairs = pairs;
@@ -549,18 +573,24 @@ int rs_set_trace(rs_batch *b, int32_t *pairs, int32_t *count, int32_t cap, int32
   return RS_OK;
 }
 
+// stats buffer, render side stream and fork/join events shared by
+// rs_step_host and rs_env_step_host; each resource guarded on its own handle
+static int ensure_host_step(rs_batch *b) {
+  if (!b->d_stats) CUDA_TRY(cudaMalloc(&b->d_stats, sizeof(double) * (size_t)b->d.n_env * 4));
+  if (!b->side) CUDA_TRY(cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking));
+  if (!b->ev_fork) CUDA_TRY(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
+  if (!b->ev_join) CUDA_TRY(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
+  return RS_OK;
+}
+
 int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double dt, int32_t substeps,
                  uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, double *h_out_stats, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !h_arm || !h_base || !h_out_stats) return fail(RS_ERR_ARG, "null argument");
   const int E = b->d.n_env, na = b->narm;
   cudaStream_t st = (cudaStream_t)stream;
-  if (!b->d_act) {
-    CUDA_TRY(cudaMalloc(&b->d_act, sizeof(double) * (size_t)E * (na + 2)));
-    CUDA_TRY(cudaMalloc(&b->d_stats, sizeof(double) * (size_t)E * 4));
-    CUDA_TRY(cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
-  }
+  if (!b->d_act) CUDA_TRY(cudaMalloc(&b->d_act, sizeof(double) * (size_t)E * (na + 2)));
+  if (int rc0 = ensure_host_step(b)) return rc0;
   if (int rc0 = ensure_phys_hp(b)) return rc0;
   cudaStream_t hp = b->phys_hp;
   // render o_t = render(s_t) on the side stream, concurrently with the physics
@@ -592,6 +622,7 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
 }
 
 int rsim_bench_render_work_detail(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counters, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !d_counters) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, d_counters));
   return RS_OK;
@@ -602,6 +633,7 @@ __global__ void work_total_kernel(const unsigned long long *w, unsigned long lon
 }
 
 int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");
   unsigned long long *w = nullptr;
   CUDA_TRY(cudaMalloc(&w, 12 * sizeof(unsigned long long)));
@@ -616,6 +648,7 @@ int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d
 // ---- observation proprioception
 int rs_proprio(rs_batch *b, const double *base_prev, const double *goals, int32_t n_goals, double *out,
                double *base_out, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !out || n_goals < 0 || (n_goals > 0 && !goals)) return fail(RS_ERR_ARG, "bad proprioception arguments");
   CUDA_TRY(launch_proprio(b->view(), base_prev, goals, n_goals, out, base_out, (cudaStream_t)stream));
   return RS_OK;
@@ -624,6 +657,7 @@ int rs_proprio(rs_batch *b, const double *base_prev, const double *goals, int32_
 // ---- point queries (physics.py:1088-1101)
 int rs_sphere_cast(rs_batch *b, const int32_t *env_of_query, const double *origins, const double *dirs,
                    const double *max_dist, int32_t n_queries, int32_t *out_body, double *out_t, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !origins || !dirs || !max_dist || !out_body || !out_t || n_queries < 0)
     return fail(RS_ERR_ARG, "bad sphere_cast arguments");
   if (!env_of_query && n_queries > b->d.n_env) return fail(RS_ERR_ARG, "env_of_query = NULL needs n_queries <= n_env");
@@ -635,6 +669,7 @@ int rs_sphere_cast(rs_batch *b, const int32_t *env_of_query, const double *origi
 // ---- batched settle (physics.py:1113-1176)
 int rs_settle(rs_batch *b, const uint64_t *placed, uint8_t *active, int32_t max_steps, double floor_z,
               int32_t *status, int32_t *info, double *value, int32_t *steps, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !placed || !active || !status || !info || !value || !steps || max_steps < 0)
     return fail(RS_ERR_ARG, "bad settle arguments");
   const int E = b->d.n_env;
@@ -670,6 +705,7 @@ int rs_settle(rs_batch *b, const uint64_t *placed, uint8_t *active, int32_t max_
 
 // ---- geodesics (navgrid.py:109-172)
 int rs_nav_shape(rs_batch *b, int32_t *nx, int32_t *ny) {
+  DeviceScope device_scope(b);
   if (!b || !nx || !ny) return fail(RS_ERR_ARG, "null argument");
   if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
   *nx = b->nav_nx; *ny = b->nav_ny;
@@ -678,6 +714,7 @@ int rs_nav_shape(rs_batch *b, int32_t *nx, int32_t *ny) {
 
 int rs_nav_fields(rs_batch *b, const int32_t *scene_of_goal, const double *goal_xy, int32_t n_goals, double *fields,
                   int32_t *goal_cell, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !goal_xy || !fields || n_goals < 0) return fail(RS_ERR_ARG, "bad nav field arguments");
   if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
   if ((size_t)b->nav_nx * b->nav_ny * 9 > 227 * 1024) return fail(RS_ERR_ARG, "walk grid too large for one CTA");
@@ -688,6 +725,7 @@ int rs_nav_fields(rs_batch *b, const int32_t *scene_of_goal, const double *goal_
 
 int rs_nav_geodesic(rs_batch *b, const double *fields, const int32_t *field_of_query, const int32_t *scene_of_query,
                     const double *from_xy, int32_t n_queries, double *out, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !fields || !field_of_query || !out || n_queries < 0) return fail(RS_ERR_ARG, "bad geodesic arguments");
   if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
   if (!from_xy && n_queries != b->d.n_env) return fail(RS_ERR_ARG, "robot-base queries need n_queries == n_env");
@@ -699,6 +737,7 @@ int rs_nav_geodesic(rs_batch *b, const double *fields, const int32_t *field_of_q
 int rs_nav_path(rs_batch *b, const double *fields, const int32_t *field_of_query, const int32_t *scene_of_query,
                 const double *from_xy, int32_t n_queries, int32_t cap, double *waypoints, int32_t *count,
                 void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !fields || !field_of_query || !from_xy || !waypoints || !count || n_queries < 0 || cap < 1)
     return fail(RS_ERR_ARG, "bad path arguments");
   if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
@@ -708,6 +747,7 @@ int rs_nav_path(rs_batch *b, const double *fields, const int32_t *field_of_query
 }
 
 int rsim_bench_force_heavy(rs_batch *b, int width) {
+  DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (width != 0 && width != 8 && width != 16) return fail(RS_ERR_ARG, "width must be 0, 8 or 16");
   b->force_heavy = width;
@@ -715,12 +755,14 @@ int rsim_bench_force_heavy(rs_batch *b, int width) {
 }
 
 int rsim_bench_env_cycles(rs_batch *b, long long *d_cycles) {
+  DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   b->d.env_cycles = d_cycles;
   return RS_OK;
 }
 
 int rsim_bench_phase_cycles(rs_batch *b, long long *d_cycles) {
+  DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   b->d.phase_cycles = d_cycles;
   return RS_OK;
@@ -728,12 +770,14 @@ int rsim_bench_phase_cycles(rs_batch *b, long long *d_cycles) {
 
 int rsim_bench_render_exact(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                             void *stream) {
+  DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   CUDA_TRY(launch_render_exact(b->view(), cam_mask, rgba, depth, ids, (cudaStream_t)stream));
   return RS_OK;
 }
 
 int rsim_bench_render_mesh_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counter, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !d_counter || !b->has_mesh) return fail(RS_ERR_ARG, "null argument or no mesh");
   unsigned long long *w = nullptr;
   CUDA_TRY(cudaMalloc(&w, 12 * sizeof(unsigned long long)));
@@ -753,16 +797,11 @@ static int ensure_env_buffers(rs_batch *b) {
     CUDA_TRY(cudaMalloc(&b->d_ik_failed, sizeof(int32_t) * (size_t)E));
     CUDA_TRY(cudaMalloc(&b->d_env_act, sizeof(double) * (size_t)E * 6));
   }
-  if (!b->d_stats) {
-    CUDA_TRY(cudaMalloc(&b->d_stats, sizeof(double) * (size_t)E * 4));
-    CUDA_TRY(cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
-  }
-  return RS_OK;
+  return ensure_host_step(b);
 }
 
 int rs_env_step(rs_batch *b, const double *action, double dt, int32_t substeps, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !action) return fail(RS_ERR_ARG, "null argument");
   if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
   int rc = ensure_env_buffers(b);
@@ -778,6 +817,7 @@ int rs_env_step(rs_batch *b, const double *action, double dt, int32_t substeps, 
 
 int rs_env_step_host(rs_batch *b, const double *h_action, double dt, int32_t substeps, uint32_t cam_mask,
                      uint8_t *rgba, float *depth, int32_t *ids, double *h_out_stats, void *stream) {
+  DeviceScope device_scope(b);
   if (!b || !h_action || !h_out_stats) return fail(RS_ERR_ARG, "null argument");
   int rc = ensure_env_buffers(b);
   if (rc) return rc;

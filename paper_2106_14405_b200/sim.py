@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import warnings
 
 import numpy as np
 import torch
@@ -123,14 +124,14 @@ class BatchSimulator:
         with torch.cuda.device(self.device):
             native.check(self.L.rs_set_state(self._batch, buf.ctypes.data, self.snap_size,
                                              None if ids is None else ids.ctypes.data, len(blobs),
-                                             _stream_ptr()), "rs_set_state")
+                                             self._sp()), "rs_set_state")
 
     def get_state(self, env_ids=None) -> list[bytes]:
         ids = np.arange(self.n_env, dtype=np.int32) if env_ids is None else np.ascontiguousarray(env_ids, np.int32)
         out = np.zeros(len(ids) * self.snap_size, np.uint8)
         with torch.cuda.device(self.device):
             native.check(self.L.rs_get_state(self._batch, out.ctypes.data, self.snap_size, ids.ctypes.data,
-                                             len(ids), _stream_ptr()), "rs_get_state")
+                                             len(ids), self._sp()), "rs_get_state")
         return [out[i * self.snap_size:(i + 1) * self.snap_size].tobytes() for i in range(len(ids))]
 
     def world_state(self, env: int) -> WorldState:
@@ -146,9 +147,26 @@ class BatchSimulator:
         base = self._dev(base_cmd, (self.n_env, 2), torch.float64)
         ht = None if has_targets is None else self._dev(has_targets, (self.n_env,), torch.uint8)
         native.check(self.L.rs_step(self._batch, _dptr(arm), _dptr(base), _dptr(ht), float(dt), int(substeps),
-                                    _stream_ptr()), "rs_step")
+                                    self._sp()), "rs_step")
         if check:
             self.raise_faults()
+
+    def _sp(self) -> int:
+        """The current torch stream of the batch's device (the library runs
+        every call on the device the batch was created on)."""
+        return int(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _host(self, t: torch.Tensor, shape, name: str) -> torch.Tensor:
+        """A host f64 buffer handed to the C side by pointer: the library
+        reads prod(shape) doubles from it, so anything else is refused."""
+        if not isinstance(t, torch.Tensor) or t.device.type != "cpu":
+            raise ValueError(f"{name}: expected a CPU (pinned) torch tensor")
+        if t.dtype != torch.float64 or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous float64 tensor of shape {tuple(shape)}, "
+                             f"got {t.dtype} {tuple(t.shape)}{'' if t.is_contiguous() else ' (non-contiguous)'}")
+        if not t.is_pinned():
+            warnings.warn(f"{name} is not in pinned memory: the copy is synchronous and slower", stacklevel=3)
+        return t
 
     def _dev(self, t, shape, dtype):
         if not isinstance(t, torch.Tensor):
@@ -217,7 +235,7 @@ class BatchSimulator:
         d = self._dev(delta_ee, (self.n_env, 3), torch.float64)
         out = out if out is not None else torch.empty((self.n_env, self.n_arm), dtype=torch.float64, device=self.device)
         failed = failed if failed is not None else torch.empty(self.n_env, dtype=torch.int32, device=self.device)
-        native.check(self.L.rs_arm_action(self._batch, _dptr(d), _dptr(out), _dptr(failed), _stream_ptr()),
+        native.check(self.L.rs_arm_action(self._batch, _dptr(d), _dptr(out), _dptr(failed), self._sp()),
                      "rs_arm_action")
         return out, failed
 
@@ -226,25 +244,30 @@ class BatchSimulator:
         """Paper action space [E, 6] = (dEE xyz, gripper, base lin, base ang) on
         device: IK -> physics -> grasp rule (rs_env_step)."""
         a = self._dev(action, (self.n_env, 6), torch.float64)
-        native.check(self.L.rs_env_step(self._batch, _dptr(a), float(dt), int(substeps), _stream_ptr()),
+        native.check(self.L.rs_env_step(self._batch, _dptr(a), float(dt), int(substeps), self._sp()),
                      "rs_env_step")
 
     def env_step_host(self, h_action: torch.Tensor, cams=("head", "arm"), out=None, h_stats=None,
                       dt: float = 1.0 / 30.0, substeps: int = 4):
-        """rs_env_step_host: host [E, 6] actions, o_t rendered concurrently, host stats back."""
+        """rs_env_step_host: host [E, 6] f64 actions, o_t = render(s_t) rendered
+        concurrently, host stats back.  Returns ``(h_stats, (rgba, depth, ids))``:
+        ``h_stats`` [E, 4] is complete on return; the observation completes in
+        the current stream's order (synchronise it before reading on the host)."""
+        self._host(h_action, (self.n_env, 6), "h_action")
         cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
         rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
         if h_stats is None:
             h_stats = torch.empty((self.n_env, 4), dtype=torch.float64).pin_memory()
+        self._host(h_stats, (self.n_env, 4), "h_stats")
         native.check(self.L.rs_env_step_host(self._batch, C.c_void_p(h_action.data_ptr()), float(dt), int(substeps),
                                              self.cam_mask(cams), _dptr(rgba), _dptr(depth), _dptr(ids),
-                                             C.c_void_p(h_stats.data_ptr()), _stream_ptr()), "rs_env_step_host")
-        return h_stats
+                                             C.c_void_p(h_stats.data_ptr()), self._sp()), "rs_env_step_host")
+        return h_stats, (rgba, depth, ids)
 
     # ------------------------------------------------------------------ grasp
     def grasp(self, gripper: torch.Tensor):
         g = self._dev(gripper, (self.n_env,), torch.float64)
-        native.check(self.L.rs_grasp(self._batch, _dptr(g), _stream_ptr()), "rs_grasp")
+        native.check(self.L.rs_grasp(self._batch, _dptr(g), self._sp()), "rs_grasp")
 
     # ----------------------------------------------------------------- render
     def alloc_obs(self, cams=("head", "arm")):
@@ -267,7 +290,7 @@ class BatchSimulator:
         cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
         rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
         native.check(self.L.rs_render(self._batch, self.cam_mask(cams), _dptr(rgba), _dptr(depth), _dptr(ids),
-                                      _stream_ptr()), "rs_render")
+                                      self._sp()), "rs_render")
         return rgba, depth, ids
 
     def render_exact(self, cams=("head", "arm"), out=None):
@@ -276,7 +299,7 @@ class BatchSimulator:
         cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
         rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
         native.check(self.L.rsim_bench_render_exact(self._batch, self.cam_mask(cams), _dptr(rgba), _dptr(depth),
-                                                    _dptr(ids), _stream_ptr()), "rsim_bench_render_exact")
+                                                    _dptr(ids), self._sp()), "rsim_bench_render_exact")
         return rgba, depth, ids
 
     def render_mesh(self, cams=("head", "arm"), out=None):
@@ -284,7 +307,7 @@ class BatchSimulator:
         cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
         rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
         native.check(self.L.rs_render_mesh(self._batch, self.cam_mask(cams), _dptr(rgba), _dptr(depth), _dptr(ids),
-                                           _stream_ptr()), "rs_render_mesh")
+                                           self._sp()), "rs_render_mesh")
         return rgba, depth, ids
 
     # ------------------------------------ proprioception
@@ -301,7 +324,7 @@ class BatchSimulator:
         base_out = base_out if base_out is not None else torch.empty((self.n_env, 3), dtype=torch.float64,
                                                                      device=self.device)
         native.check(self.L.rs_proprio(self._batch, _dptr(bp), _dptr(g), k, _dptr(out), _dptr(base_out),
-                                       _stream_ptr()), "rs_proprio")
+                                       self._sp()), "rs_proprio")
         return out, base_out
 
     # ---------------------------------------- point query (physics.py:1088-1101)
@@ -316,7 +339,7 @@ class BatchSimulator:
         body = torch.empty(n, dtype=torch.int32, device=self.device)
         t = torch.empty(n, dtype=torch.float64, device=self.device)
         native.check(self.L.rs_sphere_cast(self._batch, _dptr(ev), _dptr(o), _dptr(d), _dptr(md), n, _dptr(body),
-                                           _dptr(t), _stream_ptr()), "rs_sphere_cast")
+                                           _dptr(t), self._sp()), "rs_sphere_cast")
         return body, t
 
     # ------------------------------------------ settle (physics.py:1113-1176)
@@ -355,7 +378,7 @@ class BatchSimulator:
         steps = torch.empty(self.n_env, dtype=torch.int32, device=self.device)
         native.check(self.L.rs_settle(self._batch, _dptr(d_mask), _dptr(d_active), self.settle_steps(max_time),
                                       float(floor_z), _dptr(status), _dptr(info), _dptr(value), _dptr(steps),
-                                      _stream_ptr()), "rs_settle")
+                                      self._sp()), "rs_settle")
         sel = torch.as_tensor(ids, device=self.device)
         return status[sel], info[sel], value[sel], steps[sel]
 
@@ -377,7 +400,7 @@ class BatchSimulator:
         sc = None if layouts is None else self._dev(torch.as_tensor([self.layouts.index(v) for v in layouts]), (n,),
                                                     torch.int32)
         native.check(self.L.rs_nav_fields(self._batch, _dptr(sc), _dptr(g), n, _dptr(fields), _dptr(cells),
-                                          _stream_ptr()), "rs_nav_fields")
+                                          self._sp()), "rs_nav_fields")
         return fields, cells
 
     def geodesic_distance(self, fields, field_idx, from_xy=None, layouts=None):
@@ -390,7 +413,7 @@ class BatchSimulator:
                                                     torch.int32)
         out = torch.empty(n, dtype=torch.float64, device=self.device)
         native.check(self.L.rs_nav_geodesic(self._batch, _dptr(fields), _dptr(fi), _dptr(sc), _dptr(fx), n,
-                                            _dptr(out), _stream_ptr()), "rs_nav_geodesic")
+                                            _dptr(out), self._sp()), "rs_nav_geodesic")
         return out
 
     def shortest_path(self, fields, field_idx, from_xy, layouts=None, cap: int = 512):
@@ -403,22 +426,27 @@ class BatchSimulator:
         wp = torch.empty((n, cap, 2), dtype=torch.float64, device=self.device)
         cnt = torch.empty(n, dtype=torch.int32, device=self.device)
         native.check(self.L.rs_nav_path(self._batch, _dptr(fields), _dptr(fi), _dptr(sc), _dptr(fx), n, cap,
-                                        _dptr(wp), _dptr(cnt), _stream_ptr()), "rs_nav_path")
+                                        _dptr(wp), _dptr(cnt), self._sp()), "rs_nav_path")
         return wp, cnt
 
     # ------------------------------------------------------- end-to-end (host)
     def step_host(self, h_arm: torch.Tensor, h_base: torch.Tensor, cams=("head", "arm"), out=None,
                   h_stats: torch.Tensor | None = None, dt=1.0 / 30.0, substeps=4):
         """Env step through the C-ABI with HOST action buffers and a HOST
-        result read-back (rs_step_host): [E, 4] acc. force, fault, events, asleep."""
+        result read-back (rs_step_host): [E, 4] acc. force, fault, events, asleep.
+        Returns ``(h_stats, (rgba, depth, ids))``; the observation completes in
+        the current stream's order (synchronise it before reading on the host)."""
+        self._host(h_arm, (self.n_env, self.n_arm), "h_arm")
+        self._host(h_base, (self.n_env, 2), "h_base")
         cams = tuple(sorted(cams, key=lambda c: CAMERAS[c]))
         rgba, depth, ids = out if out is not None else self.alloc_obs(cams)
         if h_stats is None:
             h_stats = torch.empty((self.n_env, 4), dtype=torch.float64).pin_memory()
+        self._host(h_stats, (self.n_env, 4), "h_stats")
         native.check(self.L.rs_step_host(self._batch, C.c_void_p(h_arm.data_ptr()), C.c_void_p(h_base.data_ptr()),
                                          float(dt), int(substeps), self.cam_mask(cams), _dptr(rgba), _dptr(depth),
-                                         _dptr(ids), C.c_void_p(h_stats.data_ptr()), _stream_ptr()), "rs_step_host")
-        return h_stats
+                                         _dptr(ids), C.c_void_p(h_stats.data_ptr()), self._sp()), "rs_step_host")
+        return h_stats, (rgba, depth, ids)
 
 
 def _ptr_tensor(ptr, nbytes: int, dtype, device) -> torch.Tensor:

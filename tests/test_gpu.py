@@ -238,7 +238,7 @@ def test_step_host_end_to_end():
     sim.set_state([g["pre"][0].tobytes()] * n)
     h_arm = torch.tensor(np.tile(g["arm"][0], (n, 1))).pin_memory()
     h_base = torch.tensor(np.tile(g["base"][0], (n, 1))).pin_memory()
-    stats = sim.step_host(h_arm, h_base)
+    stats, _ = sim.step_host(h_arm, h_base)
     ref = WorldState.from_bytes(g["post"][0].tobytes())
     assert (stats[:, 1] == 0).all()
     assert (stats[:, 3] == ref.asleep.sum()).all()

@@ -159,7 +159,7 @@ def test_env_step_host_matches_device_env_step():
     obs_a = a.render()
     a.env_step(act.cuda())
     obs_b = b.alloc_obs()
-    stats = b.env_step_host(act.pin_memory(), out=obs_b)
+    stats, _ = b.env_step_host(act.pin_memory(), out=obs_b)
     torch.cuda.synchronize()
     assert a.get_state() == b.get_state()
     for x, y in zip(obs_a, obs_b):
