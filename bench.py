@@ -37,7 +37,8 @@ METRIC = "simulation steps/sec (128x128 RGBD + 1/30s physics) at 1/2/4/8 B200 vs
 UNIT = "env-steps/s"
 H = W = 128
 N_CAMS = 2
-PROFILE_JSON = "profiles/r1k_kernels.json"  # ncu --set full per-kernel DRAM bytes (tools/ncu_summary.py --json)
+PROFILE_JSON = "profiles/r1k_kernels.json"
+HBM_PEAK = 6450.6  # MEASURED_PEAKS.json hbm_gbs (driver-written on this pool's B200s); read at run time when present  # ncu --set full per-kernel DRAM bytes (tools/ncu_summary.py --json)
 PAPER_8GPU_SPS = 25734.0  # PAPER.md:530 (8x RTX 2080 Ti, Idle) -- different hardware, not this metric's config
 
 
@@ -349,6 +350,70 @@ def run_reference(args):
     return 0
 
 
+def grasp_leg(args, E, dev, side, hp, stream, n_tab):
+    """Timed Interact variant with grasp transitions (see the call site)."""
+    import torch
+
+    from paper_2106_14405_b200.sim import BatchSimulator
+
+    scripts = [np.load(os.path.join(ROOT, "tests", "golden", f"traj_{n}.npz")) for n in ("pick", "riders")]
+    span = [len(g["pre"]) - n_tab for g in scripts]
+    arm = np.zeros((n_tab, E, 7)); base = np.zeros((n_tab, E, 2)); has = np.zeros((n_tab, E), np.uint8)
+    grip = np.zeros((n_tab, E)); pre = []
+    for e in range(E):
+        g, sp = scripts[e % 2], span[e % 2]
+        o = (e // 2) % (sp + 1)
+        pre.append(g["pre"][o].tobytes())
+        sl = slice(o, o + n_tab)
+        arm[:, e], base[:, e], has[:, e] = g["arm"][sl], g["base"][sl], g["has_targets"][sl]
+        grip[:, e] = np.nan_to_num(g["gripper"][sl], nan=0.0)
+    gs = BatchSimulator(layouts=(0,), n_env=E, device=dev)
+    gs.set_state(pre)
+    arm_d, base_d = torch.tensor(arm, device=dev), torch.tensor(base, device=dev)
+    has_d, grip_d = torch.tensor(has, device=dev), torch.tensor(grip, device=dev)
+    obs = gs.alloc_obs(("head", "arm"))
+
+    def step(k):
+        hp.wait_stream(stream)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            gs.render(("head", "arm"), out=obs)
+        with torch.cuda.stream(hp):
+            gs.step_physics(arm_d[k], base_d[k], has_d[k])
+            gs.grasp(grip_d[k])
+        stream.wait_stream(hp)
+        stream.wait_stream(side)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize(dev)
+    held0 = np.array([gs_held(gs, e) for e in range(0, E, max(1, E // 64))])
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for k in range(args.steps):
+        step(args.warmup + k)
+    c1.record(stream)
+    torch.cuda.synchronize(dev)
+    gs.raise_faults()
+    held1 = np.array([gs_held(gs, e) for e in range(0, E, max(1, E // 64))])
+    tr = np.concatenate([g["trans"][:, 0] for g in scripts])
+    info = {"note": "apt_0, half the envs on the reference's pick & place script, half on its drawer-drag script "
+                    "(handle snap, drag with riders, release, reach into the tray); staggered offsets; "
+                    "rs_step + rs_grasp on the physics stream, 2-camera render interleaved",
+            "script_snaps_releases": [int((tr == 1).sum()), int((tr == 2).sum())],
+            "sampled_envs_holding_before_after": [int((held0 >= 0).sum()), int((held1 >= 0).sum())],
+            "sampled_envs": len(held0)}
+    ms = c0.elapsed_time(c1)
+    gs.close()
+    return ms, info
+
+
+def gs_held(sim, e):
+    from paper_2106_14405_b200.state import WorldState
+
+    return int(WorldState.from_bytes(sim.get_state([e])[0]).held)
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -464,6 +529,15 @@ def run_b200(args):
     sim.raise_faults()
     del act_i
 
+    # ---- Interact with grasps and drags inside the timed region: the reference's
+    # own pick & place and drawer-drag scripts (tests/golden/traj_pick.npz,
+    # traj_riders.npz, layout apt_0: handle snap + drag with riders, object snap,
+    # hold, carry, release, fall), teacher-forced per env from a staggered offset
+    # into its script (joint targets of the reference IK + gripper scalars), so
+    # every step of the window has envs reaching, snapping, dragging, carrying
+    # and releasing; physics + grasp rule interleaved with the 2-camera render
+    ms_grasp, grasp_info = grasp_leg(args, E, dev, side, hp, stream, n_tab)
+
     # ---- end-to-end through the C-ABI with host buffers (e2e): replay the
     # same trajectory (same initial states, same actions) as the timed region
     sim.set_state(init_states)
@@ -519,11 +593,11 @@ def run_b200(args):
     stats, tms = reduce_window({"acc": acc, "envs": float(E)},
                                {"total": ms_total, "e2e": ms_e2e, "phys": ms_phys, "rend": ms_rend,
                                 "phys_iso": ms_phys_iso, "rend_iso": ms_rend_iso, "one_cam": ms_one_cam,
-                                "interact": ms_interact},
+                                "interact": ms_interact, "grasp": ms_grasp},
                                device=dev if backend == "nccl" else "cpu")
     ms_total, ms_e2e, ms_phys, ms_rend = tms["total"], tms["e2e"], tms["phys"], tms["rend"]
     ms_phys_iso, ms_rend_iso, ms_one_cam = tms["phys_iso"], tms["rend_iso"], tms["one_cam"]
-    ms_interact = tms["interact"]
+    ms_interact, ms_grasp = tms["interact"], tms["grasp"]
     total_envs = E * world
     value = total_envs * args.steps / (ms_total * 1e-3)
     e2e_value = total_envs * args.steps / (ms_e2e * 1e-3)
@@ -548,18 +622,30 @@ def run_b200(args):
         # The render kernel dominates the GPU's work (SM-time); the physics step is
         # latency-bound (its duration is the slowest env's dependency chain on one
         # warp, see "physics_latency"), so the roofline is the render kernel's.
-        dom, ms_dom, flop, grid = "render_kernel", ms_rend_iso, render_flop, E * N_CAMS
-        achieved = flop * E / (ms_dom * 1e-3) / 1e12
-        ex_flop = 14.0 * (fp32_tests + fp64_tests)
-        ex_ach = ex_flop * E / (ms_dom * 1e-3) / 1e12
-        traffic, prof = None, None
-        try:  # dram read+write per launch of this kernel from the committed ncu --set full capture
+        dom, ms_dom, grid = "render_kernel", ms_rend_iso, E * N_CAMS
+        # roofline = the ray-plane work the kernel executes (FP32 bounded-error box
+        # tests + FP64 tests/resolutions, 14 flop each) against the two pipes' measured
+        # peaks: frac = (F32 / P32 + F64 / P64) / t, i.e. the busy fraction of an
+        # ideal machine doing exactly this work; peak = the matching harmonic mix
+        f32, f64 = 14.0 * fp32_tests * E, 14.0 * fp64_tests * E  # flop per launch
+        t_s = ms_dom * 1e-3
+        frac = (f32 / (peak32.value * 1e12) + f64 / (peak64.value * 1e12)) / t_s if peak32.value else None
+        p_eff = (f32 + f64) / (f32 / peak32.value + f64 / peak64.value) if peak32.value else None
+        traffic, prof, inst = None, None, None
+        try:  # dram read+write and warp instructions per launch of this kernel from the committed ncu --set full capture
             pj = json.load(open(os.path.join(ROOT, PROFILE_JSON)))
             kk = next((v for k, v in pj["kernels"].items() if k.startswith(dom)), None)
             if kk and kk["grid"] == grid:
-                traffic, prof = kk["dram_bytes_per_launch"], PROFILE_JSON
+                traffic, prof, inst = kk["dram_bytes_per_launch"], PROFILE_JSON, kk.get("warp_inst_per_launch")
         except (OSError, ValueError, KeyError):
             pass
+        sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+        global HBM_PEAK
+        try:
+            HBM_PEAK = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        except (OSError, ValueError, KeyError):
+            pass
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
         # per-env step latency of one more control step (rsim_bench_env_cycles probe)
         cyc = torch.zeros(E, dtype=torch.int64, device=dev)
         L.rsim_bench_env_cycles.argtypes = [C.c_void_p, C.c_void_p]
@@ -567,7 +653,7 @@ def run_b200(args):
         sim.env_step(act_d[args.warmup + args.steps - 1])
         torch.cuda.synchronize(dev)
         L.rsim_bench_env_cycles(sim._batch, None)
-        us = np.abs(cyc.cpu().numpy()) / (clk.summary().get("sm_mhz") or 1965.0)
+        us = np.abs(cyc.cpu().numpy()) / sm_mhz
         obs_bytes = E * N_CAMS * H * W * (4 + 4 + 4)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -582,22 +668,38 @@ def run_b200(args):
                        "l2": "inputs > L2: 805 MB of RGBD/id writes per step at 2048 envs evict the state slabs"},
             "kernels_ms_per_step": {"interleaved": {"ik+step+grasp": ms_phys, "render_kernel": ms_rend},
                                     "alone": {"ik+step+grasp": ms_phys_iso, "render_kernel": ms_rend_iso}},
-            "roofline": {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak32.value,
-                         "unit": "TFLOP/s", "frac": achieved / peak32.value if peak32.value else None,
+            "roofline": {"bound": "fp32+fp64 pipes", "kernel": dom, "achieved": (f32 + f64) / t_s / 1e12,
+                         "peak": p_eff, "unit": "TFLOP/s", "frac": frac,
                          "traffic": traffic, "traffic_source": prof,
-                         "algorithmic_bytes_per_launch": obs_bytes if dom == "render_kernel" else None,
-                         "peak_source": "measured FP32 FMA microbenchmark (rsim_bench_fma_peak); "
-                                        "MEASURED_PEAKS.json has no FP64/FP32 entry",
-                         "fp64_peak_tflops": peak64.value,
-                         "algorithmic_flop_per_unit": flop,
-                         "algorithmic_note": "SURVEY.md §8d W_r = brute-force proxy raycast (every ray vs every "
-                                             "plane, 14 flop per ray-plane); the kernel culls, so frac can exceed 1 "
-                                             "-- executed_frac is the FMA-pipe utilisation of the ray-plane work "
-                                             "actually done (bounded-error FP32 tests + FP64 resolution)",
+                         "algorithmic_bytes_per_launch": obs_bytes,
+                         "peak_source": "measured FMA microbenchmarks (rsim_bench_fma_peak): FP32 %.1f, FP64 %.1f "
+                                        "TFLOP/s; MEASURED_PEAKS.json has no FP32/FP64 entry; peak = their harmonic "
+                                        "mix weighted by this kernel's FP32/FP64 flop" % (peak32.value, peak64.value),
+                         "work_note": "executed ray-plane tests per env-step counted by the kernel's counting variant "
+                                      "(rsim_bench_render_work_detail, same trajectory state), 14 flop per test",
                          "executed_plane_tests_per_unit": {"fp32": fp32_tests, "fp64": fp64_tests},
-                         "executed_flop_per_unit": ex_flop, "executed_achieved": ex_ach,
-                         "executed_frac": ex_ach / peak32.value if peak32.value else None,
-                         "hbm_gbs_obs_writes": obs_bytes / (ms_rend_iso * 1e-3) / 1e9},
+                         "executed_flop_per_launch": {"fp32": f32, "fp64": f64},
+                         "fp32_peak_tflops": peak32.value, "fp64_peak_tflops": peak64.value,
+                         "issue_frac_ncu": (inst / (t_s * n_sm * 4 * sm_mhz * 1e6)) if inst else None,
+                         "issue_note": "warp instructions per launch (committed ncu capture) / (this run's kernel time "
+                                       "x SMs x 4 schedulers x SM clock): the pipe the kernel actually saturates",
+                         "brute_force_W_r": {
+                             "flop_per_unit": render_flop, "achieved_tflops": render_flop * E / t_s / 1e12,
+                             "frac_vs_fp32_peak": render_flop * E / t_s / 1e12 / peak32.value if peak32.value else None,
+                             "note": "SURVEY.md §8d W_r = every ray against every unique plane (566) and sphere; the "
+                                     "kernel culls to ~3 box tests per ray, so this ratio exceeds 1 and is not a "
+                                     "roofline fraction"},
+                         "hbm": {"achieved_gbs": obs_bytes / t_s / 1e9, "peak_gbs": HBM_PEAK,
+                                 "frac": obs_bytes / t_s / 1e9 / HBM_PEAK,
+                                 "note": "observation writes (RGBA u32 + depth f32 + id i32) per launch"}},
+            "physics_roofline": {
+                "bound": "fp64", "kernel": "ik_first+ik_fallback+step_kernel(+step_kernel_cta)+grasp, alone",
+                "W_p_flop_per_unit": phys_flop, "achieved": phys_flop * E / (ms_phys_iso * 1e-3) / 1e12,
+                "peak": peak64.value, "unit": "TFLOP/s",
+                "frac": phys_flop * E / (ms_phys_iso * 1e-3) / 1e12 / peak64.value if peak64.value else None,
+                "note": "SURVEY.md §8d W_p = 8 N_vp + 100 N_row + 120 N_fric + 20 sum m^3 with the frozen Idle "
+                        "counts (0.09 MFLOP per env-step); the step is latency-bound (serial Gauss-Seidel order "
+                        "inside an env), see physics_latency"},
             "physics_latency": {"note": "step kernel = one warp per env, latency-bound (serial Gauss-Seidel "
                                         "order inside an env); per-env SM time of one control step",
                                 "p50_us": float(np.percentile(us, 50)), "p99_us": float(np.percentile(us, 99)),
@@ -613,6 +715,8 @@ def run_b200(args):
                          "note": "Interact scenario (PAPER.md:530 second column; SURVEY.md §8d): robots at "
                                  "(1.6, 0.2) facing the light table, scripted EE pushes into the clutter; "
                                  "same interleaved physics + 2-camera render step"},
+            "interact_grasp": {"value": total_envs * args.steps / (ms_grasp * 1e-3), "unit": UNIT,
+                               "ms_per_step": ms_grasp / args.steps, **grasp_info},
             "gpu_launches": 6 * args.steps,  # ik_first, ik_fallback, step, step_cta, grasp, render per env step
             "clocks": clk.summary(),
             "episode_stats_allreduce": {"accumulated_contact_force_sum": stats["acc"], "envs": int(stats["envs"])},

@@ -87,12 +87,15 @@ def kernel_json(path):
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("rsim::", "")
         v = lambda k: float(r[hdr.index(k)])  # noqa: E731
-        a = agg.setdefault(name, {"launches": 0, "gpu_time_ms": 0.0, "dram_bytes": 0.0, "grid": int(v("launch__grid_size"))})
+        a = agg.setdefault(name, {"launches": 0, "gpu_time_ms": 0.0, "dram_bytes": 0.0, "inst": 0.0,
+                                  "grid": int(v("launch__grid_size"))})
         a["launches"] += 1
+        a["inst"] += v("smsp__inst_executed.sum") if "smsp__inst_executed.sum" in hdr else 0.0
         a["gpu_time_ms"] += v("gpu__time_duration.sum")
         a["dram_bytes"] += (v("dram__bytes_read.sum") + v("dram__bytes_write.sum")) * 1e6
     out = {k: {"launches": a["launches"], "grid": a["grid"], "gpu_time_ms": a["gpu_time_ms"] / a["launches"],
-               "dram_bytes_per_launch": a["dram_bytes"] / a["launches"]} for k, a in agg.items()}
+               "dram_bytes_per_launch": a["dram_bytes"] / a["launches"],
+               "warp_inst_per_launch": a["inst"] / a["launches"]} for k, a in agg.items()}
     print(json.dumps({"source": path.split("/")[-1], "kernels": out}, indent=1))
 
 
