@@ -938,7 +938,15 @@ __device__ void block_impulse_friction(Ctx &c, int g, int first, int m, BlockWS 
       r[RLT1] = f[19];
       r[RLT2] = f[20];
     }
-    for (int k = 0; k < 6; ++k) { c.S->u.sol.vel[a][k] = va[k]; c.S->u.sol.vel[b][k] = vb[k]; }
+    // write back only the velocities this block can change (solver inverse
+    // mass > 0): a static / kinematic partner's entry is shared with the
+    // blocks other warps solve concurrently (step_kernel_cta) and stays as is
+    bool wa = false, wb = false;
+    for (int i = 0; i < m; ++i) { wa |= F[kFastD * i + 21] > 0.0; wb |= F[kFastD * i + 22] > 0.0; }
+    for (int k = 0; k < 6; ++k) {
+      if (wa) c.S->u.sol.vel[a][k] = va[k];
+      if (wb) c.S->u.sol.vel[b][k] = vb[k];
+    }
   }
   __syncwarp();
 }
@@ -1808,7 +1816,7 @@ __device__ void substep_back(Ctx &c, double dt) {
     // events + force tally in row order: each row's impulse lanes-parallel,
     // then lane 0 visits the rows that register one, in order
     const int held = HELD(c);
-    double acc = S.sd[c.L->acc];
+    double acc = lane == 0 ? S.sd[c.L->acc] : 0.0;  // lane 0 owns the tally
     for (int i0 = 0; i0 < nc; i0 += 32) {
       double lam = 0.0;
       if (i0 + lane < nc) {
@@ -2218,7 +2226,9 @@ __global__ void __launch_bounds__(32 * kW) step_kernel_cta(DevBatch B, const dou
     if (lane == 0) H.ok = ok;
   }
   __syncthreads();
-  if (!H.ok) return;
+  const bool ok0 = H.ok;
+  __syncthreads();  // every warp has read H.ok before warp 0 rewrites it in the substep loop
+  if (!ok0) return;
   const DevScene &sc = *c.sc;
   const bool ht = has_targets == nullptr || has_targets[env];
   const double *arm = ht ? arm_targets + (size_t)env * sc.narm : nullptr;

@@ -24,6 +24,9 @@ as-is.  Fixtures:
   (``geometry.py:772-776``) in body-id order with the pinned tie rule
   (|t_b - t_min| <= 1e-9 -> lowest body id; ``physics.py:1096-1100`` keeps
   the lowest id on exact ties).
+* ``render_views.npz``  the same for layouts 0-2: random walkable views with
+  random arm joints, views with the head camera inside a static convex
+  (t = 0 pixels) and 2-8 cm in front of one (t < near pixels).
 * ``kat.npz``  known-answer values (SPEC.md examples) from the reference.
 * ``settle.npz``  per (layout, seed) of the pool recipe: the spawn state
   ``Simulator.settle`` builds, every AABB-overlapping ``parts_distance``
@@ -478,6 +481,115 @@ def gen_render():
         out[k] = np.stack([f[k] for f in frames])
     np.savez_compressed(os.path.join(OUT, "render.npz"), **out)
     print(f"  render: {len(frames)} frames")
+
+
+def view_state(sim, pool_state, base, arm):
+    """A pool state with the robot teleported to ``base`` with arm joints
+    ``arm`` (link bodies moved along, ``_update_robot_link_poses``)."""
+    st = pool_state.clone()
+    st.base = np.asarray(base, float)
+    st.joints[sim.arm_slice()] = arm
+    sim._update_robot_link_poses(st, 0.0)
+    return st
+
+
+def head_camera_pos(sim, base):
+    m = sim.robot
+    mount = m.cameras["head"]
+    return rb.base_pose3(np.asarray(base, float)).compose(mount.pose).pos
+
+
+def gen_render_views(n_random=24, n_special=4):
+    """Reference frames of all three layouts (VERDICT r1 'widen render
+    parity'): per layout ``n_random`` random views (robot at a random
+    walkable cell, random heading, random arm joints; head + arm cameras),
+    ``n_special`` views with the head camera inside a static convex (every
+    ray starts inside: t = 0 pixels) and ``n_special`` with the head camera
+    2-8 cm in front of a static body facing it (t < near pixels).  Ids and
+    ranges from the reference primitive (``render_ref``)."""
+    pool = np.load(os.path.join(OUT, "settled_pool.npz"))
+    out = {"meta": meta(), "fov": FOV, "near": NEAR, "far": FAR, "tie_eps": TIE_EPS}
+    frames = []
+    for v in range(3):
+        sim, _ = make_sim(v)
+        blobs = [b for b, (lv, _s) in zip(pool["snapshots"], pool["tags"]) if int(lv) == v]
+        rng = np.random.default_rng(500 + v)
+        g = sim.scene.navgrid
+        cells = np.argwhere(g.walkable)
+        lo, hi = np.array([j.limits[0] for j in sim.robot.joints]), np.array([j.limits[1] for j in sim.robot.joints])
+        statics = [b for b in range(sim.n_bodies) if sim.bodies[b].kind == "static"]
+
+        def pool_state():
+            return physics.WorldState.from_bytes(blobs[rng.integers(len(blobs))].tobytes())
+
+        def add(st, kind):
+            blob = st.to_bytes()
+            for cam in ("head", "arm"):
+                if kind != "random" and cam == "arm":
+                    continue
+                t, ids, pose = render_ref(sim, st, cam)
+                frames.append(dict(state=np.frombuffer(blob, np.uint8), cam=0 if cam == "head" else 1, t=t, ids=ids,
+                                   cam_pose=np.concatenate([pose.rot.reshape(9), pose.pos]), layout=v,
+                                   kind={"random": 0, "inside": 1, "near": 2}[kind]))
+            return frames[-1]["t"]
+
+        for _ in range(n_random):
+            ci, cj = cells[rng.integers(len(cells))]
+            base = [g.origin[0] + (ci + rng.uniform()) * g.cell, g.origin[1] + (cj + rng.uniform()) * g.cell,
+                    rng.uniform(-math.pi, math.pi)]
+            add(view_state(sim, pool_state(), base, lo + rng.uniform(size=len(lo)) * (hi - lo)), "random")
+        # head camera inside a static box part / 2-8 cm in front of one of its side faces,
+        # found geometrically (part frame), then confirmed by the frame itself
+        boxes = []
+        for b in statics:
+            for local, prim in sim.bodies[b].parts:
+                if isinstance(prim, geo.Box):
+                    wp = sim.scene.bodies[b].initial_pose.compose(local)
+                    h = np.asarray(prim.half, float)
+                    zlo, zhi = geo.prim_aabb(prim, wp)[0][2], geo.prim_aabb(prim, wp)[1][2]
+                    if zlo < 1.12 and zhi > 1.32 and abs(wp.rot[2, 2]) > 0.999:  # upright, spans the camera height
+                        boxes.append((wp, h))
+        found = {"inside": 0, "near": 0}
+        tries = 0
+        while (found["inside"] < n_special or found["near"] < n_special) and tries < 400 and boxes:
+            tries += 1
+            wp, h = boxes[rng.integers(len(boxes))]
+            kind = "inside" if found["inside"] < n_special else "near"
+            if kind == "inside":
+                if min(h[0], h[1]) < 0.03:
+                    continue
+                loc = np.array([rng.uniform(-0.6, 0.6) * h[0], rng.uniform(-0.6, 0.6) * h[1], 0.0])
+                yaw = rng.uniform(-math.pi, math.pi)
+            else:
+                ax, sgn = int(rng.integers(2)), float(rng.choice([-1.0, 1.0]))
+                loc = np.zeros(3)
+                loc[ax] = sgn * (h[ax] + rng.uniform(0.02, 0.08))
+                loc[1 - ax] = rng.uniform(-0.6, 0.6) * h[1 - ax]
+                nrm = wp.rot @ np.eye(3)[ax] * -sgn  # face the box
+                yaw = math.atan2(nrm[1], nrm[0])
+            tgt = wp.apply(loc)
+            cam0 = head_camera_pos(sim, [0.0, 0.0, yaw])
+            base = [tgt[0] - cam0[0], tgt[1] - cam0[1], yaw]
+            cam = head_camera_pos(sim, base)
+            cl = wp.inverse().apply(cam)
+            inside = (np.abs(cl) < h - 0.005).all()
+            if inside != (kind == "inside"):
+                continue
+            st = view_state(sim, pool_state(), base, sim.robot.resting_joints)
+            t = add(st, kind)
+            ok = (t == 0.0).any() if kind == "inside" else ((t > 0.0) & (t < NEAR)).any()
+            if ok:
+                found[kind] += 1
+            else:
+                frames.pop()
+        assert found == {"inside": n_special, "near": n_special}, found
+    for k in frames[0]:
+        out[k] = np.stack([f[k] for f in frames])
+    np.savez_compressed(os.path.join(OUT, "render_views.npz"), **out)
+    kinds = out["kind"]
+    print(f"  render_views: {len(frames)} frames ({int((kinds == 0).sum())} random, {int((kinds == 1).sum())} "
+          f"inside, {int((kinds == 2).sum())} near), t=0 px {int((out['t'] == 0).sum())}, "
+          f"t<near px {int(((out['t'] > 0) & (out['t'] < NEAR)).sum())}")
 
 
 # --------------------------------------------------------------------------
@@ -1030,7 +1142,7 @@ def gen_capacity():
 
 if __name__ == "__main__":
     t0 = time.time()
-    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "kat", "ik", "nav", "settle", "cast", "env", "grasp",
+    what = sys.argv[1:] or ["tables", "pool", "traj", "render", "views", "kat", "ik", "nav", "settle", "cast", "env", "grasp",
                             "capacity"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
@@ -1044,6 +1156,8 @@ if __name__ == "__main__":
         gen_trajectories(blobs, tags); print("traj", time.time() - t0)
     if "render" in what:
         gen_render(); print("render", time.time() - t0)
+    if "views" in what:
+        gen_render_views(); print("views", time.time() - t0)
     if "kat" in what:
         gen_kat(); print("kat", time.time() - t0)
     if "ik" in what:

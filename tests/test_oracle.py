@@ -225,3 +225,26 @@ def test_sphere_cast_matches_reference():
         assert (-1 if r is None else r[0]) == k["body"][i]
         if r is not None:
             assert r[1] == k["t"][i]
+
+
+def test_render_views_all_layouts_match_reference_primitive():
+    """render_views.npz: random walkable views of layouts 0-2 (both cameras,
+    random arm joints) plus head cameras inside a static convex (t = 0) and
+    2-8 cm in front of one (t < near -> depth clamped to near, id kept)."""
+    g = golden("render_views.npz")
+    orcs = {}
+    assert (g["t"] == 0).any() and ((g["t"] > 0) & (g["t"] < 0.1)).any()
+    for i in range(len(g["cam"])):
+        v = int(g["layout"][i])
+        orc = orcs.setdefault(v, oracle_for(v))
+        snap = g["state"][i].tobytes()
+        rgba, depth, ids, t = orc.render(snap, int(g["cam"][i]))
+        np.testing.assert_allclose(orc.camera_pose(snap, int(g["cam"][i])), g["cam_pose"][i], rtol=0, atol=1e-13)
+        ref_t = g["t"][i]
+        miss = ~(np.isfinite(ref_t) & (ref_t <= float(g["far"])))
+        np.testing.assert_array_equal(ids, np.where(miss, -1, g["ids"][i]), err_msg=f"frame {i}")
+        fin = np.isfinite(ref_t)
+        assert (np.isfinite(t) == fin).all()
+        np.testing.assert_allclose(t[fin], ref_t[fin], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(depth[~miss], np.maximum(ref_t[~miss], 0.1).astype(np.float32), rtol=1e-6)
+        assert (depth[miss] == 0).all() and (rgba[miss] == 0).all()

@@ -56,7 +56,7 @@ xy = torch.tensor(np.random.default_rng(6).uniform([-2, -1], [2, 1], (8, 2)), de
 sim.shortest_path(fields, torch.arange(8, dtype=torch.int32, device="cuda"), xy, layouts=[0, 1, 2, 0, 1, 2, 0, 1])
 o = torch.tensor(np.tile([2.3, -0.2, 0.5], (E, 1)), dtype=torch.float64, device="cuda")
 d = torch.tensor(np.tile([1.0, 0.0, 0.0], (E, 1)), dtype=torch.float64, device="cuda")
-sim.sphere_cast(o, d, torch.full((E,), 5.0, dtype=torch.float64, device="cuda"))
+sim.sphere_cast(o, d, 5.0)
 torch.cuda.synchronize()
 print("sanitize targets done", flush=True)
 sim.close()
