@@ -54,15 +54,28 @@ def _dptr(t: torch.Tensor | None):
 class BatchSimulator:
     def __init__(self, layouts=(0,), n_env: int = 1, clutter: list[str] | None = None, env_layout=None,
                  config: dict | None = None, render: dict | None = None, event_cap: int = 256,
-                 device: str | torch.device = "cuda", mesh_k: int | None = None):
+                 device: str | torch.device = "cuda", mesh_k: int | None = None, scenes: list[dict] | None = None):
+        """``scenes``: prebuilt scene tables (``compile_world`` format, e.g. from
+        a reference ``physics.Simulator`` through ``integration/rearrange_sim_b200.py``)
+        instead of the builtin layouts; ``layouts`` then labels them (default
+        0..len(scenes)-1) and ``clutter`` is ignored."""
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise native.NativeLibraryError("BatchSimulator runs on CUDA devices only (no CPU fallback)")
         self.L = native.lib()
-        clutter = clutter if clutter is not None else flat_clutter()
-        self.layouts = list(layouts)
-        self.worlds = [build_world(v, clutter) for v in self.layouts]
-        self.tables = [compile_world(w) for w in self.worlds]
+        if scenes is not None:
+            self.layouts = list(range(len(scenes))) if tuple(layouts) == (0,) and len(scenes) > 1 else list(layouts)
+            if len(self.layouts) != len(scenes):
+                raise ValueError("one layout label per scene")
+            if mesh_k is not None:
+                raise ValueError("mesh_k needs the builtin layouts (the triangle soups are built from their assets)")
+            self.worlds = None
+            self.tables = [dict(t) for t in scenes]
+        else:
+            clutter = clutter if clutter is not None else flat_clutter()
+            self.layouts = list(layouts)
+            self.worlds = [build_world(v, clutter) for v in self.layouts]
+            self.tables = [compile_world(w) for w in self.worlds]
         self.n_env = int(n_env)
         if env_layout is None:
             env_scene = np.arange(self.n_env, dtype=np.int32) % len(self.layouts)
@@ -72,14 +85,15 @@ class BatchSimulator:
         self.config = abi.physics_config(**(config or {}))
         self.rconfig = abi.render_config(**(render or {}))
         self.event_cap = int(event_cap)
-        w0 = self.worlds[0]
-        self.n_bodies, self.n_joints, self.n_arm = w0.n_bodies, w0.n_joints, w0.robot.dof
+        t0 = self.tables[0]
+        self.n_arm = int(t0["n_arm"])
+        self.n_bodies, self.n_joints = len(t0["body_kind"]), int(t0["n_scene_joints"]) + self.n_arm
         self.snap_size = snapshot_size(self.n_bodies, self.n_joints)
         with torch.cuda.device(self.device):
             self._descs = [abi.SceneDesc(t) for t in self.tables]
             self._scenes = []
             self._meshes = []
-            for w, d in zip(self.worlds, self._descs):
+            for w, d in zip(self.worlds or [None] * len(self._descs), self._descs):
                 h = C.c_void_p()
                 native.check(self.L.rs_scene_create(C.byref(d.desc), C.byref(h)), "rs_scene_create")
                 self._scenes.append(h)
@@ -187,11 +201,18 @@ class BatchSimulator:
             e = int(bad[0])
             kind, idx = int(f[e]) >> 16, int(f[e]) & 0xFFFF
             name = abi.FAULT_KINDS.get(kind, f"fault {kind}")
-            what = self.worlds[self.layouts.index(self.layouts[self.env_scene[e]])].bodies
+            names = self.body_names(int(self.env_scene[e]))
             if kind == 5:
                 raise PhysicsFault(f"env {e}: {name} ({abi.OVERFLOW_KINDS.get(idx, idx)}); state unchanged")
-            label = what[idx].name if kind in (1, 2, 3) and idx < len(what) else str(idx)
+            label = names[idx] if kind in (1, 2, 3) and idx < len(names) else str(idx)
             raise PhysicsFault(f"env {e}: {name} for {'body' if kind in (1, 2, 3) else 'index'} {idx} ({label})")
+
+    def body_names(self, scene: int = 0) -> list[str]:
+        """Body names of scene index ``scene`` (PhysicsFault messages)."""
+        if self.worlds is not None:
+            return [b.name for b in self.worlds[scene].bodies]
+        t = self.tables[scene]
+        return list(t["body_name"]) if "body_name" in t else [f"body {i}" for i in range(self.n_bodies)]
 
     def event_counts(self) -> torch.Tensor:
         return _ptr_tensor(self._bufs.event_count, 4 * self.n_env, torch.int32, self.device)

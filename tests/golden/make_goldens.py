@@ -1140,10 +1140,109 @@ def gen_capacity():
     record(sim, st, idle_targets(sim, st, 24, seed=8), "world62")
 
 
+# --------------------------------------------------------------------------
+# a non-builtin scene through the reference-side adapter (integration/)
+# --------------------------------------------------------------------------
+
+CUSTOM_CLUTTER = ["mug", "cracker_box", "sugar_box", "tomato_soup_can", "chef_can", "mug", "apple", "bowl",
+                  "cracker_box", "sponge", "orange", "tomato_soup_can"]
+
+
+def custom_sim():
+    """apt_0 with the light table moved and turned, a second kitchen cabinet
+    (3 more prismatic drawers) added, and a different clutter set (tall items,
+    mugs): 38 bodies, 7 scene joints -- not a builtin layout."""
+    j = builtin.layout_json(0)
+    j["layout_id"] = "apt_custom"
+    fur = [dict(f) for f in j["furniture"]]
+    for f in fur:
+        if f["ref"] == "light_table":
+            f["pos"], f["yaw"] = [0.3, -0.8, 0.0], 0.3
+    fur.append({"ref": "kitchen_cabinet", "kind": "articulation", "pos": [0.3, 2.45, 0.0], "yaw": 0.0})
+    j["furniture"] = fur
+    cache = builtin.default_cache()
+    sh = scene.load_scene(scene.layout_from_json(j), cache)
+    clutter = [(cache.get_asset(n), f"{n}#{i}") for i, n in enumerate(CUSTOM_CLUTTER)]
+    return physics.Simulator(sh, rb.default_model(), clutter, physics.PhysicsConfig())
+
+
+def gen_custom():
+    """traj_custom.npz: teacher-forcing records on ``custom_sim()`` plus the
+    adapter's ``rs_scene_desc`` tables (``scene_*`` keys) -- the GPU replays it
+    without the reference (tests/test_gpu_integration.py)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from integration.rearrange_sim_b200 import save_tables, scene_tables
+
+    sim = custom_sim()
+    rng = np.random.default_rng(21)
+    tab = [sj for sj in sim.scene.bodies if sj.name.startswith("light_table")][0]
+    top = tab.initial_pose
+    poses = []
+    for i, bid in enumerate(sim.clutter_body_ids):
+        lo, _ = geo.parts_aabb(sim.bodies[bid].parts, geo.Pose())
+        # tilted 3-8 degrees: a face landing flat on a plane is a symmetric, rank-deficient
+        # impact whose lateral outcome is rounding noise in the reference itself
+        ax = rng.normal(size=3)
+        ax[2] = 0.0
+        rot = geo.rot_z(rng.uniform(-math.pi, math.pi)) @ geo.rot_axis_angle(ax / np.linalg.norm(ax), math.radians(rng.uniform(3, 8)))
+        if i < 8:  # dropped onto the moved light table, 4 x 2 grid
+            x, y = (-0.39 + 0.26 * (i % 4)), (-0.18 + 0.36 * (i // 4))
+            p = top.apply(np.array([x, y, 0.87 + 0.13])) + np.array([0.0, 0.0, -lo[2] + 0.02])
+        else:  # onto the dark table (resting on the backdrop floor is chaotic in the reference
+            # itself: its state moves 2e-5 m in 3 steps between two BLAS kernels, DESIGN.md §2)
+            dk = [sj for sj in sim.scene.bodies if sj.name.startswith("dark_table")][0].initial_pose
+            p = dk.apply(np.array([-0.2 + 0.4 * ((i - 8) % 2), -0.2 + 0.4 * ((i - 8) // 2), 0.96])) + \
+                np.array([0.0, 0.0, -lo[2] + 0.02])
+        poses.append(geo.Pose(rot, p))
+    st = sim.make_initial_state(poses, base=np.array([1.0, -0.9, math.pi]), clutter_asleep=False)
+    seq = idle_targets(sim, st, 30, seed=12)
+    out = {}
+    save_tables(scene_tables(sim), out)
+    record(sim, st, seq, "custom")
+    path = os.path.join(OUT, "traj_custom.npz")
+    g = dict(np.load(path))
+    g.update(out)
+    np.savez_compressed(path, **g)
+    # the reference's own per-step sensitivity: the same teacher-forced steps under
+    # two other OpenBLAS kernels (a tall can rocking on its 12-gon face is chaotic:
+    # rounding-level differences reach 1e-4 m in one control step); the GPU / oracle
+    # tests accept per-step deviations within this spread
+    spreads = []
+    for ct in ("SkylakeX", "Prescott"):
+        tmp = os.path.join(OUT, f".spread_{ct}.npy")
+        env = dict(os.environ, OPENBLAS_CORETYPE=ct, OPENBLAS_NUM_THREADS="1")
+        import subprocess
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--spread", path, tmp], env=env, check=True)
+        spreads.append(np.load(tmp))
+        os.remove(tmp)
+    g["ref_spread"] = np.maximum(*spreads)  # [steps, 3]: max |d pos|, |d quat|, |d vel| vs this file's post
+    np.savez_compressed(path, **g)
+    print(f"  traj_custom: reference cross-BLAS spread per step: pos <= {g['ref_spread'][:, 0].max():.1e}, "
+          f"quat <= {g['ref_spread'][:, 1].max():.1e}, vel <= {g['ref_spread'][:, 2].max():.1e}")
+
+
+def spread_main(src, dst):
+    """``--spread``: teacher-forced steps of ``src`` under this process's BLAS kernel."""
+    g = np.load(src)
+    sim = custom_sim()
+    res = []
+    for s in range(len(g["pre"])):
+        st = physics.WorldState.from_bytes(g["pre"][s].tobytes())
+        tg = rb.JointTargets(arm=g["arm"][s].copy(), base=rb.BaseAction(*g["base"][s])) if g["has_targets"][s] else None
+        st2, _ = sim.step_physics(st, tg)
+        ref = physics.WorldState.from_bytes(g["post"][s].tobytes())
+        res.append([np.abs(st2.pos - ref.pos).max(), np.abs(st2.quat - ref.quat).max(),
+                    max(np.abs(st2.lin_vel - ref.lin_vel).max(), np.abs(st2.ang_vel - ref.ang_vel).max())])
+    np.save(dst, np.array(res))
+
+
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["--spread"]:
+        spread_main(sys.argv[2], sys.argv[3])
+        sys.exit(0)
     t0 = time.time()
     what = sys.argv[1:] or ["tables", "pool", "traj", "render", "views", "kat", "ik", "nav", "settle", "cast", "env", "grasp",
-                            "capacity"]
+                            "capacity", "custom"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
     blobs = tags = None
@@ -1175,3 +1274,5 @@ if __name__ == "__main__":
         gen_grasp(); print("grasp", time.time() - t0)
     if "capacity" in what:
         gen_capacity(); print("capacity", time.time() - t0)
+    if "custom" in what:
+        gen_custom(); print("custom", time.time() - t0)
