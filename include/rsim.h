@@ -233,6 +233,12 @@ int rs_step_host(rs_batch *batch, const double *h_arm_targets, const double *h_b
                  int32_t substeps, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                  double *h_out_stats, void *stream);
 
+/* Per-env results of the current state on `stream`, device out [n_env][4] f64:
+ * accumulated_contact_force (physics.py:944-959; the SPEC's StepResult
+ * info "accumulated force N"), fault word, event count of the last step,
+ * sleeping-body count -- what rs_step_host copies back, for device callers. */
+int rs_step_stats(rs_batch *batch, double *out, void *stream);
+
 /* Triangle-soup scene representation (AssetDef.visual_mesh scene.py:63-76,
  * SURVEY.md §8a R3): per part a triangle list in the part frame with a BVH
  * (paper_2106_14405_b200/mesh.py).  Must be attached before rs_batch_create. */

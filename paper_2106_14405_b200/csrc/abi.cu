@@ -621,6 +621,13 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
   return RS_OK;
 }
 
+int rs_step_stats(rs_batch *b, double *out, void *stream) {
+  DeviceScope device_scope(b);
+  if (!b || !out) return fail(RS_ERR_ARG, "null argument");
+  CUDA_TRY(launch_stats(b->view(), out, (cudaStream_t)stream));
+  return RS_OK;
+}
+
 int rsim_bench_render_work_detail(rs_batch *b, uint32_t cam_mask, unsigned long long *d_counters, void *stream) {
   DeviceScope device_scope(b);
   if (!b || !d_counters) return fail(RS_ERR_ARG, "null argument");

@@ -17,9 +17,21 @@ the render reads s_t while the step writes s_{t+1}.  Interleaved and
 sequential execution produce bit-identical states and observations
 (tests/test_gpu_env.py) -- the correctness condition of SPEC.md:336.
 
+``step(action)`` takes the SPEC action (§5.1): an
+``[E, 6]`` float64 tensor (or a dict ``{"arm": [E, 3], "gripper": [E],
+"base": [E, 2]}``) = ArmAction (EE displacement in the robot base frame,
+clamped to 1.5 cm; gripper scalar) + BaseAction (linear m/s, angular rad/s),
+executed on the device as IK -> step_physics -> grasp rule (rs_env_step).
+Joint targets can still be given directly (``arm_targets=``, ``base_cmd=``).
+
 Rewards/tasks are outside this hot path: ``reward`` is
-0 and ``done`` marks the horizon or a physics fault; ``info`` carries the
-per-env fault word and event count.  With ``set_nav_goals`` the geodesic
+0.  ``done`` marks the horizon, a physics fault or an accumulated contact
+force above ``force_limit`` (the Pick / Place thresholds, SPEC.md:480);
+``info`` follows the SPEC's StepResult: ``success``
+(False: no task), ``failure_reason`` (per env, ``FAILURE_REASONS``),
+``accumulated_force`` (N), ``step_index``, plus the fault word and event
+count.  Stepping again while any env is done raises ``EpisodeDone`` (the
+SPEC's "step after done" error) until those envs are ``reset``.  With ``set_nav_goals`` the geodesic
 navigation terms the skill rewards are built from (Navigate
 "20 Delta_agent^goal") are computed on the device every step:
 ``info["geodesic"]`` = NavGrid.geodesic_distance(robot base, goal)
@@ -34,10 +46,18 @@ import torch
 
 from .sim import BatchSimulator
 
+# info["failure_reason"] codes
+FAILURE_REASONS = {0: "none", 1: "horizon", 2: "physics_fault", 3: "force_limit"}
+
+
+class EpisodeDone(RuntimeError):
+    """step() on an env whose episode is done (SPEC.md:320 'step after done')."""
+
 
 class BatchEnv:
     def __init__(self, n_env: int, layouts=(0, 1, 2), env_layout=None, cams=("head", "arm"), obs_delay: int = 1,
-                 interleave: bool = True, horizon: int | None = None, device="cuda", **sim_kwargs):
+                 interleave: bool = True, horizon: int | None = None, force_limit: float | None = None, device="cuda",
+                 **sim_kwargs):
         if obs_delay not in (0, 1):
             raise ValueError("obs_delay must be 0 or 1")
         self.sim = BatchSimulator(layouts=layouts, n_env=n_env, env_layout=env_layout, device=device, **sim_kwargs)
@@ -47,6 +67,11 @@ class BatchEnv:
         self.obs_delay = obs_delay
         self.interleave = interleave and obs_delay == 1
         self.horizon = horizon
+        self.force_limit = force_limit
+        self._done = torch.zeros(n_env, dtype=torch.bool, device=self.sim.device)
+        self._done_host = torch.zeros(n_env, dtype=torch.bool).pin_memory()
+        self._done_ready = torch.cuda.Event()
+        self._t_env = torch.zeros(n_env, dtype=torch.int64, device=self.sim.device)
         self._obs = [self.sim.alloc_obs(self.cams) for _ in range(2)]  # double-buffered observations
         self._k = 0
         self.t = 0
@@ -95,10 +120,21 @@ class BatchEnv:
         return self._geo.clone()
 
     def reset(self, snapshots, env_ids=None):
-        """Load episode start states (reference snapshot bytes) and return o_0."""
-        torch.cuda.current_stream(self.device).wait_stream(self._render_stream)
+        """Load episode start states (reference snapshot bytes) into all envs, or
+        into ``env_ids``, and return o_0 (rendered for every env)."""
+        main = torch.cuda.current_stream(self.device)
+        main.wait_stream(self._render_stream)
         self.sim.set_state(snapshots, env_ids)
-        self.t = 0
+        if env_ids is None:
+            self.t = 0
+            self._done.zero_()
+            self._t_env.zero_()
+        else:
+            idx = torch.as_tensor(np.asarray(env_ids), dtype=torch.long, device=self.device)
+            self._done[idx] = False
+            self._t_env[idx] = 0
+        self._done_host.copy_(self._done, non_blocking=True)
+        self._done_ready.record(main)
         if self._nav_fields is not None:
             self._geo = self.sim.geodesic_distance(self._nav_fields, self._nav_idx)
         obs = self._obs[self._k]
@@ -106,7 +142,43 @@ class BatchEnv:
         self.sim.render(self.cams, out=obs)
         return self._proprio({"rgba": obs[0], "depth": obs[1], "ids": obs[2], "rendered_from_step": 0})
 
-    def step(self, arm_targets: torch.Tensor, base_cmd: torch.Tensor, gripper: torch.Tensor | None = None):
+    def _action(self, action):
+        """SPEC action -> [E, 6] float64 device tensor (dEE xyz, gripper, base lin, base ang)."""
+        if isinstance(action, dict):
+            a = torch.zeros((self.n_env, 6), dtype=torch.float64, device=self.device)
+            if "arm" in action:
+                a[:, 0:3] = torch.as_tensor(action["arm"], dtype=torch.float64).to(self.device)
+            if "gripper" in action:
+                a[:, 3] = torch.as_tensor(action["gripper"], dtype=torch.float64).to(self.device)
+            if "base" in action:
+                a[:, 4:6] = torch.as_tensor(action["base"], dtype=torch.float64).to(self.device)
+            return a
+        a = torch.as_tensor(action, dtype=torch.float64).to(self.device).contiguous()
+        if tuple(a.shape) != (self.n_env, 6):
+            raise ValueError(f"action must be [n_env, 6] (dEE xyz, gripper, base lin, base ang), got {tuple(a.shape)}")
+        return a
+
+    def step(self, action=None, *, arm_targets: torch.Tensor | None = None, base_cmd: torch.Tensor | None = None,
+             gripper: torch.Tensor | None = None):
+        """One env step.  ``action``: the SPEC action (IK -> physics -> grasp on
+        the device); or ``arm_targets`` [E, 7] + ``base_cmd`` [E, 2] (+ optional
+        ``gripper`` [E]) joint targets.  Returns (obs, reward, done, info)."""
+        if (action is None) == (arm_targets is None):
+            raise ValueError("pass either the SPEC action or arm_targets/base_cmd")
+        self._done_ready.synchronize()  # the previous step's done flags (usually complete already)
+        if bool(self._done_host.any()):
+            bad = torch.nonzero(self._done_host).flatten()[:8].tolist()
+            raise EpisodeDone(f"step after done: envs {bad} ... must be reset first (SPEC.md:320)")
+        act = self._action(action) if action is not None else None
+
+        def physics():
+            if act is not None:
+                self.sim.env_step(act)
+            else:
+                self.sim.step_physics(arm_targets, base_cmd)
+                if gripper is not None:
+                    self.sim.grasp(gripper)
+
         main = torch.cuda.current_stream(self.device)
         self._k ^= 1
         obs = self._obs[self._k]
@@ -120,7 +192,7 @@ class BatchEnv:
                 self._render_done.record(self._render_stream)
                 self._phys_stream.wait_stream(main)
                 with torch.cuda.stream(self._phys_stream):
-                    self.sim.step_physics(arm_targets, base_cmd)
+                    physics()
                 main.wait_stream(self._phys_stream)
                 # the next step overwrites the buffer this render reads: join here
                 main.wait_event(self._render_done)
@@ -131,22 +203,32 @@ class BatchEnv:
             else:
                 self.sim.render(self.cams, out=obs)
                 extra = self._proprio({})
-                self.sim.step_physics(arm_targets, base_cmd)
+                physics()
             rendered = self.t
         else:
-            self.sim.step_physics(arm_targets, base_cmd)
+            physics()
             self.sim.render(self.cams, out=obs)
             extra = self._proprio({})
             rendered = self.t + 1
-        if gripper is not None:
-            self.sim.grasp(gripper)
         self.t += 1
+        self._t_env += 1
+        stats = self.sim.step_stats(self._stats)
         fault = self.sim.faults()
-        done = fault != 0
-        if self.horizon is not None and self.t >= self.horizon:
-            done = torch.ones_like(done)
+        acc = stats[:, 0]
+        reason = torch.zeros(self.n_env, dtype=torch.int32, device=self.device)
+        if self.horizon is not None:
+            reason = torch.where(self._t_env >= self.horizon, torch.ones_like(reason), reason)
+        if self.force_limit is not None:
+            reason = torch.where(acc > self.force_limit, torch.full_like(reason, 3), reason)
+        reason = torch.where(fault != 0, torch.full_like(reason, 2), reason)
+        done = reason != 0
+        self._done.copy_(done)
+        self._done_host.copy_(done, non_blocking=True)
+        self._done_ready.record(main)
         reward = torch.zeros(self.n_env, dtype=torch.float32, device=self.device)
-        info = {"fault": fault, "event_count": self.sim.event_counts(), "step_index": self.t}
+        info = {"success": torch.zeros(self.n_env, dtype=torch.bool, device=self.device), "failure_reason": reason,
+                "accumulated_force": acc, "step_index": self.t, "fault": fault,
+                "event_count": self.sim.event_counts()}
         if self._nav_fields is not None:  # geodesic terms of s_{t+1} from every robot base
             geo = self.sim.geodesic_distance(self._nav_fields, self._nav_idx)
             info["geodesic"] = geo

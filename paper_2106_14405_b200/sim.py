@@ -285,6 +285,14 @@ class BatchSimulator:
                                              C.c_void_p(h_stats.data_ptr()), self._sp()), "rs_env_step_host")
         return h_stats, (rgba, depth, ids)
 
+    def step_stats(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """rs_step_stats: [E, 4] f64 device tensor of the current state --
+        accumulated contact force (N), fault word, events of the last step,
+        sleeping bodies -- on the current stream."""
+        out = out if out is not None else torch.empty((self.n_env, 4), dtype=torch.float64, device=self.device)
+        native.check(self.L.rs_step_stats(self._batch, _dptr(out), self._sp()), "rs_step_stats")
+        return out
+
     # ------------------------------------------------------------------ grasp
     def grasp(self, gripper: torch.Tensor):
         g = self._dev(gripper, (self.n_env,), torch.float64)

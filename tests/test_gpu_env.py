@@ -39,7 +39,7 @@ def _run(interleave, delay, n=24, steps=6):
     states, rendered = [], []
     arm, base = _actions(n, steps)
     for k in range(steps):
-        obs, rew, done, info = env.step(arm[k], base[k])
+        obs, rew, done, info = env.step(arm_targets=arm[k], base_cmd=base[k])
         frames.append(obs["depth"].clone())
         rendered.append(obs["rendered_from_step"])
         states.append(env.states())
@@ -90,7 +90,7 @@ def test_geodesic_navigation_terms_vs_oracle():
     arm, base = _actions(n, steps)
     prev = g0
     for k in range(steps):
-        _, _, _, info = env.step(arm[k], base[k])
+        _, _, _, info = env.step(arm_targets=arm[k], base_cmd=base[k])
         torch.cuda.synchronize()
         geo = info["geodesic"].cpu().numpy()
         for e, blob in enumerate(env.sim.get_state()):
@@ -144,8 +144,75 @@ def test_proprioception_fields_match_host_restatement():
     prev, cur = None, env.sim.get_state()
     expect(obs, cur, prev)
     for k in range(steps):
-        obs, _, _, _ = env.step(arm[k], base[k])  # o_t from s_t (= cur)
+        obs, _, _, _ = env.step(arm_targets=arm[k], base_cmd=base[k])  # o_t from s_t (= cur)
         torch.cuda.synchronize()
         expect(obs, cur, prev)
         prev, cur = cur, env.sim.get_state()
+    env.close()
+
+
+def test_spec_action_step_matches_device_env_step():
+    """BatchEnv.step(action) with the SPEC action (ArmAction + BaseAction as
+    [E, 6]) runs IK -> physics -> grasp (rs_env_step): the same states as
+    BatchSimulator.env_step on the same actions, in interleaved and
+    sequential mode; the dict form is the same action."""
+    from paper_2106_14405_b200.env import BatchEnv
+    from paper_2106_14405_b200.sim import BatchSimulator
+
+    n, steps = 12, 4
+    snaps, layouts = _episode(n)
+    rng = np.random.default_rng(3)
+    act = np.zeros((steps, n, 6))
+    act[..., :3] = rng.uniform(-0.02, 0.02, (steps, n, 3))
+    act[..., 4] = rng.uniform(-0.5, 1.0, (steps, n))
+    act[..., 5] = rng.uniform(-1, 1, (steps, n))
+    act = torch.tensor(act, device="cuda")
+    ref = BatchSimulator(layouts=(0, 1, 2), n_env=n, env_layout=layouts)
+    ref.set_state(snaps)
+    want = []
+    for k in range(steps):
+        ref.env_step(act[k])
+        want.append(ref.get_state())
+    ref.close()
+    for interleave in (True, False):
+        env = BatchEnv(n, layouts=(0, 1, 2), env_layout=layouts, interleave=interleave)
+        env.reset(snaps)
+        for k in range(steps):
+            a = act[k] if k % 2 == 0 else {"arm": act[k, :, :3], "gripper": act[k, :, 3], "base": act[k, :, 4:6]}
+            obs, rew, done, info = env.step(a)
+            assert env.states() == want[k], f"step {k} interleave={interleave}"
+            assert info["step_index"] == k + 1 and not bool(info["success"].any())
+            assert (info["failure_reason"] == 0).all() and not bool(done.any())
+            assert info["accumulated_force"].shape == (n,) and bool((info["accumulated_force"] >= 0).all())
+        env.close()
+
+
+def test_horizon_force_limit_and_step_after_done():
+    """stepping past the horizon ends the episode with
+    failure_reason = horizon; a force limit ends it with force_limit; a
+    further step raises EpisodeDone until the env is reset."""
+    from paper_2106_14405_b200.env import FAILURE_REASONS, BatchEnv, EpisodeDone
+
+    n = 6
+    snaps, layouts = _episode(n)
+    env = BatchEnv(n, layouts=(0, 1, 2), env_layout=layouts, horizon=2)
+    env.reset(snaps)
+    a = torch.zeros((n, 6), dtype=torch.float64, device="cuda")
+    _, _, done, info = env.step(a)
+    assert not bool(done.any())
+    _, _, done, info = env.step(a)
+    assert bool(done.all()) and FAILURE_REASONS[int(info["failure_reason"][0])] == "horizon"
+    with pytest.raises(EpisodeDone):
+        env.step(a)
+    env.reset(snaps[:2], env_ids=[0, 1])
+    with pytest.raises(EpisodeDone):  # envs 2..5 are still done
+        env.step(a)
+    env.reset(snaps)
+    _, _, done, _ = env.step(a)
+    assert not bool(done.any())
+    env.close()
+    env = BatchEnv(n, layouts=(0, 1, 2), env_layout=layouts, force_limit=-1.0)  # every env over the limit
+    env.reset(snaps)
+    _, _, done, info = env.step(a)
+    assert bool(done.all()) and FAILURE_REASONS[int(info["failure_reason"][0])] == "force_limit"
     env.close()
