@@ -283,7 +283,7 @@ class CpuOracle:
 # rows; per row a 30-step warm-up per core, then 10 runs reported as mean +-
 # 95 % CI (Student t, 9 dof).  Run lengths (env-steps per core per run) keep
 # the whole sample near 10-20 s of host time.
-CPU_ROWS = (("physics_only", 0, 40), ("one_camera", 1, 6), ("two_camera", 2, 4))
+CPU_ROWS = (("physics_only", 0, 400), ("one_camera", 1, 6), ("two_camera", 2, 4))
 CPU_RUNS, CPU_WARMUP = 10, 30
 T975_9DOF = 2.262
 

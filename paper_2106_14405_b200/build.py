@@ -14,7 +14,10 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "_lib")
+# RSIM_LIB_DIR / RSIM_NVCC_FLAGS: build an A/B variant elsewhere (e.g. _lib_w2 with
+# -DRSIM_WARPS_PER_BLOCK=2), loaded with RSIM_LIB=<dir>/librsim.so
+OUT_DIR = os.environ.get("RSIM_LIB_DIR") or os.path.join(HERE, "_lib")
+EXTRA = os.environ.get("RSIM_NVCC_FLAGS", "").split()
 LIB = os.path.join(OUT_DIR, "librsim.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -72,7 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         if not force and not _obj_stale(unit, obj):
             continue
-        cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
+        cmd = [nvcc, *ARCH, *COMMON, *extra, *EXTRA, "-c", os.path.join(CSRC, unit), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)

@@ -36,7 +36,14 @@
 
 namespace rsim {
 
-constexpr int kWarpsPerBlock = 2;
+// envs (warps) per step_kernel CTA (measured in the interleaved bench step,
+// 2048 envs: 2 -> 1.10 M env-steps/s; 3, whose CTA fits one render CTA's
+// register / shared-memory slot -> 1.08 M: a CTA lives as long as its slowest env)
+#ifndef RSIM_WARPS_PER_BLOCK
+#define RSIM_WARPS_PER_BLOCK 2
+#endif
+constexpr int kWarpsPerBlock = RSIM_WARPS_PER_BLOCK;
+constexpr int kStepMinBlocks = kWarpsPerBlock == 1 ? 10 : (kWarpsPerBlock == 2 ? 5 : (kWarpsPerBlock == 3 ? 4 : 3));
 constexpr int kMaxCand = 1024;
 constexpr int kMaxAdm = 256;
 constexpr int kMaxContacts = 512;  // rows per substep (HBM scratch); 2.8x the 26-object pile's 185
@@ -115,8 +122,10 @@ __host__ __device__ constexpr size_t warp_smem_bytes(int stage) {
 
 // 5 two-warp CTAs per SM (228 KB of shared memory, 1 KB reserved per CTA)
 static_assert(13 * kMaxBodies + 2 * kMaxJoints + 16 <= kStageD, "state slab prefix must fit the staging buffer");
-// 5 two-warp CTAs per SM even for a 64-body scene (228 KB of shared memory, 1 KB reserved per CTA)
-static_assert(5 * (2 * warp_smem_bytes(13 * kMaxBodies + 2 * kMaxJoints + 16) + 1024) <= 228 * 1024,
+// >= 9 envs per SM even for a 64-body scene (228 KB of shared memory, 1 KB reserved per CTA)
+static_assert((kWarpsPerBlock == 1 ? 10 : (kWarpsPerBlock == 2 ? 5 : (kWarpsPerBlock == 3 ? 3 : 2))) *
+                      (kWarpsPerBlock * warp_smem_bytes(13 * kMaxBodies + 2 * kMaxJoints + 16) + 1024) <=
+                  228 * 1024,
               "step_kernel occupancy");
 
 struct Ctx {
@@ -2164,7 +2173,7 @@ __device__ void env_end(Ctx &c, const DevBatch &B, int env, double dt, bool ok, 
 }
 
 // warp per env (envs not flagged heavy by the previous step)
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 5) step_kernel(DevBatch B, const double *arm_targets,
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, kStepMinBlocks) step_kernel(DevBatch B, const double *arm_targets,
                                                                    const double *base_cmd, int base_stride,
                                                                    const uint8_t *has_targets, double dt,
                                                                    int substeps, const uint8_t *heavy_in,
