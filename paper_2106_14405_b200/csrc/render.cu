@@ -689,7 +689,15 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       const int u = ux + (k % kTile), v = vy + (k / kTile);
       const double *dc = B.ray_dir + 3 * ((size_t)v * W + u);  // unit camera-frame ray (render_tables_kernel)
       double d[3];
-      matvec(S.cam.R, dc, d);
+      {  // matvec(S.cam.R, dc, d) with the rotation re-read from shared memory per pixel: hoisted out
+         // of the loop it takes 18 registers, and at the 64-register budget ptxas spilled 6 of its
+         // doubles to local memory and reloaded them (LDL) for every pixel
+        const volatile double *Rv = S.cam.R;
+        const double x = dc[0], y = dc[1], z = dc[2];
+        d[0] = Rv[0] * x + Rv[1] * y + Rv[2] * z;
+        d[1] = Rv[3] * x + Rv[4] * y + Rv[5] * z;
+        d[2] = Rv[6] * x + Rv[7] * y + Rv[8] * z;
+      }
       double tmin;
       int id, wpart, wface;
       if (kMode != kProxyMixed ||
