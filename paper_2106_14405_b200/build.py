@@ -13,7 +13,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CSRC = os.path.join(HERE, "csrc")
+CSRC = os.environ.get("RSIM_CSRC") or os.path.join(HERE, "csrc")  # RSIM_CSRC: A/B source tree
 # RSIM_LIB_DIR / RSIM_NVCC_FLAGS: build an A/B variant elsewhere (e.g. _lib_w2 with
 # -DRSIM_WARPS_PER_BLOCK=2), loaded with RSIM_LIB=<dir>/librsim.so
 OUT_DIR = os.environ.get("RSIM_LIB_DIR") or os.path.join(HERE, "_lib")
