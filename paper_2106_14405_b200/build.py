@@ -31,7 +31,7 @@ UNITS = {
     "settle.cu": ["-fmad=false"],
     "query.cu": ["-fmad=false"],
 }
-HEADERS = ["device.cuh", "se3.cuh", "navgrid.cuh"]
+HEADERS = ["device.cuh", "se3.cuh", "navgrid.cuh", "bulk.cuh"]
 
 
 def _nvcc() -> str:

@@ -31,6 +31,7 @@
 #include <cstdint>
 
 #include "../../include/rsim_bench.h"
+#include "bulk.cuh"
 #include "device.cuh"
 #include "se3.cuh"
 
@@ -83,6 +84,7 @@ struct RenderSmem {
   uint8_t order[kMaxParts];
   float color[kMaxBodies][3];  // body albedo (shading reads it per pixel)
   Pose cam;
+  uint64_t mbar;  // completion barrier of the facet-table TMA bulk copy
 };
 // world planes (n.xyz, b0 per facet; mesh variant: part rotations) follow the struct
 constexpr size_t kPlaneOff = (sizeof(RenderSmem) + 15) & ~(size_t)15;
@@ -471,6 +473,17 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
   return true;
 }
 
+// TMA bulk copy of a scene's facet table into shared memory (thread 0),
+// completed on `bar`.  Out of line: the 64-register render kernel's allocation
+// is sensitive to any extra live value.
+__device__ __noinline__ void stage_facets(double *dst, const double *facets, int nf, uint64_t *bar) {
+  const uint32_t bytes = (uint32_t)(nf * 4 * sizeof(double));  // 32-byte facets: a 16-byte multiple
+  mbar_init(bar, 1);
+  mbar_arrive_expect_tx(bar, bytes);
+  bulk_g2s(dst, facets, bytes, bar);
+}
+__device__ __noinline__ void wait_bulk(uint64_t *bar) { mbar_wait(bar, 0); }
+
 template <int kMode, bool kCount>
 __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBlocksMesh : kMinBlocksProxy)
     render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out, uint32_t *rgba, float *depth, int32_t *ids,
@@ -490,6 +503,10 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   const StateLayout &L = B.L;
   const double *sd = B.sd + (size_t)env * L.dbl_size;
   const int tid = threadIdx.x, np = sc.np;
+  // the scene's local facet table (n, offset per facet) into the plane array by
+  // one TMA bulk copy, overlapped with the camera pose and the part frames; each
+  // thread then turns its facets into world planes in place
+  if (!kMesh && tid == 0) stage_facets(plane, sc.facet, sc.nf, &S.mbar);
 
   // -- camera pose (robot.py:43-47 mounts; tools_make_robot_json.py:12-19 axes);
   //    the arm chain's joint rotations are computed by one thread each first
@@ -560,6 +577,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     P.lb = dist > 0.0 ? dist : 0.0;
     S.trace[p] = make_float2(__double2float_rd(P.lb), __int_as_float((P.kind << 8) | b));
   }
+  if (!kMesh && tid == 0) wait_bulk(&S.mbar);
   __syncthreads();
   if (!kMesh) {
     const int nf = sc.nf;
@@ -569,11 +587,11 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
         const int mid = (lo + hi + 1) >> 1;
         if (S.part[mid].f0 <= f) lo = mid; else hi = mid - 1;
       }
-      const double *F = sc.facet + 4 * f, *R = S.u.R[lo], *wpp = S.part[lo].c;
+      double *Q = plane + 4 * f;  // holds the staged local facet until overwritten below
+      const double F[4] = {Q[0], Q[1], Q[2], Q[3]}, *R = S.u.R[lo], *wpp = S.part[lo].c;
       double n[3];
       matvec(R, F, n);
       double dw = F[3] + dot3(n, wpp);
-      double *Q = plane + 4 * f;
       Q[0] = n[0]; Q[1] = n[1]; Q[2] = n[2];
       Q[3] = dw - dot3(o, n);
     }
