@@ -1236,13 +1236,31 @@ def spread_main(src, dst):
     np.save(dst, np.array(res))
 
 
+def gen_empty():
+    """traj_empty.npz: a scene without clutter (``Simulator(..., clutter=[])``,
+    22 bodies): the robot drives up to the kitchen cabinet of apt_1 and pushes
+    its arm into the drawer fronts (robot vs kinematic jointed bodies only)."""
+    sim, _ = make_sim(1, n_clutter=0)
+    st = sim.make_initial_state([], base=np.array([-3.75, -0.5, math.pi]), clutter_asleep=False)
+    m = sim.robot
+
+    def push(k):
+        def f(sim, st):
+            d = np.array([0.015, 0.0, -0.01 if k < 10 else 0.0])
+            tg = rb.apply_arm_action(m, st.joints[sim.arm_slice()], rb.ArmAction(d, 0.0), sim.counters)
+            tg.base = rb.BaseAction(0.25 if k < 16 else 0.0, 0.0)
+            return tg
+        return f
+    record(sim, st, [push(k) for k in range(28)], "empty")
+
+
 if __name__ == "__main__":
     if sys.argv[1:2] == ["--spread"]:
         spread_main(sys.argv[2], sys.argv[3])
         sys.exit(0)
     t0 = time.time()
     what = sys.argv[1:] or ["tables", "pool", "traj", "render", "views", "kat", "ik", "nav", "settle", "cast", "env", "grasp",
-                            "capacity", "custom"]
+                            "capacity", "custom", "empty"]
     if "tables" in what:
         gen_tables(); print("tables", time.time() - t0)
     blobs = tags = None
@@ -1276,3 +1294,5 @@ if __name__ == "__main__":
         gen_capacity(); print("capacity", time.time() - t0)
     if "custom" in what:
         gen_custom(); print("custom", time.time() - t0)
+    if "empty" in what:
+        gen_empty(); print("empty", time.time() - t0)

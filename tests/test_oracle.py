@@ -23,8 +23,8 @@ from paper_2106_14405_b200.state import WorldState
 
 LAYOUT = {"idle": 0, "fixed": 1, "interact": 0, "awake": 2, "drop": 0, "drop_floor": 0, "settle": 1,
           "tilt": 0, "drawer": 0, "fridge": 0, "held": 0, "riders": 0, "pick": 0,
-          "pile26": 0, "world62": 2}
-CLUTTER = {"pile26": 26, "world62": 40}  # clutter bodies (default 20)
+          "pile26": 0, "world62": 2, "empty": 1}
+CLUTTER = {"pile26": 26, "world62": 40, "empty": 0}  # clutter bodies (default 20)
 EV_NOISE = 1e-12
 POS_TOL, VEL_TOL = 1e-12, 1e-10
 
