@@ -222,6 +222,17 @@ int rs_scene_set_mesh(rs_scene *s, const rs_mesh_desc *M) {
   if (!rc) rc = upload(s, M->node_hi, (size_t)3 * M->n_nodes, &d.node_hi);
   if (!rc) rc = upload(s, M->node_meta, (size_t)2 * M->n_nodes, &d.node_meta);
   if (!rc) rc = upload(s, M->part_node_begin, (size_t)M->n_parts + 1, &d.part_node_begin);
+  if (!rc) {  // packed nodes for the render's traversal: one 32-byte record per node
+    std::vector<float4> n4(2 * (size_t)(M->n_nodes > 0 ? M->n_nodes : 1));
+    for (int n = 0; n < M->n_nodes; ++n) {
+      float mx, my;
+      memcpy(&mx, &M->node_meta[2 * n], 4);
+      memcpy(&my, &M->node_meta[2 * n + 1], 4);
+      n4[2 * n] = make_float4(M->node_lo[3 * n], M->node_lo[3 * n + 1], M->node_lo[3 * n + 2], mx);
+      n4[2 * n + 1] = make_float4(M->node_hi[3 * n], M->node_hi[3 * n + 1], M->node_hi[3 * n + 2], my);
+    }
+    rc = upload(s, n4.data(), n4.size(), &d.node4);
+  }
   if (!rc) rc = upload(s, M->part_bound, (size_t)M->n_parts, &d.mesh_bound);
   if (rc) return rc;
   d.n_tri = M->n_tris;

@@ -51,6 +51,7 @@ struct DevScene {
   const double *mtri;            // [n_tri][9]: v0, e1, e2 in the part frame
   const float *node_lo, *node_hi;  // [n_nodes][3]
   const int32_t *node_meta;      // [n_nodes][2]: leaf (first, count) | internal (right, -1)
+  const float4 *node4;           // [n_nodes][2]: (lo.xyz, meta.x bits), (hi.xyz, meta.y bits) -- 2 x 16 B per node
   const int32_t *part_node_begin;  // [np + 1] BVH root per part
   const double *mesh_bound;      // [np] bounding radius of the part's mesh
 };

@@ -207,28 +207,42 @@ __device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem 
   // BVH nodes are tested in FP32 against boxes widened by `slack` (>> the
   // FP32 rounding of (lo - o) / d for |o| <= ~1e3 m): a superset of the nodes
   // the exact test would visit; the triangles themselves are tested in FP64,
-  // so the nearest hit is unchanged
+  // so the nearest hit is unchanged.  Ordered traversal: at an internal node
+  // both children are tested, the nearer is entered and the farther pushed
+  // with its entry distance, and a popped node whose entry lies beyond the
+  // current best is skipped -- the same nearest hit (every triangle that can
+  // beat it is still tested), found sooner.  Nodes are packed 32-byte records
+  // (lo.xyz | meta.x, hi.xyz | meta.y), two 16-byte loads each.
   const float olf[3] = {(float)ol[0], (float)ol[1], (float)ol[2]};
   const float invf[3] = {1.0f / (float)dl[0], 1.0f / (float)dl[1], 1.0f / (float)dl[2]};
   const float slack = 1e-4f * (1.0f + fmaxf(fabsf(olf[0]), fmaxf(fabsf(olf[1]), fabsf(olf[2]))));
   double best = tcut;
   float bestf = tcut < INFINITY ? fmaf(__double2float_ru(tcut), 1e-5f, __double2float_ru(tcut)) + slack : INFINITY;
   face = -1;
-  int stack[40], sp = 0;
-  int node = sc.part_node_begin[p];
-  for (;;) {
-    const float *lo = sc.node_lo + 3 * node, *hi = sc.node_hi + 3 * node;
-    float tn = 0.0f, tf = bestf;
+  // slab entry of node n (conservative; NaN from 0 * inf leaves a bound unchanged)
+  auto box = [&](int n, float &tn, int2 &meta) {
+    const float4 A = sc.node4[2 * n], Bq = sc.node4[2 * n + 1];
+    meta = make_int2(__float_as_int(A.w), __float_as_int(Bq.w));
+    const float lo[3] = {A.x, A.y, A.z}, hi[3] = {Bq.x, Bq.y, Bq.z};
+    float t_n = 0.0f, t_f = bestf;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       float t0 = (lo[a] - slack - olf[a]) * invf[a], t1 = (hi[a] + slack - olf[a]) * invf[a];
       if (t0 > t1) { float x = t0; t0 = t1; t1 = x; }
-      tn = t0 > tn ? t0 : tn;  // NaN (0 * inf) leaves the bound unchanged: conservative
-      tf = t1 < tf ? t1 : tf;
+      t_n = t0 > t_n ? t0 : t_n;
+      t_f = t1 < t_f ? t1 : t_f;
     }
-    bool visit = tn <= tf;
-    const int2 meta = reinterpret_cast<const int2 *>(sc.node_meta)[node];
-    if (visit && meta.y >= 0) {  // leaf
+    tn = t_n;
+    return t_n <= t_f;
+  };
+  int2 stack[16];  // (node, entry distance bits); depth <= 11 for the 200k-triangle soups
+  int sp = 0;
+  int node = sc.part_node_begin[p];
+  float tn;
+  int2 meta;
+  if (!box(node, tn, meta)) return INFINITY;
+  for (;;) {
+    if (meta.y >= 0) {  // leaf
       for (int t = meta.x; t < meta.x + meta.y; ++t) {
         const double *T = sc.mtri + 9 * t;
         const double *v0 = T, *e1 = T + 3, *e2 = T + 6;
@@ -250,15 +264,37 @@ __device__ __forceinline__ double mesh_hit(const DevScene &sc, const RenderSmem 
         bestf = fmaf(__double2float_ru(best), 1e-5f, __double2float_ru(best)) + slack;
         face = t;
       }
-      visit = false;
+    } else {  // internal: left child follows the node, right child index in meta.x
+      int l = node + 1, r = meta.x;
+      float tl, tr;
+      int2 ml, mr;
+      const bool hl = box(l, tl, ml), hr = box(r, tr, mr);
+      if (hl && hr) {
+        if (tr < tl) {
+          const int x = l; l = r; r = x;
+          const float y = tl; tl = tr; tr = y;
+          const int2 z = ml; ml = mr; mr = z;
+        }
+        stack[sp++] = make_int2(r, __float_as_int(tr));
+        node = l; meta = ml;
+        continue;
+      }
+      if (hl || hr) {
+        node = hl ? l : r; meta = hl ? ml : mr;
+        continue;
+      }
     }
-    if (visit) {  // internal: left child follows the node
-      stack[sp++] = meta.x;
-      node = node + 1;
-      continue;
+    bool found = false;
+    while (sp > 0) {
+      const int2 e = stack[--sp];
+      if (__int_as_float(e.y) <= bestf) {
+        node = e.x;
+        float t2;
+        found = box(node, t2, meta);  // reloads the record (and re-tests against the tightened best)
+        if (found) break;
+      }
     }
-    if (sp == 0) break;
-    node = stack[--sp];
+    if (!found) break;
   }
   return face >= 0 ? best : INFINITY;
 }
