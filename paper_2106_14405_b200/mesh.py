@@ -16,11 +16,13 @@ child index is stored).  Node boxes are float32 rounded outward.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import assets as A
 
-LEAF = 4
+LEAF = int(os.environ.get("RSIM_BVH_LEAF", "4"))  # triangles per leaf (env override: experiments)
 
 
 def part_triangles(prim) -> np.ndarray:
