@@ -989,20 +989,26 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
   }
   __syncwarp();
   // lexicographic (value, row) minimum over the lanes: the oracle's serial
-  // scans ("strictly smaller, or equal with a lower row") in one reduction
+  // scans ("strictly smaller, or equal with a lower row").  Both callers order
+  // rows with lanes, so it is the lowest lane holding the minimum value.  The
+  // candidates are finite and < -1e-10 (no NaN, no signed zero) or +inf, so the
+  // order-preserving 64-bit key of a double makes the minimum two 32-bit
+  // warp reductions (redux.sync) instead of five shuffle rounds
   auto argmin = [&](double v, int r) {
-    for (int o = 16; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const int orow = __shfl_xor_sync(0xffffffffu, r, o);
-      if (ov < v || (ov == v && orow < r)) { v = ov; r = orow; }
-    }
-    return r;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+    const unsigned win = __ballot_sync(0xffffffffu, hi == mhi && lo == mlo);
+    return __shfl_sync(0xffffffffu, r, __ffs(win) - 1);
   };
   // the block's decomposition cache directory in registers for the solve
   // (lane s < kEigSlots: slot s's active-set key and last use), written back after it
   double skey = lane < kEigSlots ? P[PMASK + lane] : -2.0, sstamp = lane < kEigSlots ? P[PSTAMP + lane] : INFINITY;
   double clk = P[PCLK];
   for (int it = 0; it < 4 * m + 4; ++it) {
+    if (c.B->phase_cycles && lane == 0) c.B->phase_cycles[kPhases * (size_t)c.env + 15] += 1;  // iterations
     const int na = ws.na;
     const int act = lane < na ? ws.active[lane] : -1;  // this lane's active row (active is sorted)
     if (lane < m) ws.lam[lane] = 0.0;
@@ -1041,8 +1047,13 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
       const double *Vs = Vc + slot * m * m, *es = evc + slot * m;
       // x = sum_k (V_k . b / ev_k) V_k over ev_k > rcond * max|ev| (oracle pinv_solve
       // order; the sums stay sequential, unrolled only to overlap the loads)
-      double smax = lane < na ? fabs(es[lane]) : 0.0;  // max is exact in any order
-      for (int o = 16; o; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+      double smax;  // max is exact in any order: non-negative doubles order as their bit patterns
+      {
+        const unsigned long long b = lane < na ? (unsigned long long)__double_as_longlong(fabs(es[lane])) : 0ull;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, (unsigned)(b >> 32));
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, (unsigned)(b >> 32) == mhi ? (unsigned)b : 0u);
+        smax = __hiloint2double((int)mhi, (int)mlo);
+      }
       if (lane < na) {
         const int k = lane;
         double cc = 0.0;
