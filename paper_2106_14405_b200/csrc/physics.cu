@@ -977,7 +977,7 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
     const int i = lane;
     double s = 0.0;
 #pragma unroll 4
-    for (int j = 0; j < m; ++j) s += K[i * m + j] * ws.cur[j];
+    for (int j = 0; j < m; ++j) s += K[j * m + i] * ws.cur[j];  // K is stored exactly symmetric: coalesced
     ws.q[i] = ws.wv[i] - s;
     start = ws.cur[i] > 0.0 || ws.wv[i] < 0.0;
   }
@@ -1054,20 +1054,23 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
         const unsigned mlo = __reduce_max_sync(0xffffffffu, (unsigned)(b >> 32) == mhi ? (unsigned)b : 0u);
         smax = __hiloint2double((int)mhi, (int)mlo);
       }
+      bool keep_k = false;
       if (lane < na) {
         const int k = lane;
         double cc = 0.0;
 #pragma unroll 4
         for (int i = 0; i < na; ++i) cc += Vs[i * na + k] * ws.rhs[i];
         ws.ck[k] = cc / es[k];
+        keep_k = !(fabs(es[k]) <= 1e-8 * smax);  // the pinv cutoff, once per eigenvalue
       }
+      const unsigned keep = __ballot_sync(0xffffffffu, keep_k);
       __syncwarp();
       if (lane < na) {
         const int i = lane;
         double x = 0.0;
 #pragma unroll 4
         for (int k = 0; k < na; ++k) {
-          if (fabs(es[k]) <= 1e-8 * smax) continue;
+          if (!((keep >> k) & 1u)) continue;
           x += ws.ck[k] * Vs[i * na + k];
         }
         ws.lam[act] = x;
@@ -1095,7 +1098,7 @@ __device__ void solve_block(Ctx &c, int g, int first, int m, const double *K, Bl
       const int i = lane;
       double wi = 0.0;
 #pragma unroll 4
-      for (int j = 0; j < m; ++j) wi += K[i * m + j] * ws.lam[j];
+      for (int j = 0; j < m; ++j) wi += K[j * m + i] * ws.lam[j];  // symmetric K: coalesced
       wi += ws.q[i];
       ws.wv[i] = wi;
       if (wi < -1e-10) wv = wi;
