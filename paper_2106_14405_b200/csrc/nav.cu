@@ -65,13 +65,17 @@ __global__ void __launch_bounds__(kNavThreads) nav_field_kernel(DevBatch B, cons
           for (int w = tid; w < width; w += blockDim.x) {
             const int i = along_i ? line : w, j = along_i ? w : line, k = i * ny + j;
             if (!walk[k] || k == s_goal) continue;
+            // neighbours on the adjacent lines only: the line being swept is
+            // written concurrently, so its own cells are not read (race-free);
+            // they are relaxed by the perpendicular sweeps of the same round,
+            // so a round without change is still the 8-neighbour fixed point
             double best = d[k];
             for (int di = -1; di <= 1; ++di) {
               const int ni = i + di;
-              if (ni < 0 || ni >= nx) continue;
+              if (ni < 0 || ni >= nx || (along_i && !di)) continue;
               for (int dj = -1; dj <= 1; ++dj) {
                 const int nj = j + dj;
-                if ((!di && !dj) || nj < 0 || nj >= ny) continue;
+                if ((!di && !dj) || nj < 0 || nj >= ny || (!along_i && !dj)) continue;
                 const double du = d[ni * ny + nj];
                 const double nd = du + ((di && dj) ? diag : straight);
                 if (nd < best) best = nd;
