@@ -1,6 +1,7 @@
 // abi.cu -- C-ABI implementation (include/rsim.h): scene/batch lifetime,
 // snapshot <-> device-slab conversion, launches.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdio>
@@ -108,6 +109,13 @@ struct rs_batch {
   cudaStream_t phys_hp = nullptr;
   cudaEvent_t hp_join = nullptr;
   int device = 0;  // the CUDA device current at rs_batch_create; every entry point runs on it
+};
+
+// NVTX range per entry point (named after it): the library's calls show up as
+// ranges in Nsight Systems / ncu --nvtx timelines; free when no tool is attached
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 // Entry points run on the batch's device whatever the caller's current
@@ -419,6 +427,7 @@ static void pack_snapshot(const StateLayout &L, const double *sd, const int32_t 
 
 int rs_set_state(rs_batch *b, const uint8_t *snaps, int64_t stride, const int32_t *env_ids, int32_t n, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !snaps || n < 0) return fail(RS_ERR_ARG, "null argument");
   const DevBatch d = b->view();
   const StateLayout &L = d.L;
@@ -466,6 +475,7 @@ int rs_set_state(rs_batch *b, const uint8_t *snaps, int64_t stride, const int32_
 
 int rs_get_state(rs_batch *b, uint8_t *snaps, int64_t stride, const int32_t *env_ids, int32_t n, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !snaps || n < 0) return fail(RS_ERR_ARG, "null argument");
   const DevBatch d = b->view();
   const StateLayout &L = d.L;
@@ -526,6 +536,7 @@ static int ensure_phys_hp(rs_batch *b) {
 int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_t *has_targets, double dt,
             int32_t substeps, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
   if (!arm || !base_cmd) return fail(RS_ERR_ARG, "arm_targets and base_cmd are required device pointers");
@@ -536,6 +547,7 @@ int rs_step(rs_batch *b, const double *arm, const double *base_cmd, const uint8_
 
 int rs_render(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (cam_mask >> 2) return fail(RS_ERR_ARG, "camera mask selects a camera the robot does not have");
   CUDA_TRY(launch_render(b->view(), cam_mask, rgba, depth, ids, (cudaStream_t)stream));
@@ -544,6 +556,7 @@ int rs_render(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32
 
 int rs_render_mesh(rs_batch *b, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b) return fail(RS_ERR_ARG, "null batch");
   if (cam_mask >> 2) return fail(RS_ERR_ARG, "camera mask selects a camera the robot does not have");
   DevBatch v = b->view();
@@ -559,6 +572,7 @@ static int ensure_ik_scratch(rs_batch *b) {
 
 int rs_arm_action(rs_batch *b, const double *delta_ee, double *arm_targets, int32_t *ik_failed, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !delta_ee || !arm_targets) return fail(RS_ERR_ARG, "null argument");
   int rc = ensure_ik_scratch(b);
   if (rc) return rc;
@@ -568,6 +582,7 @@ int rs_arm_action(rs_batch *b, const double *delta_ee, double *arm_targets, int3
 
 int rs_grasp(rs_batch *b, const double *gripper, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !gripper) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_grasp(b->view(), gripper, 1, (cudaStream_t)stream));
   return RS_OK;
@@ -597,6 +612,7 @@ static int ensure_host_step(rs_batch *b) {
 int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double dt, int32_t substeps,
                  uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids, double *h_out_stats, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !h_arm || !h_base || !h_out_stats) return fail(RS_ERR_ARG, "null argument");
   const int E = b->d.n_env, na = b->narm;
   cudaStream_t st = (cudaStream_t)stream;
@@ -634,6 +650,7 @@ int rs_step_host(rs_batch *b, const double *h_arm, const double *h_base, double 
 
 int rs_step_stats(rs_batch *b, double *out, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !out) return fail(RS_ERR_ARG, "null argument");
   CUDA_TRY(launch_stats(b->view(), out, (cudaStream_t)stream));
   return RS_OK;
@@ -667,6 +684,7 @@ int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d
 int rs_proprio(rs_batch *b, const double *base_prev, const double *goals, int32_t n_goals, double *out,
                double *base_out, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !out || n_goals < 0 || (n_goals > 0 && !goals)) return fail(RS_ERR_ARG, "bad proprioception arguments");
   CUDA_TRY(launch_proprio(b->view(), base_prev, goals, n_goals, out, base_out, (cudaStream_t)stream));
   return RS_OK;
@@ -676,6 +694,7 @@ int rs_proprio(rs_batch *b, const double *base_prev, const double *goals, int32_
 int rs_sphere_cast(rs_batch *b, const int32_t *env_of_query, const double *origins, const double *dirs,
                    const double *max_dist, int32_t n_queries, int32_t *out_body, double *out_t, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !origins || !dirs || !max_dist || !out_body || !out_t || n_queries < 0)
     return fail(RS_ERR_ARG, "bad sphere_cast arguments");
   if (!env_of_query && n_queries > b->d.n_env) return fail(RS_ERR_ARG, "env_of_query = NULL needs n_queries <= n_env");
@@ -688,6 +707,7 @@ int rs_sphere_cast(rs_batch *b, const int32_t *env_of_query, const double *origi
 int rs_settle(rs_batch *b, const uint64_t *placed, uint8_t *active, int32_t max_steps, double floor_z,
               int32_t *status, int32_t *info, double *value, int32_t *steps, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !placed || !active || !status || !info || !value || !steps || max_steps < 0)
     return fail(RS_ERR_ARG, "bad settle arguments");
   const int E = b->d.n_env;
@@ -733,6 +753,7 @@ int rs_nav_shape(rs_batch *b, int32_t *nx, int32_t *ny) {
 int rs_nav_fields(rs_batch *b, const int32_t *scene_of_goal, const double *goal_xy, int32_t n_goals, double *fields,
                   int32_t *goal_cell, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !goal_xy || !fields || n_goals < 0) return fail(RS_ERR_ARG, "bad nav field arguments");
   if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
   if ((size_t)b->nav_nx * b->nav_ny * 9 > 227 * 1024) return fail(RS_ERR_ARG, "walk grid too large for one CTA");
@@ -744,6 +765,7 @@ int rs_nav_fields(rs_batch *b, const int32_t *scene_of_goal, const double *goal_
 int rs_nav_geodesic(rs_batch *b, const double *fields, const int32_t *field_of_query, const int32_t *scene_of_query,
                     const double *from_xy, int32_t n_queries, double *out, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !fields || !field_of_query || !out || n_queries < 0) return fail(RS_ERR_ARG, "bad geodesic arguments");
   if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
   if (!from_xy && n_queries != b->d.n_env) return fail(RS_ERR_ARG, "robot-base queries need n_queries == n_env");
@@ -756,6 +778,7 @@ int rs_nav_path(rs_batch *b, const double *fields, const int32_t *field_of_query
                 const double *from_xy, int32_t n_queries, int32_t cap, double *waypoints, int32_t *count,
                 void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !fields || !field_of_query || !from_xy || !waypoints || !count || n_queries < 0 || cap < 1)
     return fail(RS_ERR_ARG, "bad path arguments");
   if (b->nav_nx < 0) return fail(RS_ERR_ARG, "the batch's scenes have different walk-grid shapes");
@@ -820,6 +843,7 @@ static int ensure_env_buffers(rs_batch *b) {
 
 int rs_env_step(rs_batch *b, const double *action, double dt, int32_t substeps, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !action) return fail(RS_ERR_ARG, "null argument");
   if (!(dt > 0) || substeps < 1) return fail(RS_ERR_ARG, "bad step parameters (dt > 0, substeps >= 1)");
   int rc = ensure_env_buffers(b);
@@ -836,6 +860,7 @@ int rs_env_step(rs_batch *b, const double *action, double dt, int32_t substeps, 
 int rs_env_step_host(rs_batch *b, const double *h_action, double dt, int32_t substeps, uint32_t cam_mask,
                      uint8_t *rgba, float *depth, int32_t *ids, double *h_out_stats, void *stream) {
   DeviceScope device_scope(b);
+  NvtxRange nvtx_range(__func__);
   if (!b || !h_action || !h_out_stats) return fail(RS_ERR_ARG, "null argument");
   int rc = ensure_env_buffers(b);
   if (rc) return rc;
