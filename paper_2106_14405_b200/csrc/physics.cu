@@ -231,7 +231,9 @@ __device__ void forward_kinematics(Ctx &c) {
 // robot.py:349-368 + navgrid.py:55-105
 __device__ void move_base(const DevScene &sc, double *base, double lin, double ang, double dt) {
   double x = base[0], y = base[1], yaw = base[2];
-  double nx = x + cos(yaw) * lin * dt, ny = y + sin(yaw) * lin * dt;
+  double sy, cy;
+  sincos(yaw, &sy, &cy);
+  double nx = x + cy * lin * dt, ny = y + sy * lin * dt;
   double nyaw = py_mod(yaw + ang * dt + M_PI, 2.0 * M_PI) - M_PI;
   double p[2];
   nav_nearest_walkable(sc, nx, ny, p);

@@ -77,8 +77,12 @@ __device__ __forceinline__ void quat_mul(const double *a, const double *b, doubl
   o[0] = w; o[1] = x; o[2] = y; o[3] = z;
 }
 __device__ __forceinline__ void axis_angle_mat(const double *axis, double ang, double *R) {
-  double n = sqrt(dot3(axis, axis)), h = 0.5 * ang, s = sin(h) / n;
-  double q[4] = {cos(h), axis[0] * s, axis[1] * s, axis[2] * s};
+  // sincos: one argument reduction for both (the same values as sin / cos);
+  // a unit axis has n == 1 exactly, and x / 1 == x, so that division is skipped
+  double n = sqrt(dot3(axis, axis)), h = 0.5 * ang, sh, ch;
+  sincos(h, &sh, &ch);
+  const double s = n == 1.0 ? sh : sh / n;
+  double q[4] = {ch, axis[0] * s, axis[1] * s, axis[2] * s};
   quat_to_mat(q, R);
 }
 __device__ __forceinline__ void compose(const Pose &a, const Pose &b, Pose &o) {
@@ -99,7 +103,8 @@ __device__ __forceinline__ void pose_load12(const double *v, Pose &o) {
   o.p[0] = v[9]; o.p[1] = v[10]; o.p[2] = v[11];
 }
 __device__ __forceinline__ void rot_z(double a, double *R) {
-  double c = cos(a), s = sin(a);
+  double c, s;
+  sincos(a, &s, &c);
   R[0] = c; R[1] = -s; R[2] = 0.0; R[3] = s; R[4] = c; R[5] = 0.0; R[6] = 0.0; R[7] = 0.0; R[8] = 1.0;
 }
 // robot.py:156-158
