@@ -42,11 +42,6 @@ class PhysicsFault(RuntimeError):
     """Non-finite state (physics.py:46-47, :596-606) or capacity overflow."""
 
 
-def _stream_ptr(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
-
-
 def _dptr(t: torch.Tensor | None):
     return None if t is None else C.c_void_p(t.data_ptr())
 
