@@ -46,7 +46,8 @@ int rsim_bench_env_cycles(struct rs_batch *batch, long long *d_cycles);
 int rsim_bench_phase_cycles(struct rs_batch *batch, long long *d_cycles);
 /* Debug scheduling hook (parity tests): width 8 or 16 = every env of the
  * following rs_step calls runs in the contact-heavy CTA kernel of that many
- * warps (wavefront Gauss-Seidel); 0 = the normal heavy-env scheduling. */
+ * warps (wavefront Gauss-Seidel); -8 or -16 = the normal heavy-env
+ * selection with CTAs of that width; 0 = the normal heavy-env scheduling. */
 int rsim_bench_force_heavy(struct rs_batch *batch, int width);
 /* same for rs_render_mesh: counts candidate-part BVH traversals */
 int rsim_bench_render_mesh_work(struct rs_batch *batch, unsigned int cam_mask, unsigned long long *d_counter,
