@@ -512,12 +512,13 @@ static cudaError_t launch_step_b(rs_batch *b, const double *arm, const double *b
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_join, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
-  if (b->force_heavy) {  // debug: every env through the CTA kernel of that width
+  if (b->force_heavy > 0) {  // debug: every env through the CTA kernel of that width
     cudaError_t e = cudaMemsetAsync(b->heavy[b->cur], 1, (size_t)b->d.n_env, st);
     if (e != cudaSuccess) return e;
   }
   return launch_step(b->view(), arm, base_cmd, base_stride, has_targets, dt, substeps, st, b->heavy[b->cur],
-                     b->heavy[b->cur ^ 1], b->phys_side, b->ph_fork, b->ph_join, b->force_heavy);
+                     b->heavy[b->cur ^ 1], b->phys_side, b->ph_fork, b->ph_join,
+                     b->force_heavy < 0 ? -b->force_heavy : b->force_heavy);
 }
 
 // physics of a host-buffer step runs on a highest-priority stream so that the
@@ -790,7 +791,8 @@ int rs_nav_path(rs_batch *b, const double *fields, const int32_t *field_of_query
 int rsim_bench_force_heavy(rs_batch *b, int width) {
   DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
-  if (width != 0 && width != 8 && width != 16) return fail(RS_ERR_ARG, "width must be 0, 8 or 16");
+  if (width != 0 && width != 8 && width != 16 && width != -8 && width != -16)
+    return fail(RS_ERR_ARG, "width must be 0, +-8 or +-16");
   b->force_heavy = width;
   return RS_OK;
 }

@@ -230,7 +230,8 @@ class BatchSimulator:
 
     def force_cta(self, width: int):
         """Debug scheduling (parity tests): 8 / 16 = every env of the following
-        steps runs in the contact-heavy CTA kernel of that width; 0 = normal."""
+        steps runs in the contact-heavy CTA kernel of that width; -8 / -16 = the
+        normal heavy-env selection with CTAs of that width; 0 = normal."""
         native.check(self.L.rsim_bench_force_heavy(self._batch, int(width)), "rsim_bench_force_heavy")
 
     def trace(self, env: int):
