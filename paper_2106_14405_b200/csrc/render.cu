@@ -82,7 +82,7 @@ struct RenderSmem {
   } u;
   int nlist[kMaxTiles];
   uint8_t order[kMaxParts];
-  float color[kMaxBodies][3];  // body albedo (shading reads it per pixel)
+  float4 color[kMaxBodies];  // 255 x body albedo, rounded as the shading rule's first product (one LDS.128)
   Pose cam;
   uint64_t mbar;  // completion barrier of the facet-table TMA bulk copy
 };
@@ -572,7 +572,9 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   }
   __syncthreads();
   const double *o = S.cam.p;
-  for (int i = tid; i < 3 * sc.nb; i += blockDim.x) S.color[i / 3][i % 3] = sc.color[i];
+  for (int i = tid; i < sc.nb; i += blockDim.x)
+    S.color[i] = make_float4(__fmul_rn(255.0f, sc.color[3 * i]), __fmul_rn(255.0f, sc.color[3 * i + 1]),
+                             __fmul_rn(255.0f, sc.color[3 * i + 2]), 0.0f);
 
   // -- world part frames and bounds (lanes per part), then world planes
   //    (geometry.py:554-557), b0 = d - n.o (lanes per facet)
@@ -792,10 +794,11 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
           cosv = -(d[0] * Q[0] + d[1] * Q[1] + d[2] * Q[2]);
         }
         float shade = __fadd_rn(0.3f, __fmul_rn(0.7f, (float)(cosv > 0.0 ? cosv : 0.0)));
-        const float *col = S.color[id];
+        const float4 cw = S.color[id];  // 255 * albedo
+        const float col[3] = {cw.x, cw.y, cw.z};
         uint32_t px4 = 0xff000000u;
         for (int i = 0; i < 3; ++i) {
-          float cv = __fadd_rn(__fmul_rn(__fmul_rn(255.0f, col[i]), shade), 0.5f);
+          float cv = __fadd_rn(__fmul_rn(col[i], shade), 0.5f);
           px4 |= (uint32_t)(cv > 255.0f ? 255.0f : cv) << (8 * i);
         }
         rgba[px] = px4;
