@@ -37,7 +37,7 @@
 
 namespace rsim {
 
-constexpr int kTile = 16;
+constexpr int kTile = 16;  // the pixel loop's index arithmetic assumes 16 (k >> 4)
 constexpr int kMaxParts = 128;
 constexpr int kMaskWords = kMaxParts / 32;
 constexpr int kMaxTiles = (128 / kTile) * (128 / kTile);
@@ -742,8 +742,9 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     const int ux = (tile % tx_n) * kTile, vy = (tile / tx_n) * kTile;
 #pragma unroll 1
     for (int k = lane; k < kTile * kTile; k += 32) {
-      const int u = ux + (k % kTile), v = vy + (k / kTile);
-      const double *dc = B.ray_dir + 3 * ((size_t)v * W + u);  // unit camera-frame ray (render_tables_kernel)
+      // lane -> column ux + lane % 16 (fixed), rows vy + lane / 16 + 2 j
+      const int u = ux + (lane & (kTile - 1)), v = vy + (k >> 4);
+      const double *dc = B.ray_dir + 3 * (v * W + u);  // unit camera-frame ray (render_tables_kernel)
       double d[3];
       {  // matvec(S.cam.R, dc, d) with the rotation re-read from shared memory per pixel: hoisted out
          // of the loop it takes 18 registers, and at the 64-register budget ptxas spilled 6 of its
@@ -763,7 +764,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       }
       if (count) wk.v[7] += 1;
 
-      const size_t px = img + (size_t)v * W + u;
+      const size_t px = img + (size_t)(v * W + u);
       if (!(tmin <= zfar)) {
         if (rgba) rgba[px] = 0u;
         if (depth) depth[px] = 0.0f;
