@@ -520,7 +520,9 @@ __device__ __noinline__ void stage_facets(double *dst, const double *facets, int
 }
 __device__ __noinline__ void wait_bulk(uint64_t *bar) { mbar_wait(bar, 0); }
 
-template <int kMode, bool kCount>
+// kAll: every output pointer is non-NULL (the product launch) -- the per-pixel
+// NULL checks (uniform pointer loads and compares) compile away
+template <int kMode, bool kCount, bool kAll = false>
 __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBlocksMesh : kMinBlocksProxy)
     render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out, uint32_t *rgba, float *depth, int32_t *ids,
                   unsigned long long *work) {
@@ -766,14 +768,14 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
 
       const size_t px = img + (size_t)(v * W + u);
       if (!(tmin <= zfar)) {
-        if (rgba) rgba[px] = 0u;
-        if (depth) depth[px] = 0.0f;
-        if (ids) ids[px] = -1;
+        if (kAll || rgba) rgba[px] = 0u;
+        if (kAll || depth) depth[px] = 0.0f;
+        if (kAll || ids) ids[px] = -1;
         continue;
       }
-      if (depth) depth[px] = (float)(tmin < znear ? znear : tmin);
-      if (ids) ids[px] = id;
-      if (rgba) {
+      if (kAll || depth) depth[px] = (float)(tmin < znear ? znear : tmin);
+      if (kAll || ids) ids[px] = id;
+      if (kAll || rgba) {
         double cosv = 0.0;
         const PartW &P = S.part[wpart];
         if (kMesh) {
@@ -846,7 +848,7 @@ static size_t render_smem(const DevBatch &B, int mode) {
   return kPlaneOff + sizeof(double) * planes;
 }
 
-template <int kMode, bool kCount>
+template <int kMode, bool kCount, bool kAll>
 static cudaError_t launch_render_t(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                    cudaStream_t stream, unsigned long long *work) {
   int n_cam_out = __builtin_popcount(cam_mask);
@@ -858,12 +860,13 @@ static cudaError_t launch_render_t(const DevBatch &B, uint32_t cam_mask, uint8_t
   if (e != cudaSuccess) return e;
   if (!(configured.load() >> dev & 1ull)) {  // the largest any batch can ask for: kMaxFacets facets
     const size_t cap = kPlaneOff + sizeof(double) * (kMode == kMeshExact ? 9 * kMaxParts : 4 * kMaxFacets);
-    e = cudaFuncSetAttribute(render_kernel<kMode, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+    e = cudaFuncSetAttribute(render_kernel<kMode, kCount, kAll>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)cap);
     if (e != cudaSuccess) return e;
     configured.fetch_or(1ull << dev);
   }
   dim3 grid(B.n_env * n_cam_out);
-  render_kernel<kMode, kCount><<<grid, kRenderThreads, render_smem(B, kMode), stream>>>(
+  render_kernel<kMode, kCount, kAll><<<grid, kRenderThreads, render_smem(B, kMode), stream>>>(
       B, cam_mask, n_cam_out, reinterpret_cast<uint32_t *>(rgba), depth, ids, work);
   return cudaGetLastError();
 }
@@ -872,8 +875,9 @@ static cudaError_t launch_render_t(const DevBatch &B, uint32_t cam_mask, uint8_t
 template <int kMode>
 static cudaError_t launch_render_any(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                                      cudaStream_t stream, unsigned long long *work) {
-  return work ? launch_render_t<kMode, true>(B, cam_mask, rgba, depth, ids, stream, work)
-              : launch_render_t<kMode, false>(B, cam_mask, rgba, depth, ids, stream, nullptr);
+  if (work) return launch_render_t<kMode, true, false>(B, cam_mask, rgba, depth, ids, stream, work);
+  if (rgba && depth && ids) return launch_render_t<kMode, false, true>(B, cam_mask, rgba, depth, ids, stream, nullptr);
+  return launch_render_t<kMode, false, false>(B, cam_mask, rgba, depth, ids, stream, nullptr);
 }
 
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
