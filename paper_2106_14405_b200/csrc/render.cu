@@ -786,15 +786,15 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
             matvec(R, nl, nw);
             cosv = fabs(dot3(nw, d)) / sqrt(dot3(nw, nw));
           }
+        } else if (wface >= 0) {  // box / hull entering face (spheres report no face)
+          const double *Q = plane + 4 * wface;
+          cosv = -(d[0] * Q[0] + d[1] * Q[1] + d[2] * Q[2]);
         } else if (P.kind == RS_SPHERE) {
           if (tmin > 0.0) {
             double n[3];
             for (int i = 0; i < 3; ++i) n[i] = (o[i] + tmin * d[i] - P.c[i]) / P.r;
             cosv = -dot3(n, d);
           }
-        } else if (wface >= 0) {
-          const double *Q = plane + 4 * wface;
-          cosv = -(d[0] * Q[0] + d[1] * Q[1] + d[2] * Q[2]);
         }
         float shade = __fadd_rn(0.3f, __fmul_rn(0.7f, (float)(cosv > 0.0 ? cosv : 0.0)));
         const float4 cw = S.color[id];  // 255 * albedo
