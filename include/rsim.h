@@ -233,6 +233,16 @@ int rs_step_host(rs_batch *batch, const double *h_arm_targets, const double *h_b
                  int32_t substeps, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                  double *h_out_stats, void *stream);
 
+/* Dispatch order of the warp-per-env step kernel (a scheduling choice; no
+ * result depends on it): 0 = envs sorted by scene (default: warps resident on
+ * an SM share one layout's tables in L1); 1 = busy first -- each step, the
+ * envs that had active contact groups in the previous step go first (still
+ * scene-sorted within each group), so with more envs than resident warps the
+ * latency tail starts in the first wave.  Measured: physics-only batches of
+ * 4096 envs gain from 1; the interleaved 2048-env physics || render step does
+ * not. */
+int rs_set_env_order(rs_batch *batch, int32_t policy);
+
 /* Per-env results of the current state on `stream`, device out [n_env][4] f64:
  * accumulated_contact_force (physics.py:944-959; the SPEC's StepResult
  * info "accumulated force N"), fault word, event count of the last step,

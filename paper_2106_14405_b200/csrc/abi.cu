@@ -15,6 +15,8 @@
 #include "device.cuh"
 
 namespace rsim {
+cudaError_t launch_env_order(const DevBatch &B, const int32_t *scene_order, const uint8_t *heavy_in, int32_t *out,
+                             cudaStream_t stream);
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
                         const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream,
                         const uint8_t *heavy_in, uint8_t *heavy_out, cudaStream_t side, cudaEvent_t fork,
@@ -75,6 +77,10 @@ struct rs_batch {
   DevBatch d;
   DevScene *d_scenes = nullptr;
   int32_t *d_env_scene = nullptr;
+  int32_t *d_order = nullptr;  // busy-first dispatch order of the warp-per-env step kernel (policy 1)
+  int order_policy = 0;        // rs_set_env_order: 0 scene order, 1 busy first
+  bool order_pending = false;
+  cudaEvent_t ord_fork = nullptr, ord_done = nullptr;
   std::vector<void *> allocs;
   int narm = 0;
   bool has_mesh = false;
@@ -265,6 +271,7 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
                     const rs_physics_config *cfg, const rs_render_config *rcfg, int32_t event_cap, rs_batch **out) {
   if (!scenes || n_scenes < 1 || n_env < 1 || !cfg || !rcfg || !out || event_cap < 0)
     return fail(RS_ERR_ARG, "bad batch arguments");
+  if (n_env >= (1 << 21)) return fail(RS_ERR_CAPACITY, "n_env must be < 2^21 (dispatch order counters)");
   const DevScene &s0 = scenes[0]->d;
   for (int i = 1; i < n_scenes; ++i)
     if (scenes[i]->d.nb != s0.nb || scenes[i]->d.nsj != s0.nsj || scenes[i]->d.narm != s0.narm)
@@ -308,6 +315,7 @@ int rs_batch_create(rs_scene *const *scenes, int32_t n_scenes, const int32_t *en
 #undef BA
   if (!rc) rc = balloc(b, &p, sizeof(DevScene) * n_scenes), b->d_scenes = (DevScene *)p;
   if (!rc) rc = balloc(b, &p, sizeof(int32_t) * 2 * (size_t)n_env), b->d_env_scene = (int32_t *)p;
+  if (!rc) rc = balloc(b, &p, sizeof(int32_t) * (size_t)n_env), b->d_order = (int32_t *)p;
   if (rc) {
     rs_batch_destroy(b);
     return rc;
@@ -364,6 +372,8 @@ void rs_batch_destroy(rs_batch *b) {
   if (b->phys_side) cudaStreamDestroy(b->phys_side);
   if (b->phys_hp) cudaStreamDestroy(b->phys_hp);
   if (b->hp_join) cudaEventDestroy(b->hp_join);
+  if (b->ord_fork) cudaEventDestroy(b->ord_fork);
+  if (b->ord_done) cudaEventDestroy(b->ord_done);
   if (b->ph_fork) cudaEventDestroy(b->ph_fork);
   if (b->ph_join) cudaEventDestroy(b->ph_join);
   if (b->ev_fork) cudaEventDestroy(b->ev_fork);
@@ -500,25 +510,63 @@ int rs_get_state(rs_batch *b, uint8_t *snaps, int64_t stride, const int32_t *env
   return RS_OK;
 }
 
+static cudaError_t ensure_phys_side(rs_batch *b) {
+  if (b->phys_side) return cudaSuccess;
+  // highest priority: contact-heavy envs (the step's latency tail) get SMs
+  // ahead of queued render CTAs of an interleaved observation render
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cudaError_t e = cudaStreamCreateWithPriority(&b->phys_side, cudaStreamNonBlocking, hi);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ord_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ord_done, cudaEventDisableTiming);
+  return e;
+}
+
+// policy 1: the step's dispatch order from the previous step's contact
+// activity, built on the physics side stream so that it overlaps what `st`
+// runs before the step (the IK of rs_env_step); launch_step_b waits for it
+static cudaError_t enqueue_env_order(rs_batch *b, cudaStream_t st) {
+  cudaError_t e = ensure_phys_side(b);
+  if (e != cudaSuccess) return e;
+  if (b->force_heavy > 0) {  // debug: every env through the CTA kernel of that width
+    if ((e = cudaMemsetAsync(b->heavy[b->cur], 255, (size_t)b->d.n_env, st)) != cudaSuccess) return e;
+  }
+  if (b->order_policy != 1) return cudaSuccess;
+  if ((e = cudaEventRecord(b->ord_fork, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(b->phys_side, b->ord_fork, 0)) != cudaSuccess) return e;
+  const DevBatch v = b->view();
+  if ((e = launch_env_order(v, b->d_env_scene + v.n_env, b->heavy[b->cur], b->d_order, b->phys_side)) != cudaSuccess)
+    return e;
+  if ((e = cudaEventRecord(b->ord_done, b->phys_side)) != cudaSuccess) return e;
+  b->order_pending = true;
+  return cudaSuccess;
+}
+
 static cudaError_t launch_step_b(rs_batch *b, const double *arm, const double *base_cmd, int base_stride,
                                  const uint8_t *has_targets, double dt, int substeps, cudaStream_t st) {
-  if (!b->phys_side) {
-    // highest priority: contact-heavy envs (the step's latency tail) get SMs
-    // ahead of queued render CTAs of an interleaved observation render
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaError_t e = cudaStreamCreateWithPriority(&b->phys_side, cudaStreamNonBlocking, hi);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_fork, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_join, cudaEventDisableTiming);
-    if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  const bool pre = b->order_pending;  // enqueued by rs_env_step before its IK
+  b->order_pending = false;
+  if (!pre && (e = enqueue_env_order(b, st)) != cudaSuccess) return e;
+  DevBatch v = b->view();
+  if (b->order_policy == 1) {
+    b->order_pending = false;
+    if ((e = cudaStreamWaitEvent(st, b->ord_done, 0)) != cudaSuccess) return e;
+    v.env_order = b->d_order;
   }
-  if (b->force_heavy > 0) {  // debug: every env through the CTA kernel of that width
-    cudaError_t e = cudaMemsetAsync(b->heavy[b->cur], 1, (size_t)b->d.n_env, st);
-    if (e != cudaSuccess) return e;
-  }
-  return launch_step(b->view(), arm, base_cmd, base_stride, has_targets, dt, substeps, st, b->heavy[b->cur],
+  return launch_step(v, arm, base_cmd, base_stride, has_targets, dt, substeps, st, b->heavy[b->cur],
                      b->heavy[b->cur ^ 1], b->phys_side, b->ph_fork, b->ph_join,
                      b->force_heavy < 0 ? -b->force_heavy : b->force_heavy);
+}
+
+int rs_set_env_order(rs_batch *b, int32_t policy) {
+  DeviceScope device_scope(b);
+  if (!b) return fail(RS_ERR_ARG, "null batch");
+  if (policy != 0 && policy != 1) return fail(RS_ERR_ARG, "env order policy must be 0 (scene) or 1 (busy first)");
+  b->order_policy = policy;
+  return RS_OK;
 }
 
 // physics of a host-buffer step runs on a highest-priority stream so that the
@@ -852,6 +900,7 @@ int rs_env_step(rs_batch *b, const double *action, double dt, int32_t substeps, 
   if (!rc) rc = ensure_ik_scratch(b);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(enqueue_env_order(b, st));  // policy 1: overlaps the IK on the physics side stream
   CUDA_TRY(launch_ik(b->view(), action, 6, b->d_targets, b->d_ik_failed, b->d_ik_scratch, st));  // robot.py:293
   CUDA_TRY(launch_step_b(b, b->d_targets, action + 4, 6, nullptr, dt, substeps, st));  // physics.py:575
   b->cur ^= 1;

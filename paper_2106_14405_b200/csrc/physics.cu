@@ -26,6 +26,8 @@
 // arithmetic rounds exactly like the C oracle (tests/test_gpu_physics.py).
 #include <cuda_runtime.h>
 
+#include <cub/block/block_scan.cuh>
+
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -2166,7 +2168,9 @@ __device__ void env_end(Ctx &c, const DevBatch &B, int env, double dt, bool ok, 
   WarpSmem &S = *c.S;
   const StateLayout &L = B.L;
   const int lane = c.lane;
-  if (lane == 0 && heavy_out) heavy_out[env] = S.max_active >= heavy_groups(B.n_env) ? 1 : 0;
+  // the step's most active contact groups (saturating byte): >= heavy_groups ->
+  // the CTA kernel next step; >= 1 -> early in a busy-first dispatch order
+  if (lane == 0 && heavy_out) heavy_out[env] = (uint8_t)(S.max_active < 255 ? S.max_active : 255);
   if (!ok) {
     if (lane == 0) B.fault[env] = ((uint32_t)RS_FAULT_OVERFLOW << 16) | (uint32_t)S.fault;
     copy_through(B, env, lane);
@@ -2205,7 +2209,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kStepMinBlocks) step_kern
   const int slot = blockIdx.x * kWarpsPerBlock + warp;
   if (slot >= B.n_env) return;
   const int env = B.env_order ? B.env_order[slot] : slot;
-  if (heavy_in && heavy_in[env]) return;
+  if (heavy_in && heavy_in[env] >= heavy_groups(B.n_env)) return;
   if (B.env_active && !B.env_active[env]) {  // not stepping (rs_settle): state copied through
     copy_through(B, env, lane);
     if (lane == 0 && heavy_out) heavy_out[env] = 0;
@@ -2242,7 +2246,7 @@ __global__ void __launch_bounds__(32 * kW) step_kernel_cta(DevBatch B, const dou
   WarpSmem &S = *reinterpret_cast<WarpSmem *>(dsm);
   HeavyShared<kW> &H = *reinterpret_cast<HeavyShared<kW> *>(dsm + warp_smem_bytes(B.L.stage));
   const int env = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (!heavy_in[env]) return;
+  if (heavy_in[env] < heavy_groups(B.n_env)) return;
   if (B.env_active && !B.env_active[env]) {
     if (threadIdx.x < 32) copy_through(B, env, threadIdx.x);
     if (threadIdx.x == 0) heavy_out[env] = 0;
@@ -2293,6 +2297,48 @@ __host__ __device__ size_t step_scratch_doubles_per_env(int row_cap) {
          (size_t)kHeavyWarps * kMaxBlockRows * kMaxBlockRows;
 }
 int step_row_cap() { return kMaxContacts; }
+
+// Busy-first dispatch order of the warp-per-env kernel (rs_set_env_order,
+// policy 1): a stable partition of the scene-sorted order into envs that had
+// active contact groups last step (1 <= groups < heavy_groups: this kernel's
+// latency tail) first, then the quiet ones, then the CTA kernel's heavy envs
+// (they exit at once).  With more envs than resident warps, the expensive
+// envs then start in the first wave instead of wherever their index falls.
+// The envs are independent: the order changes no result.
+constexpr int kOrderThreads = 1024;
+__global__ void __launch_bounds__(kOrderThreads) env_order_kernel(int n, int thr, const int32_t *scene_order,
+                                                                  const uint8_t *heavy_in, int32_t *out) {
+  // one CTA: each thread takes a contiguous run of the scene order, counts its
+  // envs per bucket (3 x 21-bit fields of one 64-bit word), one block-wide
+  // exclusive scan gives every run its output offsets, then the runs are written
+  using Scan = cub::BlockScan<unsigned long long, kOrderThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ unsigned long long total;
+  const int per = (n + kOrderThreads - 1) / kOrderThreads, i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+  auto bucket = [&](int e) {
+    const int v = heavy_in[e];
+    return v >= thr ? 2 : (v >= 1 ? 0 : 1);
+  };
+  unsigned long long mine = 0ull;
+  for (int i = i0; i < i1; ++i) mine += 1ull << (21 * bucket(scene_order[i]));
+  unsigned long long before;
+  Scan(tmp).ExclusiveSum(mine, before);
+  if (threadIdx.x == kOrderThreads - 1) total = before + mine;
+  __syncthreads();
+  const unsigned long long m = (1ull << 21) - 1ull, t = total;
+  const int c0 = (int)(t & m), c1 = (int)((t >> 21) & m);
+  int off[3] = {(int)(before & m), c0 + (int)((before >> 21) & m), c0 + c1 + (int)((before >> 42) & m)};
+  for (int i = i0; i < i1; ++i) {
+    const int e = scene_order[i];
+    out[off[bucket(e)]++] = e;
+  }
+}
+
+cudaError_t launch_env_order(const DevBatch &B, const int32_t *scene_order, const uint8_t *heavy_in, int32_t *out,
+                             cudaStream_t stream) {
+  env_order_kernel<<<1, kOrderThreads, 0, stream>>>(B.n_env, heavy_groups(B.n_env), scene_order, heavy_in, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
                         const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream,

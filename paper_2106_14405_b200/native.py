@@ -18,7 +18,7 @@ EXPORTS = ("rs_abi_version", "rs_last_error", "rs_snapshot_size", "rs_scene_crea
            "rs_batch_create", "rs_batch_destroy", "rs_batch_buffers", "rs_set_state", "rs_get_state", "rs_step",
            "rs_render", "rs_grasp", "rs_step_host", "rs_set_trace", "rs_scene_set_mesh", "rs_render_mesh", "rs_arm_action", "rs_env_step", "rs_env_step_host",
            "rs_nav_shape", "rs_nav_fields", "rs_nav_geodesic", "rs_nav_path", "rs_settle",
-           "rs_sphere_cast", "rs_proprio", "rs_step_stats")
+           "rs_sphere_cast", "rs_proprio", "rs_step_stats", "rs_set_env_order")
 
 
 class NativeLibraryError(RuntimeError):
@@ -59,6 +59,7 @@ def lib():
     L.rs_render.argtypes = [vp, u32, vp, vp, vp, vp]
     L.rs_grasp.argtypes = [vp, vp, vp]
     L.rs_step_stats.argtypes = [vp, vp, vp]
+    L.rs_set_env_order.argtypes = [vp, i32]
     L.rs_step_host.argtypes = [vp, vp, vp, dbl, i32, u32, vp, vp, vp, vp, vp]
     L.rs_set_trace.argtypes = [vp, vp, vp, i32, i32]
     L.rs_scene_set_mesh.argtypes = [vp, C.POINTER(abi.rs_mesh_desc)]

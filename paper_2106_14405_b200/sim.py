@@ -228,6 +228,11 @@ class BatchSimulator:
         native.check(self.L.rs_set_trace(self._batch, _dptr(self._trace[0]), _dptr(self._trace[1]), cap, max_substeps),
                      "rs_set_trace")
 
+    def set_env_order(self, policy: str = "scene"):
+        """rs_set_env_order: "scene" (default) or "busy_first" dispatch of the
+        warp-per-env step kernel (scheduling only; results are identical)."""
+        native.check(self.L.rs_set_env_order(self._batch, {"scene": 0, "busy_first": 1}[policy]), "rs_set_env_order")
+
     def force_cta(self, width: int):
         """Debug scheduling (parity tests): 8 / 16 = every env of the following
         steps runs in the contact-heavy CTA kernel of that width; -8 / -16 = the

@@ -25,6 +25,7 @@ from paper_2106_14405_b200.sim import BatchSimulator  # noqa: E402
 from paper_2106_14405_b200.state import WorldState  # noqa: E402
 
 E = int(os.environ.get("ENVS", "4096"))
+ORDER = os.environ.get("ORDER", "busy_first")  # rs_set_env_order policy: "scene" or "busy_first"
 STEPS = int(os.environ.get("STEPS", "30"))
 WARM = 3
 
@@ -64,6 +65,7 @@ def run(name, states, actions, sim, dev):
     awake = sum(int((~WorldState.from_bytes(s).asleep[-20:].astype(bool)).any()) for s in sim.get_state())
     sim.raise_faults()
     print(json.dumps({"config": "configs[2] physics-only", "scenario": name, "envs": E, "steps": STEPS,
+                      "env_order": ORDER,
                       "env_steps_per_s": E / (ms * 1e-3), "ms_per_step": ms,
                       "latency_us": {"p50": float(np.percentile(us, 50)), "p99": float(np.percentile(us, 99)),
                                      "max": float(us.max())},
@@ -76,6 +78,7 @@ def main():
     dev = torch.device("cuda")
     gids = np.arange(E)
     sim = BatchSimulator(layouts=(0, 1, 2), n_env=E, env_layout=layout_of(gids).tolist(), device=dev)
+    sim.set_env_order(ORDER)
     pool = bench.settled_pool()
     run("idle", bench.idle_states(gids, pool), bench.action_table(E, WARM + STEPS + 1, seed=7), sim, dev)
     run("interact", bench.interact_states(gids, pool), bench.interact_actions(E, WARM + STEPS + 1), sim, dev)
