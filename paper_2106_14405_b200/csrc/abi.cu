@@ -556,9 +556,10 @@ static cudaError_t launch_step_b(rs_batch *b, const double *arm, const double *b
     if ((e = cudaStreamWaitEvent(st, b->ord_done, 0)) != cudaSuccess) return e;
     v.env_order = b->d_order;
   }
+  // force_heavy == -1 (debug): no CTA kernel, every env on the warp kernel
   return launch_step(v, arm, base_cmd, base_stride, has_targets, dt, substeps, st, b->heavy[b->cur],
-                     b->heavy[b->cur ^ 1], b->phys_side, b->ph_fork, b->ph_join,
-                     b->force_heavy < 0 ? -b->force_heavy : b->force_heavy);
+                     b->heavy[b->cur ^ 1], b->force_heavy == -1 ? nullptr : b->phys_side, b->ph_fork, b->ph_join,
+                     b->force_heavy < -1 ? -b->force_heavy : (b->force_heavy > 0 ? b->force_heavy : 0));
 }
 
 int rs_set_env_order(rs_batch *b, int32_t policy) {
@@ -839,8 +840,8 @@ int rs_nav_path(rs_batch *b, const double *fields, const int32_t *field_of_query
 int rsim_bench_force_heavy(rs_batch *b, int width) {
   DeviceScope device_scope(b);
   if (!b) return fail(RS_ERR_ARG, "null batch");
-  if (width != 0 && width != 8 && width != 16 && width != -8 && width != -16)
-    return fail(RS_ERR_ARG, "width must be 0, +-8 or +-16");
+  if (width != 0 && width != 8 && width != 16 && width != -8 && width != -16 && width != -1)
+    return fail(RS_ERR_ARG, "width must be 0, -1, +-8 or +-16");
   b->force_heavy = width;
   return RS_OK;
 }
