@@ -22,8 +22,11 @@
 //   integrate       lanes per body; per-body correction sums in contact
 //                   order (physics.py:962-1011)
 //
-// Float64 throughout; this translation unit is built with -fmad=false so
-// arithmetic rounds exactly like the C oracle (tests/test_gpu_physics.py).
+// Float64 throughout, every sum and product in the oracle's order; the unit is
+// built with FMA contraction, so continuous values may differ from the scalar
+// C oracle in the last bits (states within 1e-12) while every discrete output
+// (pair lists, contact counts, sleep flags, counters) stays bit-exact against
+// the oracle and the reference goldens (tests/test_gpu*.py).
 #include <cuda_runtime.h>
 
 #include <cub/block/block_scan.cuh>
@@ -875,8 +878,7 @@ __device__ void sym_eig_warp(int m, double *A, double *V, double *ev, double *cs
 // articulation joint.  The block's rows are staged into shared memory by the
 // warp; lane 0 then runs the order-dependent sequence with both bodies'
 // velocities and inverse inertias in registers.  Same operations in the same
-// order as the generic path (this unit is built with -fmad=false): results
-// are bit-identical.
+// order as the generic path.
 constexpr int kFastRows = 12;
 constexpr int kFastD = 23;  // n, t1, t2, ra, rb, k, mu, fric, lam_old, lt1, lt2, ima, imb
 static_assert(kFastRows * kFastD <= 2 * kSmemEig * kSmemEig, "staging area");
@@ -2514,7 +2516,7 @@ cudaError_t launch_stats(const DevBatch &B, double *out, cudaStream_t stream) {
 // One warp per env: lane 0 runs the attempt from the current joints; if it
 // fails, the 11 restart seeds and the 24 Weyl-spray seeds run one per lane
 // and the lowest-index success wins (= the reference's sequential order).
-// Same operation order as oracle/rsim_oracle.c (this unit is -fmad=false).
+// Same operation order as oracle/rsim_oracle.c.
 
 __device__ void ik_link_poses(const DevScene &sc, const double *q, Pose *links, Pose &ee) {
   Pose t, off, rot;
