@@ -20,7 +20,7 @@ cudaError_t launch_env_order(const DevBatch &B, const int32_t *scene_order, cons
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
                         const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream,
                         const uint8_t *heavy_in, uint8_t *heavy_out, cudaStream_t side, cudaEvent_t fork,
-                        cudaEvent_t join, int force_width);
+                        cudaEvent_t join, int force_width, cudaStream_t side2, cudaEvent_t join2);
 cudaError_t launch_render(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
                           cudaStream_t stream, unsigned long long *work = nullptr);
 cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rgba, float *depth, int32_t *ids,
@@ -81,6 +81,8 @@ struct rs_batch {
   int order_policy = 0;        // rs_set_env_order: 0 scene order, 1 busy first
   bool order_pending = false;
   cudaEvent_t ord_fork = nullptr, ord_done = nullptr;
+  cudaStream_t phys_busy = nullptr;  // the busy envs' step kernel (a third physics stream)
+  cudaEvent_t busy_join = nullptr;
   std::vector<void *> allocs;
   int narm = 0;
   bool has_mesh = false;
@@ -372,6 +374,8 @@ void rs_batch_destroy(rs_batch *b) {
   if (b->phys_side) cudaStreamDestroy(b->phys_side);
   if (b->phys_hp) cudaStreamDestroy(b->phys_hp);
   if (b->hp_join) cudaEventDestroy(b->hp_join);
+  if (b->phys_busy) cudaStreamDestroy(b->phys_busy);
+  if (b->busy_join) cudaEventDestroy(b->busy_join);
   if (b->ord_fork) cudaEventDestroy(b->ord_fork);
   if (b->ord_done) cudaEventDestroy(b->ord_done);
   if (b->ph_fork) cudaEventDestroy(b->ph_fork);
@@ -521,6 +525,8 @@ static cudaError_t ensure_phys_side(rs_batch *b) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ph_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ord_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->ord_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&b->phys_busy, cudaStreamNonBlocking, hi);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b->busy_join, cudaEventDisableTiming);
   return e;
 }
 
@@ -559,7 +565,8 @@ static cudaError_t launch_step_b(rs_batch *b, const double *arm, const double *b
   // force_heavy == -1 (debug): no CTA kernel, every env on the warp kernel
   return launch_step(v, arm, base_cmd, base_stride, has_targets, dt, substeps, st, b->heavy[b->cur],
                      b->heavy[b->cur ^ 1], b->force_heavy == -1 ? nullptr : b->phys_side, b->ph_fork, b->ph_join,
-                     b->force_heavy < -1 ? -b->force_heavy : (b->force_heavy > 0 ? b->force_heavy : 0));
+                     b->force_heavy < -1 ? -b->force_heavy : (b->force_heavy > 0 ? b->force_heavy : 0),
+                     b->phys_busy, b->busy_join);
 }
 
 int rs_set_env_order(rs_batch *b, int32_t policy) {

@@ -2200,7 +2200,13 @@ __device__ void env_end(Ctx &c, const DevBatch &B, int env, double dt, bool ok, 
 }
 
 // warp per env (envs not flagged heavy by the previous step)
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, kStepMinBlocks) step_kernel(DevBatch B, const double *arm_targets,
+// kClass: 0 every non-heavy env; 1 the quiet ones (no active contact group in
+// the previous step); 2 the busy ones (1 <= groups < heavy_groups), compiled
+// for 4 CTAs per SM -- 255 registers, no spills, lower latency for the envs
+// whose contact work sets the step's tail, while the many quiet envs keep the
+// 5-CTA footprint that co-resides with the render
+template <int kClass>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, kClass == 2 ? 4 : kStepMinBlocks) step_kernel(DevBatch B, const double *arm_targets,
                                                                    const double *base_cmd, int base_stride,
                                                                    const uint8_t *has_targets, double dt,
                                                                    int substeps, const uint8_t *heavy_in,
@@ -2212,6 +2218,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, kStepMinBlocks) step_kern
   if (slot >= B.n_env) return;
   const int env = B.env_order ? B.env_order[slot] : slot;
   if (heavy_in && heavy_in[env] >= heavy_groups(B.n_env)) return;
+  if (kClass == 1 && heavy_in[env] != 0) return;
+  if (kClass == 2 && heavy_in[env] == 0) return;
   if (B.env_active && !B.env_active[env]) {  // not stepping (rs_settle): state copied through
     copy_through(B, env, lane);
     if (lane == 0 && heavy_out) heavy_out[env] = 0;
@@ -2345,7 +2353,7 @@ cudaError_t launch_env_order(const DevBatch &B, const int32_t *scene_order, cons
 cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base_cmd, int base_stride,
                         const uint8_t *has_targets, double dt, int substeps, cudaStream_t stream,
                         const uint8_t *heavy_in, uint8_t *heavy_out, cudaStream_t side, cudaEvent_t fork,
-                        cudaEvent_t join, int force_width) {
+                        cudaEvent_t join, int force_width, cudaStream_t side2, cudaEvent_t join2) {
   // kernel attributes are per device context: configure each device once
   static std::atomic<unsigned long long> configured{0ull};
   const size_t ws0 = warp_smem_bytes(B.L.stage), wsmax = warp_smem_bytes(kStageD);
@@ -2356,7 +2364,11 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
   if (e != cudaSuccess) return e;
   if (!(configured.load() >> dev & 1ull)) {
     // sized for the largest staged slab any batch can have
-    e = cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsmax * kWarpsPerBlock));
+    e = cudaFuncSetAttribute(step_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsmax * kWarpsPerBlock));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsmax * kWarpsPerBlock));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wsmax * kWarpsPerBlock));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(step_kernel_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)(wsmax + sizeof(HeavyShared<16>)));
@@ -2383,8 +2395,18 @@ cudaError_t launch_step(const DevBatch &B, const double *arm, const double *base
     cudaEventRecord(join, side);
   }
   dim3 grid((B.n_env + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  step_kernel<<<grid, 32 * kWarpsPerBlock, smem, stream>>>(B, arm, base_cmd, base_stride, has_targets, dt, substeps,
-                                                           heavy_in && side ? heavy_in : nullptr, heavy_out);
+  if (heavy_in && side && side2) {  // busy envs on their own stream, quiet ones here (concurrently)
+    cudaStreamWaitEvent(side2, fork, 0);
+    step_kernel<2><<<grid, 32 * kWarpsPerBlock, smem, side2>>>(B, arm, base_cmd, base_stride, has_targets, dt,
+                                                              substeps, heavy_in, heavy_out);
+    cudaEventRecord(join2, side2);
+    step_kernel<1><<<grid, 32 * kWarpsPerBlock, smem, stream>>>(B, arm, base_cmd, base_stride, has_targets, dt,
+                                                               substeps, heavy_in, heavy_out);
+    cudaStreamWaitEvent(stream, join2, 0);
+  } else {
+    step_kernel<0><<<grid, 32 * kWarpsPerBlock, smem, stream>>>(B, arm, base_cmd, base_stride, has_targets, dt,
+                                                               substeps, heavy_in && side ? heavy_in : nullptr, heavy_out);
+  }
   if (heavy_in && side) cudaStreamWaitEvent(stream, join, 0);
   return cudaGetLastError();
 }
