@@ -41,11 +41,13 @@
 
 namespace rsim {
 
-// envs (warps) per step_kernel CTA (measured in the interleaved bench step,
-// 2048 envs: 2 -> 1.10 M env-steps/s; 3, whose CTA fits one render CTA's
-// register / shared-memory slot -> 1.08 M: a CTA lives as long as its slowest env)
+// envs (warps) per step_kernel CTA.  One: a CTA lives only as long as its env,
+// and with <= 16.5 KB of shared memory per warp three of them fit the slot a
+// finished render CTA frees (16 K registers, 53.7 KB) in the interleaved step
+// (measured, 2048 envs: 1 env/CTA at 16.6 KB +1.7 % bench, +5 % Interact over
+// 2 envs/CTA at 19.7 KB; 3 envs/CTA at 19.7 KB -2 %)
 #ifndef RSIM_WARPS_PER_BLOCK
-#define RSIM_WARPS_PER_BLOCK 2
+#define RSIM_WARPS_PER_BLOCK 1
 #endif
 constexpr int kWarpsPerBlock = RSIM_WARPS_PER_BLOCK;
 constexpr int kStepMinBlocks = kWarpsPerBlock == 1 ? 10 : (kWarpsPerBlock == 2 ? 5 : (kWarpsPerBlock == 3 ? 4 : 3));
@@ -89,9 +91,19 @@ struct BlockWS {
 
 struct WarpSmem {
   int32_t si[3 * kMaxBodies + 4];  // asleep, sleep counters, rider joints, held, held joint
-  // phase-scoped scratch: broadphase AABBs | narrowphase planes | solver velocities
+  // phase-scoped scratch: FK chain | broadphase AABBs + candidate pairs |
+  // narrowphase planes | solver velocities (nothing in it outlives its phase)
   union {
-    struct { double lo[kMaxBodies][3], hi[kMaxBodies][3]; } bp;
+    struct {
+      double raa[kMaxArm][9];       // arm joint rotations
+      double aoff[kMaxArm + 1][3];  // link offsets, then the gripper offset (staged by lanes)
+      double links[kMaxArm][12];    // link poses (R, p), read by the kinematic update
+      double ee[12];                // end-effector pose, read by the drag / held follow
+    } fk;  // written by forward_kinematics, read before the broadphase
+    struct {
+      double lo[kMaxBodies][3], hi[kMaxBodies][3];
+      uint16_t cand[kMaxCand];  // candidate pairs (a << 8 | b), sorted; read by the admission walk
+    } bp;
     struct {
       double planes[2][kMaxFacetsPerPart * 4];
       int off[kMaxAdm];  // first part-pair index of each admitted pair
@@ -101,12 +113,7 @@ struct WarpSmem {
   } u;
   DevScene sc;  // this env's scene table header (pointers), staged from global
   double jdv[kMaxJoints];
-  double links[kMaxArm][12];
-  double ee[12];
-  double raa[kMaxArm][9];
-  double aoff[kMaxArm + 1][3];  // FK: link offsets, then the gripper offset (staged by lanes)
   double budget[kMaxArm];
-  uint16_t cand[kMaxCand];
   uint16_t adm[kMaxAdm];
   int16_t g_a[kMaxGroups], g_b[kMaxGroups], g_first[kMaxGroups], g_n[kMaxGroups];
   int wake_idx[kMaxBodies];  // admission: index of the candidate pair that wakes each body
@@ -202,14 +209,14 @@ __device__ int set_kinematic(Ctx &c, int b, const Pose &p, double dt, bool zero_
 // ---------------------------------------------------------------- kinematics
 
 // FK of the arm chain (robot.py:161-169): lanes compute the joint rotations,
-// lane 0 chains them; results in S->links / S->ee.
+// lane 0 chains them; results in S->u.fk.links / ee.
 __device__ void forward_kinematics(Ctx &c) {
   const DevScene &sc = *c.sc;
   if (c.lane <= sc.narm) {  // the chain's constants staged in parallel (no global loads inside it)
     const double *src = c.lane < sc.narm ? sc.arm_offset + 3 * c.lane : sc.gripper;
-    for (int k = 0; k < 3; ++k) c.S->aoff[c.lane][k] = src[k];
+    for (int k = 0; k < 3; ++k) c.S->u.fk.aoff[c.lane][k] = src[k];
   }
-  if (c.lane < sc.narm) axis_angle_mat(sc.arm_axis + 3 * c.lane, JOINTS(c)[sc.nsj + c.lane], c.S->raa[c.lane]);
+  if (c.lane < sc.narm) axis_angle_mat(sc.arm_axis + 3 * c.lane, JOINTS(c)[sc.nsj + c.lane], c.S->u.fk.raa[c.lane]);
   __syncwarp();
   if (c.lane == 0) {
     Pose t, off, rot;
@@ -217,18 +224,18 @@ __device__ void forward_kinematics(Ctx &c) {
     rot_z(0.0, off.R);
     rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
     for (int i = 0; i < sc.narm; ++i) {
-      off.p[0] = c.S->aoff[i][0]; off.p[1] = c.S->aoff[i][1]; off.p[2] = c.S->aoff[i][2];
+      off.p[0] = c.S->u.fk.aoff[i][0]; off.p[1] = c.S->u.fk.aoff[i][1]; off.p[2] = c.S->u.fk.aoff[i][2];
       compose(t, off, t);
-      for (int k = 0; k < 9; ++k) rot.R[k] = c.S->raa[i][k];
+      for (int k = 0; k < 9; ++k) rot.R[k] = c.S->u.fk.raa[i][k];
       compose(t, rot, t);
-      for (int k = 0; k < 9; ++k) c.S->links[i][k] = t.R[k];
-      for (int k = 0; k < 3; ++k) c.S->links[i][9 + k] = t.p[k];
+      for (int k = 0; k < 9; ++k) c.S->u.fk.links[i][k] = t.R[k];
+      for (int k = 0; k < 3; ++k) c.S->u.fk.links[i][9 + k] = t.p[k];
     }
-    const double *gp = c.S->aoff[sc.narm];
+    const double *gp = c.S->u.fk.aoff[sc.narm];
     Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {gp[0], gp[1], gp[2]}}, e;
     compose(t, g, e);
-    for (int k = 0; k < 9; ++k) c.S->ee[k] = e.R[k];
-    for (int k = 0; k < 3; ++k) c.S->ee[9 + k] = e.p[k];
+    for (int k = 0; k < 9; ++k) c.S->u.fk.ee[k] = e.R[k];
+    for (int k = 0; k < 3; ++k) c.S->u.fk.ee[9 + k] = e.p[k];
   }
   __syncwarp();
 }
@@ -1248,7 +1255,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       if (lane == 0) {
         base3(S.sd + c.L->base, p);
       } else {
-        pose_load12(S.links[lane - 1], p);
+        pose_load12(S.u.fk.links[lane - 1], p);
       }
       set_kinematic(c, sc.robot_base + lane, p, dt, true);
     }
@@ -1263,7 +1270,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       body_pose(c, sc.joint_parent[ji], parent);
       pose_load12(sc.joint_origin + 12 * ji, origin);
       compose(parent, origin, jf);
-      const double *ee = S.ee + 9;
+      const double *ee = S.u.fk.ee + 9;
       double ax[3], qn = 0.0;
       matvec(jf.R, sc.joint_axis + 3 * ji, ax);
       bool skip = false;
@@ -1304,7 +1311,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
   if (HELD(c) >= 0 && HELDJ(c) < 0) {
     if (lane == 0) {  // physics.py:671-684
       Pose ee, off, hp;
-      pose_load12(S.ee, ee);
+      pose_load12(S.u.fk.ee, ee);
       const double *ho = S.sd + c.L->held_off;
       quat_to_mat(ho + 3, off.R);
       off.p[0] = ho[0]; off.p[1] = ho[1]; off.p[2] = ho[2];
@@ -1462,7 +1469,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
         const int cw = __popc(m & ((1u << w) - 1u));
         if (j >= cw) { j -= cw; m >>= w; pos += w; }
       }
-      S.cand[k] = (uint16_t)((lo << 8) | pos);
+      S.u.bp.cand[k] = (uint16_t)((lo << 8) | pos);
     }
     if (lane == 0) S.cbits_valid = 1;
     pb3.add(c, 14);
@@ -1483,7 +1490,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
     for (int b = lane; b < nb; b += 32) S.wake_idx[b] = 1 << 30;
     __syncwarp();
     for (int k = lane; k < ncand; k += 32) {
-      const int a = S.cand[k] >> 8, b = S.cand[k] & 0xff;
+      const int a = S.u.bp.cand[k] >> 8, b = S.u.bp.cand[k] & 0xff;
       const int ka = sc.body_kind[a], kb = sc.body_kind[b];
       // x asleep-dynamic at the start, the other kinematic robot/held, not x's rider joint
       if (ka == RS_DYNAMIC && ASLEEP(c, a) && kb == RS_KINEMATIC && (sc.body_robot[b] || b == held) &&
@@ -1499,7 +1506,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       const int k = k0 + lane;
       bool adm = false, skip = false;
       if (k < ncand) {
-        const int a = S.cand[k] >> 8, b = S.cand[k] & 0xff;
+        const int a = S.u.bp.cand[k] >> 8, b = S.u.bp.cand[k] & 0xff;
         const int ka = sc.body_kind[a], kb = sc.body_kind[b];
         const bool dyn_a = ka == RS_DYNAMIC, dyn_b = kb == RS_DYNAMIC, kin_a = ka == RS_KINEMATIC,
                    kin_b = kb == RS_KINEMATIC;
@@ -1522,7 +1529,7 @@ __device__ bool substep_front(Ctx &c, const double *arm, const double *basecmd, 
       const unsigned m = __ballot_sync(0xffffffffu, adm);
       if (adm) {
         const int idx = nadm + __popc(m & ((1u << lane) - 1));
-        if (idx < kMaxAdm) S.adm[idx] = S.cand[k];
+        if (idx < kMaxAdm) S.adm[idx] = S.u.bp.cand[k];
       }
       nadm += __popc(m);
       nskip += __popc(__ballot_sync(0xffffffffu, skip));
