@@ -11,7 +11,9 @@
 //      world facet planes (n, b0 = d - n.o) in shared memory (~25 KB); per
 //      part a range lower bound lb = |c - o| - r from its bounding sphere;
 //   2. cull: per 16x16-pixel tile, the parts whose bounding sphere meets the
-//      tile frustum, listed in ascending lb (one sort per image);
+//      tile frustum, listed in ascending lb (one sort per image); per part a
+//      conservative pixel rectangle (projected box corners / tangent lines of
+//      the bounding sphere, widened by one pixel) that the walk tests first;
 //   3. trace: per pixel, walk the tile list front to back; stop as soon as
 //      lb > t_min + tie_eps (every later part is farther: the early-out is
 //      exact), tracking (t_min, id) and the best other body (t_2nd); a
@@ -60,7 +62,8 @@ struct PartW {
 // fell back to the all-FP64 walk, 4 uncertain boxes, 5 hull tests in the walk,
 // 6 FP64 plane tests of the all-FP64 walk, 7 pixels, 8 FP32 box tests that
 // missed, 9 FP32 box hits that did not become candidates, 10 list entries
-// visited (incl. the one that ends the walk)
+// visited (incl. the one that ends the walk), 11 entries outside the part's
+// pixel rectangle
 constexpr int kWorkCounters = 12;
 struct Work {
   unsigned long long v[kWorkCounters];
@@ -75,6 +78,7 @@ struct RenderSmem {
   PartW part[kMaxParts];
   float4 box32[kMaxParts][4];  // FP32 box data: (u_k, b0 of +k) k = 0..2, (-b0 of -0, -1, -2, 0)
   float2 trace[kMaxParts];     // (lb rounded down, kind << 8 | body as int bits)
+  uint2 rect[kMaxParts];       // conservative pixel rectangle (u_lo | v_lo << 16, u_hi | v_hi << 16)
   uint32_t mask[kMaxTiles][kMaskWords];
   union {
     double R[kMaxParts][9];               // staging: world part rotations (proxy variants)
@@ -441,7 +445,7 @@ __device__ __forceinline__ double ray_box_axis(const double *pl, const double *d
 // resolve them in FP64 with the exact nearest / lowest-id rule.  Returns
 // false if a third candidate was live (the caller falls back to trace_exact).
 __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *plane, const uint8_t *list, int nl,
-                                            const double *o, const double *d, double eps, double &tmin, int &id,
+                                            uint32_t pk, const double *o, const double *d, double eps, double &tmin, int &id,
                                             int &wpart, int &wface, Work &w, bool count) {
   const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
   const float eps32 = __double2float_ru(eps);
@@ -454,6 +458,13 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
     const float2 tr = S.trace[p];
     if (count) w.v[10] += 1;
     if (tr.x > bound) break;  // sorted by lb: nothing later can be nearer or tie
+    {  // outside the part's pixel rectangle (16-bit fields; a borrow out of the low
+       // field only occurs when that field is already outside)
+      const uint2 rc = S.rect[p];
+      const bool out = (((pk - rc.x) | (rc.y - pk)) & 0x80008000u) != 0u;
+      if (count) w.v[11] += out;
+      if (out) continue;
+    }
     const int kind = __float_as_int(tr.y) >> 8;
     float tl, tu;
     int st = 2, ax = 0;
@@ -681,6 +692,48 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       return s * (1.0 + 1e-9) + 1e-9 * nn;
     };
     const bool front = live && c[2] > -radius(0.0, 0.0, 1.0, 1.0);
+    if (kMode == kProxyMixed && live) {
+      // conservative pixel rectangle of the part: the pixel u's ray has camera
+      // tangent x = (u + 0.5 - W/2) / f, and a ray hits the part only through
+      // one of its points (a box: the hull of its 8 corners; else its bounding
+      // sphere, whose tangent planes x = k z solve (c_x - k c_z)^2 = r^2 (1 + k^2)),
+      // so with every point in front of the camera u lies in [x_lo f + W/2 - 0.5,
+      // x_hi f + W/2 - 0.5]; widened by 1 pixel.  A part reaching z <= 1e-6 keeps
+      // the whole image.
+      const int W = B.rcfg.width, H = B.rcfg.height;
+      double xl = INFINITY, xh = -INFINITY, yl = INFINITY, yh = -INFINITY;
+      bool ok = true;
+      if (box) {
+        for (int s = 0; s < 8; ++s) {
+          double q[3];
+          for (int i = 0; i < 3; ++i)
+            q[i] = c[i] + ((s & 1) ? h[0] : -h[0]) * ax[0][i] + ((s & 2) ? h[1] : -h[1]) * ax[1][i] +
+                   ((s & 4) ? h[2] : -h[2]) * ax[2][i];
+          if (!(q[2] > 1e-6)) { ok = false; break; }
+          const double iz = 1.0 / q[2];
+          xl = fmin(xl, q[0] * iz); xh = fmax(xh, q[0] * iz);
+          yl = fmin(yl, q[1] * iz); yh = fmax(yh, q[1] * iz);
+        }
+      } else {
+        const double den = c[2] * c[2] - r * r;
+        ok = c[2] - r > 1e-6;
+        if (ok) {
+          const double sx = r * sqrt(fmax(c[0] * c[0] + den, 0.0)), sy = r * sqrt(fmax(c[1] * c[1] + den, 0.0));
+          xl = (c[0] * c[2] - sx) / den; xh = (c[0] * c[2] + sx) / den;
+          yl = (c[1] * c[2] - sy) / den; yh = (c[1] * c[2] + sy) / den;
+        }
+      }
+      int ulo = 0, uhi = W - 1, vlo = 0, vhi = H - 1;
+      if (ok) {
+        const double fpx = (W * 0.5) / tan(B.rcfg.fov * 0.5), cu = W * 0.5 - 0.5, cv = H * 0.5 - 0.5;
+        ulo = (int)fmax(floor(xl * fpx + cu) - 1.0, 0.0);
+        uhi = (int)fmin(ceil(xh * fpx + cu) + 1.0, W - 1.0);
+        vlo = (int)fmax(floor(yl * fpx + cv) - 1.0, 0.0);
+        vhi = (int)fmin(ceil(yh * fpx + cv) + 1.0, H - 1.0);
+        if (ulo > W - 1 || uhi < 0 || vlo > H - 1 || vhi < 0) { ulo = 1; uhi = 0; }  // off the image: nothing
+      }
+      S.rect[p] = make_uint2((uint32_t)ulo | ((uint32_t)vlo << 16), (uint32_t)uhi | ((uint32_t)vhi << 16));
+    }
     // B.tile_frustum[tile] = u0, u1, v0, v1, |(1,u0)|, |(1,u1)|, |(1,v0)|, |(1,v1)|; the inward side
     // planes x - u0 z >= 0, -x + u1 z >= 0 depend on the tile column only, y - v0 z >= 0,
     // -y + v1 z >= 0 on the row only: test columns and rows once each (ty_n, tx_n <= 8)
@@ -760,7 +813,8 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       double tmin;
       int id, wpart, wface;
       if (kMode != kProxyMixed ||
-          !trace_mixed(S, plane, list, nl, o, d, eps, tmin, id, wpart, wface, wk, count)) {
+          !trace_mixed(S, plane, list, nl, (uint32_t)u | ((uint32_t)v << 16), o, d, eps, tmin, id, wpart, wface, wk,
+                       count)) {
         if (count && kMode == kProxyMixed) wk.v[3] += 1;
         tmin = trace_exact<kMesh>(sc, S, plane, list, nl, S.mask[tile], o, d, eps, id, wpart, wface, wk, count);
       }

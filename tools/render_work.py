@@ -23,7 +23,7 @@ v = w.cpu().numpy().astype(float)
 px = v[7]
 names = ["fp32 box plane tests", "fp64 plane tests in walk", "fp64 resolve plane tests", "fallback pixels",
          "uncertain boxes", "hull tests in walk", "fp64 plane tests (all-FP64 walk)", "pixels", "fp32 box misses",
-         "hits not candidates", "list entries visited", "reserved"]
+         "hits not candidates", "list entries visited", "outside pixel rect"]
 for n, x in zip(names, v):
     print(f"{n:36s} {x:14.0f}  per pixel {x / px:8.4f}")
 sim.close()
