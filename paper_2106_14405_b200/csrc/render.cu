@@ -77,8 +77,9 @@ constexpr int kProxyExact = 2;  // every test in FP64 (the parity reference for 
 struct RenderSmem {
   PartW part[kMaxParts];
   float4 box32[kMaxParts][4];  // FP32 box data: (u_k, b0 of +k) k = 0..2, (-b0 of -0, -1, -2, 0)
-  float2 trace[kMaxParts];     // (lb rounded down, kind << 8 | body as int bits)
-  uint2 rect[kMaxParts];       // conservative pixel rectangle (u_lo | v_lo << 16, u_hi | v_hi << 16)
+  // per part, one 16-byte load in the walk: lb rounded down, kind << 8 | body
+  // (int bits), conservative pixel rectangle u_lo | v_lo << 16, u_hi | v_hi << 16
+  uint4 trace[kMaxParts];
   uint32_t mask[kMaxTiles][kMaskWords];
   union {
     double R[kMaxParts][9];               // staging: world part rotations (proxy variants)
@@ -455,17 +456,16 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
 #pragma unroll 1
   for (int j = 0; j < nl; ++j) {
     const int p = list[j];
-    const float2 tr = S.trace[p];
+    const uint4 tr = S.trace[p];
     if (count) w.v[10] += 1;
-    if (tr.x > bound) break;  // sorted by lb: nothing later can be nearer or tie
+    if (__uint_as_float(tr.x) > bound) break;  // sorted by lb: nothing later can be nearer or tie
     {  // outside the part's pixel rectangle (16-bit fields; a borrow out of the low
        // field only occurs when that field is already outside)
-      const uint2 rc = S.rect[p];
-      const bool out = (((pk - rc.x) | (rc.y - pk)) & 0x80008000u) != 0u;
+      const bool out = (((pk - tr.z) | (tr.w - pk)) & 0x80008000u) != 0u;
       if (count) w.v[11] += out;
       if (out) continue;
     }
-    const int kind = __float_as_int(tr.y) >> 8;
+    const int kind = (int)tr.y >> 8;
     float tl, tu;
     int st = 2, ax = 0;
     if (kind == RS_BOX) {
@@ -508,9 +508,13 @@ __device__ __forceinline__ bool trace_mixed(const RenderSmem &S, const double *p
   if (p1 >= 0 && l1 <= bound) t1 = resolve(p1, x1, f1);
   if (p2 >= 0 && l2 <= bound) t2 = resolve(p2, x2, f2);
   if (count) w.v[2] += (p1 >= 0 && l1 <= bound ? 6 : 0) + (p2 >= 0 && l2 <= bound ? 6 : 0);
-  tmin = fmin(t1, t2);
   id = -1; wpart = -1; wface = -1;
-  if (!(tmin < INFINITY)) return true;
+  if (!(t2 < INFINITY)) {  // at most one hit candidate (most pixels): no range comparison
+    tmin = t1;
+    if (t1 < INFINITY) { id = S.part[p1].body; wpart = p1; wface = f1; }
+    return true;
+  }
+  tmin = fmin(t1, t2);
   const bool in1 = t1 <= tmin + eps, in2 = t2 <= tmin + eps;
   const int b1 = in1 ? S.part[p1].body : 0x7fffffff, b2 = in2 ? S.part[p2].body : 0x7fffffff;
   // lowest body wins; within a body its nearest part, the lower part index on equal range
@@ -626,7 +630,8 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       dist = sqrt(dot3(v, v)) - P.r * (1.0 + 1e-9) - 1e-9;
     }
     P.lb = dist > 0.0 ? dist : 0.0;
-    S.trace[p] = make_float2(__double2float_rd(P.lb), __int_as_float((P.kind << 8) | b));
+    S.trace[p].x = __float_as_uint(__double2float_rd(P.lb));
+    S.trace[p].y = (uint32_t)((P.kind << 8) | b);
   }
   if (!kMesh && tid == 0) wait_bulk(&S.mbar);
   __syncthreads();
@@ -732,7 +737,8 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
         vhi = (int)fmin(ceil(yh * fpx + cv) + 1.0, H - 1.0);
         if (ulo > W - 1 || uhi < 0 || vlo > H - 1 || vhi < 0) { ulo = 1; uhi = 0; }  // off the image: nothing
       }
-      S.rect[p] = make_uint2((uint32_t)ulo | ((uint32_t)vlo << 16), (uint32_t)uhi | ((uint32_t)vhi << 16));
+      S.trace[p].z = (uint32_t)ulo | ((uint32_t)vlo << 16);
+      S.trace[p].w = (uint32_t)uhi | ((uint32_t)vhi << 16);
     }
     // B.tile_frustum[tile] = u0, u1, v0, v1, |(1,u0)|, |(1,u1)|, |(1,v0)|, |(1,v1)|; the inward side
     // planes x - u0 z >= 0, -x + u1 z >= 0 depend on the tile column only, y - v0 z >= 0,
