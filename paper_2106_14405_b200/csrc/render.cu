@@ -19,8 +19,8 @@
 //      exact), tracking (t_min, id) and the best other body (t_2nd); a
 //      near-tie (t_2nd - t_min <= tie_eps) re-resolves the pixel with the
 //      exact lowest-id rule in body order;
-//   4. write rgba (u32), depth (f32), id (i32), 16 consecutive pixels per
-//      half-warp.
+//   4. write rgba (u32), depth (f32), id (i32); a warp iteration covers an
+//      8 x 4 pixel block (8 consecutive pixels = one 32-byte sector per row).
 // Float64 arithmetic throughout (parity with the float64 oracle); boxes use
 // their 3 face normals (the -x/-y/-z planes are exact negations), and the
 // plane arg-max/arg-min uses division-free cross-multiplied compares so only
@@ -803,8 +803,9 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     const int ux = (tile % tx_n) * kTile, vy = (tile / tx_n) * kTile;
 #pragma unroll 1
     for (int k = lane; k < kTile * kTile; k += 32) {
-      // lane -> column ux + lane % 16 (fixed), rows vy + lane / 16 + 2 j
-      const int u = ux + (lane & (kTile - 1)), v = vy + (k >> 4);
+      // iteration j = k / 32 covers the 8 x 4 block (j % 2, j / 2) of the tile:
+      // lane -> column lane % 8, row lane / 8 (compact blocks walk similar lists)
+      const int u = ux + ((k >> 2) & 8) + (lane & 7), v = vy + ((k >> 4) & 12) + (lane >> 3);
       const double *dc = B.ray_dir + 3 * (v * W + u);  // unit camera-frame ray (render_tables_kernel)
       double d[3];
       {  // matvec(S.cam.R, dc, d) with the rotation re-read from shared memory per pixel: hoisted out
