@@ -703,21 +703,48 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       // one of its points (a box: the hull of its 8 corners; else its bounding
       // sphere, whose tangent planes x = k z solve (c_x - k c_z)^2 = r^2 (1 + k^2)),
       // so with every point in front of the camera u lies in [x_lo f + W/2 - 0.5,
-      // x_hi f + W/2 - 0.5]; widened by 1 pixel.  A part reaching z <= 1e-6 keeps
-      // the whole image.
+      // x_hi f + W/2 - 0.5]; widened by 1 pixel.  A box reaching behind the
+      // plane z = zc is clipped to z >= zc (its region: the corners in front and
+      // the crossings of its 12 edges with the plane), which loses no visible
+      // point when the box is farther than zc sqrt(1 + tan_x^2 + tan_y^2) from
+      // the camera (a point inside the image has z >= |p| / that root); closer
+      // boxes, and other parts reaching z <= 1e-6, keep the whole image.
       const int W = B.rcfg.width, H = B.rcfg.height;
+      const double fpx = (W * 0.5) / tan(B.rcfg.fov * 0.5);
       double xl = INFINITY, xh = -INFINITY, yl = INFINITY, yh = -INFINITY;
       bool ok = true;
       if (box) {
-        for (int s = 0; s < 8; ++s) {
-          double q[3];
+        constexpr double zc = 1e-3;
+        auto corner = [&](int s, double *q) {
           for (int i = 0; i < 3; ++i)
             q[i] = c[i] + ((s & 1) ? h[0] : -h[0]) * ax[0][i] + ((s & 2) ? h[1] : -h[1]) * ax[1][i] +
                    ((s & 4) ? h[2] : -h[2]) * ax[2][i];
-          if (!(q[2] > 1e-6)) { ok = false; break; }
-          const double iz = 1.0 / q[2];
-          xl = fmin(xl, q[0] * iz); xh = fmax(xh, q[0] * iz);
-          yl = fmin(yl, q[1] * iz); yh = fmax(yh, q[1] * iz);
+        };
+        auto add = [&](double x, double y, double z) {
+          const double iz = 1.0 / z;
+          xl = fmin(xl, x * iz); xh = fmax(xh, x * iz);
+          yl = fmin(yl, y * iz); yh = fmax(yh, y * iz);
+        };
+        bool behind = false;
+        for (int s = 0; s < 8; ++s) {
+          double q[3];
+          corner(s, q);
+          if (q[2] >= zc) add(q[0], q[1], q[2]);
+          else behind = true;
+        }
+        if (behind) {
+          const double lb = S.part[p].lb, t2 = ((double)W * W + (double)H * H) / (4.0 * fpx * fpx);
+          ok = lb * lb > 1.1 * zc * zc * (1.0 + t2);
+          for (int s = 0; ok && s < 8; ++s)
+            for (int k = 0; k < 3; ++k) {
+              if (s & (1 << k)) continue;  // edge (s, s + 2^k), each once
+              double a[3], b[3];
+              corner(s, a);
+              corner(s | (1 << k), b);
+              if ((a[2] < zc) == (b[2] < zc)) continue;
+              const double t = (zc - a[2]) / (b[2] - a[2]);
+              add(a[0] + t * (b[0] - a[0]), a[1] + t * (b[1] - a[1]), zc);
+            }
         }
       } else {
         const double den = c[2] * c[2] - r * r;
@@ -730,7 +757,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       }
       int ulo = 0, uhi = W - 1, vlo = 0, vhi = H - 1;
       if (ok) {
-        const double fpx = (W * 0.5) / tan(B.rcfg.fov * 0.5), cu = W * 0.5 - 0.5, cv = H * 0.5 - 0.5;
+        const double cu = W * 0.5 - 0.5, cv = H * 0.5 - 0.5;
         ulo = (int)fmax(floor(xl * fpx + cu) - 1.0, 0.0);
         uhi = (int)fmin(ceil(xh * fpx + cu) + 1.0, W - 1.0);
         vlo = (int)fmax(floor(yl * fpx + cv) - 1.0, 0.0);
