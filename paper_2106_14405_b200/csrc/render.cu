@@ -697,6 +697,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       return s * (1.0 + 1e-9) + 1e-9 * nn;
     };
     const bool front = live && c[2] > -radius(0.0, 0.0, 1.0, 1.0);
+    int ulo = 0, uhi = 0x7fff, vlo = 0, vhi = 0x7fff;  // pixel rectangle (the tile lists use it too)
     if (kMode == kProxyMixed && live) {
       // conservative pixel rectangle of the part: the pixel u's ray has camera
       // tangent x = (u + 0.5 - W/2) / f, and a ray hits the part only through
@@ -755,7 +756,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
           yl = (c[1] * c[2] - sy) / den; yh = (c[1] * c[2] + sy) / den;
         }
       }
-      int ulo = 0, uhi = W - 1, vlo = 0, vhi = H - 1;
+      ulo = 0; uhi = W - 1; vlo = 0; vhi = H - 1;
       if (ok) {
         const double cu = W * 0.5 - 0.5, cv = H * 0.5 - 0.5;
         ulo = (int)fmax(floor(xl * fpx + cu) - 1.0, 0.0);
@@ -774,14 +775,15 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     if (front)
       for (int ty = 0; ty < ty_n; ++ty) {
         const double *T = B.tile_frustum + 8 * (ty * tx_n);
-        rows |= (unsigned)(c[1] - T[2] * c[2] >= -radius(0.0, 1.0, -T[2], T[6]) &&
+        rows |= (unsigned)(vlo < (ty + 1) * kTile && vhi >= ty * kTile &&
+                           c[1] - T[2] * c[2] >= -radius(0.0, 1.0, -T[2], T[6]) &&
                            -c[1] + T[3] * c[2] >= -radius(0.0, -1.0, T[3], T[7])) << ty;
       }
     for (int tx = 0; tx < tx_n; ++tx) {
       bool col = false;
       if (front) {
         const double *T = B.tile_frustum + 8 * tx;
-        col = c[0] - T[0] * c[2] >= -radius(1.0, 0.0, -T[0], T[4]) &&
+        col = ulo < (tx + 1) * kTile && uhi >= tx * kTile && c[0] - T[0] * c[2] >= -radius(1.0, 0.0, -T[0], T[4]) &&
               -c[0] + T[1] * c[2] >= -radius(-1.0, 0.0, T[1], T[5]);
       }
       for (int ty = 0; ty < ty_n; ++ty) {
