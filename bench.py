@@ -613,7 +613,7 @@ def run_b200(args):
         L.rsim_bench_fma_peak(0, C.byref(peak32))
         render_flop = N_CAMS * H * W * (14 * 566 + 22 * 4)  # SURVEY.md §8d W_r (brute-force proxy raycast)
         phys_flop = 0.09e6  # SURVEY.md §8d idle W_p per env-step
-        wd = torch.zeros(12, dtype=torch.int64, device=dev)
+        wd = torch.zeros(20, dtype=torch.int64, device=dev)  # rsim_bench.h: 20 counters
         L.rsim_bench_render_work_detail.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p]
         L.rsim_bench_render_work_detail(sim._batch, 3, C.c_void_p(wd.data_ptr()), C.c_void_p(stream.cuda_stream))
         torch.cuda.synchronize(dev)

@@ -18,13 +18,16 @@ int rsim_bench_fma_peak(int fp64, double *tflops);
 struct rs_batch;
 int rsim_bench_render_work(struct rs_batch *batch, unsigned int cam_mask, unsigned long long *d_counter,
                            void *stream);
-/* The same launch with the 12 executed-work counters of the counting variant
- * (added to d_counters[12], device uint64): 0 FP32 box plane tests, 1 FP64
- * plane tests in the walk (uncertain boxes, hulls; sphere = 1), 2 FP64 plane
- * tests resolving candidates, 3 pixels that fell back to the all-FP64 walk,
+/* The same launch with the 20 counters of the counting variant (added to
+ * d_counters[20], device uint64): 0 FP32 box plane tests, 1 FP64 plane tests
+ * in the walk (uncertain boxes, hulls; sphere = 1), 2 FP64 plane tests
+ * resolving candidates, 3 pixels that fell back to the all-FP64 walk,
  * 4 uncertain boxes, 5 hull tests in the walk, 6 plane tests of the all-FP64
  * walk, 7 pixels, 8 FP32 box tests that missed, 9 hits that did not become
- * candidates, 10 tile-list entries visited, 11 reserved. */
+ * candidates, 10 tile-list entries visited, 11 entries outside the part's
+ * pixel rectangle; SM cycles summed over CTAs: 12 camera pose, 13 part
+ * frames, 14 world planes, 15 culling + ordering, 16 tile lists, 17 trace;
+ * summed over warps: 18 culling warps' own work, 19 ordering warps'. */
 int rsim_bench_render_work_detail(struct rs_batch *batch, unsigned int cam_mask, unsigned long long *d_counters,
                                   void *stream);
 /* rs_render with every ray test in FP64 (rs_render selects candidates with

@@ -728,8 +728,8 @@ int rsim_bench_render_work(rs_batch *b, uint32_t cam_mask, unsigned long long *d
   DeviceScope device_scope(b);
   if (!b || !d_counter) return fail(RS_ERR_ARG, "null argument");
   unsigned long long *w = nullptr;
-  CUDA_TRY(cudaMalloc(&w, 12 * sizeof(unsigned long long)));
-  CUDA_TRY(cudaMemsetAsync(w, 0, 12 * sizeof(unsigned long long), (cudaStream_t)stream));
+  CUDA_TRY(cudaMalloc(&w, 20 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(w, 0, 20 * sizeof(unsigned long long), (cudaStream_t)stream));
   CUDA_TRY(launch_render(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, w));
   work_total_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(w, d_counter);
   CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
@@ -879,8 +879,8 @@ int rsim_bench_render_mesh_work(rs_batch *b, uint32_t cam_mask, unsigned long lo
   DeviceScope device_scope(b);
   if (!b || !d_counter || !b->has_mesh) return fail(RS_ERR_ARG, "null argument or no mesh");
   unsigned long long *w = nullptr;
-  CUDA_TRY(cudaMalloc(&w, 12 * sizeof(unsigned long long)));
-  CUDA_TRY(cudaMemsetAsync(w, 0, 12 * sizeof(unsigned long long), (cudaStream_t)stream));
+  CUDA_TRY(cudaMalloc(&w, 20 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(w, 0, 20 * sizeof(unsigned long long), (cudaStream_t)stream));
   CUDA_TRY(launch_render_mesh(b->view(), cam_mask, nullptr, nullptr, nullptr, (cudaStream_t)stream, w));
   work_total_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(w, d_counter);
   CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));

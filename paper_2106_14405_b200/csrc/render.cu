@@ -63,8 +63,11 @@ struct PartW {
 // 6 FP64 plane tests of the all-FP64 walk, 7 pixels, 8 FP32 box tests that
 // missed, 9 FP32 box hits that did not become candidates, 10 list entries
 // visited (incl. the one that ends the walk), 11 entries outside the part's
-// pixel rectangle
-constexpr int kWorkCounters = 12;
+// pixel rectangle; SM cycles summed over CTAs: 12 camera pose, 13 part frames,
+// 14 world planes, 15 culling + ordering (to the barrier), 16 tile lists,
+// 17 trace; summed over warps: 18 culling warps' own work, 19 ordering warps'
+// own work
+constexpr int kWorkCounters = 20;
 struct Work {
   unsigned long long v[kWorkCounters];
 };
@@ -556,6 +559,8 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   const StateLayout &L = B.L;
   const double *sd = B.sd + (size_t)env * L.dbl_size;
   const int tid = threadIdx.x, np = sc.np;
+  long long clk[7];  // counting variant: SM clock at the set-up barriers (thread 0)
+  if (kCount) clk[0] = clock64();
   // the scene's local facet table (n, offset per facet) into the plane array by
   // one TMA bulk copy, overlapped with the camera pose and the part frames; each
   // thread then turns its facets into world planes in place
@@ -588,6 +593,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     compose(parent, mount, S.cam);
   }
   __syncthreads();
+  if (kCount) clk[1] = clock64();
   const double *o = S.cam.p;
   for (int i = tid; i < sc.nb; i += blockDim.x)
     S.color[i] = make_float4(__fmul_rn(255.0f, sc.color[3 * i]), __fmul_rn(255.0f, sc.color[3 * i + 1]),
@@ -635,6 +641,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   }
   if (!kMesh && tid == 0) wait_bulk(&S.mbar);
   __syncthreads();
+  if (kCount) clk[3] = clk[2] = clock64();
   if (!kMesh) {
     const int nf = sc.nf;
     for (int f = tid; f < nf; f += blockDim.x) {
@@ -652,6 +659,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       Q[3] = dw - dot3(o, n);
     }
     __syncthreads();
+    if (kCount) clk[3] = clock64();
     if (kMode == kProxyMixed)
       for (int p = tid; p < np; p += blockDim.x) {
         const PartW &P = S.part[p];
@@ -698,6 +706,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     };
     const bool front = live && c[2] > -radius(0.0, 0.0, 1.0, 1.0);
     int ulo = 0, uhi = 0x7fff, vlo = 0, vhi = 0x7fff;  // pixel rectangle (the tile lists use it too)
+    bool rect_only = false;  // the rectangle is the part's exact projected extent (+ 1 pixel): it decides the tiles
     if (kMode == kProxyMixed && live) {
       // conservative pixel rectangle of the part: the pixel u's ray has camera
       // tangent x = (u + 0.5 - W/2) / f, and a ray hits the part only through
@@ -764,6 +773,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
         vlo = (int)fmax(floor(yl * fpx + cv) - 1.0, 0.0);
         vhi = (int)fmin(ceil(yh * fpx + cv) + 1.0, H - 1.0);
         if (ulo > W - 1 || uhi < 0 || vlo > H - 1 || vhi < 0) { ulo = 1; uhi = 0; }  // off the image: nothing
+        rect_only = true;
       }
       S.trace[p].z = (uint32_t)ulo | ((uint32_t)vlo << 16);
       S.trace[p].w = (uint32_t)uhi | ((uint32_t)vhi << 16);
@@ -771,26 +781,41 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     // B.tile_frustum[tile] = u0, u1, v0, v1, |(1,u0)|, |(1,u1)|, |(1,v0)|, |(1,v1)|; the inward side
     // planes x - u0 z >= 0, -x + u1 z >= 0 depend on the tile column only, y - v0 z >= 0,
     // -y + v1 z >= 0 on the row only: test columns and rows once each (ty_n, tx_n <= 8)
-    unsigned rows = 0u;
-    if (front)
-      for (int ty = 0; ty < ty_n; ++ty) {
-        const double *T = B.tile_frustum + 8 * (ty * tx_n);
-        rows |= (unsigned)(vlo < (ty + 1) * kTile && vhi >= ty * kTile &&
-                           c[1] - T[2] * c[2] >= -radius(0.0, 1.0, -T[2], T[6]) &&
-                           -c[1] + T[3] * c[2] >= -radius(0.0, -1.0, T[3], T[7])) << ty;
-      }
-    for (int tx = 0; tx < tx_n; ++tx) {
-      bool col = false;
-      if (front) {
-        const double *T = B.tile_frustum + 8 * tx;
-        col = ulo < (tx + 1) * kTile && uhi >= tx * kTile && c[0] - T[0] * c[2] >= -radius(1.0, 0.0, -T[0], T[4]) &&
-              -c[0] + T[1] * c[2] >= -radius(-1.0, 0.0, T[1], T[5]);
-      }
-      for (int ty = 0; ty < ty_n; ++ty) {
-        const unsigned m = __ballot_sync(0xffffffffu, col && ((rows >> ty) & 1u));
-        if (lane == 0) S.mask[ty * tx_n + tx][warp] = m;
+    auto row_in = [&](int ty) {
+      const double *T = B.tile_frustum + 8 * (ty * tx_n);
+      return c[1] - T[2] * c[2] >= -radius(0.0, 1.0, -T[2], T[6]) && -c[1] + T[3] * c[2] >= -radius(0.0, -1.0, T[3], T[7]);
+    };
+    auto col_in = [&](int tx) {
+      const double *T = B.tile_frustum + 8 * tx;
+      return c[0] - T[0] * c[2] >= -radius(1.0, 0.0, -T[0], T[4]) && -c[0] + T[1] * c[2] >= -radius(-1.0, 0.0, T[1], T[5]);
+    };
+    unsigned rows = 0u, cols = 0u;
+    if (front) {
+      if (rect_only) {
+        // A valid rectangle is the projected extent of the part's points in front
+        // of the camera widened by 1 pixel: a tile strictly between its first and
+        // last tile lies inside that extent and passes the side-plane tests, so
+        // only those two tiles per axis are tested
+        if (ulo <= uhi && vlo <= vhi) {
+          const int c0 = ulo / kTile, c1 = min(uhi / kTile, tx_n - 1), r0 = vlo / kTile, r1 = min(vhi / kTile, ty_n - 1);
+          for (int t = c0; t <= c1; ++t) cols |= 1u << t;
+          for (int t = r0; t <= r1; ++t) rows |= 1u << t;
+          if (!col_in(c0)) cols &= ~(1u << c0);
+          if (c1 != c0 && !col_in(c1)) cols &= ~(1u << c1);
+          if (!row_in(r0)) rows &= ~(1u << r0);
+          if (r1 != r0 && !row_in(r1)) rows &= ~(1u << r1);
+        }
+      } else {
+        for (int ty = 0; ty < ty_n; ++ty) rows |= (unsigned)(vlo < (ty + 1) * kTile && vhi >= ty * kTile && row_in(ty)) << ty;
+        for (int tx = 0; tx < tx_n; ++tx) cols |= (unsigned)(ulo < (tx + 1) * kTile && uhi >= tx * kTile && col_in(tx)) << tx;
       }
     }
+    for (int tx = 0; tx < tx_n; ++tx)
+      for (int ty = 0; ty < ty_n; ++ty) {
+        const unsigned m = __ballot_sync(0xffffffffu, ((cols >> tx) & (rows >> ty) & 1u) != 0u);
+        if (lane == 0) S.mask[ty * tx_n + tx][warp] = m;
+      }
+    if (kCount && lane == 0) atomicAdd(work + 18, (unsigned long long)(clock64() - clk[3]));
   } else {
     for (int p = tid - 32 * kMaskWords; p < np; p += blockDim.x - 32 * kMaskWords) {
       const double lb = S.part[p].lb;
@@ -801,8 +826,10 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       }
       S.order[rank] = (uint8_t)p;
     }
+    if (kCount && lane == 0) atomicAdd(work + 19, (unsigned long long)(clock64() - clk[3]));
   }
   __syncthreads();
+  if (kCount) clk[4] = clock64();
   // -- per tile candidate lists in front-to-back order (warp per tile, ballot compaction)
   for (int tile = warp; tile < ntiles; tile += nwarps) {
     int n = 0;
@@ -817,6 +844,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     if (lane == 0) S.nlist[tile] = n;
   }
   __syncthreads();
+  if (kCount) clk[5] = clock64();
 
   // -- trace
   const double eps = B.rcfg.tie_eps, zfar = B.rcfg.zfar, znear = B.rcfg.znear;
@@ -898,8 +926,14 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       }
     }
   }
-  if (count)
-    for (int i = 0; i < kWorkCounters; ++i) atomicAdd(work + i, wk.v[i]);
+  if (count) {
+    for (int i = 0; i < 12; ++i) atomicAdd(work + i, wk.v[i]);
+    __syncthreads();
+    if (tid == 0) {
+      clk[6] = clock64();
+      for (int i = 0; i < 6; ++i) atomicAdd(work + 12 + i, (unsigned long long)(clk[i + 1] - clk[i]));
+    }
+  }
 }
 
 // Per-batch constant tables: unit camera-frame ray per pixel centre
