@@ -92,6 +92,7 @@ struct RenderSmem {
   uint8_t order[kMaxParts];
   float4 color[kMaxBodies];  // 255 x body albedo, rounded as the shading rule's first product (one LDS.128)
   Pose cam;
+  double armR[8][9];  // arm joint rotations (the arm camera's chain), beside the part frames
   uint64_t mbar;  // completion barrier of the facet-table TMA bulk copy
 };
 // world planes (n.xyz, b0 per facet; mesh variant: part rotations) follow the struct
@@ -559,6 +560,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   const StateLayout &L = B.L;
   const double *sd = B.sd + (size_t)env * L.dbl_size;
   const int tid = threadIdx.x, np = sc.np;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   long long clk[7];  // counting variant: SM clock at the set-up barriers (thread 0)
   if (kCount) clk[0] = clock64();
   // the scene's local facet table (n, offset per facet) into the plane array by
@@ -566,67 +568,76 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   // thread then turns its facets into world planes in place
   if (!kMesh && tid == 0) stage_facets(plane, sc.facet, sc.nf, &S.mbar);
 
-  // -- camera pose (robot.py:43-47 mounts; tools_make_robot_json.py:12-19 axes);
-  //    the arm chain's joint rotations are computed by one thread each first
-  const bool arm_cam = sc.cam_parent[cam] != 0;
-  if (arm_cam && tid < sc.narm) axis_angle_mat(sc.arm_axis + 3 * tid, sd[L.joints + sc.nsj + tid], S.u.R[tid]);
-  if (arm_cam) __syncthreads();
-  if (tid == 0) {
-    Pose parent, mount;
-    if (sc.cam_parent[cam] == 0) {
-      base3(sd + L.base, parent);
-    } else {
-      Pose t, off, rot;
-      base3(sd + L.base, t);
-      rot_z(0.0, off.R);
-      rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
-      for (int i = 0; i < sc.narm; ++i) {
-        off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
-        compose(t, off, t);
-        for (int k = 0; k < 9; ++k) rot.R[k] = S.u.R[i][k];
-        compose(t, rot, t);
+  // -- warp 0: camera pose (robot.py:43-47 mounts; tools_make_robot_json.py:12-19
+  //    axes; the arm chain's joint rotations one lane each, lane 0 chains them);
+  //    warps 1..7 meanwhile: world part frames (lanes per part) and body colours
+  if (warp == 0) {
+    const bool arm_cam = sc.cam_parent[cam] != 0;
+    if (arm_cam && lane < sc.narm) axis_angle_mat(sc.arm_axis + 3 * lane, sd[L.joints + sc.nsj + lane], S.armR[lane]);
+    __syncwarp();
+    if (lane == 0) {
+      Pose parent, mount;
+      if (!arm_cam) {
+        base3(sd + L.base, parent);
+      } else {
+        Pose t, off, rot;
+        base3(sd + L.base, t);
+        rot_z(0.0, off.R);
+        rot.p[0] = rot.p[1] = rot.p[2] = 0.0;
+        for (int i = 0; i < sc.narm; ++i) {
+          off.p[0] = sc.arm_offset[3 * i]; off.p[1] = sc.arm_offset[3 * i + 1]; off.p[2] = sc.arm_offset[3 * i + 2];
+          compose(t, off, t);
+          for (int k = 0; k < 9; ++k) rot.R[k] = S.armR[i][k];
+          compose(t, rot, t);
+        }
+        Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}};
+        compose(t, g, parent);
       }
-      Pose g = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {sc.gripper[0], sc.gripper[1], sc.gripper[2]}};
-      compose(t, g, parent);
+      pose_load12(sc.cam_mount + 12 * cam, mount);
+      compose(parent, mount, S.cam);
+      if (!kMesh) wait_bulk(&S.mbar);
     }
-    pose_load12(sc.cam_mount + 12 * cam, mount);
-    compose(parent, mount, S.cam);
+  } else {
+    for (int i = tid - 32; i < sc.nb; i += blockDim.x - 32)
+      S.color[i] = make_float4(__fmul_rn(255.0f, sc.color[3 * i]), __fmul_rn(255.0f, sc.color[3 * i + 1]),
+                               __fmul_rn(255.0f, sc.color[3 * i + 2]), 0.0f);
+    for (int p = tid - 32; p < np; p += blockDim.x - 32) {
+      int b = sc.part_body[p];
+      Pose bp, lp, wp;
+      quat_to_mat(sd + L.quat + 4 * b, bp.R);
+      bp.p[0] = sd[L.pos + 3 * b]; bp.p[1] = sd[L.pos + 3 * b + 1]; bp.p[2] = sd[L.pos + 3 * b + 2];
+      pose_load12(sc.part_local + 12 * p, lp);
+      compose(bp, lp, wp);
+      PartW &P = S.part[p];
+      P.c[0] = wp.p[0]; P.c[1] = wp.p[1]; P.c[2] = wp.p[2];
+      P.kind = sc.part_kind[p];
+      P.body = b;
+      P.f0 = sc.part_facet_begin[p];
+      P.nf = sc.part_facet_begin[p + 1] - P.f0;
+      if (kMesh) {
+        P.r = sc.mesh_bound[p];
+        for (int k = 0; k < 9; ++k) plane[9 * p + k] = wp.R[k];
+      } else {
+        P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : sc.part_bound[p];
+      }
+      for (int k = 0; k < 9; ++k) S.u.R[p][k] = wp.R[k];
+    }
   }
   __syncthreads();
-  if (kCount) clk[1] = clock64();
+  if (kCount) clk[2] = clk[1] = clock64();
   const double *o = S.cam.p;
-  for (int i = tid; i < sc.nb; i += blockDim.x)
-    S.color[i] = make_float4(__fmul_rn(255.0f, sc.color[3 * i]), __fmul_rn(255.0f, sc.color[3 * i + 1]),
-                             __fmul_rn(255.0f, sc.color[3 * i + 2]), 0.0f);
 
-  // -- world part frames and bounds (lanes per part), then world planes
-  //    (geometry.py:554-557), b0 = d - n.o (lanes per facet)
+  // -- per part the range lower bound from the camera (lanes per part), then
+  //    world planes (geometry.py:554-557), b0 = d - n.o (lanes per facet)
   for (int p = tid; p < np; p += blockDim.x) {
-    int b = sc.part_body[p];
-    Pose bp, lp, wp;
-    quat_to_mat(sd + L.quat + 4 * b, bp.R);
-    bp.p[0] = sd[L.pos + 3 * b]; bp.p[1] = sd[L.pos + 3 * b + 1]; bp.p[2] = sd[L.pos + 3 * b + 2];
-    pose_load12(sc.part_local + 12 * p, lp);
-    compose(bp, lp, wp);
     PartW &P = S.part[p];
-    P.c[0] = wp.p[0]; P.c[1] = wp.p[1]; P.c[2] = wp.p[2];
-    P.kind = sc.part_kind[p];
-    P.body = b;
-    P.f0 = sc.part_facet_begin[p];
-    P.nf = sc.part_facet_begin[p + 1] - P.f0;
-    if (kMesh) {
-      P.r = sc.mesh_bound[p];
-      for (int k = 0; k < 9; ++k) plane[9 * p + k] = wp.R[k];
-    } else {
-      P.r = P.kind == RS_SPHERE ? sc.part_param[3 * p] : sc.part_bound[p];
-    }
-    for (int k = 0; k < 9; ++k) S.u.R[p][k] = wp.R[k];
-    double v[3] = {wp.p[0] - o[0], wp.p[1] - o[1], wp.p[2] - o[2]};
+    const double *R = S.u.R[p];
+    double v[3] = {P.c[0] - o[0], P.c[1] - o[1], P.c[2] - o[2]};
     double dist;
     if (P.kind == RS_BOX) {  // distance from the camera to the box (tighter than its sphere; a box
                              // part's triangle soup lies on the box surface, mesh.py part_triangles)
       double l[3], q2 = 0.0;
-      mattvec(wp.R, v, l);
+      mattvec(R, v, l);
       for (int k = 0; k < 3; ++k) {
         const double e = fabs(l[k]) - sc.part_param[3 * p + k];
         q2 += e > 0.0 ? e * e : 0.0;
@@ -637,11 +648,9 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     }
     P.lb = dist > 0.0 ? dist : 0.0;
     S.trace[p].x = __float_as_uint(__double2float_rd(P.lb));
-    S.trace[p].y = (uint32_t)((P.kind << 8) | b);
+    S.trace[p].y = (uint32_t)((P.kind << 8) | P.body);
   }
-  if (!kMesh && tid == 0) wait_bulk(&S.mbar);
-  __syncthreads();
-  if (kCount) clk[3] = clk[2] = clock64();
+  if (kCount) clk[3] = clock64();
   if (!kMesh) {
     const int nf = sc.nf;
     for (int f = tid; f < nf; f += blockDim.x) {
@@ -672,7 +681,6 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   }
   const int W = B.rcfg.width, H = B.rcfg.height;
   const int tx_n = W / kTile, ty_n = H / kTile, ntiles = tx_n * ty_n;
-  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   if (kMesh) __syncthreads();
 
   // -- warps 0..3: tile culling, lane = part (sphere vs the 4 side planes of
