@@ -894,13 +894,15 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
 
       const size_t px = img + (size_t)(v * W + u);
       if (!(tmin <= zfar)) {
-        if (kAll || rgba) rgba[px] = 0u;
-        if (kAll || depth) depth[px] = 0.0f;
-        if (kAll || ids) ids[px] = -1;
+        if (kAll || rgba) __stcs(rgba + px, 0u);
+        if (kAll || depth) __stcs(depth + px, 0.0f);
+        if (kAll || ids) __stcs(ids + px, -1);
         continue;
       }
-      if (kAll || depth) depth[px] = (float)(tmin < znear ? znear : tmin);
-      if (kAll || ids) ids[px] = id;
+      // streaming stores (evict-first): the 100 MB of images per step pass through
+      // L2 without evicting the physics kernel's scratch running beside the render
+      if (kAll || depth) __stcs(depth + px, (float)(tmin < znear ? znear : tmin));
+      if (kAll || ids) __stcs(ids + px, id);
       if (kAll || rgba) {
         double cosv = 0.0;
         const PartW &P = S.part[wpart];
@@ -930,7 +932,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
           float cv = __fadd_rn(__fmul_rn(col[i], shade), 0.5f);
           px4 |= (uint32_t)(cv > 255.0f ? 255.0f : cv) << (8 * i);
         }
-        rgba[px] = px4;
+        __stcs(rgba + px, px4);
       }
     }
   }
