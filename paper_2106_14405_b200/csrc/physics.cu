@@ -132,9 +132,9 @@ __host__ __device__ constexpr size_t warp_smem_bytes(int stage) {
   return (sizeof(WarpSmem) - sizeof(double) * 2 + sizeof(double) * (size_t)stage + 15) & ~(size_t)15;
 }
 
-// 5 two-warp CTAs per SM (228 KB of shared memory, 1 KB reserved per CTA)
 static_assert(13 * kMaxBodies + 2 * kMaxJoints + 16 <= kStageD, "state slab prefix must fit the staging buffer");
-// >= 9 envs per SM even for a 64-body scene (228 KB of shared memory, 1 KB reserved per CTA)
+// the occupancy the launch bounds ask for must fit even a 64-body scene's
+// staged slab (228 KB of shared memory per SM, 1 KB reserved per CTA)
 static_assert((kWarpsPerBlock == 1 ? 10 : (kWarpsPerBlock == 2 ? 5 : (kWarpsPerBlock == 3 ? 3 : 2))) *
                       (kWarpsPerBlock * warp_smem_bytes(13 * kMaxBodies + 2 * kMaxJoints + 16) + 1024) <=
                   228 * 1024,
