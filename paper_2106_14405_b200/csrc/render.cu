@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
     const uint8_t *list = S.u.list[tile];
     const int nl = S.nlist[tile];
     const int ux = (tile % tx_n) * kTile, vy = (tile / tx_n) * kTile;
-    if (kMode == kProxyMixed && nl == 0) {  // an empty tile: every pixel misses
+    if (nl == 0) {  // an empty tile: every pixel misses
       for (int k = lane; k < kTile * kTile; k += 32) {
         const int u = ux + ((k >> 2) & 8) + (lane & 7), v = vy + ((k >> 4) & 12) + (lane >> 3);
         const size_t px = img + (size_t)(v * W + u);
@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       }
       continue;
     }
-    if (kMode == kProxyMixed) __builtin_assume(nl > 0);
+    __builtin_assume(nl > 0);
 #pragma unroll 1
     for (int k = lane; k < kTile * kTile; k += 32) {
       // iteration j = k / 32 covers the 8 x 4 block (j % 2, j / 2) of the tile:
