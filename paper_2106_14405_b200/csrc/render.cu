@@ -776,10 +776,12 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       ulo = 0; uhi = W - 1; vlo = 0; vhi = H - 1;
       if (ok) {
         const double cu = W * 0.5 - 0.5, cv = H * 0.5 - 0.5;
-        ulo = (int)fmax(floor(xl * fpx + cu) - 1.0, 0.0);
-        uhi = (int)fmin(ceil(xh * fpx + cu) + 1.0, W - 1.0);
-        vlo = (int)fmax(floor(yl * fpx + cv) - 1.0, 0.0);
-        vhi = (int)fmin(ceil(yh * fpx + cv) + 1.0, H - 1.0);
+        // clamped to [-1, W] x [-1, H] before the conversion (a clipped box with no
+        // point in front leaves the bounds at +-inf: it lands off the image)
+        ulo = (int)fmin(fmax(floor(xl * fpx + cu) - 1.0, 0.0), (double)W);
+        uhi = (int)fmax(fmin(ceil(xh * fpx + cu) + 1.0, W - 1.0), -1.0);
+        vlo = (int)fmin(fmax(floor(yl * fpx + cv) - 1.0, 0.0), (double)H);
+        vhi = (int)fmax(fmin(ceil(yh * fpx + cv) + 1.0, H - 1.0), -1.0);
         if (ulo > W - 1 || uhi < 0 || vlo > H - 1 || vhi < 0) { ulo = 1; uhi = 0; }  // off the image: nothing
         rect_only = true;
       }
