@@ -29,10 +29,12 @@ def _oracle(layout=0):
 
 
 @pytest.mark.parametrize("w,h,fov", [(64, 64, np.pi / 2), (96, 48, np.pi / 2), (16, 16, np.pi / 2),
-                                     (128, 32, np.pi / 3), (128, 128, 2.0)])
+                                     (128, 32, np.pi / 3), (128, 128, 2.0), (128, 128, 2.8), (64, 32, 2.5)])
 def test_render_other_resolutions_and_fov(w, h, fov):
     """rs_render at W x H (multiples of 16, <= 128) and another field of view:
-    ids bit-exact, depth <= 1e-6 vs the oracle restated at the same config."""
+    ids bit-exact, depth <= 1e-6 vs the oracle restated at the same config.
+    The wide fields of view (2.5, 2.8 rad) exercise the pixel-rectangle cull's
+    clipping threshold zc sqrt(1 + tan_x^2 + tan_y^2) at large tangents."""
     from paper_2106_14405_b200.sim import BatchSimulator
 
     g = golden("render.npz")
@@ -136,3 +138,31 @@ def test_single_env_and_side_stream():
     assert outs[0][0] == outs[1][0]
     for a, b in zip(outs[0][1], outs[1][1]):
         assert torch.equal(a, b)
+
+
+def test_wide_fov_random_views_all_layouts():
+    """The reference's random views of all three layouts (render_views.npz:
+    walkable views, cameras inside / just in front of static boxes) at a
+    2.6 rad field of view, both cameras: ids bit-exact and depth <= 1e-6 vs
+    the oracle at the same config (the pixel-rectangle cull clips boxes that
+    reach behind the camera; wide tangents stress its threshold)."""
+    from oracle.oracle import Oracle
+    from paper_2106_14405_b200.compiler import compile_world
+    from paper_2106_14405_b200.scene import build_world, flat_clutter
+    from paper_2106_14405_b200.sim import BatchSimulator
+
+    g = golden("render_views.npz")
+    sel = list(range(0, len(g["cam"]), 3))
+    lay = [int(g["layout"][i]) for i in sel]
+    fov = 2.6
+    sim = BatchSimulator(layouts=(0, 1, 2), n_env=len(sel), env_layout=lay, render={"fov": fov})
+    sim.set_state([g["state"][i].tobytes() for i in sel])
+    rgba, depth, ids = (t.cpu().numpy() for t in sim.render(("head", "arm")))
+    sim.close()
+    orcs = {v: Oracle(compile_world(build_world(v, flat_clutter()))) for v in range(3)}
+    for j, i in enumerate(sel):
+        for cam in (0, 1):
+            o_rgba, o_depth, o_ids, _ = orcs[lay[j]].render(g["state"][i].tobytes(), cam, fov=fov)
+            np.testing.assert_array_equal(ids[j, cam], o_ids, err_msg=f"view {i} cam {cam}")
+            np.testing.assert_allclose(depth[j, cam], o_depth, rtol=1e-6, atol=1e-6)
+            assert np.abs(rgba[j, cam].astype(int) - o_rgba.astype(int)).max() <= 1
