@@ -549,7 +549,10 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RenderSmem &S = *reinterpret_cast<RenderSmem *>(smem_raw);
   double *plane = reinterpret_cast<double *>(smem_raw + kPlaneOff);
-  const int env = blockIdx.x / n_cam_out, slot = blockIdx.x % n_cam_out;
+  // camera-major block order: every env's first camera, then every env's
+  // second one -- the head camera's images cost ~2-3x the arm camera's, so the
+  // grid's tail is made of the cheaper images (longest-first scheduling)
+  const int env = blockIdx.x % B.n_env, slot = blockIdx.x / B.n_env;
   int cam = -1;
   for (int c = 0, k = 0; c < 32; ++c)
     if (cam_mask & (1u << c)) {
