@@ -541,6 +541,12 @@ __device__ __noinline__ void wait_bulk(uint64_t *bar) { mbar_wait(bar, 0); }
 
 // kAll: every output pointer is non-NULL (the product launch) -- the per-pixel
 // NULL checks (uniform pointer loads and compares) compile away
+#ifdef RSIM_RENDER_TIMELINE
+// diagnostic build only (tools/render_timeline.py): per CTA begin / end
+// (%globaltimer) and SM of the last render launch
+__device__ unsigned long long g_timeline[16384][3];
+#endif
+
 template <int kMode, bool kCount, bool kAll = false>
 __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBlocksMesh : kMinBlocksProxy)
     render_kernel(DevBatch B, uint32_t cam_mask, int n_cam_out, uint32_t *rgba, float *depth, int32_t *ids,
@@ -563,6 +569,10 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
   const StateLayout &L = B.L;
   const double *sd = B.sd + (size_t)env * L.dbl_size;
   const int tid = threadIdx.x, np = sc.np;
+#ifdef RSIM_RENDER_TIMELINE
+  unsigned long long t_begin;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+#endif
   const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   long long clk[7];  // counting variant: SM clock at the set-up barriers (thread 0)
   if (kCount) clk[0] = clock64();
@@ -953,6 +963,16 @@ __global__ void __launch_bounds__(kRenderThreads, kMode == kMeshExact ? kMinBloc
       }
     }
   }
+#ifdef RSIM_RENDER_TIMELINE
+  __syncthreads();
+  if (tid == 0 && !count && blockIdx.x < 16384) {
+    unsigned long long t_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_timeline[blockIdx.x][0] = t_begin; g_timeline[blockIdx.x][1] = t_end; g_timeline[blockIdx.x][2] = smid;
+  }
+#endif
   if (count) {
     for (int i = 0; i < 12; ++i) atomicAdd(work + i, wk.v[i]);
     __syncthreads();
@@ -1047,3 +1067,9 @@ cudaError_t launch_render_mesh(const DevBatch &B, uint32_t cam_mask, uint8_t *rg
 }
 
 }  // namespace rsim
+
+#ifdef RSIM_RENDER_TIMELINE
+extern "C" int rsim_debug_render_timeline(void *host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, rsim::g_timeline, sizeof(unsigned long long) * 3 * (size_t)n);
+}
+#endif

@@ -1,10 +1,12 @@
-"""Per-CTA timeline of the render kernel (a variant library built with the
-timeline probe): CTA begin / end (%globaltimer) and SM, for the
-render alone and inside the interleaved bench step (2048 envs, 2 cameras).
-Reports the mean CTA duration per camera, the resident-CTA count over time and
-the tail (time after the last CTA started).
+"""Per-CTA timeline of the render kernel (a diagnostic library built with
+-DRSIM_RENDER_TIMELINE): CTA begin / end (%globaltimer) and SM, for the render
+alone and inside the interleaved bench step (2048 envs, 2 cameras).  Reports
+the mean CTA duration per camera, the mean resident-CTA count and the tail
+(time after the last CTA started).
 
-    RSIM_LIB=<variant>/librsim.so python tools/render_timeline.py
+    RSIM_NVCC_FLAGS=-DRSIM_RENDER_TIMELINE RSIM_LIB_DIR=paper_2106_14405_b200/_lib_tl \
+        python -c "from paper_2106_14405_b200 import build; build.build()"
+    RSIM_LIB=paper_2106_14405_b200/_lib_tl/librsim.so python tools/render_timeline.py
 """
 import ctypes as C
 import os
