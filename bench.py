@@ -37,7 +37,7 @@ METRIC = "simulation steps/sec (128x128 RGBD + 1/30s physics) at 1/2/4/8 B200 vs
 UNIT = "env-steps/s"
 H = W = 128
 N_CAMS = 2
-PROFILE_JSON = "profiles/r2g_kernels.json"
+PROFILE_JSON = "profiles/r2i_kernels.json"
 HBM_PEAK = 6450.6  # MEASURED_PEAKS.json hbm_gbs (driver-written on this pool's B200s); read at run time when present  # ncu --set full per-kernel DRAM bytes (tools/ncu_summary.py --json)
 PAPER_8GPU_SPS = 25734.0  # PAPER.md:530 (8x RTX 2080 Ti, Idle) -- different hardware, not this metric's config
 
